@@ -1,0 +1,76 @@
+"""Shared test helpers.
+
+`-m "not gpu"` runs here (no GPU): oracle vs golden fixtures, host logic,
+C-ABI symbol exports, gloo multi-process layout tests.
+`-m gpu` runs on a B200: CUDA path vs oracle / golden fixtures.
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLDEN = ROOT / "tests" / "golden"
+for p in (str(ROOT), str(ROOT / "oracle")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+def load(name: str) -> dict:
+    with np.load(GOLDEN / f"{name}.npz", allow_pickle=False) as z:
+        return {k: z[k] for k in z.files}
+
+
+def jload(arr) -> object:
+    return json.loads(str(arr))
+
+
+def graph_keys(fx: dict, prefix: str = "g_"):
+    """(n, [(rows, cols, vals)] per t) from a fixture."""
+    n, T = int(fx[f"{prefix}n"]), int(fx[f"{prefix}T"])
+    return n, [(fx[f"{prefix}rows{t}"], fx[f"{prefix}cols{t}"], fx[f"{prefix}vals{t}"])
+               for t in range(T)]
+
+
+def params_from(fx: dict, prefix: str) -> dict:
+    return {k[len(prefix):]: fx[k].copy() for k in fx if k.startswith(prefix)}
+
+
+def labels_from(fx: dict, prefix: str) -> dict:
+    frames = fx[f"{prefix}frames"]
+    return {int(t): (fx[f"{prefix}pairs{int(t)}"], fx[f"{prefix}labels{int(t)}"]) for t in frames}
+
+
+def guarded_close(got: np.ndarray, ref: np.ndarray, rtol: float, atol_frac: float = 1e-6):
+    """|g - r| <= rtol * max(|g|, |r|) + atol, atol = atol_frac * ||r||_inf
+    (the reference's guarded form, conftest.py:71-86, at a given rtol)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    atol = atol_frac * float(np.max(np.abs(ref))) if ref.size else 0.0
+    err = np.abs(got - ref)
+    bound = rtol * np.maximum(np.abs(got), np.abs(ref)) + atol
+    bad = err > bound
+    return (not bad.any()), (float(err.max()) if err.size else 0.0), int(bad.sum())
+
+
+def assert_grads_close(got: dict, ref: dict, rtol: float, atol_frac: float = 1e-6):
+    assert sorted(got) == sorted(ref)
+    for k in sorted(ref):
+        assert got[k].shape == ref[k].shape, k
+        ok, worst, nbad = guarded_close(got[k], ref[k], rtol, atol_frac)
+        assert ok, f"{k}: {nbad} entries off, worst abs err {worst:.3e}"
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    import dtgnn_oracle
+    return dtgnn_oracle
