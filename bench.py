@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""Training-epoch benchmark of the dynamic-GNN hot path (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "Epinions-scale"): cd-gcn (skip-GCN +
+LSTM, 2 layers, hidden = embed = 64) on a synthetic exact-churn dynamic
+graph with N = 750k vertices, T = 32 snapshots, 468,750 edges per snapshot
+(15M edges in total), 10% churn per step, link-prediction labels with
+theta = 0.1, gradient checkpointing with nblk = 4 (bsize = 8).  Under
+torchrun with N GPUs the graph grows with N (N x 750k vertices, N x 468,750
+edges per snapshot: weak scaling, snapshot-partitioned as in the paper).
+
+A step = one full training epoch (checkpointed forward sweep + rerun +
+backward + gradient all-reduce + Adam).  `value` = edge*snapshots/s of the
+whole job with the graph encoding resident in HBM (the per-pass CSR
+rebuild still runs on device); `e2e` = the same metric through the public
+drop-in API `distributed_epoch` with host parameters in, host gradients
+out and every pass's graph deltas copied from pinned host memory.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_PER_GPU = 750_000
+EDGES_PER_GPU = 468_750
+T = 32
+HIDDEN = 64
+CHURN = 0.10
+THETA = 0.10
+NBLK = 4
+METRIC = "training epoch time and edges·snapshots/sec at 1/2/4/8 B200; SpMM HBM GB/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int, out: Path | None):
+        self.proc = None
+        self.gpu = gpu
+        self.out = out
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+            if self.out is not None:
+                self.out.write_text("\n".join(self.lines) + "\n")
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+
+def make_workload(P: int, seed: int = 1):
+    import paper_2109_07893_b200 as pk
+    from paper_2109_07893_b200.synth import churn_graph, sample_pairs_fast
+    n = N_PER_GPU * P
+    g = churn_graph(n, T, EDGES_PER_GPU * P, CHURN, seed=seed)
+    cfg = pk.ModelConfig("cd-gcn", in_features=2, hidden_features=HIDDEN, embed_features=HIDDEN)
+    data = pk.prepare_training_data(cfg, g)
+    train, _ = sample_pairs_fast(g, THETA, seed + 1000003)
+    params = pk.init_params(cfg, 0)
+    rng = np.random.default_rng(77)          # non-zero head: every upstream gradient is live
+    params["head.w"] = rng.uniform(-0.5, 0.5, size=params["head.w"].shape)
+    params["head.b"] = rng.uniform(-0.1, 0.1, size=params["head.b"].shape)
+    return cfg, g, data, train, params
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per kernel call (for the roofline)
+
+
+def kernel_work(name, args, l2_bytes, layers_real):
+    """(flops, bytes) of one C-ABI call, from its arguments."""
+    if name == "dgnn_lstm_forward_step":
+        rows, kx, hp, gates = args[0], args[1], args[2], args[11]
+        kin, h = layers_real.get(kx, (kx, hp))
+        flops = 2 * rows * (kin + h) * 4 * h
+        byts = 4 * rows * (kin + 4 * h + (4 * h if gates else 0))
+        return flops, byts
+    if name == "dgnn_lstm_backward_step":
+        rows, kx, hp = args[0], args[1], args[2]
+        kin, h = layers_real.get(kx, (kx, hp))
+        flops = 2 * rows * 4 * h * (kin + h)
+        byts = 4 * rows * (h * 4 + 4 * h + 4 * h + kin + 2 * h)
+        return flops, byts
+    if name == "dgnn_gemm_tn":
+        rows, m, n = args[0], args[1], args[2]
+        return 2 * rows * m * n, 4 * rows * (m + n)
+    if name == "dgnn_gcn_forward":
+        n, rp, fp, hp = args[0], args[1], args[5], args[7]
+        return 0, None
+    return 0, 0
+
+
+def spmm_bytes(n, nnz, f, write_width, l2):
+    gather = 4 * f * nnz if 4 * n * f > l2 else 4 * n * f
+    return 4 * (n + 1) + 8 * nnz + gather + 4 * n * write_width, 4 * n * f > l2
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    P = world
+    if args.gpus != P:
+        if P == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if P > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2109_07893_b200 as pk
+    from paper_2109_07893_b200 import _lib
+    from paper_2109_07893_b200.engine import Engine, LocalFabric, NcclFabric
+
+    t0 = time.time()
+    cfg, g, data, train, params = make_workload(P)
+    prep_s = time.time() - t0
+    fabric = NcclFabric() if P > 1 else LocalFabric()
+    eng = Engine(cfg, g, P, NBLK, resident=True, fabric=fabric)
+    eng.set_labels(train.by_time, None)
+    eng.params.load(params)
+    count = train.total_pairs()
+    total_es = int(sum(s.nnz for s in g.snapshots))     # whole job: edge*snapshots per epoch
+
+    def step():
+        loss_dev, grads = eng.epoch(None, None, None, count, "mean")
+        eng.params.adam(0.01)
+        return loss_dev
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    layers_real = {}
+    for Ly in eng.layout.layers:
+        layers_real[Ly.kx] = (Ly.fin + Ly.gout, Ly.out)
+    timed_names = ["dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_gemm_tn", "dgnn_gcn_forward",
+                   "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows", "dgnn_csr_apply_delta",
+                   "dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_head_loss", "dgnn_head_grad",
+                   "dgnn_head_scatter"]
+    timer = _lib.KernelTimer(timed_names)
+    clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_rank{rank}.csv"
+                          if (ROOT / "gpurun_out").exists() else None)
+    if P > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    _lib.set_timer(timer)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with clocks:
+        e0.record()
+        for _ in range(args.steps):
+            loss_dev = step()
+        e1.record()
+        torch.cuda.synchronize()
+    _lib.set_timer(None)
+    launches = _lib.launch_count() - launches0
+    if P > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if P > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    loss = float(loss_dev.item()) * eng.scale
+    durs = timer.durations()
+
+    # ---- roofline of the dominant kernel (time share over the timed region)
+    hbm, bf16, bf16_s, peak_kind = peaks()
+    tot = {k: sum(d for d, _ in v) for k, v in durs.items()}
+    dom = max(tot, key=tot.get) if tot else None
+    roof = None
+    if dom in ("dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_gemm_tn"):
+        fl = sum(kernel_work(dom, a, l2, layers_real)[0] for _, a in durs[dom])
+        by = sum(kernel_work(dom, a, l2, layers_real)[1] for _, a in durs[dom])
+        secs = tot[dom] / 1e3
+        roof = {"kernel": dom, "bound": "tensor", "achieved": fl / secs / 1e12, "peak": bf16_s,
+                "unit": "TFLOP/s", "frac": fl / secs / 1e12 / bf16_s, "traffic": None,
+                "peak_source": f"{peak_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
+                "note": "SIMT fp32 kernel; fp32-accurate tensor-core path (3xTF32) would peak at 1/6 of bf16",
+                "hbm_achieved_gbs": by / secs / 1e9, "hbm_frac": by / secs / 1e9 / hbm,
+                "share_of_step": tot[dom] / (ms * args.steps),
+                "launches": len(durs[dom]), "avg_launch_us": tot[dom] / len(durs[dom]) * 1e3}
+    # SpMM (fused GCN forward with aggregation, layer 1) HBM rate
+    spmm = None
+    sl = [(d, a) for d, a in durs.get("dgnn_gcn_forward", []) if a[1] is not None]
+    if sl:
+        r0 = eng.ranks[0]
+        nnz_mean = float(np.mean(eng.enc.nnz_hat))
+        Ly = eng.layout.layers[1]
+        n = eng.plan.N
+        byts, gath = spmm_bytes(n, nnz_mean, Ly.fp, Ly.rw, l2)
+        secs = sum(d for d, _ in sl) / 1e3
+        achieved = byts * len(sl) / secs / 1e9
+        cb, _ = spmm_bytes(n, nnz_mean, Ly.fp, Ly.rw, 1 << 62)
+        spmm = {"kernel": "dgnn_gcn_forward (CSR SpMM + W + ReLU, layer 1)", "bound": "hbm",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "bytes_model": "gather-inclusive" if gath else "compulsory",
+                "compulsory_gbs": cb * len(sl) / secs / 1e9, "avg_launch_us": secs / len(sl) * 1e6,
+                "nnz_per_snapshot": nnz_mean, "launches": len(sl)}
+    kernel_table = {k: {"ms_total": v, "launches": len(durs[k]), "share": v / (ms * args.steps)}
+                    for k, v in sorted(tot.items(), key=lambda kv: -kv[1])}
+
+    # ---- e2e through the public drop-in API (host buffers, deltas streamed)
+    e2e = None
+    if not args.skip_e2e:
+        comm, transfer = pk.CommLedger(), pk.TransferLedger()
+        hp = {k: v.copy() for k, v in params.items()}
+        st = pk.init_adam(hp)
+        pk.distributed_epoch(cfg, data, train, hp, P, NBLK)        # build + warm the engine
+        torch.cuda.synchronize()
+        if P > 1:
+            dist.barrier()
+        h0 = transfer.h2d_bytes
+        ts = time.perf_counter()
+        for _ in range(args.steps):
+            loss_e, grads, _, _ = pk.distributed_epoch(cfg, data, train, hp, P, NBLK, comm=comm,
+                                                       transfer=transfer)
+            pk.adam_step(hp, grads, st, 0.01)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - ts) / args.steps
+        if P > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        pbytes = 8 * eng.layout.count
+        e2e = {"value": total_es / e2e_s, "unit": "edge*snapshots/s", "ms_per_step": e2e_s * 1e3,
+               "h2d_bytes_per_step": int((transfer.h2d_bytes - h0) / args.steps) + pbytes,
+               "d2h_bytes_per_step": pbytes + 8,
+               "delta_vs_full_bytes": (transfer.full_equiv_bytes / transfer.h2d_bytes) if transfer.h2d_bytes else None,
+               "api": "paper_2109_07893_b200.distributed_epoch + adam_step"}
+
+    cpu = None
+    if rank == 0 and P == 1 and not args.skip_cpu:
+        cpu = cpu_baseline(sample_scale=args.cpu_scale, threads=True)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": total_es / (ms / 1e3), "unit": "edge*snapshots/s", "n_gpus": P,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (fp64 graph values / master weights)",
+            "data": "synthetic exact-churn dynamic graph, random-init weights",
+            "config": {"workload": "configs[1] Epinions-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=64, "
+                                   "N=750k/GPU, T=32, 468,750 edges/snapshot/GPU (15M/GPU total), 10% churn",
+                       "model": "cd-gcn", "num_vertices": N_PER_GPU * P, "num_timesteps": T,
+                       "edges_per_snapshot": EDGES_PER_GPU * P, "hidden": HIDDEN, "nblk": NBLK,
+                       "theta": THETA, "train_pairs": count, "parallelism": f"snapshot-partitioned x{P}",
+                       "l2": "inputs larger than L2 (per-epoch working set ~tens of GB)",
+                       "graph_in_timed_region": "delta-encoded graph resident in HBM, CSR/Laplacian "
+                                                "rebuilt on device every pass"},
+            "loss": loss,
+            "gpu_launches": launches,
+            "roofline": roof,
+            "spmm_roofline": spmm,
+            "kernels": kernel_table,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "prep_seconds": prep_s,
+        }
+        print(json.dumps(line))
+    if P > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle port of the reference algorithm
+
+
+def cpu_sample(scale: int):
+    n = N_PER_GPU // scale
+    n -= n % 8
+    m = EDGES_PER_GPU // scale
+    return n, m
+
+
+def cpu_baseline(sample_scale: int = 128, threads: bool = True, steps: int = 1, warmup: int = 0):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import dtgnn_oracle as O
+    from paper_2109_07893_b200.synth import churn_keys
+    n, m = cpu_sample(sample_scale)
+    keys = churn_keys(n, T, m, CHURN, seed=1)
+    snaps = [O.Coo(n, k // n, k % n, np.ones(k.shape[0])) for k in keys]
+    cfg = O.Cfg("cd-gcn", 2, HIDDEN, HIDDEN)
+    Pp = O.prepare(cfg, snaps)
+    train, _ = O.sample_labels(snaps, THETA, 1 + 1000003)
+    params = O.init_params(cfg, 0)
+    rng = np.random.default_rng(77)
+    params["head.w"] = rng.uniform(-0.5, 0.5, size=params["head.w"].shape)
+    cores = os.cpu_count() or 1
+    bsize = T // NBLK
+    workers = max(p for p in range(1, min(cores, bsize) + 1) if bsize % p == 0 and n % p == 0) if threads else 1
+    st = O.adam_state(params)
+
+    def step():
+        loss, grads, _, _ = O.distributed_epoch(cfg, Pp, train, params, workers, NBLK, threads=threads)
+        O.adam(params, grads, st, 0.01)
+
+    for _ in range(warmup):
+        step()
+    c0 = time.process_time()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    util = (time.process_time() - c0) / (dt * steps)
+    es = T * m
+    return {"value": es / dt, "unit": "edge*snapshots/s", "cores": workers, "kind": "port",
+            "seconds_per_epoch": dt, "cpu_utilisation": util, "host_cpus": cores,
+            "sample": f"oracle port (numpy fp64 restatement of dtgnn distributed_epoch, threads scheduler, "
+                      f"P={workers}) + Adam on the configs[1] shape scaled 1/{sample_scale}: N={n}, T={T}, "
+                      f"{m} edges/snapshot, 10% churn, cd-gcn H={HIDDEN}, nblk={NBLK}; metric is linear in "
+                      f"N and nnz"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = cpu_baseline(sample_scale=args.cpu_scale_ref, threads=True, steps=args.steps, warmup=args.warmup)
+    line = {"metric": METRIC, "value": cb["value"], "unit": "edge*snapshots/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_epoch"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+            "data": "synthetic exact-churn dynamic graph, random-init weights",
+            "config": {"workload": "configs[1] Epinions-scale cd-gcn hidden=64 (CPU sample, see cpu_baseline)",
+                       "model": "cd-gcn"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "edge*snapshots/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-scale", type=int, default=128)
+    ap.add_argument("--cpu-scale-ref", type=int, default=256)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

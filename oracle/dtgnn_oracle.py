@@ -951,6 +951,11 @@ def distributed_epoch(cfg: Cfg, P: Prepared, by_time, params, workers: int, nblk
             run("set_input", b, l, per=own(fr, b))
 
     try:
+        from threadpoolctl import threadpool_limits  # BLAS pinned to 1 thread (core.py:195-209)
+        blas = threadpool_limits(limits=1)
+    except ImportError:  # pragma: no cover
+        blas = None
+    try:
         tot = 0.0
         for b in range(plan.nblk):
             run("begin", b, False)
@@ -980,6 +985,8 @@ def distributed_epoch(cfg: Cfg, P: Prepared, by_time, params, workers: int, nblk
     finally:
         if pool is not None:
             pool.shutdown(wait=True)
+        if blas is not None:
+            blas.unregister()
     return loss, grads, comm, transfer
 
 

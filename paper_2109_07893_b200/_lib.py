@@ -1,0 +1,166 @@
+"""ctypes binding of libdgnn_b200.so (the C ABI in include/dgnn_b200.h).
+
+This is the only place the package touches native code.  The library is
+loaded lazily on first use and the product path fails loudly when it is
+missing -- there is no CPU fallback anywhere in the package.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_void_p
+from pathlib import Path
+
+from .errors import CorruptDeltaError, DeviceError, InputError
+
+LIB_PATH = Path(__file__).resolve().parent / "libdgnn_b200.so"
+
+
+class Frame(ctypes.Structure):
+    """`dgnn_frame`: row i at ptr + (i / rows_per_slab) * slab_stride + (i % rows_per_slab) * ld."""
+    _fields_ = [("ptr", c_void_p), ("ld", c_int64), ("rows_per_slab", c_int64), ("slab_stride", c_int64)]
+
+
+P = c_void_p
+_SIGS = {
+    "dgnn_last_error": (ctypes.c_char_p, []),
+    "dgnn_abi_version": (c_int, []),
+    "dgnn_launch_count": (ctypes.c_longlong, []),
+    "dgnn_device_check": (c_int, [c_int]),
+    "dgnn_rowptr_from_sorted_rows": (c_int, [c_int32, c_int64, P, P, P]),
+    "dgnn_csr_apply_delta_workspace": (c_size_t, [c_int32]),
+    "dgnn_csr_apply_delta": (c_int, [c_int32, P, P, c_int64, P, P, c_int64, P, P, P, P, c_int64, P,
+                                     c_size_t, P, P]),
+    "dgnn_csr_transpose_workspace": (c_size_t, [c_int32]),
+    "dgnn_csr_transpose_staged": (c_int, [c_int32, c_int64, P, P, P, P, P, P, P, P, P, c_size_t, P]),
+    "dgnn_laplacian_workspace": (c_size_t, [c_int32]),
+    "dgnn_laplacian": (c_int, [c_int32, P, P, P, P, c_int, P, P, P, P, c_int64, P, c_size_t, P]),
+    "dgnn_degree_features": (c_int, [c_int32, P, P, P, c_int64, P]),
+    "dgnn_spmm_f64": (c_int, [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, P]),
+    "dgnn_spmm_f32": (c_int, [c_int32, P, P, P, Frame, c_int32, Frame, P]),
+    "dgnn_gcn_forward": (c_int, [c_int32, P, P, P, Frame, c_int32, P, c_int32, c_int, Frame, Frame, P]),
+    "dgnn_gcn_backward_rows": (c_int, [c_int32, Frame, Frame, c_int32, P, c_int32, c_int, Frame, P]),
+    "dgnn_gcn_weight_grad_workspace": (c_size_t, [c_int32, c_int32]),
+    "dgnn_gcn_weight_grad": (c_int, [c_int32, Frame, Frame, Frame, c_int32, c_int32, c_int, P, P,
+                                     c_size_t, P]),
+    "dgnn_lstm_forward_step": (c_int, [c_int64, c_int32, c_int32, P, c_int64, P, P, P, P, P, P, P, P]),
+    "dgnn_lstm_backward_step": (c_int, [c_int64, c_int32, c_int32, P, P, P, P, P, P, P, P, P, c_int64,
+                                        P, P, P]),
+    "dgnn_gemm_tn_workspace": (c_size_t, [c_int32, c_int32]),
+    "dgnn_gemm_tn": (c_int, [c_int64, c_int32, c_int32, P, c_int64, P, c_int64, P, c_int64, P, P,
+                             c_size_t, P]),
+    "dgnn_axpy_frame": (c_int, [c_int64, c_float, P, P, c_int, P]),
+    "dgnn_head_loss": (c_int, [c_int64, P, P, P, Frame, c_int32, c_int32, P, P, c_double, P, c_int32,
+                               P, P]),
+    "dgnn_head_grad_workspace": (c_size_t, [c_int32, c_int32]),
+    "dgnn_head_grad": (c_int, [c_int64, P, P, Frame, c_int32, c_int32, P, P, P, P, c_size_t, P]),
+    "dgnn_head_scatter": (c_int, [c_int32, P, P, P, P, c_int32, c_int32, Frame, P]),
+    "dgnn_head_predict": (c_int, [c_int64, P, P, P, Frame, c_int32, c_int32, P, P, P, P]),
+    "dgnn_sum_f64": (c_int, [c_int64, P, P, c_int, P]),
+    "dgnn_adam": (c_int, [c_int64, P, P, P, P, c_double, c_double, c_double, c_double, c_double,
+                          c_double, c_double, c_double, P]),
+    "dgnn_params_to_device": (c_int, [c_int64, P, P, P, P, P]),
+    "dgnn_grads_gather": (c_int, [c_int64, P, P, P, P]),
+    "dgnn_fill_f32": (c_int, [c_int64, c_float, P, P]),
+    "dgnn_cast_f64_to_f32_frame": (c_int, [c_int32, c_int32, P, c_int64, Frame, P]),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise DeviceError(f"{LIB_PATH.name} is missing; build it with "
+                              "`python -m paper_2109_07893_b200.build` (nvcc, sm_100a)")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list:
+    return sorted(_SIGS)
+
+
+class KernelTimer:
+    """Records CUDA events around every C-ABI call whose name is in `names`,
+    on the stream the call was enqueued on (its last argument).  Used by
+    bench.py for per-kernel durations inside the timed region."""
+
+    def __init__(self, names):
+        self.names = set(names)
+        self.records = {}      # name -> list of (start, end, args)
+        self._streams = {}
+
+    def stream(self, handle):
+        import torch
+        if handle not in self._streams:
+            self._streams[handle] = torch.cuda.ExternalStream(handle)
+        return self._streams[handle]
+
+    def durations(self):
+        """name -> list of (ms, args); synchronises."""
+        import torch
+        torch.cuda.synchronize()
+        return {k: [(s.elapsed_time(e), a) for s, e, a in v] for k, v in self.records.items()}
+
+
+_timer: KernelTimer | None = None
+
+
+def set_timer(timer: KernelTimer | None) -> None:
+    global _timer
+    _timer = timer
+
+
+def launch_count() -> int:
+    return int(lib().dgnn_launch_count())
+
+
+def call(name: str, *args) -> None:
+    t = _timer
+    if t is not None and name in t.names:
+        import torch
+        s = t.stream(args[-1]) if args[-1] else torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        rc = getattr(lib(), name)(*args)
+        e1.record(s)
+        t.records.setdefault(name, []).append((e0, e1, args))
+    else:
+        rc = getattr(lib(), name)(*args)
+    if rc:
+        msg = lib().dgnn_last_error().decode(errors="replace")
+        if rc == 1:
+            raise InputError(f"{name}: {msg}")
+        if rc == 2:
+            raise CorruptDeltaError(f"{name}: {msg}")
+        raise DeviceError(f"{name} failed (code {rc}): {msg}")
+
+
+def query(name: str, *args) -> int:
+    return int(getattr(lib(), name)(*args))
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None passes NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def frame(t, ld: int | None = None, rows_per_slab: int = 0, slab_stride: int = 0) -> Frame:
+    if t is None:
+        return Frame(None, 0, 0, 0)
+    return Frame(t.data_ptr(), int(ld if ld is not None else t.shape[-1]), int(rows_per_slab),
+                 int(slab_stride))
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

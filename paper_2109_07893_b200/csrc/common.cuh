@@ -1,0 +1,64 @@
+// Shared helpers for the sm_100a kernels of libdgnn_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dgnn_b200.h"
+
+namespace dgnn {
+
+void set_error(const char* fmt, ...);
+// Counts every kernel launch made through the C ABI (dgnn_launch_count).
+void note_launch();
+// Checks cudaGetLastError after a launch sequence.
+int launch_status(const char* what);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+constexpr int kSMs = 148;  // B200
+
+// ---- frames -------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T* frame_row(const dgnn_frame& f, int64_t i) {
+    if (f.rows_per_slab <= 0) return reinterpret_cast<T*>(f.ptr) + i * f.ld;
+    const int64_t s = i / f.rows_per_slab;
+    const int64_t r = i - s * f.rows_per_slab;
+    return reinterpret_cast<T*>(f.ptr) + s * f.slab_stride + r * f.ld;
+}
+
+// ---- warp helpers -------------------------------------------------------
+__device__ __forceinline__ int warp_inclusive_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float sigmoidf_acc(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+// device-wide exclusive scan (in place), implemented in graph.cu
+size_t scan_workspace_bytes(int64_t n);
+int exclusive_scan_i32(int32_t* data, int64_t n, void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace dgnn
+
+#define DGNN_CHECK_ARG(cond, msg)                 \
+    do {                                          \
+        if (!(cond)) {                            \
+            ::dgnn::set_error("%s", msg);         \
+            return DGNN_EINPUT;                   \
+        }                                         \
+    } while (0)

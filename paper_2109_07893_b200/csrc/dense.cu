@@ -1,0 +1,227 @@
+// Deterministic weight-gradient reductions and small dense helpers.
+//
+// Weight gradients in the reference are sums over every vertex row of
+// every timestep (training.py:365, 422-424, 730-731).  Here they are split-K
+// GEMMs: CTA (tile, chunk) accumulates a 64x64 fp32 partial over a fixed row
+// range in registers (4x4 per thread), partials are reduced in a fixed order
+// in fp64 and added to an fp64 gradient accumulator -- bit-reproducible from
+// run to run, no floating-point atomics anywhere.
+#include "common.cuh"
+
+namespace dgnn {
+
+constexpr int TN_BM = 64, TN_BN = 64, TN_BR = 16;
+
+// Loaders map (row r, column c) of the logical A / B operands to memory; c is
+// always a multiple of 4 and the 4 columns are contiguous.
+struct PlainLoader {
+    const float* p;
+    int64_t ld;
+    int ncols;
+    __device__ __forceinline__ float4 load(int64_t r, int c) const {
+        if (c >= ncols) return make_float4(0.f, 0.f, 0.f, 0.f);
+        return *reinterpret_cast<const float4*>(p + r * ld + c);
+    }
+};
+
+struct FrameLoader {
+    dgnn_frame f;
+    int off, ncols;
+    __device__ __forceinline__ float4 load(int64_t r, int c) const {
+        if (c >= ncols) return make_float4(0.f, 0.f, 0.f, 0.f);
+        return *reinterpret_cast<const float4*>(frame_row<const float>(f, r) + off + c);
+    }
+};
+
+// dq = dr[off + c] * [r[off + c] > 0]
+struct MaskedFrameLoader {
+    dgnn_frame dr, r;
+    int off, ncols;
+    __device__ __forceinline__ float4 load(int64_t row, int c) const {
+        if (c >= ncols) return make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 g = *reinterpret_cast<const float4*>(frame_row<const float>(dr, row) + off + c);
+        const float4 m = *reinterpret_cast<const float4*>(frame_row<const float>(r, row) + off + c);
+        return make_float4(m.x > 0.f ? g.x : 0.f, m.y > 0.f ? g.y : 0.f, m.z > 0.f ? g.z : 0.f,
+                           m.w > 0.f ? g.w : 0.f);
+    }
+};
+
+// partial[chunk][m][n] = sum_{r in chunk} A[r][m] * B[r][n]   (64x64 tile per CTA)
+// colsum partial (row m = M) when with_colsum: sum_r B[r][n].
+template <typename LA, typename LB>
+__global__ void __launch_bounds__(256) tn_partial_kernel(int64_t rows, int M, int N, LA la, LB lb,
+                                                         int64_t rows_per_chunk, float* __restrict__ part,
+                                                         int ldp, int with_colsum) {
+    __shared__ __align__(16) float As[TN_BR][TN_BM];
+    __shared__ __align__(16) float Bs[TN_BR][TN_BN];
+    const int tiles_n = (N + TN_BN - 1) / TN_BN;
+    const int tile = blockIdx.x, chunk = blockIdx.y;
+    const int m0 = (tile / tiles_n) * TN_BM, n0 = (tile % tiles_n) * TN_BN;
+    const int tid = threadIdx.x, tm = tid / 16, tn = tid % 16;
+    const int64_t r0 = chunk * rows_per_chunk;
+    const int64_t r1 = min(rows, r0 + rows_per_chunk);
+    float acc[4][4];
+    float csum[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    const int lr = tid / 16, lc = (tid % 16) * 4;  // loader: row lr of the 16-row stage, 4 columns
+    for (int64_t rb = r0; rb < r1; rb += TN_BR) {
+        const int64_t r = rb + lr;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (r < r1) {
+            a = la.load(r, m0 + lc);
+            b = lb.load(r, n0 + lc);
+        }
+        *reinterpret_cast<float4*>(&As[lr][lc]) = a;
+        *reinterpret_cast<float4*>(&Bs[lr][lc]) = b;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < TN_BR; ++k) {
+            const float4 av = *reinterpret_cast<const float4*>(&As[k][4 * tm]);
+            const float4 bv = *reinterpret_cast<const float4*>(&Bs[k][4 * tn]);
+            const float x[4] = {av.x, av.y, av.z, av.w}, y[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(x[i], y[j], acc[i][j]);
+            if (with_colsum && tm == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) csum[j] += y[j];
+            }
+        }
+        __syncthreads();
+    }
+    float* out = part + (int64_t)chunk * ldp * (M + 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + 4 * tm + i;
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + 4 * tn + j;
+            if (n < N) out[(int64_t)m * ldp + n] = acc[i][j];
+        }
+    }
+    if (with_colsum && tm == 0 && m0 == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + 4 * tn + j;
+            if (n < N) out[(int64_t)M * ldp + n] = csum[j];
+        }
+    }
+}
+
+// out[m][n] += sum_chunk part[chunk][m][n]  (fp64, ascending chunk order)
+__global__ void tn_reduce_kernel(int M, int N, int nchunks, const float* __restrict__ part, int ldp,
+                                 double* __restrict__ out, int64_t ldo, double* __restrict__ colsum) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)(M + (colsum ? 1 : 0)) * N;
+    if (i >= total) return;
+    const int m = (int)(i / N), n = (int)(i % N);
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += (double)part[((int64_t)c * (M + 1) + m) * ldp + n];
+    if (m < M) out[(int64_t)m * ldo + n] += s;
+    else colsum[n] += s;
+}
+
+constexpr int kMaxChunks = 2 * kSMs;
+
+static int chunks_for(int64_t rows, int tiles) {
+    int64_t c = cdiv(2 * kSMs, tiles);             // ~2 CTAs per SM in total
+    const int64_t by_rows = cdiv(rows, 4 * TN_BR);  // at least 64 rows per chunk
+    if (c > by_rows) c = by_rows;
+    if (c < 1) c = 1;
+    if (c > kMaxChunks) c = kMaxChunks;
+    return (int)c;
+}
+
+size_t tn_workspace_bytes(int M, int N) {
+    return (size_t)kMaxChunks * (M + 1) * N * sizeof(float) + 256;
+}
+
+template <typename LA, typename LB>
+int tn_run(int64_t rows, int M, int N, LA la, LB lb, double* out, int64_t ldo, double* colsum, void* ws,
+           size_t ws_bytes, cudaStream_t st, const char* what) {
+    if (rows <= 0 || M <= 0 || N <= 0) return DGNN_OK;
+    if (ws_bytes < tn_workspace_bytes(M, N)) {
+        set_error("%s: workspace too small", what);
+        return DGNN_EWORKSPACE;
+    }
+    const int tiles = (int)(cdiv(M, TN_BM) * cdiv(N, TN_BN));
+    const int nch = chunks_for(rows, tiles);
+    const int64_t per = cdiv(cdiv(rows, nch), TN_BR) * TN_BR;
+    const int nch_eff = (int)cdiv(rows, per);
+    float* part = reinterpret_cast<float*>(ws);
+    ::dgnn::note_launch();
+    tn_partial_kernel<LA, LB><<<dim3(tiles, nch_eff), 256, 0, st>>>(rows, M, N, la, lb, per, part, N,
+                                                                     colsum ? 1 : 0);
+    const int64_t total = (int64_t)(M + (colsum ? 1 : 0)) * N;
+    ::dgnn::note_launch();
+    tn_reduce_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(M, N, nch_eff, part, N, out, ldo, colsum);
+    return launch_status(what);
+}
+
+// deterministic fp64 sum (single CTA, fixed order)
+__global__ void __launch_bounds__(1024) sum_f64_kernel(int64_t n, const double* __restrict__ x,
+                                                        double* __restrict__ out, int accumulate) {
+    __shared__ double sh[1024];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 512; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = accumulate ? (*out + sh[0]) : sh[0];
+}
+
+__global__ void axpy_kernel(int64_t n, float coef, const float* __restrict__ y, float* __restrict__ z,
+                            int init) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float t = coef * y[i];
+    z[i] = init ? t : z[i] + t;
+}
+
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" {
+
+size_t dgnn_gemm_tn_workspace(int32_t m, int32_t n) { return tn_workspace_bytes(m, n); }
+
+int dgnn_gemm_tn(int64_t rows, int32_t m, int32_t n, const float* a, int64_t lda, const float* b, int64_t ldb,
+                 double* out, int64_t ldo, double* colsum, void* ws, size_t ws_bytes, void* stream) {
+    DGNN_CHECK_ARG(m % 4 == 0 && n % 4 == 0 && lda % 4 == 0 && ldb % 4 == 0, "gemm_tn: widths must be x4");
+    return tn_run(rows, m, n, PlainLoader{a, lda, m}, PlainLoader{b, ldb, n}, out, ldo, colsum, ws, ws_bytes,
+                  as_stream(stream), "gemm_tn");
+}
+
+size_t dgnn_gcn_weight_grad_workspace(int32_t fp, int32_t hp) { return tn_workspace_bytes(fp, hp); }
+
+int dgnn_gcn_weight_grad(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int32_t fp, int32_t hp, int skip,
+                         double* gw, void* ws, size_t ws_bytes, void* stream) {
+    DGNN_CHECK_ARG(fp % 4 == 0 && hp % 4 == 0, "gcn_weight_grad: widths must be x4");
+    const int off = skip ? fp : 0;
+    return tn_run((int64_t)n, fp, hp, FrameLoader{s, 0, fp}, MaskedFrameLoader{dr, r, off, hp}, gw, hp, nullptr,
+                  ws, ws_bytes, as_stream(stream), "gcn_weight_grad");
+}
+
+int dgnn_sum_f64(int64_t n, const double* x, double* out, int accumulate, void* stream) {
+    ::dgnn::note_launch();
+    sum_f64_kernel<<<1, 1024, 0, as_stream(stream)>>>(n, x, out, accumulate);
+    return launch_status("sum_f64");
+}
+
+int dgnn_axpy_frame(int64_t count, float coef, const float* y, float* z, int init, void* stream) {
+    if (count == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    axpy_kernel<<<(unsigned)cdiv(count, 256), 256, 0, as_stream(stream)>>>(count, coef, y, z, init);
+    return launch_status("axpy_frame");
+}
+
+}  // extern "C"

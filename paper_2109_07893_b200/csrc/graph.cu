@@ -1,0 +1,511 @@
+// Snapshot materialisation on device: CSR rebuild from graph-difference
+// deltas (K1), deterministic transpose, normalised Laplacian values in fp64
+// (K2), degree features and the exact fp64 SpMM used for the first-layer
+// precompute.  Reference: delta.py:126-146, dtdg.py:178-191, dtdg.py:255-266,
+// core.py:142-161.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace dgnn {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+int launch_status(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return DGNN_ECUDA;
+    }
+    return DGNN_OK;
+}
+
+const char* last_error() { return g_err; }
+
+// ---------------------------------------------------------------------------
+// device-wide exclusive scan of int32 (tile = 1024 threads x 4 items)
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int64_t kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(int32_t* d, int64_t n,
+                                                                  int32_t* sums) {
+    __shared__ int warp_tot[32];
+    const int64_t base = blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int v[kScanItems];
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = (base + i < n) ? d[base + i] : 0;
+        s += v[i];
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int incl = warp_inclusive_scan(s);
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int x = warp_tot[lane];
+        x = warp_inclusive_scan(x);
+        warp_tot[lane] = x;
+    }
+    __syncthreads();
+    int run = incl - s + (wid > 0 ? warp_tot[wid - 1] : 0);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < n) d[base + i] = run;
+        run += v[i];
+    }
+    if (threadIdx.x == kScanThreads - 1) sums[blockIdx.x] = run;
+}
+
+__global__ void scan_add_kernel(int32_t* d, int64_t n, const int32_t* sums) {
+    const int32_t add = sums[blockIdx.x];
+    const int64_t base = blockIdx.x * kScanTile;
+    for (int64_t i = base + threadIdx.x; i < base + kScanTile && i < n; i += blockDim.x) d[i] += add;
+}
+
+static int64_t round64(int64_t x) { return (x + 63) / 64 * 64; }
+
+size_t scan_workspace_bytes(int64_t n) {
+    int64_t total = 0;
+    do {
+        const int64_t nb = cdiv(n, kScanTile);
+        total += round64(nb);
+        n = nb;
+    } while (n > 1);
+    return (size_t)total * sizeof(int32_t) + 256;
+}
+
+int exclusive_scan_i32(int32_t* d, int64_t n, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (n <= 0) return DGNN_OK;
+    if (ws_bytes < scan_workspace_bytes(n)) {
+        set_error("scan workspace too small");
+        return DGNN_EWORKSPACE;
+    }
+    const int64_t nb = cdiv(n, kScanTile);
+    int32_t* sums = reinterpret_cast<int32_t*>(ws);
+    ::dgnn::note_launch();
+    scan_tiles_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(d, n, sums);
+    if (nb > 1) {
+        const int64_t used = round64(nb) * (int64_t)sizeof(int32_t);
+        int rc = exclusive_scan_i32(sums, nb, reinterpret_cast<char*>(ws) + used, ws_bytes - used, st);
+        if (rc) return rc;
+        ::dgnn::note_launch();
+        scan_add_kernel<<<(unsigned)nb, 256, 0, st>>>(d, n, sums);
+    }
+    return launch_status("exclusive_scan_i32");
+}
+
+// ---------------------------------------------------------------------------
+// sorted rows -> CSR row pointer
+
+__global__ void rowptr_kernel(int32_t n, int64_t nnz, const int32_t* __restrict__ rows,
+                              int32_t* __restrict__ rowptr) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r > n) return;
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (rows[mid] < r) lo = mid + 1; else hi = mid;
+    }
+    rowptr[r] = (int32_t)lo;
+}
+
+static int rowptr_launch(int32_t n, int64_t nnz, const int32_t* rows, int32_t* rowptr, cudaStream_t st) {
+    ::dgnn::note_launch();
+    rowptr_kernel<<<(unsigned)cdiv((int64_t)n + 1, 256), 256, 0, st>>>(n, nnz, rows, rowptr);
+    return launch_status("rowptr_from_sorted_rows");
+}
+
+// ---------------------------------------------------------------------------
+// K1: delta apply (delta.py:126-146), one thread per row, two-pointer merge
+
+__global__ void delta_count_kernel(int32_t n, const int32_t* __restrict__ orp,
+                                   const int32_t* __restrict__ drp, const int32_t* __restrict__ irp,
+                                   int32_t* __restrict__ nrp) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) { nrp[n] = 0; return; }
+    nrp[r] = (orp[r + 1] - orp[r]) - (drp[r + 1] - drp[r]) + (irp[r + 1] - irp[r]);
+}
+
+__global__ void delta_merge_kernel(int32_t n, const int32_t* __restrict__ orp,
+                                   const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
+                                   const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
+                                   const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
+                                   int32_t* __restrict__ ncol, int64_t cap, int32_t* status) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int di = drp[r];
+    const int de = drp[r + 1];
+    int ii = irp[r];
+    const int ie = irp[r + 1];
+    int64_t pos = nrp[r];
+    const int64_t end = min((int64_t)nrp[r + 1], cap);
+    int bad = 0;
+    for (int o = orp[r], oe = orp[r + 1]; o < oe; ++o) {
+        const int c = ocol[o];
+        while (di < de && dcol[di] < c) { ++bad; ++di; }       // deletion of an absent entry
+        if (di < de && dcol[di] == c) { ++di; continue; }       // deleted
+        while (ii < ie && icol[ii] < c) { if (pos < end) ncol[pos] = icol[ii]; ++pos; ++ii; }
+        if (ii < ie && icol[ii] == c) { ++bad; ++ii; }         // insertion overlaps the common set
+        if (pos < end) ncol[pos] = c;
+        ++pos;
+    }
+    bad += de - di;
+    while (ii < ie) { if (pos < end) ncol[pos] = icol[ii]; ++pos; ++ii; }
+    if (pos != (int64_t)nrp[r + 1]) ++bad;
+    if (bad) atomicAdd(status, bad);
+}
+
+// ---------------------------------------------------------------------------
+// deterministic transpose
+
+__global__ void zero_i32_kernel(int32_t* p, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = 0;
+}
+
+__global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ col, int32_t* cnt) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < nnz) atomicAdd(&cnt[col[e]], 1);
+}
+
+__global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ rp,
+                                         const int32_t* __restrict__ col, const double* __restrict__ val,
+                                         int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    for (int e = rp[r]; e < rp[r + 1]; ++e) {
+        const int pos = atomicAdd(&cursor[col[e]], 1);
+        tcol[pos] = (int32_t)r;
+        if (val) tval[pos] = val[e];
+    }
+}
+
+constexpr int kSmallSeg = 32;
+
+// Short segments: one thread sorts its column in registers/local memory.
+__global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp,
+                                      const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
+                                      int32_t* __restrict__ dst_col, double* __restrict__ dst_val) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const int b = trp[c], e = trp[c + 1], d = e - b;
+    if (d > kSmallSeg) return;
+    int key[kSmallSeg];
+    int idx[kSmallSeg];
+    for (int i = 0; i < d; ++i) {
+        int k = src_col[b + i], j = i;
+        while (j > 0 && key[j - 1] > k) { key[j] = key[j - 1]; idx[j] = idx[j - 1]; --j; }
+        key[j] = k;
+        idx[j] = b + i;
+    }
+    for (int i = 0; i < d; ++i) {
+        dst_col[b + i] = key[i];
+        if (dst_val) dst_val[b + i] = src_val[idx[i]];
+    }
+}
+
+// Long segments: one block per segment, rank = #smaller keys (keys are distinct rows).
+__global__ void seg_sort_large_kernel(int32_t n, const int32_t* __restrict__ trp,
+                                      const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
+                                      int32_t* __restrict__ dst_col, double* __restrict__ dst_val) {
+    for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+        const int b = trp[c], e = trp[c + 1], d = e - b;
+        if (d <= kSmallSeg) continue;
+        for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            const int k = src_col[b + i];
+            int rank = 0;
+            for (int j = 0; j < d; ++j) rank += src_col[b + j] < k;
+            dst_col[b + rank] = k;
+            if (dst_val) dst_val[b + rank] = src_val[b + i];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: Laplacian values (dtdg.py:178-191), fp64, no contraction
+
+__global__ void inv_sqrt_deg_kernel(int32_t n, const int32_t* __restrict__ arp, double* __restrict__ is) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double deg = (double)(arp[i + 1] - arp[i]);
+    is[i] = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, deg)));
+}
+
+__device__ __forceinline__ double lap_value(int64_t r, int c, double a, const double* is,
+                                            int transposed) {
+    if (c == r) {
+        const double ir = is[r];
+        return __dadd_rn(__dmul_rn(__dmul_rn(a, ir), ir), __dmul_rn(ir, ir));
+    }
+    // A entry (i, j): (a * is[i]) * is[j]; in the transposed structure row r is A's column.
+    return transposed ? __dmul_rn(__dmul_rn(a, is[c]), is[r]) : __dmul_rn(__dmul_rn(a, is[r]), is[c]);
+}
+
+__global__ void lap_count_kernel(int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+                                 const double* __restrict__ mval, const double* __restrict__ is, int transposed,
+                                 int32_t* __restrict__ cnt) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) { cnt[n] = 0; return; }
+    int k = 0;
+    bool diag = false;
+    for (int e = mrp[r]; e < mrp[r + 1]; ++e) {
+        const int c = mcol[e];
+        const double a = mval ? mval[e] : 1.0;
+        if (c == r) diag = true;
+        k += lap_value(r, c, a, is, transposed) != 0.0;
+    }
+    if (!diag) k += lap_value(r, (int)r, 0.0, is, transposed) != 0.0;
+    cnt[r] = k;
+}
+
+__global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+                                 const double* __restrict__ mval, const double* __restrict__ is, int transposed,
+                                 const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
+                                 float* __restrict__ o32, double* __restrict__ o64, int64_t cap) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int64_t pos = orp[r];
+    bool diag_done = false;
+    auto emit = [&](int c, double v) {
+        if (v != 0.0 && pos < cap) {
+            ocol[pos] = c;
+            o32[pos] = (float)v;
+            if (o64) o64[pos] = v;
+        }
+        pos += v != 0.0;
+    };
+    for (int e = mrp[r]; e < mrp[r + 1]; ++e) {
+        const int c = mcol[e];
+        const double a = mval ? mval[e] : 1.0;
+        if (!diag_done && c > r) {
+            emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
+            diag_done = true;
+        }
+        if (c == r) diag_done = true;
+        emit(c, lap_value(r, c, a, is, transposed));
+    }
+    if (!diag_done) emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
+}
+
+__global__ void degree_kernel(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ trp,
+                              double* __restrict__ x, int64_t ld) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i * ld + 0] = (double)(rp[i + 1] - rp[i]);
+    x[i * ld + 1] = (double)(trp[i + 1] - trp[i]);
+}
+
+// exact fp64 SpMM: thread per (row, column), sequential in canonical order
+__global__ void spmm_f64_kernel(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                const double* __restrict__ val, const double* __restrict__ x, int64_t ldx,
+                                int32_t f, double* __restrict__ out, int64_t ldo) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * f) return;
+    const int64_t r = t / f;
+    const int j = (int)(t - r * f);
+    double acc = 0.0;
+    for (int e = rp[r]; e < rp[r + 1]; ++e) acc = __dadd_rn(acc, __dmul_rn(val[e], x[(int64_t)col[e] * ldx + j]));
+    out[r * ldo + j] = acc;
+}
+
+__global__ void cast_frame_kernel(int32_t n, int32_t f, const double* __restrict__ x, int64_t ldx,
+                                  dgnn_frame out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * f) return;
+    const int64_t r = t / f;
+    const int j = (int)(t - r * f);
+    frame_row<float>(out, r)[j] = (float)x[r * ldx + j];
+}
+
+__global__ void fill_kernel(int64_t n, float v, float* x) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = v;
+}
+
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" {
+
+const char* dgnn_last_error(void) { return dgnn::last_error(); }
+
+int dgnn_abi_version(void) { return 1; }
+
+long long dgnn_launch_count(void) { return dgnn::launch_count(); }
+
+int dgnn_device_check(int device) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess) {
+        set_error("cudaGetDeviceProperties failed");
+        return 0;
+    }
+    return p.major == 10 && p.minor == 0;
+}
+
+int dgnn_rowptr_from_sorted_rows(int32_t n, int64_t nnz, const int32_t* rows, int32_t* rowptr,
+                                 void* stream) {
+    DGNN_CHECK_ARG(n >= 0 && nnz >= 0, "rowptr: negative size");
+    return rowptr_launch(n, nnz, rows, rowptr, as_stream(stream));
+}
+
+size_t dgnn_csr_apply_delta_workspace(int32_t n) {
+    return 2 * (size_t)round64((int64_t)n + 1) * sizeof(int32_t) + scan_workspace_bytes((int64_t)n + 1);
+}
+
+int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* old_col, int64_t n_del,
+                         const int32_t* del_row, const int32_t* del_col, int64_t n_ins,
+                         const int32_t* ins_row, const int32_t* ins_col, int32_t* new_rowptr,
+                         int32_t* new_col, int64_t new_cap, void* ws, size_t ws_bytes, int32_t* status,
+                         void* stream) {
+    DGNN_CHECK_ARG(n >= 0 && n_del >= 0 && n_ins >= 0, "apply_delta: negative size");
+    if (ws_bytes < dgnn_csr_apply_delta_workspace(n)) {
+        set_error("apply_delta: workspace too small");
+        return DGNN_EWORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    int32_t* drp = reinterpret_cast<int32_t*>(ws);
+    int32_t* irp = drp + round64((int64_t)n + 1);
+    void* sws = irp + round64((int64_t)n + 1);
+    size_t sws_bytes = ws_bytes - 2 * (size_t)round64((int64_t)n + 1) * sizeof(int32_t);
+    int rc = rowptr_launch(n, n_del, del_row, drp, st);
+    if (!rc) rc = rowptr_launch(n, n_ins, ins_row, irp, st);
+    if (rc) return rc;
+    const unsigned g1 = (unsigned)cdiv((int64_t)n + 1, 256);
+    ::dgnn::note_launch();
+    delta_count_kernel<<<g1, 256, 0, st>>>(n, old_rowptr, drp, irp, new_rowptr);
+    rc = exclusive_scan_i32(new_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
+    if (rc) return rc;
+    ::dgnn::note_launch();
+    delta_merge_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, old_rowptr, old_col, drp, del_col, irp,
+                                                               ins_col, new_rowptr, new_col, new_cap, status);
+    return launch_status("csr_apply_delta");
+}
+
+size_t dgnn_csr_transpose_workspace(int32_t n) {
+    // cursor[n] + scan; the scatter staging (nnz) lives in the output of a
+    // caller-visible second buffer pair, see dgnn_csr_transpose2.
+    return (size_t)round64((int64_t)n + 1) * sizeof(int32_t) + scan_workspace_bytes((int64_t)n + 1);
+}
+
+// Staging for the scatter: t_col/t_val are written twice (scatter into the
+// tail of the workspace given by the caller via t_stage_* pointers).
+int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* col,
+                              const double* val, int32_t* t_rowptr, int32_t* t_col, double* t_val,
+                              int32_t* stage_col, double* stage_val, void* ws, size_t ws_bytes,
+                              void* stream) {
+    DGNN_CHECK_ARG(n >= 0 && nnz >= 0, "transpose: negative size");
+    if (ws_bytes < dgnn_csr_transpose_workspace(n)) {
+        set_error("transpose: workspace too small");
+        return DGNN_EWORKSPACE;
+    }
+    DGNN_CHECK_ARG(!val || (t_val && stage_val), "transpose: values need t_val and stage_val");
+    cudaStream_t st = as_stream(stream);
+    int32_t* cursor = reinterpret_cast<int32_t*>(ws);
+    void* sws = cursor + round64((int64_t)n + 1);
+    size_t sws_bytes = ws_bytes - (size_t)round64((int64_t)n + 1) * sizeof(int32_t);
+    ::dgnn::note_launch();
+    zero_i32_kernel<<<(unsigned)cdiv((int64_t)n + 1, 256), 256, 0, st>>>(t_rowptr, (int64_t)n + 1);
+    if (nnz) {
+        ::dgnn::note_launch();
+        col_hist_kernel<<<(unsigned)cdiv(nnz, 256), 256, 0, st>>>(nnz, col, t_rowptr);
+    }
+    int rc = exclusive_scan_i32(t_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
+    if (rc) return rc;
+    cudaMemcpyAsync(cursor, t_rowptr, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+    ::dgnn::note_launch();
+    transpose_scatter_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, rowptr, col, val, cursor, stage_col,
+                                                                      stage_val);
+    ::dgnn::note_launch();
+    seg_sort_small_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, t_rowptr, stage_col, stage_val, t_col,
+                                                                   val ? t_val : nullptr);
+    ::dgnn::note_launch();
+    seg_sort_large_kernel<<<4 * kSMs, 256, 0, st>>>(n, t_rowptr, stage_col, stage_val, t_col,
+                                                    val ? t_val : nullptr);
+    return launch_status("csr_transpose");
+}
+
+size_t dgnn_laplacian_workspace(int32_t n) {
+    return (size_t)round64(n) * sizeof(double) + scan_workspace_bytes((int64_t)n + 1);
+}
+
+int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, const int32_t* m_col,
+                   const double* m_val, int transposed, int32_t* out_rowptr, int32_t* out_col,
+                   float* out_val32, double* out_val64, int64_t out_cap, void* ws, size_t ws_bytes,
+                   void* stream) {
+    DGNN_CHECK_ARG(n >= 0, "laplacian: negative size");
+    if (ws_bytes < dgnn_laplacian_workspace(n)) {
+        set_error("laplacian: workspace too small");
+        return DGNN_EWORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    double* is = reinterpret_cast<double*>(ws);
+    void* sws = is + round64(n);
+    size_t sws_bytes = ws_bytes - (size_t)round64(n) * sizeof(double);
+    const unsigned g = (unsigned)cdiv((int64_t)n + 1, 128);
+    ::dgnn::note_launch();
+    inv_sqrt_deg_kernel<<<g, 128, 0, st>>>(n, a_rowptr, is);
+    ::dgnn::note_launch();
+    lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr);
+    int rc = exclusive_scan_i32(out_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
+    if (rc) return rc;
+    ::dgnn::note_launch();
+    lap_write_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
+                                        out_val32, out_val64, out_cap);
+    return launch_status("laplacian");
+}
+
+int dgnn_degree_features(int32_t n, const int32_t* rowptr, const int32_t* t_rowptr, double* x, int64_t ld,
+                         void* stream) {
+    DGNN_CHECK_ARG(ld >= 2, "degree_features: ld < 2");
+    ::dgnn::note_launch();
+    degree_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(n, rowptr, t_rowptr, x, ld);
+    return launch_status("degree_features");
+}
+
+int dgnn_spmm_f64(int32_t n, const int32_t* rowptr, const int32_t* col, const double* val, const double* x,
+                  int64_t ldx, int32_t f, double* out, int64_t ldo, void* stream) {
+    DGNN_CHECK_ARG(n >= 0 && f >= 0, "spmm_f64: negative size");
+    const int64_t total = (int64_t)n * f;
+    if (total == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    spmm_f64_kernel<<<(unsigned)cdiv(total, 256), 256, 0, as_stream(stream)>>>(n, rowptr, col, val, x, ldx, f,
+                                                                                out, ldo);
+    return launch_status("spmm_f64");
+}
+
+int dgnn_cast_f64_to_f32_frame(int32_t n, int32_t f, const double* x, int64_t ldx, dgnn_frame out,
+                               void* stream) {
+    const int64_t total = (int64_t)n * f;
+    if (total == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    cast_frame_kernel<<<(unsigned)cdiv(total, 256), 256, 0, as_stream(stream)>>>(n, f, x, ldx, out);
+    return launch_status("cast_f64_to_f32_frame");
+}
+
+int dgnn_fill_f32(int64_t n, float value, float* x, void* stream) {
+    if (n == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    fill_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(n, value, x);
+    return launch_status("fill_f32");
+}
+
+}  // extern "C"

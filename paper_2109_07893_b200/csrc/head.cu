@@ -1,0 +1,313 @@
+// Link-prediction head, softmax cross-entropy and its gradients (K8), plus
+// the optimiser and parameter plumbing (K9).
+// Reference: models.py:335-348, training.py:102-126, 698-735, 886-900.
+#include "common.cuh"
+
+namespace dgnn {
+
+constexpr int kMaxClasses = 8;
+
+// One warp per pair: logits_c = z[u] . hw[:E, c] + z[v] . hw[E:, c] + hb_c
+// (lanes stride the embedding), CE in fp64 from the fp32 logits.
+__global__ void __launch_bounds__(256) head_loss_kernel(int64_t npairs, const int32_t* __restrict__ u,
+                                                        const int32_t* __restrict__ v,
+                                                        const int32_t* __restrict__ y, dgnn_frame z, int ep,
+                                                        int C, const float* __restrict__ hw,
+                                                        const float* __restrict__ hb, double scale,
+                                                        double* __restrict__ loss_pp, float* __restrict__ dlogits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = warp; p < npairs; p += nwarps) {
+        const float* zu = frame_row<const float>(z, u[p]);
+        const float* zv = frame_row<const float>(z, v[p]);
+        float lg[kMaxClasses];
+#pragma unroll
+        for (int c = 0; c < kMaxClasses; ++c) lg[c] = 0.f;
+        for (int k = lane; k < ep; k += 32) {
+            const float a = zu[k], b = zv[k];
+#pragma unroll
+            for (int c = 0; c < kMaxClasses; ++c)
+                if (c < C) lg[c] += a * hw[k * C + c] + b * hw[(ep + k) * C + c];
+        }
+#pragma unroll
+        for (int c = 0; c < kMaxClasses; ++c) lg[c] = warp_sum(lg[c]);
+        if (lane == 0) {
+            double l[kMaxClasses];
+            double mx = -1e300;
+            for (int c = 0; c < C; ++c) {
+                l[c] = (double)(lg[c] + hb[c]);
+                mx = l[c] > mx ? l[c] : mx;
+            }
+            double se = 0.0;
+            for (int c = 0; c < C; ++c) se += exp(l[c] - mx);
+            const double lz = log(se);
+            const int lab = y[p];
+            loss_pp[p] = -((l[lab] - mx) - lz);
+            if (dlogits) {
+                for (int c = 0; c < C; ++c) {
+                    const double pr = exp((l[c] - mx) - lz);
+                    dlogits[p * C + c] = (float)((pr - (c == lab ? 1.0 : 0.0)) * scale);
+                }
+            }
+        }
+    }
+}
+
+// Prediction accuracy (training.py:189-197): first-index argmax of the logits.
+__global__ void __launch_bounds__(256) head_predict_kernel(int64_t npairs, const int32_t* __restrict__ u,
+                                                           const int32_t* __restrict__ v,
+                                                           const int32_t* __restrict__ y, dgnn_frame z, int ep,
+                                                           int C, const float* __restrict__ hw,
+                                                           const float* __restrict__ hb,
+                                                           unsigned long long* correct) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = warp; p < npairs; p += nwarps) {
+        const float* zu = frame_row<const float>(z, u[p]);
+        const float* zv = frame_row<const float>(z, v[p]);
+        float lg[kMaxClasses];
+#pragma unroll
+        for (int c = 0; c < kMaxClasses; ++c) lg[c] = 0.f;
+        for (int k = lane; k < ep; k += 32) {
+            const float a = zu[k], b = zv[k];
+#pragma unroll
+            for (int c = 0; c < kMaxClasses; ++c)
+                if (c < C) lg[c] += a * hw[k * C + c] + b * hw[(ep + k) * C + c];
+        }
+#pragma unroll
+        for (int c = 0; c < kMaxClasses; ++c) lg[c] = warp_sum(lg[c]);
+        if (lane == 0) {
+            int best = 0;
+            float bv = lg[0] + hb[0];
+            for (int c = 1; c < C; ++c) {
+                const float x = lg[c] + hb[c];
+                if (x > bv) { bv = x; best = c; }
+            }
+            if (best == y[p]) atomicAdd(correct, 1ull);
+        }
+    }
+}
+
+// Head parameter gradient partials: rows 0..2ep-1 of cat^T dlogits, row 2ep = colsum.
+// CTA = chunk of pairs; thread t owns output row k = t (k <= 2ep) for all classes.
+__global__ void __launch_bounds__(256) head_grad_partial_kernel(int64_t npairs, const int32_t* __restrict__ u,
+                                                                const int32_t* __restrict__ v, dgnn_frame z,
+                                                                int ep, int C, const float* __restrict__ dl,
+                                                                int64_t per, float* __restrict__ part) {
+    const int64_t p0 = blockIdx.x * per, p1 = min(npairs, p0 + per);
+    const int rows = 2 * ep + 1;
+    for (int k = threadIdx.x; k < rows; k += blockDim.x) {
+        float acc[kMaxClasses];
+#pragma unroll
+        for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.f;
+        for (int64_t p = p0; p < p1; ++p) {
+            float a;
+            if (k < ep) a = frame_row<const float>(z, u[p])[k];
+            else if (k < 2 * ep) a = frame_row<const float>(z, v[p])[k - ep];
+            else a = 1.f;
+#pragma unroll
+            for (int c = 0; c < kMaxClasses; ++c)
+                if (c < C) acc[c] = fmaf(a, dl[p * C + c], acc[c]);
+        }
+        for (int c = 0; c < C; ++c) part[((int64_t)blockIdx.x * rows + k) * C + c] = acc[c];
+    }
+}
+
+__global__ void head_grad_reduce_kernel(int nchunks, int ep, int C, const float* __restrict__ part,
+                                        double* __restrict__ ghw, double* __restrict__ ghb) {
+    const int rows = 2 * ep + 1;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * C) return;
+    const int k = i / C, c = i % C;
+    double s = 0.0;
+    for (int b = 0; b < nchunks; ++b) s += (double)part[((int64_t)b * rows + k) * C + c];
+    if (k < 2 * ep) ghw[k * C + c] += s;
+    else ghb[c] += s;
+}
+
+// dz[x][k] = sum_{slot s of x} sum_c dl[s/2][c] hw[side(s)*ep + k][c]; group of ep/4 lanes per vertex.
+template <int EP>
+__global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int32_t* __restrict__ ptr,
+                                                           const int32_t* __restrict__ slot,
+                                                           const float* __restrict__ dl,
+                                                           const float* __restrict__ hw, int C, dgnn_frame dz) {
+    constexpr int G = EP / 4 >= 32 ? 32 : EP / 4;  // lanes per vertex
+    constexpr int V = EP / (4 * G);                // float4 per lane
+    constexpr int RW = 32 / G;
+    extern __shared__ float hws[];                 // [2*EP][C]
+    for (int i = threadIdx.x; i < 2 * EP * C; i += blockDim.x) hws[i] = hw[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t x = warp * RW + sub; x < n; x += nwarps * RW) {
+        float4 acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e = ptr[x]; e < ptr[x + 1]; ++e) {
+            const int s = slot[e];
+            const int p = s >> 1, side = s & 1;
+            for (int c = 0; c < C; ++c) {
+                const float d = dl[(int64_t)p * C + c];
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    const int k = 4 * (gl + G * i);
+                    const float* hr = hws + (side * EP + k) * C + c;
+                    acc[i].x = fmaf(d, hr[0], acc[i].x);
+                    acc[i].y = fmaf(d, hr[C], acc[i].y);
+                    acc[i].z = fmaf(d, hr[2 * C], acc[i].z);
+                    acc[i].w = fmaf(d, hr[3 * C], acc[i].w);
+                }
+            }
+        }
+        float* out = frame_row<float>(dz, x);
+#pragma unroll
+        for (int i = 0; i < V; ++i) *reinterpret_cast<float4*>(out + 4 * (gl + G * i)) = acc[i];
+    }
+}
+
+// Adam (training.py:886-900), IEEE-rounded ops in the reference's order.
+__global__ void adam_kernel(int64_t n, double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
+                            double* __restrict__ v, double lr, double b1, double one_m_b1, double b2,
+                            double one_m_b2, double bc1, double bc2, double eps) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double gi = g[i];
+    const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(one_m_b1, gi));
+    const double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(one_m_b2, __dmul_rn(gi, gi)));
+    m[i] = mi;
+    v[i] = vi;
+    const double mh = __ddiv_rn(mi, bc1), vh = __ddiv_rn(vi, bc2);
+    const double step = __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), eps));
+    p[i] = __dsub_rn(p[i], step);
+}
+
+__global__ void params_to_device_kernel(int64_t n, const double* __restrict__ p, const int64_t* __restrict__ pos0,
+                                        const int64_t* __restrict__ pos1, float* __restrict__ w) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float f = (float)p[i];
+    w[pos0[i]] = f;
+    if (pos1 && pos1[i] >= 0) w[pos1[i]] = f;
+}
+
+__global__ void grads_gather_kernel(int64_t n, const double* __restrict__ gp, const int64_t* __restrict__ pos0,
+                                    double* __restrict__ g) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) g[i] = gp[pos0[i]];
+}
+
+template <int EP>
+int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const float* dl, const float* hw, int C,
+                   dgnn_frame dz, cudaStream_t st) {
+    constexpr int G = EP / 4 >= 32 ? 32 : EP / 4;
+    constexpr int RW = 32 / G;
+    int64_t blocks = cdiv(cdiv(n, RW), 8);
+    blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+    ::dgnn::note_launch();
+    head_scatter_kernel<EP><<<(unsigned)blocks, 256, (size_t)2 * EP * C * sizeof(float), st>>>(n, ptr, slot, dl,
+                                                                                                hw, C, dz);
+    return launch_status("head_scatter");
+}
+
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" {
+
+int dgnn_head_loss(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y, dgnn_frame z,
+                   int32_t ep, int32_t c, const float* hw, const float* hb, double scale, double* loss_pp,
+                   int32_t n_partials, float* dlogits, void* stream) {
+    DGNN_CHECK_ARG(c >= 2 && c <= kMaxClasses, "head_loss: classes outside [2, 8]");
+    DGNN_CHECK_ARG(n_partials >= npairs, "head_loss: per-pair loss buffer too small");
+    if (npairs == 0) return DGNN_OK;
+    int64_t blocks = cdiv(npairs, 8);
+    blocks = blocks > 32 * kSMs ? 32 * kSMs : blocks;
+    ::dgnn::note_launch();
+    head_loss_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(npairs, u, v, y, z, ep, c, hw, hb, scale,
+                                                                      loss_pp, dlogits);
+    return launch_status("head_loss");
+}
+
+int dgnn_head_predict(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y, dgnn_frame z,
+                      int32_t ep, int32_t c, const float* hw, const float* hb, int64_t* correct, void* stream) {
+    DGNN_CHECK_ARG(c >= 2 && c <= kMaxClasses, "head_predict: classes outside [2, 8]");
+    if (npairs == 0) return DGNN_OK;
+    int64_t blocks = cdiv(npairs, 8);
+    blocks = blocks > 32 * kSMs ? 32 * kSMs : blocks;
+    ::dgnn::note_launch();
+    head_predict_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+        npairs, u, v, y, z, ep, c, hw, hb, reinterpret_cast<unsigned long long*>(correct));
+    return launch_status("head_predict");
+}
+
+size_t dgnn_head_grad_workspace(int32_t ep, int32_t c) {
+    return (size_t)(4 * kSMs) * (2 * ep + 1) * c * sizeof(float) + 256;
+}
+
+int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_frame z, int32_t ep, int32_t c,
+                   const float* dlogits, double* ghw, double* ghb, void* ws, size_t ws_bytes, void* stream) {
+    DGNN_CHECK_ARG(c >= 2 && c <= kMaxClasses, "head_grad: classes outside [2, 8]");
+    if (ws_bytes < dgnn_head_grad_workspace(ep, c)) {
+        set_error("head_grad: workspace too small");
+        return DGNN_EWORKSPACE;
+    }
+    if (npairs == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    int64_t nch = cdiv(npairs, 256);
+    nch = nch > 4 * kSMs ? 4 * kSMs : nch;
+    const int64_t per = cdiv(npairs, nch);
+    nch = cdiv(npairs, per);
+    float* part = reinterpret_cast<float*>(ws);
+    ::dgnn::note_launch();
+    head_grad_partial_kernel<<<(unsigned)nch, 256, 0, st>>>(npairs, u, v, z, ep, c, dlogits, per, part);
+    const int outs = (2 * ep + 1) * c;
+    ::dgnn::note_launch();
+    head_grad_reduce_kernel<<<(unsigned)cdiv(outs, 256), 256, 0, st>>>((int)nch, ep, c, part, ghw, ghb);
+    return launch_status("head_grad");
+}
+
+int dgnn_head_scatter(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot, const float* dlogits,
+                      const float* hw, int32_t ep, int32_t c, dgnn_frame dz, void* stream) {
+    DGNN_CHECK_ARG(c >= 1 && c <= kMaxClasses, "head_scatter: classes outside [1, 8]");
+    if (n == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (ep) {
+        case 16: return head_scatter_t<16>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st);
+        case 32: return head_scatter_t<32>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st);
+        case 64: return head_scatter_t<64>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st);
+        case 128: return head_scatter_t<128>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st);
+    }
+    set_error("head_scatter: unsupported width %d", ep);
+    return DGNN_EUNSUPPORTED;
+}
+
+int dgnn_adam(int64_t n, double* p, const double* g, double* m, double* v, double lr, double beta1,
+                 double one_m_beta1, double beta2, double one_m_beta2, double bc1, double bc2, double eps,
+                 void* stream) {
+    if (n == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    adam_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(n, p, g, m, v, lr, beta1, one_m_beta1,
+                                                                       beta2, one_m_beta2, bc1, bc2, eps);
+    return launch_status("adam");
+}
+
+int dgnn_params_to_device(int64_t n, const double* p, const int64_t* pos0, const int64_t* pos1, float* w32,
+                          void* stream) {
+    if (n == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    params_to_device_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(n, p, pos0, pos1, w32);
+    return launch_status("params_to_device");
+}
+
+int dgnn_grads_gather(int64_t n, const double* gpad, const int64_t* pos0, double* g, void* stream) {
+    if (n == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    grads_gather_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(n, gpad, pos0, g);
+    return launch_status("grads_gather");
+}
+
+}  // extern "C"

@@ -1,0 +1,337 @@
+// Sparse aggregation kernels (K3/K4): vectorised CSR SpMM with the dense
+// GCN transform and activation fused into the epilogue, and the row part of
+// the GCN backward.  Reference: core.py:142-161 (spmm / spmm_transpose),
+// training.py:342-367 (plain / skip-concat GCN cells), models.py:200-212.
+//
+// Layout: a row group of G = F/4 lanes owns one CSR row; every lane holds a
+// float4 slice of the aggregated row, so each gathered neighbour row is one
+// fully coalesced F*4-byte read.  The dense transform reads W from shared
+// memory and broadcasts the aggregated row across the group with shuffles.
+#include "common.cuh"
+
+namespace dgnn {
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 relu4(float4 v) {
+    return make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+}
+__device__ __forceinline__ void fma4(float4& a, float s, float4 b) {
+    a.x = fmaf(s, b.x, a.x);
+    a.y = fmaf(s, b.y, a.y);
+    a.z = fmaf(s, b.z, a.z);
+    a.w = fmaf(s, b.w, a.w);
+}
+__device__ __forceinline__ float comp(const float4& v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// Row aggregation: acc = sum_e val[e] * x[col[e]][4gl .. 4gl+3], 4-way unrolled
+// so four independent gathers are in flight per lane.
+__device__ __forceinline__ float4 gather_row(int64_t row, const int32_t* __restrict__ rp,
+                                             const int32_t* __restrict__ col,
+                                             const float* __restrict__ val, const dgnn_frame& x,
+                                             int gl) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int e = rp[row];
+    const int ee = rp[row + 1];
+    for (; e + 3 < ee; e += 4) {
+        const int c0 = __ldg(col + e), c1 = __ldg(col + e + 1), c2 = __ldg(col + e + 2),
+                  c3 = __ldg(col + e + 3);
+        const float v0 = __ldg(val + e), v1 = __ldg(val + e + 1), v2 = __ldg(val + e + 2),
+                    v3 = __ldg(val + e + 3);
+        const float4 x0 = ldg4(frame_row<const float>(x, c0) + 4 * gl);
+        const float4 x1 = ldg4(frame_row<const float>(x, c1) + 4 * gl);
+        const float4 x2 = ldg4(frame_row<const float>(x, c2) + 4 * gl);
+        const float4 x3 = ldg4(frame_row<const float>(x, c3) + 4 * gl);
+        fma4(acc, v0, x0);
+        fma4(acc, v1, x1);
+        fma4(acc, v2, x2);
+        fma4(acc, v3, x3);
+    }
+    for (; e < ee; ++e) fma4(acc, __ldg(val + e), ldg4(frame_row<const float>(x, __ldg(col + e)) + 4 * gl));
+    return acc;
+}
+
+template <int F>
+__global__ void __launch_bounds__(256) spmm_f32_kernel(int32_t n, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ col,
+                                                       const float* __restrict__ val, dgnn_frame x,
+                                                       dgnn_frame out) {
+    constexpr int G = F / 4, RW = 32 / G;
+    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = warp * RW + sub; row < n; row += nwarps * RW)
+        st4(frame_row<float>(out, row) + 4 * gl, gather_row(row, rp, col, val, x, gl));
+}
+
+// K3: s = Ahat x (or x), q = s W, r = relu([s, q]) | relu(q)
+template <int FP, int HP, bool SKIP, bool AGG>
+__global__ void __launch_bounds__(256) gcn_fwd_kernel(int32_t n, const int32_t* __restrict__ rp,
+                                                      const int32_t* __restrict__ col,
+                                                      const float* __restrict__ val, dgnn_frame x,
+                                                      const float* __restrict__ w, dgnn_frame s_out,
+                                                      dgnn_frame r_out) {
+    constexpr int G = FP / 4, RW = 32 / G;
+    constexpr int QLANES = HP >= FP ? G : HP / 4;   // lanes that own q columns
+    constexpr int QV = HP >= FP ? HP / FP : 1;      // float4 q chunks per owning lane
+    extern __shared__ float4 wsm4[];
+    for (int i = threadIdx.x; i < FP * HP / 4; i += blockDim.x) wsm4[i] = reinterpret_cast<const float4*>(w)[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * RW; base < n; base += nwarps * RW) {
+        const int64_t row = base + sub;
+        const bool valid = row < n;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            if constexpr (AGG) s = gather_row(row, rp, col, val, x, gl);
+            else s = ldg4(frame_row<const float>(x, row) + 4 * gl);
+        }
+        float4 q[QV];
+#pragma unroll
+        for (int i = 0; i < QV; ++i) q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k4 = 0; k4 < G; ++k4) {
+            const int src = sub * G + k4;
+            float4 sk;
+            sk.x = __shfl_sync(0xffffffffu, s.x, src);
+            sk.y = __shfl_sync(0xffffffffu, s.y, src);
+            sk.z = __shfl_sync(0xffffffffu, s.z, src);
+            sk.w = __shfl_sync(0xffffffffu, s.w, src);
+            if (gl < QLANES) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const float sv = comp(sk, kk);
+                    const float4* wr = wsm4 + (4 * k4 + kk) * (HP / 4);
+#pragma unroll
+                    for (int i = 0; i < QV; ++i) fma4(q[i], sv, wr[gl + G * i]);
+                }
+            }
+        }
+        if (valid) {
+            if (s_out.ptr) st4(frame_row<float>(s_out, row) + 4 * gl, s);
+            float* rr = frame_row<float>(r_out, row);
+            if constexpr (SKIP) {
+                st4(rr + 4 * gl, relu4(s));
+                if (gl < QLANES) {
+#pragma unroll
+                    for (int i = 0; i < QV; ++i) st4(rr + FP + 4 * (gl + G * i), relu4(q[i]));
+                }
+            } else {
+                if (gl < QLANES) {
+#pragma unroll
+                    for (int i = 0; i < QV; ++i) st4(rr + 4 * (gl + G * i), relu4(q[i]));
+                }
+            }
+        }
+    }
+}
+
+// K4 row part: dpre = dr (.) [r > 0]; ds = [dpre_s] + dq W^T
+template <int FP, int HP, bool SKIP>
+__global__ void __launch_bounds__(256) gcn_bwd_rows_kernel(int32_t n, dgnn_frame dr, dgnn_frame r,
+                                                           const float* __restrict__ w, dgnn_frame ds) {
+    constexpr int G = FP / 4, RW = 32 / G;
+    constexpr int QLANES = HP >= FP ? G : HP / 4;
+    constexpr int QV = HP >= FP ? HP / FP : 1;
+    constexpr int OFF = SKIP ? FP : 0;
+    extern __shared__ float4 wt4[];  // W^T: [HP][FP]
+    float* wt = reinterpret_cast<float*>(wt4);
+    for (int i = threadIdx.x; i < FP * HP; i += blockDim.x) {
+        const int k = i / HP, j = i % HP;
+        wt[j * FP + k] = w[i];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * RW; base < n; base += nwarps * RW) {
+        const int64_t row = base + sub;
+        const bool valid = row < n;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 dq[QV];
+#pragma unroll
+        for (int i = 0; i < QV; ++i) dq[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            const float* drr = frame_row<const float>(dr, row);
+            const float* rr = frame_row<const float>(r, row);
+            if constexpr (SKIP) {
+                const float4 g = ldg4(drr + 4 * gl), m = ldg4(rr + 4 * gl);
+                acc = make_float4(m.x > 0.f ? g.x : 0.f, m.y > 0.f ? g.y : 0.f, m.z > 0.f ? g.z : 0.f,
+                                  m.w > 0.f ? g.w : 0.f);
+            }
+            if (gl < QLANES) {
+#pragma unroll
+                for (int i = 0; i < QV; ++i) {
+                    const int c = OFF + 4 * (gl + G * i);
+                    const float4 g = ldg4(drr + c), m = ldg4(rr + c);
+                    dq[i] = make_float4(m.x > 0.f ? g.x : 0.f, m.y > 0.f ? g.y : 0.f, m.z > 0.f ? g.z : 0.f,
+                                        m.w > 0.f ? g.w : 0.f);
+                }
+            }
+        }
+#pragma unroll
+        for (int src = 0; src < QLANES; ++src) {
+#pragma unroll
+            for (int i = 0; i < QV; ++i) {
+                float4 d;
+                const int sl = sub * G + src;
+                d.x = __shfl_sync(0xffffffffu, dq[i].x, sl);
+                d.y = __shfl_sync(0xffffffffu, dq[i].y, sl);
+                d.z = __shfl_sync(0xffffffffu, dq[i].z, sl);
+                d.w = __shfl_sync(0xffffffffu, dq[i].w, sl);
+                const int j0 = 4 * (src + G * i);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) fma4(acc, comp(d, jj), wt4[((j0 + jj) * FP) / 4 + gl]);
+            }
+        }
+        if (valid) st4(frame_row<float>(ds, row) + 4 * gl, acc);
+    }
+}
+
+}  // namespace dgnn
+
+using namespace dgnn;
+
+namespace {
+
+template <int F>
+int spmm_f32_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x,
+               dgnn_frame out, cudaStream_t st) {
+    constexpr int RW = 32 / (F / 4);
+    int64_t blocks = cdiv(cdiv(n, RW), 8);
+    blocks = blocks < 1 ? 1 : (blocks > 32 * kSMs ? 32 * kSMs : blocks);
+    ::dgnn::note_launch();
+    spmm_f32_kernel<F><<<(unsigned)blocks, 256, 0, st>>>(n, rp, col, val, x, out);
+    return launch_status("spmm_f32");
+}
+
+template <int FP, int HP, bool SKIP, bool AGG>
+int gcn_fwd_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x, const float* w,
+              dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+    constexpr int RW = 32 / (FP / 4);
+    const size_t smem = (size_t)FP * HP * sizeof(float);
+    auto k = gcn_fwd_kernel<FP, HP, SKIP, AGG>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t blocks = cdiv(cdiv(n, RW), 8);
+    blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+    ::dgnn::note_launch();
+    k<<<(unsigned)blocks, 256, smem, st>>>(n, rp, col, val, x, w, s_out, r_out);
+    return launch_status("gcn_forward");
+}
+
+template <int FP, int HP, bool SKIP>
+int gcn_bwd_t(int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame ds, cudaStream_t st) {
+    constexpr int RW = 32 / (FP / 4);
+    const size_t smem = (size_t)FP * HP * sizeof(float);
+    auto k = gcn_bwd_rows_kernel<FP, HP, SKIP>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t blocks = cdiv(cdiv(n, RW), 8);
+    blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+    ::dgnn::note_launch();
+    k<<<(unsigned)blocks, 256, smem, st>>>(n, dr, r, w, ds);
+    return launch_status("gcn_backward_rows");
+}
+
+template <int FP, bool SKIP, bool AGG>
+int gcn_fwd_hp(int32_t hp, int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x,
+               const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+    switch (hp) {
+        case 16: return gcn_fwd_t<FP, 16, SKIP, AGG>(n, rp, col, val, x, w, s_out, r_out, st);
+        case 32: return gcn_fwd_t<FP, 32, SKIP, AGG>(n, rp, col, val, x, w, s_out, r_out, st);
+        case 64: return gcn_fwd_t<FP, 64, SKIP, AGG>(n, rp, col, val, x, w, s_out, r_out, st);
+        case 128: return gcn_fwd_t<FP, 128, SKIP, AGG>(n, rp, col, val, x, w, s_out, r_out, st);
+    }
+    set_error("gcn_forward: unsupported hp %d", hp);
+    return DGNN_EUNSUPPORTED;
+}
+
+template <bool SKIP, bool AGG>
+int gcn_fwd_fp(int32_t fp, int32_t hp, int32_t n, const int32_t* rp, const int32_t* col, const float* val,
+               dgnn_frame x, const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+    switch (fp) {
+        case 4:
+            if (AGG) break;
+            return gcn_fwd_hp<4, SKIP, false>(hp, n, rp, col, val, x, w, s_out, r_out, st);
+        case 16: return gcn_fwd_hp<16, SKIP, AGG>(hp, n, rp, col, val, x, w, s_out, r_out, st);
+        case 32: return gcn_fwd_hp<32, SKIP, AGG>(hp, n, rp, col, val, x, w, s_out, r_out, st);
+        case 64: return gcn_fwd_hp<64, SKIP, AGG>(hp, n, rp, col, val, x, w, s_out, r_out, st);
+        case 128: return gcn_fwd_hp<128, SKIP, AGG>(hp, n, rp, col, val, x, w, s_out, r_out, st);
+    }
+    set_error("gcn_forward: unsupported fp %d (aggregation %d)", fp, (int)AGG);
+    return DGNN_EUNSUPPORTED;
+}
+
+template <int FP, bool SKIP>
+int gcn_bwd_hp(int32_t hp, int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame ds, cudaStream_t st) {
+    switch (hp) {
+        case 16: return gcn_bwd_t<FP, 16, SKIP>(n, dr, r, w, ds, st);
+        case 32: return gcn_bwd_t<FP, 32, SKIP>(n, dr, r, w, ds, st);
+        case 64: return gcn_bwd_t<FP, 64, SKIP>(n, dr, r, w, ds, st);
+        case 128: return gcn_bwd_t<FP, 128, SKIP>(n, dr, r, w, ds, st);
+    }
+    set_error("gcn_backward_rows: unsupported hp %d", hp);
+    return DGNN_EUNSUPPORTED;
+}
+
+template <bool SKIP>
+int gcn_bwd_fp(int32_t fp, int32_t hp, int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame ds,
+               cudaStream_t st) {
+    switch (fp) {
+        case 4: return gcn_bwd_hp<4, SKIP>(hp, n, dr, r, w, ds, st);
+        case 16: return gcn_bwd_hp<16, SKIP>(hp, n, dr, r, w, ds, st);
+        case 32: return gcn_bwd_hp<32, SKIP>(hp, n, dr, r, w, ds, st);
+        case 64: return gcn_bwd_hp<64, SKIP>(hp, n, dr, r, w, ds, st);
+        case 128: return gcn_bwd_hp<128, SKIP>(hp, n, dr, r, w, ds, st);
+    }
+    set_error("gcn_backward_rows: unsupported fp %d", fp);
+    return DGNN_EUNSUPPORTED;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dgnn_spmm_f32(int32_t n, const int32_t* rowptr, const int32_t* col, const float* val, dgnn_frame x,
+                  int32_t f, dgnn_frame out, void* stream) {
+    DGNN_CHECK_ARG(n >= 0, "spmm_f32: negative size");
+    if (n == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (f) {
+        case 4: return spmm_f32_t<4>(n, rowptr, col, val, x, out, st);
+        case 16: return spmm_f32_t<16>(n, rowptr, col, val, x, out, st);
+        case 32: return spmm_f32_t<32>(n, rowptr, col, val, x, out, st);
+        case 64: return spmm_f32_t<64>(n, rowptr, col, val, x, out, st);
+        case 128: return spmm_f32_t<128>(n, rowptr, col, val, x, out, st);
+    }
+    set_error("spmm_f32: unsupported width %d", f);
+    return DGNN_EUNSUPPORTED;
+}
+
+int dgnn_gcn_forward(int32_t n, const int32_t* rowptr, const int32_t* col, const float* val, dgnn_frame x,
+                     int32_t fp, const float* w, int32_t hp, int skip, dgnn_frame s_out, dgnn_frame r_out,
+                     void* stream) {
+    DGNN_CHECK_ARG(n >= 0, "gcn_forward: negative size");
+    if (n == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    const bool agg = rowptr != nullptr;
+    if (skip) {
+        return agg ? gcn_fwd_fp<true, true>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st)
+                   : gcn_fwd_fp<true, false>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st);
+    }
+    return agg ? gcn_fwd_fp<false, true>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st)
+               : gcn_fwd_fp<false, false>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st);
+}
+
+int dgnn_gcn_backward_rows(int32_t n, dgnn_frame dr, dgnn_frame r, int32_t fp, const float* w, int32_t hp,
+                           int skip, dgnn_frame ds, void* stream) {
+    DGNN_CHECK_ARG(n >= 0, "gcn_backward_rows: negative size");
+    if (n == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    return skip ? gcn_bwd_fp<true>(fp, hp, n, dr, r, w, ds, st) : gcn_bwd_fp<false>(fp, hp, n, dr, r, w, ds, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,651 @@
+"""The device training engine: one epoch of the snapshot-partitioned dynamic
+GNN (cd-gcn: skip-GCN + LSTM; tm-gcn: GCN + banded M-product).
+
+Structure mirrors the reference's simulated workers (`dist.py:235-589`) so
+ledgers and results line up call for call, but every phase is device work:
+
+* `Rank` = one participant.  Inside checkpoint block b it owns the
+  timesteps `steps_of(q, b)` for the graph convolutions (snapshot-major,
+  communication free) and the vertex rows [q*N/P, (q+1)*N/P) for the
+  temporal stage (vertex-major).  A process drives either one Rank (one GPU
+  per process, NCCL fabric) or all P Ranks on one device (emulated fabric,
+  used for 1-GPU parity of the multi-rank schedule).
+* Snapshot-major frames use the owner layout [dest chunk q][owned step][N/P
+  rows][width]; vertex-major frames are [block step][N/P rows][width].  With
+  that choice the all-to-all of `redistribute_to_vertex_major` /
+  `..._snapshot_major` (`dist.py:176-228`) is exactly one equal-split
+  `all_to_all_single` on the raw buffers, no pack/unpack kernels; at P = 1
+  the two layouts coincide and the exchange disappears.
+* Gradient checkpointing (`training.py:798-865`): the forward sweep keeps
+  only pi_b (LSTM state per layer, or the trailing M-product frames); the
+  reverse sweep re-runs each block with caches, then backpropagates.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, frame, ptr
+from .errors import ConfigError, ProtocolError
+from .labels import frame_labels
+from .materialize import Materializer, SnapshotEncoding
+from .params import DeviceParams, ParamLayout
+
+F32 = 4
+
+
+class Plan:
+    """Block-wise snapshot ownership (`dist.py:125-173`)."""
+
+    def __init__(self, T: int, P: int, nblk: int, N: int):
+        if P < 1:
+            raise ConfigError("worker count must be >= 1")
+        if nblk < 1 or T % nblk:
+            raise ConfigError(f"block count {nblk} must divide the timeline length {T}")
+        self.T, self.P, self.nblk = T, P, nblk
+        self.bsize = T // nblk
+        if self.bsize % P:
+            raise ConfigError(f"worker count {P} must divide the block size {self.bsize}")
+        if N % P:
+            raise ConfigError(f"worker count {P} must divide the vertex count {N}")
+        self.chunk = self.bsize // P
+        self.N, self.NP = N, N // P
+
+    def owner_of(self, t):
+        return (t % self.bsize) // self.chunk
+
+    def block_steps(self, b):
+        return list(range(b * self.bsize, (b + 1) * self.bsize))
+
+    def steps_of(self, p, b):
+        s = b * self.bsize + p * self.chunk
+        return list(range(s, s + self.chunk))
+
+    def owned(self, p):
+        return [t for b in range(self.nblk) for t in self.steps_of(p, b)]
+
+
+def _zeros(n, dtype=torch.float32, device=None):
+    return torch.zeros(int(n), dtype=dtype, device=device)
+
+
+class Rank:
+    """Device state and phases of one participant (`dist.py:235-458`)."""
+
+    def __init__(self, eng: "Engine", q: int, device):
+        self.eng, self.q = eng, q
+        self.dev = torch.device(device)
+        plan, layers = eng.plan, eng.layout.layers
+        P, C, B, N, NP = plan.P, plan.chunk, plan.bsize, plan.N, plan.NP
+        dev = self.dev
+        self.mat = Materializer(eng.enc, dev, slots=C, resident=eng.resident)
+        self.skip = eng.skip
+        L = len(layers)
+        # snapshot-major (owner layout) and vertex-major buffers
+        self.R_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
+        self.Y_own = [_zeros(P * C * NP * Ly.ho, device=dev) for Ly in layers]
+        self.S_own = [None] + [_zeros(C * N * Ly.fp, device=dev) for Ly in layers[1:]]
+        same = P == 1
+        self.R_vm = self.R_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
+        self.Y_vm = self.Y_own if same else [_zeros(B * NP * Ly.ho, device=dev) for Ly in layers]
+        wmax = max(Ly.ho for Ly in layers)
+        self.dZ_own = _zeros(P * C * NP * wmax, device=dev)
+        self.dY_vm = self.dZ_own if same else _zeros(B * NP * wmax, device=dev)
+        self.dR_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
+        self.dR_vm = self.dR_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
+        self.dS = _zeros(N * max(Ly.fp for Ly in layers), device=dev)
+        if self.skip:
+            self.G_vm = [_zeros(B * NP * 4 * Ly.ho, device=dev) for Ly in layers]
+            self.C_vm = [_zeros(B * NP * Ly.ho, device=dev) for Ly in layers]
+            self.cbuf = [_zeros(2 * NP * Ly.ho, device=dev) for Ly in layers]
+            self.state = [(_zeros(NP * Ly.ho, device=dev), _zeros(NP * Ly.ho, device=dev)) for Ly in layers]
+            self.zero_state = [(_zeros(NP * Ly.ho, device=dev), _zeros(NP * Ly.ho, device=dev)) for Ly in layers]
+            self.dstate = [(_zeros(NP * Ly.ho, device=dev), _zeros(NP * Ly.ho, device=dev)) for Ly in layers]
+            self.dcarry = [(_zeros(2 * NP * Ly.ho, device=dev), _zeros(2 * NP * Ly.ho, device=dev))
+                           for Ly in layers]
+        else:
+            # M-product: trailing operator-input frames (training.py:598-603) and
+            # owed gradients for frames of earlier blocks (training.py:644-647)
+            self.trail = [dict() for _ in layers]
+            self.dtrail = [dict() for _ in layers]
+            self.Z_vm = self.Y_vm    # M-product output, vertex-major
+        self.pi = {}
+        # first-layer products s1[t] = Ahat_t X_t for owned steps, [N, fp0] fp32
+        self.s1 = {}
+        # labels for owned frames
+        self.lab = {}
+        self.loss_acc = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.correct = torch.zeros(1, dtype=torch.int64, device=dev)
+        gl = eng.layout
+        self.ws_tn = torch.empty(max(
+            max(_lib.query("dgnn_gemm_tn_workspace", Ly.kx, 4 * Ly.ho) for Ly in layers) if self.skip else 0,
+            max(_lib.query("dgnn_gcn_weight_grad_workspace", Ly.fp, Ly.hg) for Ly in layers)),
+            dtype=torch.uint8, device=dev)
+        self.ws_head = torch.empty(_lib.query("dgnn_head_grad_workspace", gl.ep, gl.classes), dtype=torch.uint8,
+                                   device=dev)
+        self.slots = []
+
+    # ---------------------------------------------------------------- frames
+    def own(self, buf, W, c) -> _lib.Frame:
+        """Frame of owned step c in the owner layout [P][C][NP][W]."""
+        plan = self.eng.plan
+        return _lib.Frame(buf.data_ptr() + F32 * c * plan.NP * W, W, plan.NP, plan.chunk * plan.NP * W)
+
+    def own_slab_rows(self, buf, W, c, q):
+        plan = self.eng.plan
+        o = (q * plan.chunk + c) * plan.NP * W
+        return buf[o:o + plan.NP * W]
+
+    def vm(self, buf, W, i):
+        NP = self.eng.plan.NP
+        return buf[i * NP * W:(i + 1) * NP * W]
+
+    def plain(self, buf, W, c=0) -> _lib.Frame:
+        N = self.eng.plan.N
+        return _lib.Frame(buf.data_ptr() + F32 * c * N * W, W, 0, 0)
+
+    # ----------------------------------------------------------- preparation
+    def prepare_inputs(self, feats_host, labels_by_time, test_by_time):
+        """s1 for every owned step (layer 0 is parameter free, `models.py:326-332`)
+        and device labels for owned frames."""
+        eng, plan = self.eng, self.eng.plan
+        N = plan.N
+        fp0 = eng.layout.layers[0].fp
+        fin = eng.cfg.in_features
+        st = _lib.stream_handle()
+        prep = Materializer(eng.enc, self.dev, slots=1, resident=False, with_f64=True)
+        x64 = torch.zeros(N * max(2, fin), dtype=torch.float64, device=self.dev)
+        s64 = torch.zeros(N * fin, dtype=torch.float64, device=self.dev)
+        for t in plan.owned(self.q):
+            slot = prep.materialize([t], ledger=None, count_bytes=False)[0]
+            prep.wait()
+            if feats_host is None:     # degree features of the (raw) graph, dtdg.py:255-266
+                call("dgnn_degree_features", N, ptr(slot.a_rowptr), ptr(slot.a_t_rowptr), ptr(x64), 2, st)
+            else:
+                x64.view(-1)[:N * fin].copy_(torch.from_numpy(np.ascontiguousarray(feats_host[t], np.float64)).view(-1))
+            call("dgnn_spmm_f64", N, ptr(slot.rowptr), ptr(slot.col), ptr(slot.val64), ptr(x64), fin, fin,
+                 ptr(s64), fin, st)
+            out = _zeros(N * fp0, device=self.dev)
+            call("dgnn_cast_f64_to_f32_frame", N, fin, ptr(s64), fin, frame(out, fp0), st)
+            self.s1[t] = out
+        prep.check()
+        del prep
+        owned = set(plan.owned(self.q))
+        self.lab = {}
+        for key, bt in (("train", labels_by_time), ("test", test_by_time)):
+            d = {}
+            for t, (pairs, lab) in (bt or {}).items():
+                if t not in owned:
+                    continue
+                fl = frame_labels(pairs, lab, N, eng.cfg.classes)
+                d[t] = dict(n=fl.count, u=torch.from_numpy(fl.u).to(self.dev),
+                            v=torch.from_numpy(fl.v).to(self.dev), y=torch.from_numpy(fl.y).to(self.dev),
+                            ptr=torch.from_numpy(fl.inc_ptr).to(self.dev),
+                            slot=torch.from_numpy(fl.inc_slot).to(self.dev))
+            self.lab[key] = d
+        mx = max([v["n"] for d in self.lab.values() for v in d.values()] + [1])
+        self.loss_pp = torch.zeros(mx, dtype=torch.float64, device=self.dev)
+        self.dlogits = torch.zeros(mx * eng.cfg.classes, dtype=torch.float32, device=self.dev)
+
+    # ---------------------------------------------------------------- phases
+    def reset_state(self):
+        if self.skip:
+            for h, c in self.state:
+                h.zero_()
+                c.zero_()
+            for dh, dc in self.dstate:
+                dh.zero_()
+                dc.zero_()
+        else:
+            self.trail = [dict() for _ in self.eng.layout.layers]
+            self.dtrail = [dict() for _ in self.eng.layout.layers]
+        self.pi = {}
+        self.loss_acc.zero_()
+        self.correct.zero_()
+
+    def begin_block(self, b, keep, ledger=None, count_bytes=True):
+        """`dist.py:301-318`: stream the owned chunk through the codec and pick
+        the carried state (forward sweep) or pi_{b-1} (checkpoint rerun)."""
+        self.b, self.keep = b, keep
+        self.ts = self.eng.plan.steps_of(self.q, b)
+        self.slots = self.mat.materialize(self.ts, ledger=ledger, count_bytes=count_bytes)
+        self.graph_waited = False
+        if self.skip:
+            if keep:
+                self.act = self.pi[b - 1] if b > 0 else self.zero_state
+            else:
+                self.act = self.state
+
+    def _wait_graph(self):
+        if not self.graph_waited:
+            self.mat.wait()
+            self.graph_waited = True
+
+    def gcn_forward(self, b, l):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        st = _lib.stream_handle()
+        w = eng.params.w(f"gcn{l}.w")
+        for c, t in enumerate(self.ts):
+            if l == 0:
+                x = self.plain(self.s1[t], Ly.fp)
+                rp = col = val = None
+            else:
+                self._wait_graph()
+                x = self.own(self.Y_own[l - 1], Ly.fp, c)
+                s = self.slots[c]
+                rp, col, val = ptr(s.rowptr), ptr(s.col), ptr(s.val)
+            s_out = self.plain(self.S_own[l], Ly.fp, c) if (self.keep and l > 0) else _lib.Frame(None, 0, 0, 0)
+            call("dgnn_gcn_forward", eng.plan.N, rp, col, val, x, Ly.fp, ptr(w), Ly.hg, int(self.skip),
+                 s_out, self.own(self.R_own[l], Ly.rw, c), st)
+
+    def rnn_forward(self, b, l):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        NP, B = eng.plan.NP, eng.plan.bsize
+        st = _lib.stream_handle()
+        if not self.skip:
+            self._mprod_forward(b, l)
+            return
+        wcat, bias = eng.params.w(f"lstm{l}.wcat"), eng.params.w(f"lstm{l}.b")
+        h_prev, c_prev = self.act[l]
+        ho = Ly.ho
+        for i in range(B):
+            x = self.vm(self.R_vm[l], Ly.rw, i)
+            h_out = self.vm(self.Y_vm[l], ho, i)
+            c_out = self.vm(self.C_vm[l], ho, i) if self.keep else self.vm(self.cbuf[l], ho, i % 2)
+            gates = self.vm(self.G_vm[l], 4 * ho, i) if self.keep else None
+            call("dgnn_lstm_forward_step", NP, Ly.kx, ho, ptr(x), Ly.rw, ptr(h_prev), ptr(c_prev), ptr(wcat),
+                 ptr(bias), ptr(h_out), ptr(c_out), ptr(gates), st)
+            h_prev, c_prev = h_out, c_out
+        if not self.keep:
+            self.state[l][0].copy_(h_prev)
+            self.state[l][1].copy_(c_prev)
+
+    def _mprod_forward(self, b, l):
+        """`training.py:430-441` over the vertex chunk; trailing frames from
+        earlier blocks are kept as device copies (`training.py:598-603`)."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        NP = eng.plan.NP
+        ts = eng.plan.block_steps(b)
+        m, w = eng.m_matrix, eng.cfg.window
+        st = _lib.stream_handle()
+        cnt = NP * Ly.ho
+
+        def src(k):
+            if k >= ts[0]:
+                return self.vm(self.R_vm[l], Ly.rw, k - ts[0])
+            return self.trail[l][k]
+
+        for i, t in enumerate(ts):
+            out = self.vm(self.Z_vm[l], Ly.ho, i)
+            lo = max(0, t - w + 1)
+            for j, k in enumerate(range(lo, t + 1)):
+                call("dgnn_axpy_frame", cnt, float(m[t, k]), ptr(src(k)), ptr(out), int(j == 0), st)
+        if not self.keep:
+            # the rerun of block b+1 reads these again (reference keeps them all, dist.py:359-361)
+            keepn = min(w, len(ts))
+            for t in ts[-keepn:]:
+                self.trail[l][t] = self.vm(self.R_vm[l], Ly.rw, t - ts[0]).clone()
+
+    def store_pi(self, b):
+        if self.skip and b < self.eng.plan.nblk - 1:
+            self.pi[b] = [(h.clone(), c.clone()) for h, c in self.state]
+
+    def block_loss(self, b):
+        eng = self.eng
+        Ly = eng.layout.layers[-1]
+        st = _lib.stream_handle()
+        zsrc = self.Y_own[-1]
+        for c, t in enumerate(self.ts):
+            d = self.lab["train"].get(t)
+            if d is None:
+                continue
+            call("dgnn_head_loss", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), self.own(zsrc, Ly.ho, c),
+                 eng.layout.ep, eng.cfg.classes, ptr(eng.params.w("head.w")), ptr(eng.params.w("head.b")),
+                 1.0, ptr(self.loss_pp), self.loss_pp.numel(), None, st)
+            call("dgnn_sum_f64", d["n"], ptr(self.loss_pp), ptr(self.loss_acc), 1, st)
+
+    def predict(self, b, key="test"):
+        eng = self.eng
+        Ly = eng.layout.layers[-1]
+        st = _lib.stream_handle()
+        for c, t in enumerate(self.ts):
+            d = self.lab.get(key, {}).get(t)
+            if d is None:
+                continue
+            call("dgnn_head_predict", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), self.own(self.Y_own[-1], Ly.ho, c),
+                 eng.layout.ep, eng.cfg.classes, ptr(eng.params.w("head.w")), ptr(eng.params.w("head.b")),
+                 ptr(self.correct), st)
+
+    def loss_grads(self, b):
+        """`training.py:713-735`: head grads + dz seeds (owner layout)."""
+        eng = self.eng
+        Ly = eng.layout.layers[-1]
+        st = _lib.stream_handle()
+        ep, C = eng.layout.ep, eng.cfg.classes
+        hw, hb = eng.params.w("head.w"), eng.params.w("head.b")
+        for c, t in enumerate(self.ts):
+            d = self.lab["train"].get(t)
+            dz = self.own(self.dZ_own, Ly.ho, c)
+            if d is None:
+                for q in range(eng.plan.P):
+                    self.own_slab_rows(self.dZ_own, Ly.ho, c, q).zero_()
+                continue
+            z = self.own(self.Y_own[-1], Ly.ho, c)
+            call("dgnn_head_loss", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), z, ep, C, ptr(hw), ptr(hb),
+                 eng.scale, ptr(self.loss_pp), self.loss_pp.numel(), ptr(self.dlogits), st)
+            call("dgnn_head_grad", d["n"], ptr(d["u"]), ptr(d["v"]), z, ep, C, ptr(self.dlogits),
+                 ptr(eng.params.gw("head.w")), ptr(eng.params.gw("head.b")), ptr(self.ws_head),
+                 self.ws_head.numel(), st)
+            call("dgnn_head_scatter", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), ptr(self.dlogits), ptr(hw), ep, C,
+                 dz, st)
+
+    def rnn_backward(self, b, l):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        if not self.skip:
+            self._mprod_backward(b, l)
+            return
+        NP, B = eng.plan.NP, eng.plan.bsize
+        ho = Ly.ho
+        st = _lib.stream_handle()
+        wt = eng.params.w(f"lstm{l}.wcat_t")
+        dh_buf, dc_buf = self.dcarry[l]
+        dh_in, dc_in = self.dstate[l]
+        for step, i in enumerate(reversed(range(B))):
+            dy = self.vm(self.dY_vm, ho, i)
+            gates = self.vm(self.G_vm[l], 4 * ho, i)
+            c_prev = self.vm(self.C_vm[l], ho, i - 1) if i > 0 else self.act[l][1]
+            c_new = self.vm(self.C_vm[l], ho, i)
+            dx = self.vm(self.dR_vm[l], Ly.rw, i)
+            dh_out = self.vm(dh_buf, ho, step % 2)
+            dc_out = self.vm(dc_buf, ho, step % 2)
+            call("dgnn_lstm_backward_step", NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates),
+                 ptr(c_prev), ptr(c_new), ptr(wt), ptr(gates), ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
+            dh_in, dc_in = dh_out, dc_out
+        self.dstate[l][0].copy_(dh_in)
+        self.dstate[l][1].copy_(dc_in)
+        # weight gradients over every (row, step) of the block (training.py:422-424)
+        g_wcat = eng.params.gw(f"lstm{l}.wcat")
+        g_b = eng.params.gw(f"lstm{l}.b")
+        ws = self.ws_tn
+        K4 = 4 * ho
+        call("dgnn_gemm_tn", B * NP, Ly.kx, K4, ptr(self.R_vm[l]), Ly.rw, ptr(self.G_vm[l]), K4, ptr(g_wcat), K4,
+             ptr(g_b), ptr(ws), ws.numel(), st)
+        g_wh = g_wcat[Ly.kx:]
+        if B > 1:
+            call("dgnn_gemm_tn", (B - 1) * NP, ho, K4, ptr(self.Y_vm[l]), ho, ptr(self.vm(self.G_vm[l], K4, 1)),
+                 K4, ptr(g_wh), K4, None, ptr(ws), ws.numel(), st)
+        call("dgnn_gemm_tn", NP, ho, K4, ptr(self.act[l][0]), ho, ptr(self.G_vm[l]), K4, ptr(g_wh), K4, None,
+             ptr(ws), ws.numel(), st)
+
+    def _mprod_backward(self, b, l):
+        """`training.py:444-460` + owed trailing gradients (`dist.py:396-407`)."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        NP = eng.plan.NP
+        ts = eng.plan.block_steps(b)
+        m, w = eng.m_matrix, eng.cfg.window
+        st = _lib.stream_handle()
+        cnt = NP * Ly.ho
+        out = self.dR_vm[l]
+        first = {}
+        for t in ts:
+            lo = max(0, t - w + 1)
+            dzt = self.vm(self.dY_vm, Ly.ho, t - ts[0])
+            for k in range(lo, t + 1):
+                coef = float(m[t, k])
+                if k >= ts[0]:
+                    dst = self.vm(out, Ly.rw, k - ts[0])
+                    init = k not in first
+                    first[k] = True
+                else:
+                    if k not in self.dtrail[l]:
+                        self.dtrail[l][k] = torch.zeros(cnt, dtype=torch.float32, device=self.dev)
+                    dst = self.dtrail[l][k]
+                    init = 0
+                call("dgnn_axpy_frame", cnt, coef, ptr(dzt), ptr(dst), int(init), st)
+        for k in ts:
+            if k not in first:
+                self.vm(out, Ly.rw, k - ts[0]).zero_()
+            if k in self.dtrail[l]:
+                g = self.dtrail[l].pop(k)
+                call("dgnn_axpy_frame", cnt, 1.0, ptr(g), ptr(self.vm(out, Ly.rw, k - ts[0])), 0, st)
+
+    def gcn_backward(self, b, l):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        st = _lib.stream_handle()
+        N = eng.plan.N
+        w = eng.params.w(f"gcn{l}.w")
+        gw = eng.params.gw(f"gcn{l}.w")
+        for c, t in enumerate(self.ts):
+            dr = self.own(self.dR_own[l], Ly.rw, c)
+            r = self.own(self.R_own[l], Ly.rw, c)
+            s = self.plain(self.s1[t], Ly.fp) if l == 0 else self.plain(self.S_own[l], Ly.fp, c)
+            call("dgnn_gcn_weight_grad", N, s, dr, r, Ly.fp, Ly.hg, int(self.skip), ptr(gw), ptr(self.ws_tn),
+                 self.ws_tn.numel(), st)
+            if l > 0:
+                ds = self.plain(self.dS, Ly.fp)
+                call("dgnn_gcn_backward_rows", N, dr, r, Ly.fp, ptr(w), Ly.hg, int(self.skip), ds, st)
+                sl = self.slots[c]
+                call("dgnn_spmm_f32", N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val), ds, Ly.fp,
+                     self.own(self.dZ_own, Ly.fp, c), st)
+
+
+class LocalFabric:
+    """All P ranks in this process on one device: the all-to-all is a block
+    transpose of device buffers, the all-reduce a rank-order sum."""
+
+    distributed = False
+
+    def exchange(self, ranks, src, dst, count):
+        """dst[q][p-block] = src[p][q-block] with blocks of `count` elements."""
+        P = len(ranks)
+        if P == 1:
+            return
+        for p, rp in enumerate(ranks):
+            s = src(rp)
+            for q, rq in enumerate(ranks):
+                dst(rq)[p * count:(p + 1) * count].copy_(s[q * count:(q + 1) * count])
+
+    def allreduce(self, tensors):
+        total = tensors[0].clone()
+        for t in tensors[1:]:
+            total += t
+        return total
+
+
+class NcclFabric:
+    """One rank per process over torch.distributed (NCCL on GPUs)."""
+
+    distributed = True
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+
+    def exchange(self, ranks, src, dst, count):
+        (r,) = ranks
+        P = self.dist.get_world_size()
+        if P == 1:
+            return
+        self.dist.all_to_all_single(dst(r)[:P * count], src(r)[:P * count])
+
+    def allreduce(self, tensors):
+        (t,) = tensors
+        out = t.clone()
+        if self.dist.get_world_size() > 1:
+            self.dist.all_reduce(out)
+        return out
+
+
+class Engine:
+    """One epoch of snapshot-partitioned training on device (`dist.py:505-589`)."""
+
+    def __init__(self, cfg, graph, workers: int, nblk: int, feats_host=None, m_matrix=None,
+                 resident: bool = False, fabric=None, device=None, encoding=None):
+        if cfg.architecture not in ("cd-gcn", "tm-gcn"):
+            raise ConfigError(f"architecture {cfg.architecture!r} is outside this package's hot path")
+        self.cfg = cfg
+        self.skip = cfg.architecture == "cd-gcn"
+        N, T = graph.num_vertices, graph.num_timesteps
+        self.plan = Plan(T, workers, nblk, N)
+        self.layout = ParamLayout(cfg)
+        self.m_matrix = None if m_matrix is None else np.asarray(m_matrix, dtype=np.float64)
+        if not self.skip and self.m_matrix is None:
+            from .graph import build_m_matrix
+            self.m_matrix = build_m_matrix(T, cfg.window).matrix
+        self.resident = resident
+        self.enc = encoding if encoding is not None else SnapshotEncoding(graph)
+        self.fabric = fabric or LocalFabric()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.params = DeviceParams(self.layout, dev)
+        if self.fabric.distributed:
+            import torch.distributed as dist
+            if dist.get_world_size() != workers:
+                raise ConfigError(f"workers={workers} but the process group has {dist.get_world_size()} ranks")
+            ids = [dist.get_rank()]
+        else:
+            ids = list(range(workers))
+        self.ranks = [Rank(self, q, dev) for q in ids]
+        self.feats_host = feats_host
+        self.prepared_labels = None
+        self.scale = 1.0
+
+    # ------------------------------------------------------------------ setup
+    def set_labels(self, train_by_time, test_by_time=None, key=None):
+        key = key if key is not None else (id(train_by_time), id(test_by_time))
+        if self.prepared_labels == key:
+            return
+        for r in self.ranks:
+            r.prepare_inputs(self.feats_host, train_by_time, test_by_time)
+        self.prepared_labels = key
+
+    # ------------------------------------------------------------- schedule
+    def _xchg(self, src, dst, W, comm, phase, b, l):
+        plan = self.plan
+        count = plan.chunk * plan.NP * W
+        self.fabric.exchange(self.ranks, src, dst, count)
+        if comm is not None:
+            units = plan.bsize * plan.NP * (plan.P - 1)
+            msgs = plan.P * (plan.P - 1)
+            comm.record_alltoall(units, msgs, phase, b, l)
+
+    def _layers_forward(self, b, phase, comm):
+        layers = self.layout.layers
+        for l, Ly in enumerate(layers):
+            for r in self.ranks:
+                r.gcn_forward(b, l)
+            self._xchg(lambda r: r.R_own[l], lambda r: r.R_vm[l], Ly.rw, comm, phase, b, l)
+            for r in self.ranks:
+                r.rnn_forward(b, l)
+            src = (lambda r: r.Y_vm[l]) if self.skip else (lambda r: r.Z_vm[l])
+            self._xchg(src, lambda r: r.Y_own[l], Ly.ho, comm, phase, b, l)
+
+    def epoch(self, comm=None, transfer=None, act=None, count_total=None, reduction="mean"):
+        """Forward sweep + checkpointed reverse sweep; returns (loss, flat fp64 grads)."""
+        plan = self.plan
+        layers = self.layout.layers
+        L = len(layers)
+        cnt = count_total
+        if reduction == "sum":
+            self.scale = 1.0
+        else:
+            self.scale = (1.0 / cnt) if cnt else 1.0
+        for r in self.ranks:
+            r.reset_state()
+        self.params.zero_grad()
+        for b in range(plan.nblk):
+            for r in self.ranks:
+                r.begin_block(b, keep=False, ledger=transfer)
+            self._layers_forward(b, "forward", comm)
+            for r in self.ranks:
+                r.block_loss(b)
+                r.store_pi(b)
+            if act is not None:
+                act.alloc_checkpoint(1.0)
+        for b in reversed(range(plan.nblk)):
+            if act is not None:
+                act.alloc_activations(plan.bsize * 2 * L)
+            for r in self.ranks:
+                r.begin_block(b, keep=True, ledger=transfer)
+            self._layers_forward(b, "rerun", comm)
+            for r in self.ranks:
+                r.loss_grads(b)
+            for l in reversed(range(L)):
+                Ly = layers[l]
+                self._xchg(lambda r: r.dZ_own, lambda r: r.dY_vm, Ly.ho, comm, "backward", b, l)
+                for r in self.ranks:
+                    r.rnn_backward(b, l)
+                self._xchg(lambda r: r.dR_vm[l], lambda r: r.dR_own[l], Ly.rw, comm, "backward", b, l)
+                for r in self.ranks:
+                    r.gcn_backward(b, l)
+            if act is not None:
+                act.free_activations(plan.bsize * 2 * L)
+                act.free_checkpoint(1.0)
+        grads = self.fabric.allreduce([self.params.gather_grads()])
+        self.params.g.copy_(grads)
+        if comm is not None:
+            comm.record_allreduce(self.layout.count, plan.P)
+        loss_dev = self.fabric.allreduce([sum_ranks([r.loss_acc for r in self.ranks])])
+        return loss_dev, grads
+
+    def finish(self, loss_dev, grads):
+        loss = float(loss_dev.item()) * (self.scale if self.scale else 1.0)
+        for r in self.ranks:
+            r.mat.check()
+        return loss
+
+    def evaluate(self):
+        """Straight-line forward with the current parameters (`models.py:275-323`)
+        and test accuracy at the owned test frames (`training.py:189-197`)."""
+        plan = self.plan
+        for r in self.ranks:
+            r.reset_state()
+        for b in range(plan.nblk):
+            for r in self.ranks:
+                r.begin_block(b, keep=False, ledger=None, count_bytes=False)
+            self._layers_forward(b, "eval", None)
+            for r in self.ranks:
+                r.predict(b)
+        correct = self.fabric.allreduce([sum_ranks([r.correct for r in self.ranks])])
+        total = sum(d["n"] for r in self.ranks for d in r.lab.get("test", {}).values())
+        if self.fabric.distributed:
+            t = torch.tensor([total], dtype=torch.int64, device=self.device)
+            total = int(self.fabric.allreduce([t]).item())
+        return (int(correct.item()) / total) if total else None
+
+    def forward_frames(self):
+        """All T output frames (host fp64) of the straight-line forward."""
+        plan = self.plan
+        Ly = self.layout.layers[-1]
+        E = self.cfg.embed_features
+        frames = [None] * plan.T
+        for r in self.ranks:
+            r.reset_state()
+        for b in range(plan.nblk):
+            for r in self.ranks:
+                r.begin_block(b, keep=False, ledger=None, count_bytes=False)
+            self._layers_forward(b, "eval", None)
+            for r in self.ranks:
+                for c, t in enumerate(r.ts):
+                    rows = []
+                    for q in range(plan.P):
+                        rows.append(r.own_slab_rows(r.Y_own[-1], Ly.ho, c, q).view(plan.NP, Ly.ho)[:, :E])
+                    frames[t] = torch.cat(rows).double().cpu().numpy()
+        return frames
+
+
+def sum_ranks(ts):
+    if len(ts) == 1:
+        return ts[0]
+    out = ts[0].clone()
+    for t in ts[1:]:
+        out += t
+    return out

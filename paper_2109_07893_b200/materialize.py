@@ -1,0 +1,332 @@
+"""Graph-difference snapshot materialisation.
+
+Host side (`SnapshotEncoding`, built once per graph -- the encoding is
+input-static, so the reference's per-pass `diff` (`delta.py:110-123`,
+recomputed inside `stream_block` every pass) becomes a one-time prep):
+
+* full snapshot t: sorted (row, col) int32 pairs of the raw adjacency A_t;
+* delta t (t >= 1): ext_prev / ext_next of A_{t-1} -> A_t as sorted pairs;
+* values (fp64) only when A is not unit-valued (value-carrying mode, like
+  the reference which always ships `values_next`); unit-valued graphs ship
+  structure only and the device recomputes the Laplacian values bit-exactly.
+
+The reference streams the normalised Laplacians (`dist.py:308-312`); the
+ledger counters it would charge for them (index / value entries of Ahat) are
+computed exactly here at prep so `TransferLedger` stays reference-equivalent,
+next to the real bytes this package moves.
+
+Device side (`Materializer`): per pass and per owned chunk of a checkpoint
+block, the first snapshot arrives in full and the rest as deltas (pinned
+host -> HBM `cudaMemcpyAsync` on a copy stream), and kernels on a graph
+stream rebuild CSR(A_t) (K1), transpose it, and build CSR(Ahat_t) and
+CSR(Ahat_t^T) with fp64 values (K2) -- overlapped with the layer-0 compute,
+which does not need the graph (its aggregation is precomputed).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, query
+from .errors import CorruptDeltaError, InputError
+
+
+def _lap_keys(n: int, rows: np.ndarray, cols: np.ndarray, vals: np.ndarray | None) -> np.ndarray:
+    """Sorted int64 keys of normalize_laplacian(A) (dtdg.py:178-191), i.e. the
+    structure of A plus the diagonal, minus entries whose value is exactly 0."""
+    keys = rows * np.int64(n) + cols
+    diag = np.arange(n, dtype=np.int64) * (n + 1)
+    if vals is None:                                   # unit values: nothing can vanish
+        return np.union1d(keys, diag)
+    deg = np.bincount(rows, minlength=n).astype(np.float64)
+    isq = 1.0 / np.sqrt(1.0 + deg)
+    v = (vals * isq[rows]) * isq[cols]
+    on_diag = rows == cols
+    dvals = isq * isq                                  # identity term
+    dsum = dvals.copy()
+    dsum[rows[on_diag]] = v[on_diag] + dvals[rows[on_diag]]
+    off = keys[(~on_diag) & (v != 0.0)]
+    dk = diag[dsum != 0.0]
+    return np.union1d(off, dk)
+
+
+@dataclass
+class ChunkPlan:
+    ts: list
+    full_range: tuple      # (offset, count) int32 elements in the full region
+    delta_range: tuple     # (offset, count) int32 elements in the delta region
+    val_range: tuple       # (offset, count) fp64 elements (value-carrying only)
+
+
+class SnapshotEncoding:
+    """Pinned host encoding of a dynamic graph (see module docstring)."""
+
+    def __init__(self, graph, pin: bool = True):
+        n = int(graph.num_vertices)
+        T = int(graph.num_timesteps)
+        if n >= 2 ** 31 - 1:
+            raise InputError("vertex ids must fit int32")
+        self.n, self.T = n, T
+        snaps = graph.snapshots
+        rows = [np.asarray(s.rows, np.int64) for s in snaps]
+        cols = [np.asarray(s.cols, np.int64) for s in snaps]
+        vals = [np.asarray(s.vals, np.float64) for s in snaps]
+        self.unit = all(bool(np.all(v == 1.0)) for v in vals)
+        keys = [r * np.int64(n) + c for r, c in zip(rows, cols)]
+        for t, k in enumerate(keys):
+            if k.size > 1 and not np.all(k[1:] > k[:-1]):
+                raise InputError(f"snapshot {t} is not canonical (sorted, duplicate-free)")
+        self.nnz = np.array([k.shape[0] for k in keys], dtype=np.int64)
+
+        # full region: [rows_t | cols_t] per t
+        full_off = np.zeros(T + 1, dtype=np.int64)
+        full_off[1:] = np.cumsum(2 * self.nnz)
+        # delta region: [del_r | del_c | ins_r | ins_c] per t >= 1
+        self.n_del = np.zeros(T, dtype=np.int64)
+        self.n_ins = np.zeros(T, dtype=np.int64)
+        deltas = [None]
+        for t in range(1, T):
+            gone = np.setdiff1d(keys[t - 1], keys[t], assume_unique=True)
+            new = np.setdiff1d(keys[t], keys[t - 1], assume_unique=True)
+            self.n_del[t], self.n_ins[t] = gone.shape[0], new.shape[0]
+            deltas.append((gone, new))
+        delta_off = np.zeros(T + 1, dtype=np.int64)
+        delta_off[1:] = np.cumsum(2 * (self.n_del + self.n_ins))
+        self.full_off, self.delta_off = full_off, delta_off
+        val_off = np.zeros(T + 1, dtype=np.int64)
+        val_off[1:] = np.cumsum(self.nnz)
+        self.val_off = val_off
+
+        full = np.empty(int(full_off[-1]), dtype=np.int32)
+        for t in range(T):
+            o, m = int(full_off[t]), int(self.nnz[t])
+            full[o:o + m] = rows[t]
+            full[o + m:o + 2 * m] = cols[t]
+        dl = np.empty(int(delta_off[-1]), dtype=np.int32)
+        for t in range(1, T):
+            gone, new = deltas[t]
+            o = int(delta_off[t])
+            a, b = gone.shape[0], new.shape[0]
+            dl[o:o + a] = gone // n
+            dl[o + a:o + 2 * a] = gone % n
+            dl[o + 2 * a:o + 2 * a + b] = new // n
+            dl[o + 2 * a + b:o + 2 * a + 2 * b] = new % n
+        self.full = torch.from_numpy(full)
+        self.delta = torch.from_numpy(dl)
+        self.vals = None if self.unit else torch.from_numpy(np.concatenate(vals) if vals else np.zeros(0))
+        if pin and torch.cuda.is_available():
+            self.full = self.full.pin_memory()
+            self.delta = self.delta.pin_memory()
+            if self.vals is not None:
+                self.vals = self.vals.pin_memory()
+
+        # reference-equivalent ledger counts for the Laplacians (delta.py:75-84)
+        self.nnz_hat = np.zeros(T, dtype=np.int64)
+        self.dhat = np.zeros(T, dtype=np.int64)
+        if self.unit:
+            # Ahat = A + I structurally and nothing can cancel: the diagonal is
+            # always present, so diagonal entries of the A-delta do not change Ahat
+            for t in range(T):
+                self.nnz_hat[t] = self.nnz[t] + n - int(np.count_nonzero(rows[t] == cols[t]))
+            for t in range(1, T):
+                gone, new = deltas[t]
+                off = int(np.count_nonzero(gone // n != gone % n) + np.count_nonzero(new // n != new % n))
+                self.dhat[t] = off
+        else:
+            hat = [_lap_keys(n, rows[t], cols[t], vals[t]) for t in range(T)]
+            self.nnz_hat = np.array([h.shape[0] for h in hat], dtype=np.int64)
+            for t in range(1, T):
+                self.dhat[t] = (np.setdiff1d(hat[t - 1], hat[t], assume_unique=True).shape[0]
+                                + np.setdiff1d(hat[t], hat[t - 1], assume_unique=True).shape[0])
+        self.cap_a = int(max(1, self.nnz.max()))
+        self.cap_hat = int(max(1, self.nnz_hat.max()))
+
+    # -- accounting ---------------------------------------------------------
+    def chunk(self, ts) -> ChunkPlan:
+        t0, t1 = ts[0], ts[-1]
+        if list(ts) != list(range(t0, t1 + 1)):
+            raise InputError("a streamed chunk must be a contiguous run of timesteps")
+        fr = (int(self.full_off[t0]), int(2 * self.nnz[t0]))
+        dr = (int(self.delta_off[t0 + 1]), int(self.delta_off[t1 + 1] - self.delta_off[t0 + 1]))
+        vr = (int(self.val_off[t0]), int(self.val_off[t1 + 1] - self.val_off[t0]))
+        return ChunkPlan(list(ts), fr, dr, vr)
+
+    def chunk_bytes(self, ts) -> int:
+        c = self.chunk(ts)
+        b = 4 * (c.full_range[1] + c.delta_range[1])
+        if not self.unit:
+            b += 8 * c.val_range[1]
+        return b
+
+    def full_bytes(self, ts) -> int:
+        """Bytes if every snapshot of the chunk travelled in full (same encoding)."""
+        b = sum(8 * int(self.nnz[t]) for t in ts)
+        if not self.unit:
+            b += sum(8 * int(self.nnz[t]) for t in ts)
+        return b
+
+    def charge(self, ledger, ts) -> None:
+        """Reference TransferLedger charges of stream_block over the
+        chunk's Laplacians (delta.py:75-84, 161-167)."""
+        t0 = ts[0]
+        ledger.index_entries_sent += int(self.nnz_hat[t0])
+        ledger.value_entries_sent += int(self.nnz_hat[t0])
+        ledger.snapshots_full += 1
+        for t in ts[1:]:
+            ledger.index_entries_sent += int(self.dhat[t])
+            ledger.value_entries_sent += int(self.nnz_hat[t])
+            ledger.snapshots_delta += 1
+
+
+@dataclass
+class LapSlot:
+    """CSR of Ahat_t and of Ahat_t^T for one materialised timestep."""
+    rowptr: torch.Tensor
+    col: torch.Tensor
+    val: torch.Tensor
+    t_rowptr: torch.Tensor
+    t_col: torch.Tensor
+    t_val: torch.Tensor
+    val64: torch.Tensor | None = None
+    t_val64: torch.Tensor | None = None
+    a_rowptr: torch.Tensor | None = None   # raw CSR of A_t (valid until the next rebuild)
+    a_t_rowptr: torch.Tensor | None = None
+    t: int = -1
+
+
+class Materializer:
+    """Device-side rebuild of the snapshots a rank owns, chunk by chunk."""
+
+    def __init__(self, enc: SnapshotEncoding, device, slots: int, resident: bool = False,
+                 with_f64: bool = False):
+        self.enc = enc
+        self.device = torch.device(device)
+        n = enc.n
+        i32 = dict(dtype=torch.int32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.resident = resident
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.graph_stream = torch.cuda.Stream(device=self.device)
+        # encoded input on device: everything (resident) or a chunk-sized staging area
+        if resident:
+            self.full_dev = enc.full.to(self.device)
+            self.delta_dev = enc.delta.to(self.device)
+            self.vals_dev = None if enc.unit else enc.vals.to(self.device)
+        else:
+            self.full_dev = torch.empty(int(2 * enc.nnz.max()) + 1, **i32)
+            self.delta_dev = torch.empty(int(enc.delta_off[-1]) + 1, **i32)
+            self.vals_dev = None if enc.unit else torch.empty(int(enc.val_off[-1]) + 1, **f64)
+        cap_a, cap_h = enc.cap_a, enc.cap_hat
+        self.a_rowptr = [torch.empty(n + 1, **i32) for _ in range(2)]
+        self.a_col = [torch.empty(cap_a, **i32) for _ in range(2)]
+        self.at_rowptr = torch.empty(n + 1, **i32)
+        self.at_col = torch.empty(cap_a, **i32)
+        self.stage_col = torch.empty(cap_a, **i32)
+        self.at_val = None if enc.unit else torch.empty(cap_a, **f64)
+        self.stage_val = None if enc.unit else torch.empty(cap_a, **f64)
+        self.ws_apply = torch.empty(query("dgnn_csr_apply_delta_workspace", n), dtype=torch.uint8,
+                                    device=self.device)
+        self.ws_tr = torch.empty(query("dgnn_csr_transpose_workspace", n), dtype=torch.uint8,
+                                 device=self.device)
+        self.ws_lap = torch.empty(query("dgnn_laplacian_workspace", n), dtype=torch.uint8,
+                                  device=self.device)
+        self.status = torch.zeros(4, **i32)
+        self.slots = []
+        for _ in range(slots):
+            self.slots.append(LapSlot(
+                torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
+                torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
+                torch.empty(cap_h, **f64) if with_f64 else None,
+                torch.empty(cap_h, **f64) if with_f64 else None))
+        self.bytes_h2d = 0
+        self.bytes_full_equiv = 0
+        self.ready = torch.cuda.Event()
+
+    def materialize(self, ts, ledger=None, count_bytes: bool = True):
+        """Rebuild Ahat_t for the contiguous run `ts` into slots 0..len(ts)-1.
+        Returns the slots; `self.ready` is recorded on the graph stream."""
+        enc = self.enc
+        if len(ts) > len(self.slots):
+            raise InputError("chunk longer than the materialiser's slot count")
+        plan = enc.chunk(ts)
+        n = enc.n
+        gs = self.graph_stream
+        gsh = gs.cuda_stream
+        # inputs: H2D on the copy stream (pinned -> HBM) unless resident
+        if self.resident:
+            fbase, dbase, vbase = plan.full_range[0], plan.delta_range[0], plan.val_range[0]
+        else:
+            fbase = dbase = vbase = 0
+            cs = self.copy_stream
+            cs.wait_stream(gs)                 # staging is free once the previous chunk's rebuild ran
+            with torch.cuda.stream(cs):
+                fo, fc = plan.full_range
+                self.full_dev[:fc].copy_(enc.full[fo:fo + fc], non_blocking=True)
+                do, dc = plan.delta_range
+                if dc:
+                    self.delta_dev[:dc].copy_(enc.delta[do:do + dc], non_blocking=True)
+                if not enc.unit:
+                    vo, vc = plan.val_range
+                    self.vals_dev[:vc].copy_(enc.vals[vo:vo + vc], non_blocking=True)
+            gs.wait_stream(cs)
+        if count_bytes:
+            self.bytes_h2d += enc.chunk_bytes(ts)
+            self.bytes_full_equiv += enc.full_bytes(ts)
+        if ledger is not None:
+            enc.charge(ledger, ts)
+        cur = 0
+        voff = vbase
+        # slots are overwritten: wait for every consumer already enqueued on the compute stream
+        gs.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(gs):
+            for i, t in enumerate(ts):
+                m = int(enc.nnz[t])
+                if i == 0:
+                    rows = self.full_dev[fbase:fbase + m]
+                    a_col = self.full_dev[fbase + m:fbase + 2 * m]
+                    call("dgnn_rowptr_from_sorted_rows", n, m, ptr(rows), ptr(self.a_rowptr[cur]), gsh)
+                    a_rowptr = self.a_rowptr[cur]
+                    dpos = dbase
+                else:
+                    nd, ni = int(enc.n_del[t]), int(enc.n_ins[t])
+                    d = self.delta_dev[dpos:dpos + 2 * (nd + ni)]
+                    dpos += 2 * (nd + ni)
+                    nxt = 1 - cur
+                    call("dgnn_csr_apply_delta", n, ptr(a_rowptr), ptr(a_col), nd, ptr(d[:nd]),
+                         ptr(d[nd:2 * nd]), ni, ptr(d[2 * nd:2 * nd + ni]), ptr(d[2 * nd + ni:]),
+                         ptr(self.a_rowptr[nxt]), ptr(self.a_col[nxt]), enc.cap_a, ptr(self.ws_apply),
+                         self.ws_apply.numel(), ptr(self.status), gsh)
+                    cur = nxt
+                    a_rowptr, a_col = self.a_rowptr[cur], self.a_col[cur]
+                a_val = None
+                if not enc.unit:
+                    a_val = self.vals_dev[voff:voff + m]
+                voff += m
+                call("dgnn_csr_transpose_staged", n, m, ptr(a_rowptr), ptr(a_col), ptr(a_val),
+                     ptr(self.at_rowptr), ptr(self.at_col), ptr(self.at_val), ptr(self.stage_col),
+                     ptr(self.stage_val), ptr(self.ws_tr), self.ws_tr.numel(), gsh)
+                s = self.slots[i]
+                call("dgnn_laplacian", n, ptr(a_rowptr), ptr(a_rowptr), ptr(a_col), ptr(a_val), 0,
+                     ptr(s.rowptr), ptr(s.col), ptr(s.val), ptr(s.val64), enc.cap_hat,
+                     ptr(self.ws_lap), self.ws_lap.numel(), gsh)
+                call("dgnn_laplacian", n, ptr(a_rowptr), ptr(self.at_rowptr), ptr(self.at_col),
+                     ptr(self.at_val), 1, ptr(s.t_rowptr), ptr(s.t_col), ptr(s.t_val), ptr(s.t_val64),
+                     enc.cap_hat, ptr(self.ws_lap), self.ws_lap.numel(), gsh)
+                s.a_rowptr, s.a_t_rowptr, s.t = a_rowptr, self.at_rowptr, t
+            self.ready.record(gs)
+        return self.slots[:len(ts)]
+
+    def wait(self, stream=None):
+        (stream or torch.cuda.current_stream(self.device)).wait_event(self.ready)
+
+    def check(self):
+        """Raise CorruptDeltaError if any rebuild saw an inconsistent delta."""
+        bad = int(self.status[0].item())
+        if bad:
+            self.status.zero_()
+            raise CorruptDeltaError(f"{bad} inconsistent delta entries during CSR rebuild")

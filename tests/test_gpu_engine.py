@@ -1,0 +1,181 @@
+"""GPU parity of the training engine (drop-in API) against the reference's
+golden runs and the CPU oracle.
+
+Tolerance (north star): losses and gradients within 1e-4 relative in fp32,
+guarded as |g - r| <= 1e-4 max(|g|, |r|) + 1e-6 ||r||_inf per tensor (the
+reference's own guarded form, conftest.py:71-86).  Ledgers (communication
+and transfer counters) must be exactly equal.  Test accuracy is an argmax,
+compared with a small count tolerance.
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2109_07893_b200 as pk
+
+from conftest import assert_grads_close, guarded_close, jload, labels_from, load, params_from
+from helpers import product_case, product_graph
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _fresh_engines():
+    yield
+    pk.api.clear_engines()
+
+
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+@pytest.mark.parametrize("nblk", [1, 2, 4])
+def test_backward_checkpoint_vs_reference(name, nblk):
+    fx, cfg, data, train, _, params = product_case(name)
+    loss, grads = pk.backward_checkpoint(cfg, data, train, params, nblk)
+    assert loss == pytest.approx(float(fx[f"ckpt{nblk}_loss"]), rel=RTOL)
+    assert_grads_close(grads, params_from(fx, f"ckpt{nblk}_g_"), RTOL)
+
+
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+def test_backward_full_vs_reference(name):
+    fx, cfg, data, train, _, params = product_case(name)
+    loss, grads = pk.backward_full(cfg, data, train, params)
+    assert loss == pytest.approx(float(fx["full_loss"]), rel=RTOL)
+    assert_grads_close(grads, params_from(fx, "full_g_"), RTOL)
+
+
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+@pytest.mark.parametrize("workers,nblk", [(2, 2), (4, 1), (2, 1)])
+def test_distributed_epoch_vs_reference(name, workers, nblk):
+    fx, cfg, data, train, _, params = product_case(name)
+    tag = f"dist{workers}x{nblk}"
+    for sched in ("round-robin", "threads"):
+        loss, grads, comm, tr = pk.distributed_epoch(cfg, data, train, params, workers, nblk, scheduler=sched)
+        assert loss == pytest.approx(float(fx[f"{tag}_loss"]), rel=RTOL)
+        assert_grads_close(grads, params_from(fx, f"{tag}_g_"), RTOL)
+        assert comm.as_dict() == jload(fx[f"{tag}_comm"])
+        assert comm.events == jload(fx[f"{tag}_events"])
+        assert tr.as_dict() == jload(fx[f"{tag}_transfer"])
+
+
+def test_results_are_bit_reproducible():
+    fx, cfg, data, train, _, params = product_case("cdgcn_small")
+    a = pk.distributed_epoch(cfg, data, train, params, 2, 2)
+    pk.api.clear_engines()
+    b = pk.distributed_epoch(cfg, data, train, params, 2, 2)
+    assert a[0] == b[0]
+    for k in a[1]:
+        assert np.array_equal(a[1][k], b[1][k])
+
+
+def test_multi_rank_matches_single_rank():
+    fx, cfg, data, train, _, params = product_case("cdgcn_small")
+    l1, g1 = pk.backward_checkpoint(cfg, data, train, params, 2)
+    l4, g4, _, _ = pk.distributed_epoch(cfg, data, train, params, 4, 1)
+    assert l4 == pytest.approx(l1, rel=RTOL)
+    assert_grads_close(g4, g1, RTOL)
+
+
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+def test_train_distributed_vs_reference(name):
+    fx, cfg, data, train, test, _ = product_case(name)
+    seed = 3 if name.startswith("cd") else 2
+    trace, params, comm, tr, act = pk.train_distributed(cfg, data, train, test, epochs=3, seed=seed,
+                                                        workers=2, nblk=2)
+    ref = jload(fx["train_trace"])
+    for a, b in zip(trace, ref):
+        assert a["epoch"] == b["epoch"]
+        assert a["loss"] == pytest.approx(b["loss"], rel=RTOL)
+        npairs = sum(p.shape[0] for p, _ in test.by_time.values())
+        assert abs(a["test_accuracy"] - b["test_accuracy"]) <= 1.0 / npairs + 1e-12
+    ref_p = params_from(fx, "train_p_")
+    for k in ref_p:
+        ok, worst, _ = guarded_close(params[k], ref_p[k], 1e-4, 1e-5)
+        assert ok, (k, worst)
+    assert comm.as_dict() == jload(fx["train_comm"])
+    assert tr.as_dict() == jload(fx["train_transfer"])
+    assert act.peak == float(fx["train_act_peak"])
+
+
+def test_cli_golden_report_through_engine():
+    """The reference CLI's frozen golden run (tm-gcn, P=2, nblk=2, 2 epochs)."""
+    fx = load("cli_report")
+    rep = jload(fx["report"])
+    c = rep["config"]
+    g = product_graph(fx)
+    cfg = pk.ModelConfig(c["model"], hidden_features=c["hidden"], embed_features=c["embed"], window=c["window"])
+    data = pk.prepare_training_data(cfg, g)
+    train, test = pk.sample_link_prediction_sets(g, c["theta"], c["seed"] + 1000003)
+    trace, _, comm, tr, act = pk.train_distributed(cfg, data, train, test, c["epochs"], c["seed"],
+                                                   c["workers"], c["blocks"], lr=c["lr"])
+    assert comm.as_dict() == rep["comm"]
+    assert tr.as_dict() == rep["transfer"]
+    assert act.peak == rep["activation_peak"]
+    for a, b in zip(trace, rep["epochs"]):
+        assert a["loss"] == pytest.approx(b["loss"], rel=RTOL)
+
+
+def test_c1_config_vs_reference():
+    """BASELINE config 1 (N=10k, T=8, 50k edges/snapshot, 10% churn,
+    cd-gcn H=32) against the reference's stored loss and gradients."""
+    from paper_2109_07893_b200.synth import churn_graph
+    fx = load("c1_pins")
+    g = churn_graph(10_000, 8, 50_000, 0.10, seed=1)
+    cfg = pk.ModelConfig("cd-gcn", hidden_features=32, embed_features=32)
+    data = pk.prepare_training_data(cfg, g)
+    train, _ = pk.sample_link_prediction_sets(g, 0.1, 1 + 1000003)
+    params = pk.init_params(cfg, 0)
+    rng = np.random.default_rng(77)
+    params["head.w"] = rng.uniform(-0.5, 0.5, size=params["head.w"].shape)
+    params["head.b"] = rng.uniform(-0.1, 0.1, size=params["head.b"].shape)
+    loss, grads = pk.backward_checkpoint(cfg, data, train, params, 2)
+    assert loss == pytest.approx(float(fx["loss"]), rel=RTOL)
+    assert_grads_close(grads, {k[2:]: fx[k] for k in fx if k.startswith("g_")}, RTOL)
+
+
+def test_midsize_multi_rank_parity_vs_oracle(oracle):
+    """N=20k, T=8, H=64: emulated P=4 vs P=1 vs the oracle."""
+    from paper_2109_07893_b200.synth import churn_graph
+    g = churn_graph(20_000, 8, 30_000, 0.10, seed=5)
+    cfg = pk.ModelConfig("cd-gcn", hidden_features=64, embed_features=64)
+    data = pk.prepare_training_data(cfg, g)
+    train, _ = pk.sample_link_prediction_sets(g, 0.1, 9)
+    params = pk.init_params(cfg, 4)
+    rng = np.random.default_rng(1)
+    params["head.w"] = rng.uniform(-0.5, 0.5, size=params["head.w"].shape)
+    l1, g1 = pk.backward_checkpoint(cfg, data, train, params, 2)
+    l4, g4, comm, tr = pk.distributed_epoch(cfg, data, train, params, 4, 2)
+    ocfg = oracle.Cfg("cd-gcn", 2, 64, 64)
+    P = oracle.prepare(ocfg, [oracle.Coo(s.dim, s.rows, s.cols, s.vals) for s in g.snapshots])
+    lo, go = oracle.backward_checkpoint(ocfg, P, train.by_time, params, 2)
+    assert l1 == pytest.approx(lo, rel=RTOL)
+    assert l4 == pytest.approx(lo, rel=RTOL)
+    assert_grads_close(g1, go, RTOL)
+    assert_grads_close(g4, go, RTOL)
+    assert comm.redistribution_units == 6 * 2 * 8 * 20_000 * 3 // 4
+
+
+def test_reference_objects_are_accepted():
+    """Duck typing: a reference-shaped TrainingData/ModelConfig works."""
+    fx, cfg, data, train, _, params = product_case("cdgcn_small")
+
+    class RefCfg:
+        architecture, in_features, hidden_features, embed_features = "cd-gcn", 2, 8, 8
+        layers, window, edge_life, classes = 2, 2, 2, 2
+
+    loss, grads = pk.backward_checkpoint(RefCfg, data, train, params, 1)
+    assert loss == pytest.approx(float(fx["ckpt1_loss"]), rel=RTOL)
+
+
+def test_errors_match_reference_types():
+    fx, cfg, data, train, _, params = product_case("cdgcn_small")
+    with pytest.raises(pk.ConfigError):
+        pk.distributed_epoch(cfg, data, train, params, 3, 1)
+    with pytest.raises(pk.ConfigError):
+        pk.distributed_epoch(cfg, data, train, params, 2, 3)
+    with pytest.raises(pk.ConfigError):
+        pk.distributed_epoch(cfg, data, train, params, 1, 1, scheduler="fibers")
+    with pytest.raises(pk.ConfigError):
+        pk.backward_checkpoint(cfg, data, train, params, 3)

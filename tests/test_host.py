@@ -1,0 +1,158 @@
+"""CPU tests: C-ABI library exports, host-side logic of the boundary (no
+kernel launches)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2109_07893_b200 as pk
+from paper_2109_07893_b200 import _lib
+from paper_2109_07893_b200.params import ParamLayout, padded_layers
+
+from conftest import ROOT, load, params_from
+from helpers import product_graph
+
+
+def header_symbols():
+    text = (ROOT / "include" / "dgnn_b200.h").read_text()
+    return sorted(set(re.findall(r"^(?:int|size_t|long long|const char\*)\s+(dgnn_\w+)\(", text, re.M)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = _lib.lib()
+    declared = header_symbols()
+    assert len(declared) >= 30
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.dgnn_abi_version() == 1
+
+
+def test_binding_covers_the_header():
+    assert set(_lib.exported_symbols()) == set(header_symbols())
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_init_params_matches_reference_fixture():
+    for name, seed in (("cdgcn_small", 3), ("tmgcn_small", 2)):
+        fx = load(name)
+        arch = "cd-gcn" if name.startswith("cd") else "tm-gcn"
+        cfg = pk.ModelConfig(arch, hidden_features=8, embed_features=8)
+        got = pk.init_params(cfg, seed)
+        ref = params_from(fx, "init_")
+        assert sorted(got) == sorted(ref)
+        for k in ref:
+            assert np.array_equal(got[k], ref[k])
+
+
+def test_param_layout_round_trip_and_disjoint_positions():
+    for arch, h in (("cd-gcn", 8), ("cd-gcn", 64), ("tm-gcn", 6)):
+        cfg = pk.ModelConfig(arch, hidden_features=h, embed_features=h)
+        lay = ParamLayout(cfg)
+        p = pk.init_params(cfg, 1)
+        flat = lay.flatten(p)
+        back = lay.unflatten(flat)
+        for k in p:
+            assert np.array_equal(back[k], p[k])
+        assert np.unique(lay.pos0).shape[0] == lay.count
+        assert lay.pos0.max() < lay.size
+        sec = lay.pos1[lay.pos1 >= 0]
+        assert np.intersect1d(sec, lay.pos0).size == 0
+
+
+def test_padding_rules():
+    cfg = pk.ModelConfig("cd-gcn", hidden_features=64, embed_features=64)
+    l0, l1 = padded_layers(cfg)
+    assert (l0.fp, l0.hg, l0.ho, l0.rw) == (4, 64, 64, 68)
+    assert (l1.fp, l1.hg, l1.ho, l1.rw) == (64, 64, 64, 128)
+    with pytest.raises(pk.ConfigError):
+        padded_layers(pk.ModelConfig("cd-gcn", hidden_features=200, embed_features=200))
+
+
+def test_encoding_matches_reference_deltas_and_ledger():
+    from paper_2109_07893_b200.materialize import SnapshotEncoding
+    fx = load("codec")
+    g = product_graph(fx)
+    enc = SnapshotEncoding(g, pin=False)
+    for t in range(1, g.num_timesteps):
+        o = int(enc.delta_off[t])
+        nd, ni = int(enc.n_del[t]), int(enc.n_ins[t])
+        d = enc.delta[o:o + 2 * (nd + ni)].numpy()
+        assert np.array_equal(np.stack([d[:nd], d[nd:2 * nd]], 1), fx[f"ext_prev{t}"])
+        assert np.array_equal(np.stack([d[2 * nd:2 * nd + ni], d[2 * nd + ni:]], 1), fx[f"ext_next{t}"])
+    led = pk.TransferLedger()
+    enc.charge(led, list(range(g.num_timesteps)))
+    import json
+    assert led.as_dict() == json.loads(str(fx["stream_ledger"]))
+    # weighted graph: value-carrying mode, Laplacian structure counts exact
+    gw = product_graph(fx, "gw_")
+    encw = SnapshotEncoding(gw, pin=False)
+    assert not encw.unit
+    for t in range(gw.num_timesteps):
+        assert encw.nnz_hat[t] == fx[f"lapw{t}_vals"].shape[0]
+
+
+def test_delta_bytes_ratio_formula():
+    """Like-for-like per-pass ratio L / (1 + (L-1) 2 churn)."""
+    from paper_2109_07893_b200.materialize import SnapshotEncoding
+    from paper_2109_07893_b200.synth import churn_graph
+    g = churn_graph(2000, 8, 4000, 0.10, seed=3)
+    enc = SnapshotEncoding(g, pin=False)
+    ts = list(range(8))
+    ratio = enc.full_bytes(ts) / enc.chunk_bytes(ts)
+    assert ratio == pytest.approx(8 / (1 + 7 * 0.2), rel=1e-9)
+
+
+def test_plan_and_partition_errors():
+    from paper_2109_07893_b200.engine import Plan
+    p = Plan(12, 3, 2, 9)
+    assert p.steps_of(1, 1) == [8, 9]
+    assert [p.owner_of(t) for t in range(6)] == [0, 0, 1, 1, 2, 2]
+    with pytest.raises(pk.ConfigError):
+        Plan(6, 4, 1, 8)
+    with pytest.raises(pk.ConfigError):
+        Plan(8, 2, 3, 8)
+    with pytest.raises(pk.ConfigError):
+        Plan(8, 4, 1, 6)
+    sp = pk.plan_snapshot_partition(12, 3, 2)
+    assert sp.steps_of(2, 1) == [10, 11]
+
+
+def test_label_incidence_order():
+    from paper_2109_07893_b200.labels import frame_labels
+    pairs = np.array([[1, 2], [2, 1], [1, 1], [0, 2]])
+    fl = frame_labels(pairs, np.array([1, 0, 1, 0]), 3, 2)
+    # vertex 1: side-0 slots of pairs 0, 2 then side-1 slots of pairs 1, 2
+    s = fl.inc_slot[fl.inc_ptr[1]:fl.inc_ptr[2]].tolist()
+    assert s == [0, 4, 3, 5]
+
+
+def test_engines_refuse_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    fx = load("cdgcn_small")
+    g = product_graph(fx)
+    cfg = pk.ModelConfig("cd-gcn", hidden_features=8, embed_features=8)
+    data = pk.prepare_training_data(cfg, g)
+    with pytest.raises(pk.ConfigError):
+        pk.backward_checkpoint(cfg, data, pk.LabelSet(2, {}), pk.init_params(cfg, 0), 1)
+
+
+def test_synthetic_generator_exact_churn():
+    from paper_2109_07893_b200.synth import churn_keys
+    ks = churn_keys(500, 5, 1000, 0.1, seed=2)
+    for a, b in zip(ks, ks[1:]):
+        assert a.shape[0] == b.shape[0] == 1000
+        assert np.setdiff1d(a, b).shape[0] == 100
+    assert all(np.all(k[1:] > k[:-1]) for k in ks)
+    ks2 = churn_keys(500, 5, 1000, 0.1, seed=2)
+    assert all(np.array_equal(a, b) for a, b in zip(ks, ks2))
