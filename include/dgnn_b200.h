@@ -188,24 +188,27 @@ int dgnn_axpy_frame(int64_t count, float coef, const float* y, float* z, int ini
  *   logits_p = z[u_p] . hw[:E] + z[v_p] . hw[E:] + hb   (hw: 2*ep x c, rows
  *              [0,E) and [ep, ep+E) real)
  *   loss_per_pair[p] = CE_p in fp64 (sum it with dgnn_sum_f64)
- *   dlogits_p = (softmax - onehot) * scale  (if dlogits != NULL) */
+ *   dlogits_p = (softmax - onehot) * scale in fp64 (if dlogits != NULL): the
+ *   head reductions stay fp64 so exact cancellations (e.g. the bias gradient
+ *   of a balanced label set) stay ~0 as in the reference, which Adam's
+ *   g / (|g| + eps) would otherwise amplify */
 int dgnn_head_loss(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y,
                    dgnn_frame z, int32_t ep, int32_t c, const float* hw, const float* hb,
-                   double scale, double* loss_per_pair, int32_t n_loss, float* dlogits,
+                   double scale, double* loss_per_pair, int32_t n_loss, double* dlogits,
                    void* stream);
 
 /* Head parameter grads: ghw[k][j] += sum_p cat_p[k] dlogits_p[j], ghb += sum_p dlogits_p
  * (deterministic split + fp64 reduce).  Workspace from dgnn_head_grad_workspace. */
 size_t dgnn_head_grad_workspace(int32_t ep, int32_t c);
 int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_frame z, int32_t ep,
-                   int32_t c, const float* dlogits, double* ghw, double* ghb, void* workspace,
+                   int32_t c, const double* dlogits, double* ghw, double* ghb, void* workspace,
                    size_t workspace_bytes, void* stream);
 
 /* dz seeds (training.py:732-734) as a gather over the vertex->slot
  * incidence (ascending slot order = the np.add.at order):
  *   dz[x] = sum_{slot s of x} dlogits[s/2] . hw[side(s)]^T ; zero rows elsewhere. */
 int dgnn_head_scatter(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot,
-                      const float* dlogits, const float* hw, int32_t ep, int32_t c,
+                      const double* dlogits, const float* hw, int32_t ep, int32_t c,
                       dgnn_frame dz, void* stream);
 
 /* Test accuracy (training.py:189-197): *correct += #pairs whose first-index

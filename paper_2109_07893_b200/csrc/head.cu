@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(256) head_loss_kernel(int64_t npairs, const in
                                                         const int32_t* __restrict__ y, dgnn_frame z, int ep,
                                                         int C, const float* __restrict__ hw,
                                                         const float* __restrict__ hb, double scale,
-                                                        double* __restrict__ loss_pp, float* __restrict__ dlogits) {
+                                                        double* __restrict__ loss_pp, double* __restrict__ dlogits) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) head_loss_kernel(int64_t npairs, const in
             if (dlogits) {
                 for (int c = 0; c < C; ++c) {
                     const double pr = exp((l[c] - mx) - lz);
-                    dlogits[p * C + c] = (float)((pr - (c == lab ? 1.0 : 0.0)) * scale);
+                    dlogits[p * C + c] = (pr - (c == lab ? 1.0 : 0.0)) * scale;
                 }
             }
         }
@@ -94,35 +94,35 @@ __global__ void __launch_bounds__(256) head_predict_kernel(int64_t npairs, const
 // CTA = chunk of pairs; thread t owns output row k = t (k <= 2ep) for all classes.
 __global__ void __launch_bounds__(256) head_grad_partial_kernel(int64_t npairs, const int32_t* __restrict__ u,
                                                                 const int32_t* __restrict__ v, dgnn_frame z,
-                                                                int ep, int C, const float* __restrict__ dl,
-                                                                int64_t per, float* __restrict__ part) {
+                                                                int ep, int C, const double* __restrict__ dl,
+                                                                int64_t per, double* __restrict__ part) {
     const int64_t p0 = blockIdx.x * per, p1 = min(npairs, p0 + per);
     const int rows = 2 * ep + 1;
     for (int k = threadIdx.x; k < rows; k += blockDim.x) {
-        float acc[kMaxClasses];
+        double acc[kMaxClasses];
 #pragma unroll
-        for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.f;
+        for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.0;
         for (int64_t p = p0; p < p1; ++p) {
-            float a;
+            double a;
             if (k < ep) a = frame_row<const float>(z, u[p])[k];
             else if (k < 2 * ep) a = frame_row<const float>(z, v[p])[k - ep];
-            else a = 1.f;
+            else a = 1.0;
 #pragma unroll
             for (int c = 0; c < kMaxClasses; ++c)
-                if (c < C) acc[c] = fmaf(a, dl[p * C + c], acc[c]);
+                if (c < C) acc[c] += a * dl[p * C + c];
         }
         for (int c = 0; c < C; ++c) part[((int64_t)blockIdx.x * rows + k) * C + c] = acc[c];
     }
 }
 
-__global__ void head_grad_reduce_kernel(int nchunks, int ep, int C, const float* __restrict__ part,
+__global__ void head_grad_reduce_kernel(int nchunks, int ep, int C, const double* __restrict__ part,
                                         double* __restrict__ ghw, double* __restrict__ ghb) {
     const int rows = 2 * ep + 1;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows * C) return;
     const int k = i / C, c = i % C;
     double s = 0.0;
-    for (int b = 0; b < nchunks; ++b) s += (double)part[((int64_t)b * rows + k) * C + c];
+    for (int b = 0; b < nchunks; ++b) s += part[((int64_t)b * rows + k) * C + c];
     if (k < 2 * ep) ghw[k * C + c] += s;
     else ghb[c] += s;
 }
@@ -131,7 +131,7 @@ __global__ void head_grad_reduce_kernel(int nchunks, int ep, int C, const float*
 template <int EP>
 __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int32_t* __restrict__ ptr,
                                                            const int32_t* __restrict__ slot,
-                                                           const float* __restrict__ dl,
+                                                           const double* __restrict__ dl,
                                                            const float* __restrict__ hw, int C, dgnn_frame dz) {
     constexpr int G = EP / 4 >= 32 ? 32 : EP / 4;  // lanes per vertex
     constexpr int V = EP / (4 * G);                // float4 per lane
@@ -143,28 +143,30 @@ __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int3
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t x = warp * RW + sub; x < n; x += nwarps * RW) {
-        float4 acc[V];
+        double acc[V][4];
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < V; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
         for (int e = ptr[x]; e < ptr[x + 1]; ++e) {
             const int s = slot[e];
             const int p = s >> 1, side = s & 1;
             for (int c = 0; c < C; ++c) {
-                const float d = dl[(int64_t)p * C + c];
+                const double d = dl[(int64_t)p * C + c];
 #pragma unroll
                 for (int i = 0; i < V; ++i) {
                     const int k = 4 * (gl + G * i);
                     const float* hr = hws + (side * EP + k) * C + c;
-                    acc[i].x = fmaf(d, hr[0], acc[i].x);
-                    acc[i].y = fmaf(d, hr[C], acc[i].y);
-                    acc[i].z = fmaf(d, hr[2 * C], acc[i].z);
-                    acc[i].w = fmaf(d, hr[3 * C], acc[i].w);
+                    acc[i][0] += d * (double)hr[0];
+                    acc[i][1] += d * (double)hr[C];
+                    acc[i][2] += d * (double)hr[2 * C];
+                    acc[i][3] += d * (double)hr[3 * C];
                 }
             }
         }
         float* out = frame_row<float>(dz, x);
 #pragma unroll
-        for (int i = 0; i < V; ++i) *reinterpret_cast<float4*>(out + 4 * (gl + G * i)) = acc[i];
+        for (int i = 0; i < V; ++i)
+            *reinterpret_cast<float4*>(out + 4 * (gl + G * i)) =
+                make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
     }
 }
 
@@ -200,7 +202,7 @@ __global__ void grads_gather_kernel(int64_t n, const double* __restrict__ gp, co
 }
 
 template <int EP>
-int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const float* dl, const float* hw, int C,
+int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const double* dl, const float* hw, int C,
                    dgnn_frame dz, cudaStream_t st) {
     constexpr int G = EP / 4 >= 32 ? 32 : EP / 4;
     constexpr int RW = 32 / G;
@@ -220,7 +222,7 @@ extern "C" {
 
 int dgnn_head_loss(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y, dgnn_frame z,
                    int32_t ep, int32_t c, const float* hw, const float* hb, double scale, double* loss_pp,
-                   int32_t n_partials, float* dlogits, void* stream) {
+                   int32_t n_partials, double* dlogits, void* stream) {
     DGNN_CHECK_ARG(c >= 2 && c <= kMaxClasses, "head_loss: classes outside [2, 8]");
     DGNN_CHECK_ARG(n_partials >= npairs, "head_loss: per-pair loss buffer too small");
     if (npairs == 0) return DGNN_OK;
@@ -245,11 +247,11 @@ int dgnn_head_predict(int64_t npairs, const int32_t* u, const int32_t* v, const 
 }
 
 size_t dgnn_head_grad_workspace(int32_t ep, int32_t c) {
-    return (size_t)(4 * kSMs) * (2 * ep + 1) * c * sizeof(float) + 256;
+    return (size_t)(4 * kSMs) * (2 * ep + 1) * c * sizeof(double) + 256;
 }
 
 int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_frame z, int32_t ep, int32_t c,
-                   const float* dlogits, double* ghw, double* ghb, void* ws, size_t ws_bytes, void* stream) {
+                   const double* dlogits, double* ghw, double* ghb, void* ws, size_t ws_bytes, void* stream) {
     DGNN_CHECK_ARG(c >= 2 && c <= kMaxClasses, "head_grad: classes outside [2, 8]");
     if (ws_bytes < dgnn_head_grad_workspace(ep, c)) {
         set_error("head_grad: workspace too small");
@@ -261,7 +263,7 @@ int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_fram
     nch = nch > 4 * kSMs ? 4 * kSMs : nch;
     const int64_t per = cdiv(npairs, nch);
     nch = cdiv(npairs, per);
-    float* part = reinterpret_cast<float*>(ws);
+    double* part = reinterpret_cast<double*>(ws);
     ::dgnn::note_launch();
     head_grad_partial_kernel<<<(unsigned)nch, 256, 0, st>>>(npairs, u, v, z, ep, c, dlogits, per, part);
     const int outs = (2 * ep + 1) * c;
@@ -270,7 +272,7 @@ int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_fram
     return launch_status("head_grad");
 }
 
-int dgnn_head_scatter(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot, const float* dlogits,
+int dgnn_head_scatter(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot, const double* dlogits,
                       const float* hw, int32_t ep, int32_t c, dgnn_frame dz, void* stream) {
     DGNN_CHECK_ARG(c >= 1 && c <= kMaxClasses, "head_scatter: classes outside [1, 8]");
     if (n == 0) return DGNN_OK;

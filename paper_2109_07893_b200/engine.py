@@ -187,7 +187,7 @@ class Rank:
             self.lab[key] = d
         mx = max([v["n"] for d in self.lab.values() for v in d.values()] + [1])
         self.loss_pp = torch.zeros(mx, dtype=torch.float64, device=self.dev)
-        self.dlogits = torch.zeros(mx * eng.cfg.classes, dtype=torch.float32, device=self.dev)
+        self.dlogits = torch.zeros(mx * eng.cfg.classes, dtype=torch.float64, device=self.dev)
 
     # ---------------------------------------------------------------- phases
     def reset_state(self):
