@@ -157,6 +157,27 @@ int dgnn_lstm_forward_step(int64_t rows, int32_t kx, int32_t hp, const float* x,
                            const float* bias, float* h_out, float* c_out, float* gates,
                            void* stream);
 
+/* Tensor-core operand image of a K-major weight matrix w (n x k, leading
+ * dimension ldw): per 16-wide K chunk, the tf32 hi and lo parts
+ * (hi = rna_tf32(w), lo = w - hi) as SWIZZLE_64B tiles, byte-identical to
+ * their shared-memory copies.  n must be a multiple of 16 (<= 512). */
+size_t dgnn_tc_weight_image_bytes(int32_t n, int32_t k);
+int dgnn_tc_weight_image(int32_t n, int32_t k, const float* w, int64_t ldw, float* img, void* stream);
+
+/* Self-test of the tcgen05 3xTF32 mainloop: d[m x n] = a[m x k] * w^T with
+ * w given by its image (n in {64, 128, 256}). */
+int dgnn_tc_gemm_test(int32_t m, int32_t n, int32_t k, const float* a, int64_t lda, const float* img,
+                      float* d, int64_t ldd, void* stream);
+
+/* K5 on tcgen05: same contract as dgnn_lstm_forward_step, the gate GEMM on
+ * the tensor cores (kind::tf32, 3xTF32 = fp32-accurate, accumulator in TMEM)
+ * with the cell update as the TMEM epilogue.  wimg = image of wcat^T
+ * (4hp x (kx+hp)) from dgnn_tc_weight_image. */
+int dgnn_lstm_forward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float* x, int64_t ldx,
+                              const float* h_prev, const float* c_prev, const float* wimg,
+                              const float* bias, float* h_out, float* c_out, float* gates,
+                              void* stream);
+
 /* K6 -- one reverse LSTM step (training.py:404-426):
  *   dh = dy + dh_in; do, dc, df, di, dg as the reference; dc_out = dc f
  *   dz = [di i(1-i) | df f(1-f) | do o(1-o) | dg (1-g^2)]  (written, 4hp wide)

@@ -249,7 +249,11 @@ class Rank:
         if not self.skip:
             self._mprod_forward(b, l)
             return
-        wcat, bias = eng.params.w(f"lstm{l}.wcat"), eng.params.w(f"lstm{l}.b")
+        if eng.tensor_cores:
+            fn, wop = "dgnn_lstm_forward_step_tc", eng.params.image(f"lstm{l}.fwd")
+        else:
+            fn, wop = "dgnn_lstm_forward_step", eng.params.w(f"lstm{l}.wcat")
+        bias = eng.params.w(f"lstm{l}.b")
         h_prev, c_prev = self.act[l]
         ho = Ly.ho
         for i in range(B):
@@ -257,8 +261,8 @@ class Rank:
             h_out = self.vm(self.Y_vm[l], ho, i)
             c_out = self.vm(self.C_vm[l], ho, i) if self.keep else self.vm(self.cbuf[l], ho, i % 2)
             gates = self.vm(self.G_vm[l], 4 * ho, i) if self.keep else None
-            call("dgnn_lstm_forward_step", NP, Ly.kx, ho, ptr(x), Ly.rw, ptr(h_prev), ptr(c_prev), ptr(wcat),
-                 ptr(bias), ptr(h_out), ptr(c_out), ptr(gates), st)
+            call(fn, NP, Ly.kx, ho, ptr(x), Ly.rw, ptr(h_prev), ptr(c_prev), ptr(wop), ptr(bias), ptr(h_out),
+                 ptr(c_out), ptr(gates), st)
             h_prev, c_prev = h_out, c_out
         if not self.keep:
             self.state[l][0].copy_(h_prev)
@@ -488,7 +492,10 @@ class Engine:
     """One epoch of snapshot-partitioned training on device (`dist.py:505-589`)."""
 
     def __init__(self, cfg, graph, workers: int, nblk: int, feats_host=None, m_matrix=None,
-                 resident: bool = False, fabric=None, device=None, encoding=None):
+                 resident: bool = False, fabric=None, device=None, encoding=None, tensor_cores: bool = True):
+        # tensor_cores: LSTM gate GEMMs on tcgen05 (3xTF32); False selects the
+        # SIMT fp32 kernels (kept as the measured baseline and for A/B tests)
+        self.tensor_cores = bool(tensor_cores)
         if cfg.architecture not in ("cd-gcn", "tm-gcn"):
             raise ConfigError(f"architecture {cfg.architecture!r} is outside this package's hot path")
         self.cfg = cfg

@@ -258,12 +258,33 @@ def _lstm_weights(wx, wh, b, dev):
     return H, hp, kx, torch.from_numpy(wc).to(dev), torch.from_numpy(wct).to(dev), torch.from_numpy(bb).to(dev)
 
 
-def lstm_block_forward(cell, state_in, ts, xs: dict):
+def tc_gemm(a: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """a @ w.T on the tcgen05 3xTF32 mainloop (self-test of the tensor-core
+    path); a: m x k, w: n x k with n in {64, 128, 256}, k % 4 == 0."""
+    dev = _dev()
+    m, k = a.shape
+    n = w.shape[0]
+    ad = torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev)
+    wd = torch.from_numpy(np.ascontiguousarray(w, np.float32)).to(dev)
+    img = torch.zeros(query("dgnn_tc_weight_image_bytes", n, k) // 4, dtype=torch.float32, device=dev)
+    st = _lib.stream_handle()
+    call("dgnn_tc_weight_image", n, k, ptr(wd), k, ptr(img), st)
+    out = torch.zeros(m, n, dtype=torch.float32, device=dev)
+    call("dgnn_tc_gemm_test", m, n, k, ptr(ad), k, ptr(img), ptr(out), n, st)
+    return out.double().cpu().numpy()
+
+
+def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True):
     """fp32 device LSTM over a block (training.py:370-391).  Returns
     (ys, (h, c), cache) with a device cache for lstm_block_backward."""
     dev = _dev()
     wx, wh, b = (np.asarray(cell.wx), np.asarray(cell.wh), np.asarray(cell.b))
     H, hp, kx, wc, wct, bb = _lstm_weights(wx, wh, b, dev)
+    img = None
+    if tensor_cores:
+        img = torch.zeros(query("dgnn_tc_weight_image_bytes", 4 * hp, kx + hp) // 4, dtype=torch.float32,
+                          device=dev)
+        call("dgnn_tc_weight_image", 4 * hp, kx + hp, ptr(wct), kx + hp, ptr(img), _lib.stream_handle())
     h0, c0 = state_in
     rows = h0.shape[0]
     st = _lib.stream_handle()
@@ -277,8 +298,12 @@ def lstm_block_forward(cell, state_in, ts, xs: dict):
         hn = torch.zeros(rows, hp, device=dev)
         cn = torch.zeros(rows, hp, device=dev)
         g = torch.zeros(rows, 4 * hp, device=dev)
-        call("dgnn_lstm_forward_step", rows, kx, hp, ptr(x), kx, ptr(h), ptr(c), ptr(wc), ptr(bb), ptr(hn),
-             ptr(cn), ptr(g), st)
+        if img is not None:
+            call("dgnn_lstm_forward_step_tc", rows, kx, hp, ptr(x), kx, ptr(h), ptr(c), ptr(img), ptr(bb),
+                 ptr(hn), ptr(cn), ptr(g), st)
+        else:
+            call("dgnn_lstm_forward_step", rows, kx, hp, ptr(x), kx, ptr(h), ptr(c), ptr(wc), ptr(bb), ptr(hn),
+                 ptr(cn), ptr(g), st)
         cache["x"].append(x)
         cache["h"].append(hn)
         cache["c"].append(cn)

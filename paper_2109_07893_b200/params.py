@@ -296,6 +296,15 @@ class DeviceParams:
         self.pos0 = torch.from_numpy(layout.pos0).to(dev)
         self.pos1 = torch.from_numpy(layout.pos1).to(dev)
         self.step = 0
+        # tensor-core operand images of the LSTM weights (tf32 hi/lo, swizzled)
+        self.images = {}
+        for l, L in enumerate(layout.layers):
+            if L.skip:
+                nbytes = _lib.query("dgnn_tc_weight_image_bytes", 4 * L.ho, L.kx + L.ho)
+                self.images[f"lstm{l}.fwd"] = torch.zeros(nbytes // 4, dtype=torch.float32, device=dev)
+
+    def image(self, name: str) -> torch.Tensor:
+        return self.images[name]
 
     def load(self, params: dict, stream=None):
         flat = torch.from_numpy(self.layout.flatten(params))
@@ -303,8 +312,14 @@ class DeviceParams:
         self.sync_image(stream)
 
     def sync_image(self, stream=None):
+        sh = _lib.stream_handle(stream)
         call("dgnn_params_to_device", self.layout.count, ptr(self.p64), ptr(self.pos0), ptr(self.pos1),
-             ptr(self.w32), _lib.stream_handle(stream))
+             ptr(self.w32), sh)
+        for l, L in enumerate(self.layout.layers):
+            if L.skip:
+                K = L.kx + L.ho
+                call("dgnn_tc_weight_image", 4 * L.ho, K, ptr(self.w(f"lstm{l}.wcat_t")), K,
+                     ptr(self.images[f"lstm{l}.fwd"]), sh)
 
     def w(self, name: str) -> torch.Tensor:
         return self.layout.block(self.w32, name)

@@ -219,3 +219,40 @@ def test_lstm_kernels_wide_vs_oracle(oracle, H):
         assert ok, (worst, nbad)
     for t in ts:
         assert guarded_close(dxs[t], rdxs[t], RTOL)[0]
+
+
+@pytest.mark.parametrize("n", [64, 128, 256])
+@pytest.mark.parametrize("m,k", [(128, 16), (300, 132), (1000, 192)])
+def test_tcgen05_3xtf32_gemm_is_fp32_accurate(n, m, k):
+    """tcgen05 kind::tf32 mainloop with the 3xTF32 split: descriptor /
+    swizzle / TMEM plumbing check against an fp64 product."""
+    from paper_2109_07893_b200.ops import tc_gemm
+    rng = np.random.default_rng(n + m + k)
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    w = rng.standard_normal((n, k)).astype(np.float32)
+    got = tc_gemm(a, w)
+    ref = a.astype(np.float64) @ w.astype(np.float64).T
+    err = np.abs(got - ref) / (np.abs(a).astype(np.float64) @ np.abs(w).astype(np.float64).T)
+    assert err.max() < 2e-6, err.max()
+
+
+@pytest.mark.parametrize("H", [16, 32, 64, 128])
+def test_lstm_forward_tensor_cores_vs_oracle(oracle, H):
+    rng = np.random.default_rng(10 + H)
+    rows, fin = 777, 2 * H + 2
+
+    class Cell:
+        wx = rng.uniform(-0.3, 0.3, (fin, 4 * H))
+        wh = rng.uniform(-0.3, 0.3, (H, 4 * H))
+        b = rng.uniform(-0.1, 0.1, 4 * H)
+
+    ts = [0, 1, 2]
+    xs = {t: np.maximum(rng.standard_normal((rows, fin)), 0) for t in ts}
+    st = (rng.standard_normal((rows, H)) * 0.2, rng.standard_normal((rows, H)) * 0.2)
+    ys, (h, c), _ = pk.lstm_block_forward(Cell, st, ts, xs, tensor_cores=True)
+    ys2, _, _ = pk.lstm_block_forward(Cell, st, ts, xs, tensor_cores=False)
+    rys, (rh, rc), _ = oracle.lstm_fwd(Cell.wx, Cell.wh, Cell.b, st, ts, xs)
+    for t in ts:
+        assert np.abs(ys[t] - rys[t]).max() < 5e-6
+        assert np.abs(ys[t] - ys2[t]).max() < 5e-6
+    assert np.abs(c - rc).max() < 5e-6
