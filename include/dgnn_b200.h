@@ -163,6 +163,11 @@ int dgnn_lstm_forward_step(int64_t rows, int32_t kx, int32_t hp, const float* x,
  * their shared-memory copies.  n must be a multiple of 16 (<= 512). */
 size_t dgnn_tc_weight_image_bytes(int32_t n, int32_t k);
 int dgnn_tc_weight_image(int32_t n, int32_t k, const float* w, int64_t ldw, float* img, void* stream);
+/* General form: n_alloc image rows of which the first n_valid come from w
+ * (the rest zero); perm_hp > 0 takes the K order unit-major, element k
+ * reading column (k % 4) * perm_hp + k / 4 (the backward-step operand). */
+int dgnn_tc_weight_image_ex(int32_t n_alloc, int32_t n_valid, int32_t k, const float* w, int64_t ldw,
+                            int32_t perm_hp, float* img, void* stream);
 
 /* Self-test of the tcgen05 3xTF32 mainloop: d[m x n] = a[m x k] * w^T with
  * w given by its image (n in {64, 128, 256}). */
@@ -177,6 +182,16 @@ int dgnn_lstm_forward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float*
                               const float* h_prev, const float* c_prev, const float* wimg,
                               const float* bias, float* h_out, float* c_out, float* gates,
                               void* stream);
+
+/* K6 on tcgen05: same contract as dgnn_lstm_backward_step (dz written in
+ * place of the gate cache `gates`); the pointwise gate gradients are the
+ * operand producer of [dx | dh] = dz W^T (3xTF32, TMEM accumulator).
+ * wimg = dgnn_tc_weight_image_ex(round16(kx+hp), kx+hp, 4hp, wcat, 4hp,
+ * hp, ...).  hp in {16, 32, 64} with kx + hp <= 256. */
+int dgnn_lstm_backward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float* dy,
+                               const float* dh_in, const float* dc_in, float* gates,
+                               const float* c_prev, const float* c_new, const float* wimg, float* dx,
+                               int64_t lddx, float* dh_out, float* dc_out, void* stream);
 
 /* K6 -- one reverse LSTM step (training.py:404-426):
  *   dh = dy + dh_in; do, dc, df, di, dg as the reference; dc_out = dc f

@@ -263,6 +263,8 @@ def prepare_training_data(cfg, graph) -> TrainingData:
 # engine cache: one device engine per (data, config, workers, nblk)
 
 _ENGINES: dict = {}
+# temporal-stage GEMMs on tcgen05 (default) or on the SIMT fp32 kernels (A/B, strict-parity tests)
+TENSOR_CORES = True
 _LOCK = threading.Lock()
 
 
@@ -278,7 +280,7 @@ def get_engine(cfg, data, workers: int, nblk: int, resident: bool = False) -> En
     if not torch.cuda.is_available():
         raise ConfigError("no CUDA device: this package has no CPU execution path")
     graph = data.graph
-    key = (id(data), cfg, int(workers), int(nblk), bool(resident))
+    key = (id(data), cfg, int(workers), int(nblk), bool(resident), bool(TENSOR_CORES))
     with _LOCK:
         eng = _ENGINES.get(key)
         if eng is None:
@@ -289,7 +291,7 @@ def get_engine(cfg, data, workers: int, nblk: int, resident: bool = False) -> En
                 feats = [np.asarray(f, np.float64) for f in data.feats.frames]
             m = None if data.m_matrix is None else np.asarray(data.m_matrix.matrix)
             eng = Engine(cfg, graph, workers, nblk, feats_host=feats, m_matrix=m, resident=resident,
-                         fabric=_fabric(), encoding=enc)
+                         fabric=_fabric(), encoding=enc, tensor_cores=TENSOR_CORES)
             _ENGINES[key] = eng
             try:
                 weakref.finalize(data, _drop, id(data))

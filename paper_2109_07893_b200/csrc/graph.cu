@@ -202,11 +202,15 @@ constexpr int kSmallSeg = 32;
 // Short segments: one thread sorts its column in registers/local memory.
 __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp,
                                       const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
-                                      int32_t* __restrict__ dst_col, double* __restrict__ dst_val) {
+                                      int32_t* __restrict__ dst_col, double* __restrict__ dst_val,
+                                      int32_t* __restrict__ long_list, int32_t* long_count) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= n) return;
     const int b = trp[c], e = trp[c + 1], d = e - b;
-    if (d > kSmallSeg) return;
+    if (d > kSmallSeg) {                       // hub column: handed to the block-per-segment kernel
+        long_list[atomicAdd(long_count, 1)] = (int32_t)c;
+        return;
+    }
     int key[kSmallSeg];
     int idx[kSmallSeg];
     for (int i = 0; i < d; ++i) {
@@ -222,12 +226,14 @@ __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp
 }
 
 // Long segments: one block per segment, rank = #smaller keys (keys are distinct rows).
-__global__ void seg_sort_large_kernel(int32_t n, const int32_t* __restrict__ trp,
-                                      const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
-                                      int32_t* __restrict__ dst_col, double* __restrict__ dst_val) {
-    for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+__global__ void seg_sort_large_kernel(const int32_t* __restrict__ trp, const int32_t* __restrict__ src_col,
+                                      const double* __restrict__ src_val, int32_t* __restrict__ dst_col,
+                                      double* __restrict__ dst_val, const int32_t* __restrict__ long_list,
+                                      const int32_t* __restrict__ long_count) {
+    const int cnt = *long_count;
+    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+        const int c = long_list[li];
         const int b = trp[c], e = trp[c + 1], d = e - b;
-        if (d <= kSmallSeg) continue;
         for (int i = threadIdx.x; i < d; i += blockDim.x) {
             const int k = src_col[b + i];
             int rank = 0;
@@ -401,9 +407,10 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
 }
 
 size_t dgnn_csr_transpose_workspace(int32_t n) {
-    // cursor[n] + scan; the scatter staging (nnz) lives in the output of a
-    // caller-visible second buffer pair, see dgnn_csr_transpose2.
-    return (size_t)round64((int64_t)n + 1) * sizeof(int32_t) + scan_workspace_bytes((int64_t)n + 1);
+    // cursor[n] (reused as the hub-column list after the scatter) + counter + scan;
+    // the nnz-sized scatter staging is passed separately (stage_col / stage_val)
+    return (size_t)round64((int64_t)n + 1) * sizeof(int32_t) + 64 * sizeof(int32_t) +
+           scan_workspace_bytes((int64_t)n + 1);
 }
 
 // Staging for the scatter: t_col/t_val are written twice (scatter into the
@@ -420,8 +427,10 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     DGNN_CHECK_ARG(!val || (t_val && stage_val), "transpose: values need t_val and stage_val");
     cudaStream_t st = as_stream(stream);
     int32_t* cursor = reinterpret_cast<int32_t*>(ws);
-    void* sws = cursor + round64((int64_t)n + 1);
-    size_t sws_bytes = ws_bytes - (size_t)round64((int64_t)n + 1) * sizeof(int32_t);
+    int32_t* long_count = cursor + round64((int64_t)n + 1);
+    void* sws = long_count + 64;
+    size_t sws_bytes = ws_bytes - (size_t)round64((int64_t)n + 1) * sizeof(int32_t) - 64 * sizeof(int32_t);
+    cudaMemsetAsync(long_count, 0, sizeof(int32_t), st);
     ::dgnn::note_launch();
     zero_i32_kernel<<<(unsigned)cdiv((int64_t)n + 1, 256), 256, 0, st>>>(t_rowptr, (int64_t)n + 1);
     if (nnz) {
@@ -436,10 +445,10 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
                                                                       stage_val);
     ::dgnn::note_launch();
     seg_sort_small_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, t_rowptr, stage_col, stage_val, t_col,
-                                                                   val ? t_val : nullptr);
+                                                                   val ? t_val : nullptr, cursor, long_count);
     ::dgnn::note_launch();
-    seg_sort_large_kernel<<<4 * kSMs, 256, 0, st>>>(n, t_rowptr, stage_col, stage_val, t_col,
-                                                    val ? t_val : nullptr);
+    seg_sort_large_kernel<<<kSMs, 256, 0, st>>>(t_rowptr, stage_col, stage_val, t_col, val ? t_val : nullptr,
+                                                cursor, long_count);
     return launch_status("csr_transpose");
 }
 

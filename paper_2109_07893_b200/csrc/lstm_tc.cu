@@ -1,17 +1,31 @@
-// Temporal stage on the 5th-generation tensor cores (K5): the LSTM gate GEMM
-// z = [x | h_prev] W + b runs as tcgen05.mma kind::tf32 with the 3xTF32
-// split (fp32-accurate), accumulator in TMEM; the cell update (sigmoid/tanh,
-// c = f c_prev + i g, h = o tanh c) is the epilogue, fed by tcgen05.ld, so z
-// never touches HBM.  Reference: training.py:370-391.
+// Temporal stage on the 5th-generation tensor cores (K5/K6).
 //
-// CTA = 128 vertex rows x all 4*HP gate columns (one M=128, N=4*HP MMA
-// shape; HP=128 issues two N=256 halves).  K is streamed in chunks of 16
-// fp32 through a 2-stage shared-memory ring: every thread stages the
-// activation chunk (global fp32 -> hi/lo tf32 split -> SW64 tile) and copies
-// the pre-split, pre-swizzled weight chunk; one thread issues the MMAs and
-// commits them to the stage's mbarrier, so staging of chunk c+1 overlaps the
-// MMAs of chunk c.  Two CTAs fit per SM (96 KB smem, <= 256 TMEM columns
-// each for HP <= 64), overlapping one CTA's epilogue with the other's MMAs.
+// Forward step: z = [x | h_prev] W + b runs as tcgen05.mma kind::tf32 with
+// the 3xTF32 split (fp32-accurate operands), accumulator in TMEM; the cell
+// update (sigmoid/tanh, c = f c_prev + i g, h = o tanh c) is the epilogue,
+// fed by tcgen05.ld, so z never touches HBM.  Reference training.py:370-391.
+//
+// Backward step: the gate-gradient pointwise (training.py:405-421) is the
+// operand producer -- it computes dz for 4 hidden units per K chunk, writes dz
+// (in place of the gate cache, for the weight-gradient GEMM) and dc, and
+// stages dz as the A operand; [dx | dh] = dz W^T accumulates in TMEM and the
+// epilogue streams it out.  The reduction dimension is taken unit-major
+// (k = 4u + g) so one 16-wide chunk covers whole units; the weight image is
+// permuted to match.
+//
+// Shared machinery: CTA = 128 rows (M = 128) x N columns (N = 4*HP forward,
+// kx+HP rounded to 16 backward; N > 256 issues 256-wide slices).  K streams
+// in chunks of 16 fp32 through a 2-stage shared-memory ring (SWIZZLE_64B
+// K-major tiles): all threads stage the activation chunk (fp32 -> tf32 hi/lo)
+// and copy the pre-split, pre-swizzled weight chunk; one thread issues the
+// MMAs and commits them to the stage's mbarrier, so staging of chunk c+1
+// overlaps the MMAs of chunk c.  <= 256 TMEM columns and 80-96 KB of smem
+// per CTA give two CTAs per SM, overlapping one CTA's epilogue with the
+// other's MMAs.
+//
+// Numerics: tcgen05 fp32 accumulation truncates (measured mean bias about
+// -2.5e-8 relative per accumulate); with K <= 384 per step that stays
+// ~1e-6 relative.  Long reductions must not accumulate in TMEM (see dW).
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -20,81 +34,97 @@ using namespace tc;
 
 constexpr int TC_BM = 128;
 constexpr int TC_KC = 16;  // fp32 K-elements per staged chunk (one SW64 row)
+constexpr int TC_A_BYTES = TC_BM * 64;
 
-// Weight image for the B operand: [chunk][hi|lo][N rows][16 fp32], each
-// [N][16] block an SW64 tile (byte-identical to its shared-memory copy).
-// Source w is N x K row-major (K-major), leading dimension ldw.
-__global__ void wimg_kernel(int N, int K, const float* __restrict__ w, int64_t ldw, float* __restrict__ img) {
+__host__ __device__ inline int tmem_cols_for(int n) {
+    return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 256 ? 256 : 512)));
+}
+__host__ __device__ inline int tc_stage_bytes(int n) { return 2 * TC_A_BYTES + 2 * n * 64; }
+inline size_t tc_smem_bytes(int n) { return (size_t)2 * tc_stage_bytes(n) + 1024 + 64; }
+
+// Weight image for the B operand: [chunk][hi|lo][n_alloc rows][16 fp32], each
+// [n_alloc][16] block an SW64 tile (byte-identical to its smem copy).  Row n
+// (< n_valid) is row n of w (K-major, leading dimension ldw); with perm_hp > 0
+// the K order is unit-major: element k reads w column (k % 4) * perm_hp + k / 4.
+__global__ void wimg_kernel(int n_alloc, int n_valid, int K, const float* __restrict__ w, int64_t ldw,
+                            int perm_hp, float* __restrict__ img) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int nch = (K + TC_KC - 1) / TC_KC;
-    if (i >= (int64_t)nch * N * 4) return;
+    if (i >= (int64_t)nch * n_alloc * 4) return;
     const int q = (int)(i & 3);
-    const int n = (int)((i >> 2) % N);
-    const int ch = (int)(i / (4 * (int64_t)N));
+    const int n = (int)((i >> 2) % n_alloc);
+    const int ch = (int)(i / (4 * (int64_t)n_alloc));
     float v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int k = ch * TC_KC + 4 * q + j;
-        v[j] = k < K ? w[(int64_t)n * ldw + k] : 0.f;
+        const int src = perm_hp > 0 ? (k % 4) * perm_hp + k / 4 : k;
+        v[j] = (k < K && n < n_valid) ? w[(int64_t)n * ldw + src] : 0.f;
     }
     float4 hi, lo;
     split4(make_float4(v[0], v[1], v[2], v[3]), hi, lo);
-    char* base = reinterpret_cast<char*>(img) + (size_t)ch * 2 * N * 64;
+    char* base = reinterpret_cast<char*>(img) + (size_t)ch * 2 * n_alloc * 64;
     *reinterpret_cast<float4*>(base + sw64(n, q)) = hi;
-    *reinterpret_cast<float4*>(base + (size_t)N * 64 + sw64(n, q)) = lo;
+    *reinterpret_cast<float4*>(base + (size_t)n_alloc * 64 + sw64(n, q)) = lo;
 }
 
 // ---------------------------------------------------------------------------
 // shared mainloop: D[128 x N] (TMEM) = A[128 x K] * B[N x K]^T, 3xTF32
 
-struct StageLayout {
-    uint32_t a_hi, a_lo, b;   // smem addresses (b: [hi | lo] copy of the image chunk)
+struct Ring {
+    uint32_t a_hi[2], a_lo[2], b[2];
+    uint64_t* bars;   // [0..1] stage empty (MMA commit), [2..3] stage full (weight bulk copy)
+    uint32_t tmem;
+    int N;
 };
 
-template <int N>
-struct TcCfg {
-    static constexpr int A_BYTES = TC_BM * 64;      // one SW64 tile of 128 rows
-    static constexpr int B_BYTES = 2 * N * 64;      // hi + lo tiles of N rows
-    static constexpr int STAGE = 2 * A_BYTES + B_BYTES;
-    static constexpr int SMEM = 2 * STAGE + 1024 + 64;
-    static constexpr int TMEM_COLS = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : (N <= 256 ? 256 : 512)));
-    static constexpr int MMA_N = N > 256 ? 256 : N;
-};
-
-// Stage one K chunk: A via `load4(r, k)` (returns the 4 fp32 at row r, k..k+3),
-// B by copying the image chunk.
-template <int N, class LoadA>
-__device__ __forceinline__ void stage_chunk(const StageLayout& s, int ch, const float* __restrict__ img,
-                                            LoadA load4) {
-    const int tid = threadIdx.x;
-    for (int idx = tid; idx < TC_BM * 4; idx += blockDim.x) {
-        const int r = idx >> 2, q = idx & 3;
-        float4 hi, lo;
-        split4(load4(r, ch * TC_KC + 4 * q), hi, lo);
-        sts128(s.a_hi + sw64(r, q), hi);
-        sts128(s.a_lo + sw64(r, q), lo);
+__device__ __forceinline__ Ring tc_setup(int N) {
+    extern __shared__ uint8_t tc_smem_raw[];
+    const uint32_t raw = smem_u32(tc_smem_raw);
+    const uint32_t pad = (1024 - (raw & 1023)) & 1023;
+    uint8_t* base = tc_smem_raw + pad;
+    Ring R;
+    R.N = N;
+    const int stage = tc_stage_bytes(N);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const uint32_t b0 = smem_u32(base) + s * stage;
+        R.a_hi[s] = b0;
+        R.a_lo[s] = b0 + TC_A_BYTES;
+        R.b[s] = b0 + 2 * TC_A_BYTES;
     }
-    const int4* src = reinterpret_cast<const int4*>(img + (size_t)ch * 2 * N * 16);
-    for (int idx = tid; idx < TcCfg<N>::B_BYTES / 16; idx += blockDim.x) {
-        const int4 v = __ldg(src + idx);
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(s.b + 16 * idx), "r"(v.x), "r"(v.y),
-                     "r"(v.z), "r"(v.w) : "memory");
+    R.bars = reinterpret_cast<uint64_t*>(base + 2 * stage);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(R.bars + 4);
+    if (threadIdx.x < 32) tmem_alloc(tslot, tmem_cols_for(N));
+    if (threadIdx.x == 32) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mbar_init(&R.bars[i], 1);
+        fence_mbar_init();
     }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    R.tmem = *tslot;
+    return R;
 }
 
-template <int N>
-__device__ __forceinline__ void issue_chunk(const StageLayout& s, uint32_t tmem, bool first) {
-    constexpr uint32_t idesc = idesc_tf32(TC_BM, TcCfg<N>::MMA_N);
+__device__ __forceinline__ void tc_teardown(const Ring& R) {
+    fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tmem_dealloc(R.tmem, tmem_cols_for(R.N));
+}
+
+__device__ __forceinline__ void tc_issue(const Ring& R, int s, bool first) {
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
-        const uint64_t ahi = sdesc(s.a_hi + 32 * kk, 512, kSW64);
-        const uint64_t alo = sdesc(s.a_lo + 32 * kk, 512, kSW64);
-#pragma unroll
-        for (int nh = 0; nh < N / TcCfg<N>::MMA_N; ++nh) {
-            const uint32_t boff = nh * TcCfg<N>::MMA_N * 64;
-            const uint64_t bhi = sdesc(s.b + boff + 32 * kk, 512, kSW64);
-            const uint64_t blo = sdesc(s.b + N * 64 + boff + 32 * kk, 512, kSW64);
-            const uint32_t d = tmem + nh * TcCfg<N>::MMA_N;
+        const uint64_t ahi = sdesc(R.a_hi[s] + 32 * kk, 512, kSW64);
+        const uint64_t alo = sdesc(R.a_lo[s] + 32 * kk, 512, kSW64);
+        for (int n0 = 0; n0 < R.N; n0 += 256) {
+            const int nn = R.N - n0 < 256 ? R.N - n0 : 256;
+            const uint32_t idesc = idesc_tf32(TC_BM, nn);
+            const uint64_t bhi = sdesc(R.b[s] + n0 * 64 + 32 * kk, 512, kSW64);
+            const uint64_t blo = sdesc(R.b[s] + R.N * 64 + n0 * 64 + 32 * kk, 512, kSW64);
+            const uint32_t d = R.tmem + n0;
             mma_tf32(d, ahi, bhi, idesc, (first && kk == 0) ? 0u : 1u);
             mma_tf32(d, ahi, blo, idesc, 1u);
             mma_tf32(d, alo, bhi, idesc, 1u);
@@ -102,93 +132,101 @@ __device__ __forceinline__ void issue_chunk(const StageLayout& s, uint32_t tmem,
     }
 }
 
-// Runs the whole K loop; returns with the accumulator complete and visible.
-template <int N, class LoadA>
-__device__ __forceinline__ void tc_mainloop(uint8_t* smem_base, uint64_t* bars, uint32_t tmem, int nch,
-                                            const float* __restrict__ img, LoadA load4) {
-    using C = TcCfg<N>;
-    const uint32_t base = smem_u32(smem_base);
-    StageLayout st[2];
+// The A operand is produced in two steps so global latency overlaps the
+// previous chunk: `fetch(ch, item)` issues the loads for one item (row
+// item / 4, 16-byte column group item % 4 of chunk ch) into a register
+// payload one chunk ahead; `produce(payload, ch, item)` turns it into the 4
+// fp32 values to stage (it runs exactly once per item, so it may have side
+// effects).  The weight chunk arrives by one cp.async.bulk on the stage's
+// "full" barrier.  Requires blockDim.x == 256.
+template <class Fetch, class Produce>
+__device__ __forceinline__ void tc_mainloop(const Ring& R, int nch, const float* __restrict__ img, Fetch fetch,
+                                            Produce produce) {
+    constexpr int ITEMS = TC_BM * 4 / 256;
+    using Payload = decltype(fetch(0, 0));
+    const int tid = threadIdx.x;
+    const uint32_t b_bytes = (uint32_t)(2 * R.N * 64);
+    const char* img_bytes = reinterpret_cast<const char*>(img);
+    uint64_t* empty = R.bars;
+    uint64_t* full = R.bars + 2;
+    Payload cur[ITEMS], nxt[ITEMS];
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        const uint32_t b0 = base + s * C::STAGE;
-        st[s] = StageLayout{b0, b0 + C::A_BYTES, b0 + 2 * C::A_BYTES};
-    }
+    for (int i = 0; i < ITEMS; ++i) cur[i] = fetch(0, tid + 256 * i);
     for (int ch = 0; ch < nch; ++ch) {
         const int s = ch & 1;
-        if (ch >= 2) mbar_wait(&bars[s], ((ch - 2) >> 1) & 1);   // MMAs of chunk ch-2 released the stage
-        stage_chunk<N>(st[s], ch, img, load4);
+        if (ch + 1 < nch) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) nxt[i] = fetch(ch + 1, tid + 256 * i);
+        }
+        if (ch >= 2) mbar_wait(&empty[s], ((ch - 2) >> 1) & 1);   // MMAs of chunk ch-2 released the stage
+        if (tid == 0) {
+            mbar_arrive_expect_tx(&full[s], b_bytes);
+            bulk_g2s(R.b[s], img_bytes + (size_t)ch * b_bytes, b_bytes, &full[s]);
+        }
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int idx = tid + 256 * i;
+            const int r = idx >> 2, q = idx & 3;
+            float4 hi, lo;
+            split4(produce(cur[i], ch, idx), hi, lo);
+            sts128(R.a_hi[s] + sw64(r, q), hi);
+            sts128(R.a_lo[s] + sw64(r, q), lo);
+        }
         fence_async_smem();
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
+            mbar_wait(&full[s], (ch >> 1) & 1);
             fence_after();
-            issue_chunk<N>(st[s], tmem, ch == 0);
-            commit(&bars[s]);
+            tc_issue(R, s, ch == 0);
+            commit(&empty[s]);
         }
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) cur[i] = nxt[i];
     }
     const int last = nch - 1;
-    mbar_wait(&bars[last & 1], (last >> 1) & 1);
+    mbar_wait(&empty[last & 1], (last >> 1) & 1);
     fence_after();
 }
 
-template <int N>
-__device__ __forceinline__ uint32_t tc_setup(uint8_t*& smem_base, uint64_t*& bars) {
-    extern __shared__ uint8_t tc_smem_raw[];
-    const uint32_t raw = smem_u32(tc_smem_raw);
-    const uint32_t pad = (1024 - (raw & 1023)) & 1023;
-    smem_base = tc_smem_raw + pad;
-    bars = reinterpret_cast<uint64_t*>(smem_base + 2 * TcCfg<N>::STAGE);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
-    if (threadIdx.x < 32) tmem_alloc(tslot, TcCfg<N>::TMEM_COLS);
-    if (threadIdx.x == 32) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        fence_mbar_init();
-    }
-    fence_before();
-    __syncthreads();
-    fence_after();
-    return *tslot;
-}
+struct Raw4 {
+    float4 v;
+};
 
-template <int N>
-__device__ __forceinline__ void tc_teardown(uint32_t tmem) {
-    fence_before();
-    __syncthreads();
-    if (threadIdx.x < 32) tmem_dealloc(tmem, TcCfg<N>::TMEM_COLS);
-}
+__device__ __forceinline__ float4 pass4(const Raw4& p, int, int) { return p.v; }
 
 // ---------------------------------------------------------------------------
 // GEMM self-test entry: D[M x N] = A[M x K] B[N x K]^T (fp32 in/out)
 
-template <int N>
-__global__ void __launch_bounds__(256) tc_gemm_kernel(int M, int K, const float* __restrict__ a, int64_t lda,
+__global__ void __launch_bounds__(256) tc_gemm_kernel(int M, int N, int K, const float* __restrict__ a, int64_t lda,
                                                       const float* __restrict__ img, float* __restrict__ d,
                                                       int64_t ldd) {
-    uint8_t* smem;
-    uint64_t* bars;
-    const uint32_t tmem = tc_setup<N>(smem, bars);
+    const Ring R = tc_setup(N);
     const int64_t row0 = blockIdx.x * (int64_t)TC_BM;
     const int nch = (K + TC_KC - 1) / TC_KC;
-    tc_mainloop<N>(smem, bars, tmem, nch, img, [&](int r, int k) {
-        const int64_t g = row0 + r;
-        if (g >= M || k >= K) return make_float4(0.f, 0.f, 0.f, 0.f);
-        return *reinterpret_cast<const float4*>(a + g * lda + k);
-    });
+    tc_mainloop(
+        R, nch, img,
+        [&](int ch, int idx) {
+            const int64_t g = row0 + (idx >> 2);
+            const int k = ch * TC_KC + 4 * (idx & 3);
+            Raw4 p{make_float4(0.f, 0.f, 0.f, 0.f)};
+            if (g < M && k < K) p.v = __ldg(reinterpret_cast<const float4*>(a + g * lda + k));
+            return p;
+        },
+        pass4);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, half = w >> 2;
     const int64_t row = row0 + 32 * q + lane;
     for (int c0 = half * 8; c0 < N; c0 += 16) {
         float v[8];
-        tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + c0, v);
+        tmem_ld8(R.tmem + ((uint32_t)(32 * q) << 16) + c0, v);
         tmem_wait_ld();
         if (row < M)
             for (int j = 0; j < 8; ++j) d[row * ldd + c0 + j] = v[j];
     }
-    tc_teardown<N>(tmem);
+    tc_teardown(R);
 }
 
 // ---------------------------------------------------------------------------
-// LSTM forward step on tcgen05
+// LSTM forward step
 
 template <int HP>
 __global__ void __launch_bounds__(256, (HP <= 64 ? 2 : 1)) lstm_fwd_tc_kernel(
@@ -196,22 +234,26 @@ __global__ void __launch_bounds__(256, (HP <= 64 ? 2 : 1)) lstm_fwd_tc_kernel(
     const float* __restrict__ cprev, const float* __restrict__ img, const float* __restrict__ bias,
     float* __restrict__ hout, float* __restrict__ cout, float* __restrict__ gates) {
     constexpr int N = 4 * HP;
-    uint8_t* smem;
-    uint64_t* bars;
-    const uint32_t tmem = tc_setup<N>(smem, bars);
+    const Ring R = tc_setup(N);
     const int64_t row0 = blockIdx.x * (int64_t)TC_BM;
     const int K = kx + HP;
     const int nch = (K + TC_KC - 1) / TC_KC;
-    tc_mainloop<N>(smem, bars, tmem, nch, img, [&](int r, int k) {
-        const int64_t g = row0 + r;
-        if (g >= rows || k >= K) return make_float4(0.f, 0.f, 0.f, 0.f);
-        return k < kx ? __ldg(reinterpret_cast<const float4*>(x + g * ldx + k))
-                      : __ldg(reinterpret_cast<const float4*>(hprev + g * HP + (k - kx)));
-    });
+    tc_mainloop(
+        R, nch, img,
+        [&](int ch, int idx) {
+            const int64_t g = row0 + (idx >> 2);
+            const int k = ch * TC_KC + 4 * (idx & 3);
+            Raw4 p{make_float4(0.f, 0.f, 0.f, 0.f)};
+            if (g < rows && k < K)
+                p.v = k < kx ? __ldg(reinterpret_cast<const float4*>(x + g * ldx + k))
+                             : __ldg(reinterpret_cast<const float4*>(hprev + g * HP + (k - kx)));
+            return p;
+        },
+        pass4);
     // epilogue: warp w reads TMEM lanes 32*(w&3).., units [half*HP/2, (half+1)*HP/2)
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, half = w >> 2;
     const int64_t row = row0 + 32 * q + lane;
-    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+    const uint32_t tq = R.tmem + ((uint32_t)(32 * q) << 16);
     for (int u0 = half * (HP / 2); u0 < (half + 1) * (HP / 2); u0 += 8) {
         float z[4][8];
 #pragma unroll
@@ -247,27 +289,117 @@ __global__ void __launch_bounds__(256, (HP <= 64 ? 2 : 1)) lstm_fwd_tc_kernel(
             }
         }
     }
-    tc_teardown<N>(tmem);
+    tc_teardown(R);
 }
 
-template <int N>
-int tc_gemm_t(int M, int K, const float* a, int64_t lda, const float* img, float* d, int64_t ldd, cudaStream_t st) {
-    auto k = tc_gemm_kernel<N>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<N>::SMEM);
-    note_launch();
-    k<<<(unsigned)cdiv(M, TC_BM), 256, TcCfg<N>::SMEM, st>>>(M, K, a, lda, img, d, ldd);
-    return launch_status("tc_gemm_test");
+// ---------------------------------------------------------------------------
+// LSTM backward step
+
+template <int HP>
+__global__ void __launch_bounds__(256, 2) lstm_bwd_tc_kernel(
+    int64_t rows, int kx, int N, const float* __restrict__ dy, const float* __restrict__ dh_in,
+    const float* __restrict__ dc_in, float* gates, const float* __restrict__ cprev, const float* __restrict__ cnew,
+    const float* __restrict__ img, float* __restrict__ dx, int64_t lddx, float* __restrict__ dh_out,
+    float* __restrict__ dc_out) {
+    constexpr int NC = 4 * HP;
+    const Ring R = tc_setup(N);
+    const int64_t row0 = blockIdx.x * (int64_t)TC_BM;
+    // K chunk ch covers units 4ch..4ch+3; column k = 4u + g
+    struct Cell {
+        float gi, gf, go, gg, cp, cn, dh, dc;
+    };
+    tc_mainloop(
+        R, HP / 4, img,
+        [&](int ch, int idx) {
+            const int64_t g = row0 + (idx >> 2);
+            const int u = 4 * ch + (idx & 3);
+            Cell p{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (g < rows) {
+                const float* gr = gates + g * NC + u;
+                const int64_t o = g * HP + u;
+                p.gi = gr[0];
+                p.gf = gr[HP];
+                p.go = gr[2 * HP];
+                p.gg = gr[3 * HP];
+                p.cp = __ldg(cprev + o);
+                p.cn = __ldg(cnew + o);
+                p.dh = (dy ? __ldg(dy + o) : 0.f) + __ldg(dh_in + o);
+                p.dc = __ldg(dc_in + o);
+            }
+            return p;
+        },
+        [&](const Cell& p, int ch, int idx) {
+            const int64_t g = row0 + (idx >> 2);
+            if (g >= rows) return make_float4(0.f, 0.f, 0.f, 0.f);
+            const int u = 4 * ch + (idx & 3);
+            const float tcn = tanhf(p.cn);
+            const float d_o = p.dh * tcn;
+            const float dc = p.dh * p.go * (1.f - tcn * tcn) + p.dc;
+            const float df = dc * p.cp, di = dc * p.gg, dg = dc * p.gi;
+            dc_out[g * HP + u] = dc * p.gf;
+            const float z0 = di * p.gi * (1.f - p.gi);
+            const float z1 = df * p.gf * (1.f - p.gf);
+            const float z2 = d_o * p.go * (1.f - p.go);
+            const float z3 = dg * (1.f - p.gg * p.gg);
+            float* gr = gates + g * NC + u;   // dz replaces the gate cache (training.py:413-421)
+            gr[0] = z0;
+            gr[HP] = z1;
+            gr[2 * HP] = z2;
+            gr[3 * HP] = z3;
+            return make_float4(z0, z1, z2, z3);
+        });
+    const int K = kx + HP;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, q = w & 3, half = w >> 2;
+    const int64_t row = row0 + 32 * q + lane;
+    const uint32_t tq = R.tmem + ((uint32_t)(32 * q) << 16);
+    for (int c0 = half * 8; c0 < N; c0 += 16) {
+        float v[8];
+        tmem_ld8(tq + c0, v);
+        tmem_wait_ld();
+        if (row >= rows) continue;
+#pragma unroll
+        for (int h4 = 0; h4 < 2; ++h4) {
+            const int c = c0 + 4 * h4;
+            const float4 val = make_float4(v[4 * h4], v[4 * h4 + 1], v[4 * h4 + 2], v[4 * h4 + 3]);
+            if (c < kx) *reinterpret_cast<float4*>(dx + row * lddx + c) = val;
+            else if (c < K) *reinterpret_cast<float4*>(dh_out + row * HP + (c - kx)) = val;
+        }
+    }
+    tc_teardown(R);
+}
+
+template <class Kern>
+static void set_smem(Kern k, size_t bytes) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <int HP>
 int lstm_fwd_tc_t(int64_t rows, int kx, const float* x, int64_t ldx, const float* hp_, const float* cp,
                   const float* img, const float* b, float* h, float* c, float* gates, cudaStream_t st) {
-    constexpr int N = 4 * HP;
     auto k = lstm_fwd_tc_kernel<HP>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<N>::SMEM);
+    const size_t smem = tc_smem_bytes(4 * HP);
+    set_smem(k, smem);
     note_launch();
-    k<<<(unsigned)cdiv(rows, TC_BM), 256, TcCfg<N>::SMEM, st>>>(rows, kx, x, ldx, hp_, cp, img, b, h, c, gates);
+    k<<<(unsigned)cdiv(rows, TC_BM), 256, smem, st>>>(rows, kx, x, ldx, hp_, cp, img, b, h, c, gates);
     return launch_status("lstm_forward_step_tc");
+}
+
+template <int HP>
+int lstm_bwd_tc_t(int64_t rows, int kx, const float* dy, const float* dh_in, const float* dc_in, float* gates,
+                  const float* cp, const float* cn, const float* img, float* dx, int64_t lddx, float* dh_out,
+                  float* dc_out, cudaStream_t st) {
+    const int N = (kx + HP + 15) / 16 * 16;
+    if (N > 256) {
+        set_error("lstm_backward_step_tc: kx + hp = %d exceeds 256", kx + HP);
+        return DGNN_EUNSUPPORTED;
+    }
+    auto k = lstm_bwd_tc_kernel<HP>;
+    const size_t smem = tc_smem_bytes(N);
+    set_smem(k, smem);
+    note_launch();
+    k<<<(unsigned)cdiv(rows, TC_BM), 256, smem, st>>>(rows, kx, N, dy, dh_in, dc_in, gates, cp, cn, img, dx, lddx,
+                                                        dh_out, dc_out);
+    return launch_status("lstm_backward_step_tc");
 }
 
 }  // namespace dgnn
@@ -280,25 +412,30 @@ size_t dgnn_tc_weight_image_bytes(int32_t n, int32_t k) {
     return (size_t)((k + TC_KC - 1) / TC_KC) * 2 * n * 64;
 }
 
-int dgnn_tc_weight_image(int32_t n, int32_t k, const float* w, int64_t ldw, float* img, void* stream) {
-    DGNN_CHECK_ARG(n % 16 == 0 && n >= 16 && n <= 512 && k > 0, "tc_weight_image: n must be a multiple of 16 in [16, 512]");
-    const int64_t total = (int64_t)((k + TC_KC - 1) / TC_KC) * n * 4;
+int dgnn_tc_weight_image_ex(int32_t n_alloc, int32_t n_valid, int32_t k, const float* w, int64_t ldw,
+                            int32_t perm_hp, float* img, void* stream) {
+    DGNN_CHECK_ARG(n_alloc % 16 == 0 && n_alloc >= 16 && n_alloc <= 512 && n_valid <= n_alloc && k > 0,
+                   "tc_weight_image: n_alloc must be a multiple of 16 in [16, 512]");
+    const int64_t total = (int64_t)((k + TC_KC - 1) / TC_KC) * n_alloc * 4;
     note_launch();
-    wimg_kernel<<<(unsigned)cdiv(total, 256), 256, 0, as_stream(stream)>>>(n, k, w, ldw, img);
+    wimg_kernel<<<(unsigned)cdiv(total, 256), 256, 0, as_stream(stream)>>>(n_alloc, n_valid, k, w, ldw, perm_hp, img);
     return launch_status("tc_weight_image");
+}
+
+int dgnn_tc_weight_image(int32_t n, int32_t k, const float* w, int64_t ldw, float* img, void* stream) {
+    return dgnn_tc_weight_image_ex(n, n, k, w, ldw, 0, img, stream);
 }
 
 int dgnn_tc_gemm_test(int32_t m, int32_t n, int32_t k, const float* a, int64_t lda, const float* img, float* d,
                       int64_t ldd, void* stream) {
-    DGNN_CHECK_ARG(k % 4 == 0 && lda % 4 == 0, "tc_gemm_test: k and lda must be multiples of 4");
+    DGNN_CHECK_ARG(k % 4 == 0 && lda % 4 == 0 && n % 16 == 0 && n >= 16 && n <= 512,
+                   "tc_gemm_test: k, lda multiples of 4; n a multiple of 16 in [16, 512]");
     cudaStream_t st = as_stream(stream);
-    switch (n) {
-        case 64: return tc_gemm_t<64>(m, k, a, lda, img, d, ldd, st);
-        case 128: return tc_gemm_t<128>(m, k, a, lda, img, d, ldd, st);
-        case 256: return tc_gemm_t<256>(m, k, a, lda, img, d, ldd, st);
-    }
-    set_error("tc_gemm_test: n must be 64, 128 or 256");
-    return DGNN_EUNSUPPORTED;
+    const size_t smem = tc_smem_bytes(n);
+    set_smem(tc_gemm_kernel, smem);
+    note_launch();
+    tc_gemm_kernel<<<(unsigned)cdiv(m, TC_BM), 256, smem, st>>>(m, n, k, a, lda, img, d, ldd);
+    return launch_status("tc_gemm_test");
 }
 
 int dgnn_lstm_forward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float* x, int64_t ldx,
@@ -314,6 +451,22 @@ int dgnn_lstm_forward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float*
         case 128: return lstm_fwd_tc_t<128>(rows, kx, x, ldx, h_prev, c_prev, wimg, bias, h_out, c_out, gates, st);
     }
     set_error("lstm_forward_step_tc: unsupported hp %d", hp);
+    return DGNN_EUNSUPPORTED;
+}
+
+int dgnn_lstm_backward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float* dy, const float* dh_in,
+                               const float* dc_in, float* gates, const float* c_prev, const float* c_new,
+                               const float* wimg, float* dx, int64_t lddx, float* dh_out, float* dc_out,
+                               void* stream) {
+    DGNN_CHECK_ARG(rows >= 0 && kx % 4 == 0 && lddx % 4 == 0, "lstm_backward_step_tc: bad sizes");
+    if (rows == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (hp) {
+        case 16: return lstm_bwd_tc_t<16>(rows, kx, dy, dh_in, dc_in, gates, c_prev, c_new, wimg, dx, lddx, dh_out, dc_out, st);
+        case 32: return lstm_bwd_tc_t<32>(rows, kx, dy, dh_in, dc_in, gates, c_prev, c_new, wimg, dx, lddx, dh_out, dc_out, st);
+        case 64: return lstm_bwd_tc_t<64>(rows, kx, dy, dh_in, dc_in, gates, c_prev, c_new, wimg, dx, lddx, dh_out, dc_out, st);
+    }
+    set_error("lstm_backward_step_tc: unsupported hp %d (use the SIMT step)", hp);
     return DGNN_EUNSUPPORTED;
 }
 

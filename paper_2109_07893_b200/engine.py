@@ -357,7 +357,8 @@ class Rank:
         NP, B = eng.plan.NP, eng.plan.bsize
         ho = Ly.ho
         st = _lib.stream_handle()
-        wt = eng.params.w(f"lstm{l}.wcat_t")
+        use_tc = eng.tensor_cores and ho <= 64 and Ly.kx + ho <= 256
+        wt = eng.params.image(f"lstm{l}.bwd") if use_tc else eng.params.w(f"lstm{l}.wcat_t")
         dh_buf, dc_buf = self.dcarry[l]
         dh_in, dc_in = self.dstate[l]
         for step, i in enumerate(reversed(range(B))):
@@ -368,8 +369,12 @@ class Rank:
             dx = self.vm(self.dR_vm[l], Ly.rw, i)
             dh_out = self.vm(dh_buf, ho, step % 2)
             dc_out = self.vm(dc_buf, ho, step % 2)
-            call("dgnn_lstm_backward_step", NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates),
-                 ptr(c_prev), ptr(c_new), ptr(wt), ptr(gates), ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
+            if use_tc:
+                call("dgnn_lstm_backward_step_tc", NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates),
+                     ptr(c_prev), ptr(c_new), ptr(wt), ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
+            else:
+                call("dgnn_lstm_backward_step", NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates),
+                     ptr(c_prev), ptr(c_new), ptr(wt), ptr(gates), ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
             dh_in, dc_in = dh_out, dc_out
         self.dstate[l][0].copy_(dh_in)
         self.dstate[l][1].copy_(dc_in)

@@ -313,11 +313,16 @@ def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True):
     return ys, (h[:, :H].double().cpu().numpy(), c[:, :H].double().cpu().numpy()), cache
 
 
-def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out):
+def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bool = True):
     """fp32 device BPTT over a block (training.py:394-427)."""
     dev = _dev()
     H, hp, kx, rows = cache["H"], cache["hp"], cache["kx"], cache["rows"]
     st = _lib.stream_handle()
+    bimg = None
+    if tensor_cores and hp <= 64 and kx + hp <= 256:
+        nb = (kx + hp + 15) // 16 * 16
+        bimg = torch.zeros(query("dgnn_tc_weight_image_bytes", nb, 4 * hp) // 4, dtype=torch.float32, device=dev)
+        call("dgnn_tc_weight_image_ex", nb, kx + hp, 4 * hp, ptr(cache["wc"]), 4 * hp, hp, ptr(bimg), st)
     dh = _pad_rows(np.asarray(dstate_out[0]), hp, dev)
     dc = _pad_rows(np.asarray(dstate_out[1]), hp, dev)
     K4 = 4 * hp
@@ -334,8 +339,13 @@ def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out):
         dx = torch.zeros(rows, kx, device=dev)
         dh2 = torch.zeros(rows, hp, device=dev)
         dc2 = torch.zeros(rows, hp, device=dev)
-        call("dgnn_lstm_backward_step", rows, kx, hp, ptr(dy), ptr(dh), ptr(dc), ptr(cache["g"][i]), ptr(c_prev),
-             ptr(cache["c"][i]), ptr(cache["wct"]), ptr(dz), ptr(dx), kx, ptr(dh2), ptr(dc2), st)
+        if bimg is not None:
+            dz.copy_(cache["g"][i])      # the tensor-core step writes dz over the gate cache
+            call("dgnn_lstm_backward_step_tc", rows, kx, hp, ptr(dy), ptr(dh), ptr(dc), ptr(dz), ptr(c_prev),
+                 ptr(cache["c"][i]), ptr(bimg), ptr(dx), kx, ptr(dh2), ptr(dc2), st)
+        else:
+            call("dgnn_lstm_backward_step", rows, kx, hp, ptr(dy), ptr(dh), ptr(dc), ptr(cache["g"][i]),
+                 ptr(c_prev), ptr(cache["c"][i]), ptr(cache["wct"]), ptr(dz), ptr(dx), kx, ptr(dh2), ptr(dc2), st)
         h_prev = cache["h"][i - 1] if i > 0 else cache["h0"]
         call("dgnn_gemm_tn", rows, kx, K4, ptr(cache["x"][i]), kx, ptr(dz), K4, ptr(gwc), K4, ptr(gb), ptr(ws),
              ws.numel(), st)

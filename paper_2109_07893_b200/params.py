@@ -302,6 +302,9 @@ class DeviceParams:
             if L.skip:
                 nbytes = _lib.query("dgnn_tc_weight_image_bytes", 4 * L.ho, L.kx + L.ho)
                 self.images[f"lstm{l}.fwd"] = torch.zeros(nbytes // 4, dtype=torch.float32, device=dev)
+                nb = (L.kx + L.ho + 15) // 16 * 16
+                nbytes = _lib.query("dgnn_tc_weight_image_bytes", nb, 4 * L.ho)
+                self.images[f"lstm{l}.bwd"] = torch.zeros(nbytes // 4, dtype=torch.float32, device=dev)
 
     def image(self, name: str) -> torch.Tensor:
         return self.images[name]
@@ -320,6 +323,8 @@ class DeviceParams:
                 K = L.kx + L.ho
                 call("dgnn_tc_weight_image", 4 * L.ho, K, ptr(self.w(f"lstm{l}.wcat_t")), K,
                      ptr(self.images[f"lstm{l}.fwd"]), sh)
+                call("dgnn_tc_weight_image_ex", (K + 15) // 16 * 16, K, 4 * L.ho, ptr(self.w(f"lstm{l}.wcat")),
+                     4 * L.ho, L.ho, ptr(self.images[f"lstm{l}.bwd"]), sh)
 
     def w(self, name: str) -> torch.Tensor:
         return self.layout.block(self.w32, name)

@@ -62,12 +62,24 @@ def guarded_close(got: np.ndarray, ref: np.ndarray, rtol: float, atol_frac: floa
     return (not bad.any()), (float(err.max()) if err.size else 0.0), int(bad.sum())
 
 
-def assert_grads_close(got: dict, ref: dict, rtol: float, atol_frac: float = 1e-6):
+def assert_grads_close(got: dict, ref: dict, rtol: float, atol_frac: float = 1e-6, norm_rtol: float = 1e-5):
+    """Per tensor: elementwise guarded check plus a normwise relative check
+    ||g - r||_2 <= norm_rtol ||r||_2."""
     assert sorted(got) == sorted(ref)
     for k in sorted(ref):
         assert got[k].shape == ref[k].shape, k
         ok, worst, nbad = guarded_close(got[k], ref[k], rtol, atol_frac)
-        assert ok, f"{k}: {nbad} entries off, worst abs err {worst:.3e}"
+        scale = float(np.max(np.abs(ref[k]))) if ref[k].size else 0.0
+        assert ok, f"{k}: {nbad} entries off, worst abs err {worst:.3e} (||r||_inf {scale:.3e})"
+        nr = float(np.linalg.norm(ref[k]))
+        assert float(np.linalg.norm(got[k] - ref[k])) <= norm_rtol * nr + 1e-30, k
+
+
+# Engine-level floor: the temporal GEMMs run on tcgen05 (3xTF32 operands, fp32
+# accumulation that truncates, ~1e-6 relative per step), and gradients are
+# reductions over ~1e5-1e7 terms, so entries near zero carry an absolute error
+# at the 1e-6..1e-5 x ||r||_inf level; everything else meets 1e-4 relative.
+ENGINE_ATOL = 1e-5
 
 
 @pytest.fixture(scope="session")
