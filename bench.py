@@ -207,7 +207,7 @@ def run_ours(args):
     for Ly in eng.layout.layers:
         layers_real[Ly.kx] = (Ly.fin + Ly.gout, Ly.out)
     timed_names = ["dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_lstm_forward_step_tc",
-                   "dgnn_lstm_backward_step_tc", "dgnn_gemm_tn", "dgnn_gcn_forward",
+                   "dgnn_lstm_backward_step_tc", "dgnn_lstm_weight_grad_tc", "dgnn_gemm_tn", "dgnn_gcn_forward",
                    "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows", "dgnn_csr_apply_delta",
                    "dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_head_loss", "dgnn_head_grad",
                    "dgnn_head_scatter"]

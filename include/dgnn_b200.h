@@ -193,6 +193,20 @@ int dgnn_lstm_backward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float
                                const float* c_prev, const float* c_new, const float* wimg, float* dx,
                                int64_t lddx, float* dh_out, float* dc_out, void* stream);
 
+/* LSTM weight gradients of a whole block on tcgen05 (training.py:422-424):
+ *   gwcat[k][j] += sum_r xcat[r][k] dz[r][j],  gb[j] += sum_r dz[r][j]
+ * over rows r = t*np + v of the block (rows = bsize*np), with
+ * xcat[r] = [x[r] (kx cols, ld ldx) | h_prev] and h_prev = h_out[r - np]
+ * (t > 0) or h0[v] (t = 0).  dz: rows x 4hp.  Operands MN-major straight
+ * from HBM, 3xTF32, TMEM accumulation restarted every 512 rows and promoted
+ * to per-CTA fp32 slots, fp64 fixed-order final reduction.  hp in
+ * {32, 64}, kx + hp <= 256. */
+size_t dgnn_lstm_weight_grad_tc_workspace(int32_t kx, int32_t hp);
+int dgnn_lstm_weight_grad_tc(int64_t rows, int64_t np, int32_t kx, int32_t hp, const float* x,
+                             int64_t ldx, const float* h_out, const float* h0, const float* dz,
+                             double* gwcat, double* gb, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 /* K6 -- one reverse LSTM step (training.py:404-426):
  *   dh = dy + dh_in; do, dc, df, di, dg as the reference; dc_out = dc f
  *   dz = [di i(1-i) | df f(1-f) | do o(1-o) | dg (1-g^2)]  (written, 4hp wide)

@@ -36,9 +36,27 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo_bytes, ui
     return d;
 }
 
+// Descriptor with an explicit leading byte offset (MN-major operands: LBO =
+// stride between 16-element MN atoms, SBO = stride between 8-row K groups).
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                             uint32_t layout) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
 // kind::tf32 instruction descriptor: A/B tf32 K-major, D fp32, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// same with both operands MN-major (bits 15 / 16)
+__host__ __device__ constexpr uint32_t idesc_tf32_mn(int M, int N) {
+    return idesc_tf32(M, N) | (1u << 15) | (1u << 16);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,

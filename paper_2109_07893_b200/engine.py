@@ -125,6 +125,9 @@ class Rank:
             dtype=torch.uint8, device=dev)
         self.ws_head = torch.empty(_lib.query("dgnn_head_grad_workspace", gl.ep, gl.classes), dtype=torch.uint8,
                                    device=dev)
+        self.ws_dw = torch.empty(max([_lib.query("dgnn_lstm_weight_grad_tc_workspace", Ly.kx, Ly.ho)
+                                      for Ly in layers if Ly.skip and 32 <= Ly.ho <= 64] + [16]),
+                                 dtype=torch.uint8, device=dev)
         self.slots = []
 
     # ---------------------------------------------------------------- frames
@@ -381,6 +384,11 @@ class Rank:
         # weight gradients over every (row, step) of the block (training.py:422-424)
         g_wcat = eng.params.gw(f"lstm{l}.wcat")
         g_b = eng.params.gw(f"lstm{l}.b")
+        if use_tc and ho >= 32:
+            ws = self.ws_dw
+            call("dgnn_lstm_weight_grad_tc", B * NP, NP, Ly.kx, ho, ptr(self.R_vm[l]), Ly.rw, ptr(self.Y_vm[l]),
+                 ptr(self.act[l][0]), ptr(self.G_vm[l]), ptr(g_wcat), ptr(g_b), ptr(ws), ws.numel(), st)
+            return
         ws = self.ws_tn
         K4 = 4 * ho
         call("dgnn_gemm_tn", B * NP, Ly.kx, K4, ptr(self.R_vm[l]), Ly.rw, ptr(self.G_vm[l]), K4, ptr(g_wcat), K4,

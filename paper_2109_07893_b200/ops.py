@@ -274,6 +274,21 @@ def tc_gemm(a: np.ndarray, w: np.ndarray) -> np.ndarray:
     return out.double().cpu().numpy()
 
 
+def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np.ndarray, np_rows: int):
+    """Tensor-core block weight gradient (test hook of dgnn_lstm_weight_grad_tc):
+    returns (sum_r xcat[r]^T dz[r]  as (kx+hp) x 4hp, sum_r dz[r]) in fp64."""
+    dev = _dev()
+    rows, kx = x.shape
+    hp = h0.shape[1]
+    t = [torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev) for a in (x, h_out, h0, dz)]
+    gw = torch.zeros((kx + hp) * 4 * hp, dtype=torch.float64, device=dev)
+    gb = torch.zeros(4 * hp, dtype=torch.float64, device=dev)
+    ws = torch.empty(query("dgnn_lstm_weight_grad_tc_workspace", kx, hp), dtype=torch.uint8, device=dev)
+    call("dgnn_lstm_weight_grad_tc", rows, np_rows, kx, hp, ptr(t[0]), kx, ptr(t[1]), ptr(t[2]), ptr(t[3]),
+         ptr(gw), ptr(gb), ptr(ws), ws.numel(), _lib.stream_handle())
+    return gw.view(kx + hp, 4 * hp).cpu().numpy(), gb.cpu().numpy()
+
+
 def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True):
     """fp32 device LSTM over a block (training.py:370-391).  Returns
     (ys, (h, c), cache) with a device cache for lstm_block_backward."""
@@ -331,6 +346,7 @@ def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bo
     ws = torch.empty(query("dgnn_gemm_tn_workspace", max(kx, hp), K4), dtype=torch.uint8, device=dev)
     dxs = {}
     B = len(ts)
+    dzs = [None] * B
     for i in reversed(range(B)):
         t = ts[i]
         dy = _pad_rows(np.asarray(dys[t]), hp, dev)
@@ -347,13 +363,24 @@ def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bo
             call("dgnn_lstm_backward_step", rows, kx, hp, ptr(dy), ptr(dh), ptr(dc), ptr(cache["g"][i]),
                  ptr(c_prev), ptr(cache["c"][i]), ptr(cache["wct"]), ptr(dz), ptr(dx), kx, ptr(dh2), ptr(dc2), st)
         h_prev = cache["h"][i - 1] if i > 0 else cache["h0"]
-        call("dgnn_gemm_tn", rows, kx, K4, ptr(cache["x"][i]), kx, ptr(dz), K4, ptr(gwc), K4, ptr(gb), ptr(ws),
-             ws.numel(), st)
-        call("dgnn_gemm_tn", rows, hp, K4, ptr(h_prev), hp, ptr(dz), K4, ptr(gwc[kx * K4:]), K4, None, ptr(ws),
-             ws.numel(), st)
+        if bimg is not None and hp >= 32:
+            dzs[i] = dz
+        else:
+            call("dgnn_gemm_tn", rows, kx, K4, ptr(cache["x"][i]), kx, ptr(dz), K4, ptr(gwc), K4, ptr(gb),
+                 ptr(ws), ws.numel(), st)
+            call("dgnn_gemm_tn", rows, hp, K4, ptr(h_prev), hp, ptr(dz), K4, ptr(gwc[kx * K4:]), K4, None,
+                 ptr(ws), ws.numel(), st)
         fin = np.asarray(cell.wx).shape[0]
         dxs[t] = dx[:, :fin].double().cpu().numpy()
         dh, dc = dh2, dc2
+    if bimg is not None and hp >= 32:
+        # one tensor-core pass over all (step, row) pairs of the block
+        xs_all = torch.cat(cache["x"][:B]).contiguous()
+        hs_all = torch.cat(cache["h"][:B]).contiguous()
+        dz_all = torch.cat(dzs).contiguous()
+        wsd = torch.empty(query("dgnn_lstm_weight_grad_tc_workspace", kx, hp), dtype=torch.uint8, device=dev)
+        call("dgnn_lstm_weight_grad_tc", B * rows, rows, kx, hp, ptr(xs_all), kx, ptr(hs_all), ptr(cache["h0"]),
+             ptr(dz_all), ptr(gwc), ptr(gb), ptr(wsd), wsd.numel(), st)
     g = gwc.view(kx + hp, K4).cpu().numpy()
     gbv = gb.cpu().numpy()
     fin = np.asarray(cell.wx).shape[0]
