@@ -134,13 +134,13 @@ def make_workload(P: int, seed: int = 1):
 
 def kernel_work(name, args, l2_bytes, layers_real):
     """(flops, bytes) of one C-ABI call, from its arguments."""
-    if name in ("dgnn_lstm_forward_step", "dgnn_lstm_forward_step_tc"):
+    if name in ("dgnn_lstm_forward_step", "dgnn_lstm_forward_step_tc", "dgnn_lstm_forward_step_ws"):
         rows, kx, hp, gates = args[0], args[1], args[2], args[11]
         kin, h = layers_real.get(kx, (kx, hp))
         flops = 2 * rows * (kin + h) * 4 * h
         byts = 4 * rows * (kin + 4 * h + (4 * h if gates else 0))
         return flops, byts
-    if name in ("dgnn_lstm_backward_step", "dgnn_lstm_backward_step_tc"):
+    if name in ("dgnn_lstm_backward_step", "dgnn_lstm_backward_step_tc", "dgnn_lstm_backward_step_ws"):
         rows, kx, hp = args[0], args[1], args[2]
         kin, h = layers_real.get(kx, (kx, hp))
         flops = 2 * rows * 4 * h * (kin + h)
@@ -207,6 +207,7 @@ def run_ours(args):
     for Ly in eng.layout.layers:
         layers_real[Ly.kx] = (Ly.fin + Ly.gout, Ly.out)
     timed_names = ["dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_lstm_forward_step_tc",
+                   "dgnn_lstm_forward_step_ws", "dgnn_lstm_backward_step_ws",
                    "dgnn_lstm_backward_step_tc", "dgnn_lstm_weight_grad_tc", "dgnn_gemm_tn", "dgnn_gcn_forward",
                    "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows", "dgnn_csr_apply_delta",
                    "dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_head_loss", "dgnn_head_grad",
@@ -245,6 +246,7 @@ def run_ours(args):
     dom = max(tot, key=tot.get) if tot else None
     roof = None
     if dom in ("dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_lstm_forward_step_tc",
+               "dgnn_lstm_forward_step_ws", "dgnn_lstm_backward_step_ws", "dgnn_lstm_weight_grad_tc",
                "dgnn_lstm_backward_step_tc", "dgnn_gemm_tn"):
         fl = sum(kernel_work(dom, a, l2, layers_real)[0] for _, a in durs[dom])
         by = sum(kernel_work(dom, a, l2, layers_real)[1] for _, a in durs[dom])

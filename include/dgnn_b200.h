@@ -183,6 +183,19 @@ int dgnn_lstm_forward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float*
                               const float* bias, float* h_out, float* c_out, float* gates,
                               void* stream);
 
+/* Persistent, warp-specialised versions (producer warps -> one MMA thread ->
+ * epilogue warps, 4-stage smem ring, double-buffered TMEM accumulator; one
+ * CTA per SM).  Same contracts and operand images as the _tc entries;
+ * hp in {16, 32, 64}. */
+int dgnn_lstm_forward_step_ws(int64_t rows, int32_t kx, int32_t hp, const float* x, int64_t ldx,
+                              const float* h_prev, const float* c_prev, const float* wimg,
+                              const float* bias, float* h_out, float* c_out, float* gates,
+                              void* stream);
+int dgnn_lstm_backward_step_ws(int64_t rows, int32_t kx, int32_t hp, const float* dy,
+                               const float* dh_in, const float* dc_in, float* gates,
+                               const float* c_prev, const float* c_new, const float* wimg, float* dx,
+                               int64_t lddx, float* dh_out, float* dc_out, void* stream);
+
 /* K6 on tcgen05: same contract as dgnn_lstm_backward_step (dz written in
  * place of the gate cache `gates`); the pointwise gate gradients are the
  * operand producer of [dx | dh] = dz W^T (3xTF32, TMEM accumulator).

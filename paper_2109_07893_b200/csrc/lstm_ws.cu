@@ -1,0 +1,460 @@
+// Persistent, warp-specialised tcgen05 LSTM step kernels (K5 forward, K6
+// backward).  Same math and operand conventions as lstm_tc.cu (3xTF32,
+// SW64 K-major tiles, pre-split weight images), restructured so that HBM
+// traffic, tensor-core work and the cell epilogue overlap:
+//
+//   warps 0..3  producers: fetch the activation chunk one chunk ahead,
+//               split fp32 -> tf32 hi/lo, store the SW64 tile, arrive on
+//               full_a[s]; producer 0 lane 0 also bulk-copies the weight
+//               chunk (cp.async.bulk, complete_tx on full_b[s]).
+//   warp 4      MMA issuer (one lane): waits full_a/full_b, issues the
+//               3xTF32 MMAs into TMEM accumulator a (two buffers), commits
+//               empty[s] per chunk and accfull[a] per tile.
+//   warps 5..12 epilogue: wait accfull[a], tcgen05.ld, cell update (forward)
+//               or dx/dh stores (backward), arrive accempty[a].
+//
+// One CTA per SM loops over 128-row tiles; a 4-stage smem ring (48 KB per
+// stage at N = 256) and 2 x N TMEM columns let tile i's epilogue run under
+// tile i+1's MMAs.  Reference: training.py:370-427.
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace dgnn {
+using namespace tc;
+
+namespace wsk {
+constexpr int BM = 128;
+constexpr int KC = 16;
+constexpr int A_TILE = BM * 64;
+constexpr int NPROD = 4;
+constexpr int MMA_WARP = NPROD;
+constexpr int NEPI = 8;
+constexpr int THREADS = 32 * (NPROD + 1 + NEPI);
+constexpr int STAGES = 4;
+}  // namespace wsk
+
+__host__ __device__ constexpr int ws_tmem_cols(int n2) {
+    return n2 <= 32 ? 32 : (n2 <= 64 ? 64 : (n2 <= 128 ? 128 : (n2 <= 256 ? 256 : 512)));
+}
+
+struct WsBars {
+    uint64_t full_a[wsk::STAGES], full_b[wsk::STAGES], empty[wsk::STAGES], accfull[2], accempty[2];
+    uint32_t tmem;
+};
+
+// stage layout: [A hi | A lo | B hi+lo]
+struct WsSmem {
+    uint32_t base;   // smem address of stage 0 (1024-aligned)
+    int stage;       // stage bytes
+    __device__ uint32_t a_hi(int s) const { return base + s * stage; }
+    __device__ uint32_t a_lo(int s) const { return base + s * stage + wsk::A_TILE; }
+    __device__ uint32_t b(int s) const { return base + s * stage + 2 * wsk::A_TILE; }
+};
+
+inline size_t ws_smem_bytes(int n) {
+    return (size_t)wsk::STAGES * (2 * wsk::A_TILE + 2 * n * 64) + 1024 + sizeof(WsBars) + 64;
+}
+
+__device__ __forceinline__ WsBars* ws_setup(WsSmem& sm, int n) {
+    extern __shared__ uint8_t ws_smem_raw[];
+    const uint32_t raw = smem_u32(ws_smem_raw);
+    const uint32_t pad = (1024 - (raw & 1023)) & 1023;
+    sm.base = raw + pad;
+    sm.stage = 2 * wsk::A_TILE + 2 * n * 64;
+    WsBars* bars = reinterpret_cast<WsBars*>(ws_smem_raw + pad + wsk::STAGES * sm.stage);
+    const int warp = threadIdx.x >> 5;
+    if (warp == wsk::MMA_WARP) tmem_alloc(&bars->tmem, ws_tmem_cols(2 * n));
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < wsk::STAGES; ++s) {
+            mbar_init(&bars->full_a[s], wsk::NPROD);
+            mbar_init(&bars->full_b[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->accfull[a], 1);
+            mbar_init(&bars->accempty[a], wsk::NEPI);
+        }
+        fence_mbar_init();
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    return bars;
+}
+
+__device__ __forceinline__ void ws_teardown(WsBars* bars, int n) {
+    fence_before();
+    __syncthreads();
+    if ((threadIdx.x >> 5) == wsk::MMA_WARP) tmem_dealloc(bars->tmem, ws_tmem_cols(2 * n));
+}
+
+// MMA issuer: for every tile of this CTA, all K chunks into accumulator a.
+__device__ __forceinline__ void ws_mma_loop(const WsSmem& sm, WsBars* bars, int n, int ntiles, int nch) {
+    uint32_t gc = 0, it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const uint32_t a = it & 1, u = it >> 1;
+        if (u >= 1) mbar_wait(&bars->accempty[a], (u - 1) & 1);
+        fence_after();
+        const uint32_t d = bars->tmem + a * n;
+        for (int ch = 0; ch < nch; ++ch, ++gc) {
+            const int s = gc % wsk::STAGES;
+            const uint32_t j = gc / wsk::STAGES;
+            mbar_wait(&bars->full_a[s], j & 1);
+            mbar_wait(&bars->full_b[s], j & 1);
+            fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                const uint64_t ahi = sdesc(sm.a_hi(s) + 32 * kk, 512, kSW64);
+                const uint64_t alo = sdesc(sm.a_lo(s) + 32 * kk, 512, kSW64);
+                for (int n0 = 0; n0 < n; n0 += 256) {
+                    const int nn = n - n0 < 256 ? n - n0 : 256;
+                    const uint32_t idesc = idesc_tf32(wsk::BM, nn);
+                    const uint64_t bhi = sdesc(sm.b(s) + n0 * 64 + 32 * kk, 512, kSW64);
+                    const uint64_t blo = sdesc(sm.b(s) + n * 64 + n0 * 64 + 32 * kk, 512, kSW64);
+                    mma_tf32(d + n0, ahi, bhi, idesc, (ch == 0 && kk == 0) ? 0u : 1u);
+                    mma_tf32(d + n0, ahi, blo, idesc, 1u);
+                    mma_tf32(d + n0, alo, bhi, idesc, 1u);
+                }
+            }
+            commit(&bars->empty[s]);
+        }
+        commit(&bars->accfull[a]);
+    }
+}
+
+// Producer side of one chunk: wait for the stage, launch the weight copy,
+// store the activation split.  `vals[i]` holds the 4 fp32 of item
+// ptid + 128 i (row item / 4, column group item % 4).
+template <int ITEMS>
+__device__ __forceinline__ void ws_produce(const WsSmem& sm, WsBars* bars, uint32_t gc, const float* img, int ch,
+                                           uint32_t b_bytes, const float4 (&vals)[ITEMS]) {
+    const int ptid = threadIdx.x;   // producers are threads 0 .. 127
+    const int s = gc % wsk::STAGES;
+    const uint32_t j = gc / wsk::STAGES;
+    if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
+    if (ptid == 0) {
+        mbar_arrive_expect_tx(&bars->full_b[s], b_bytes);
+        bulk_g2s(sm.b(s), reinterpret_cast<const char*>(img) + (size_t)ch * b_bytes, b_bytes, &bars->full_b[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int idx = ptid + 128 * i;
+        const int r = idx >> 2, q = idx & 3;
+        float4 hi, lo;
+        split4(vals[i], hi, lo);
+        sts128(sm.a_hi(s) + sw64(r, q), hi);
+        sts128(sm.a_lo(s) + sw64(r, q), lo);
+    }
+    fence_async_smem();
+    __syncwarp();
+    if ((ptid & 31) == 0) mbar_arrive(&bars->full_a[s]);
+}
+
+// ---------------------------------------------------------------------------
+// forward
+
+template <int HP>
+__global__ void __launch_bounds__(wsk::THREADS, 1) lstm_fwd_ws_kernel(
+    int64_t rows, int kx, const float* __restrict__ x, int64_t ldx, const float* __restrict__ hprev,
+    const float* __restrict__ cprev, const float* __restrict__ img, const float* __restrict__ bias,
+    float* __restrict__ hout, float* __restrict__ cout, float* __restrict__ gates) {
+    constexpr int N = 4 * HP;
+    constexpr int ITEMS = wsk::BM * 4 / (wsk::NPROD * 32);   // 4
+    WsSmem sm;
+    WsBars* bars = ws_setup(sm, N);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = (int)cdiv(rows, wsk::BM);
+    const int K = kx + HP;
+    const int nch = (K + wsk::KC - 1) / wsk::KC;
+    const uint32_t b_bytes = 2 * N * 64;
+
+    if (warp < wsk::NPROD) {
+        const int ptid = threadIdx.x;
+        auto fetch = [&](int tile, int ch, float4 (&v)[ITEMS]) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const int idx = ptid + 128 * i;
+                const int64_t g = (int64_t)tile * wsk::BM + (idx >> 2);
+                const int k = ch * wsk::KC + 4 * (idx & 3);
+                float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (g < rows && k < K)
+                    val = k < kx ? __ldg(reinterpret_cast<const float4*>(x + g * ldx + k))
+                                 : __ldg(reinterpret_cast<const float4*>(hprev + g * HP + (k - kx)));
+                v[i] = val;
+            }
+        };
+        float4 cur[ITEMS], nxt[ITEMS];
+        uint32_t gc = 0;
+        int tile = blockIdx.x, ch = 0;
+        if (tile < ntiles) fetch(tile, 0, cur);
+        while (tile < ntiles) {
+            int nt = tile, nc = ch + 1;
+            if (nc == nch) { nc = 0; nt += gridDim.x; }
+            if (nt < ntiles) fetch(nt, nc, nxt);
+            ws_produce<ITEMS>(sm, bars, gc, img, ch, b_bytes, cur);
+            ++gc;
+            tile = nt;
+            ch = nc;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) cur[i] = nxt[i];
+        }
+    } else if (warp == wsk::MMA_WARP) {
+        if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
+        __syncwarp();
+    } else {
+        const int e = warp - wsk::MMA_WARP - 1;
+        const int q = warp & 3, half = e >> 2;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        uint32_t it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const uint32_t a = it & 1, u = it >> 1;
+            const int64_t row = (int64_t)tile * wsk::BM + 32 * q + lane;
+            const bool valid = row < rows;
+            float cp[HP / 2];
+#pragma unroll
+            for (int i = 0; i < HP / 8; ++i) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (valid) v = __ldg(reinterpret_cast<const float4*>(cprev + row * HP + half * (HP / 2) + 4 * i));
+                cp[4 * i] = v.x;
+                cp[4 * i + 1] = v.y;
+                cp[4 * i + 2] = v.z;
+                cp[4 * i + 3] = v.w;
+            }
+            mbar_wait(&bars->accfull[a], u & 1);
+            fence_after();
+            const uint32_t tq = bars->tmem + lane_off + a * N;
+#pragma unroll
+            for (int g8 = 0; g8 < HP / 16; ++g8) {
+                const int u0 = half * (HP / 2) + 8 * g8;
+                float z[4][8];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) tmem_ld8(tq + g * HP + u0, z[g]);
+                tmem_wait_ld();
+                if (!valid) continue;
+                float hv[8], cv[8], gi[8], gf[8], go[8], gg[8];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    gi[jj] = sigmoidf_acc(z[0][jj] + __ldg(bias + 0 * HP + u0 + jj));
+                    gf[jj] = sigmoidf_acc(z[1][jj] + __ldg(bias + 1 * HP + u0 + jj));
+                    go[jj] = sigmoidf_acc(z[2][jj] + __ldg(bias + 2 * HP + u0 + jj));
+                    gg[jj] = tanhf(z[3][jj] + __ldg(bias + 3 * HP + u0 + jj));
+                    cv[jj] = gf[jj] * cp[8 * g8 + jj] + gi[jj] * gg[jj];
+                    hv[jj] = go[jj] * tanhf(cv[jj]);
+                }
+                float4* ho = reinterpret_cast<float4*>(hout + row * HP + u0);
+                float4* co = reinterpret_cast<float4*>(cout + row * HP + u0);
+                ho[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                ho[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                co[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+                co[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+                if (gates) {
+                    float* gr = gates + row * N + u0;
+                    const float* src[4] = {gi, gf, go, gg};
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        float4* o = reinterpret_cast<float4*>(gr + g * HP);
+                        o[0] = make_float4(src[g][0], src[g][1], src[g][2], src[g][3]);
+                        o[1] = make_float4(src[g][4], src[g][5], src[g][6], src[g][7]);
+                    }
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->accempty[a]);
+        }
+    }
+    ws_teardown(bars, N);
+}
+
+// ---------------------------------------------------------------------------
+// backward: producers compute dz (unit-major K chunk = 4 units x 4 gates)
+
+template <int HP>
+__global__ void __launch_bounds__(wsk::THREADS, 1) lstm_bwd_ws_kernel(
+    int64_t rows, int kx, int N, const float* __restrict__ dy, const float* __restrict__ dh_in,
+    const float* __restrict__ dc_in, float* gates, const float* __restrict__ cprev, const float* __restrict__ cnew,
+    const float* __restrict__ img, float* __restrict__ dx, int64_t lddx, float* __restrict__ dh_out,
+    float* __restrict__ dc_out) {
+    constexpr int NC = 4 * HP;
+    constexpr int ITEMS = wsk::BM * 4 / (wsk::NPROD * 32);   // 4 (row, unit) items per producer thread
+    WsSmem sm;
+    WsBars* bars = ws_setup(sm, N);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = (int)cdiv(rows, wsk::BM);
+    const int nch = HP / 4;
+    const uint32_t b_bytes = 2 * N * 64;
+
+    if (warp < wsk::NPROD) {
+        const int ptid = threadIdx.x;
+        struct Cell {
+            float gi, gf, go, gg, cp, cn, dh, dc;
+        };
+        auto fetch = [&](int tile, int ch, Cell (&v)[ITEMS]) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const int idx = ptid + 128 * i;
+                const int64_t g = (int64_t)tile * wsk::BM + (idx >> 2);
+                const int u = 4 * ch + (idx & 3);
+                Cell p{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (g < rows) {
+                    const float* gr = gates + g * NC + u;
+                    const int64_t o = g * HP + u;
+                    p.gi = gr[0];
+                    p.gf = gr[HP];
+                    p.go = gr[2 * HP];
+                    p.gg = gr[3 * HP];
+                    p.cp = __ldg(cprev + o);
+                    p.cn = __ldg(cnew + o);
+                    p.dh = (dy ? __ldg(dy + o) : 0.f) + __ldg(dh_in + o);
+                    p.dc = __ldg(dc_in + o);
+                }
+                v[i] = p;
+            }
+        };
+        Cell cur[ITEMS], nxt[ITEMS];
+        float4 vals[ITEMS];
+        uint32_t gc = 0;
+        int tile = blockIdx.x, ch = 0;
+        if (tile < ntiles) fetch(tile, 0, cur);
+        while (tile < ntiles) {
+            int nt = tile, nc = ch + 1;
+            if (nc == nch) { nc = 0; nt += gridDim.x; }
+            if (nt < ntiles) fetch(nt, nc, nxt);
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const int idx = ptid + 128 * i;
+                const int64_t g = (int64_t)tile * wsk::BM + (idx >> 2);
+                const int u = 4 * ch + (idx & 3);
+                const Cell& p = cur[i];
+                float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (g < rows) {
+                    const float tcn = tanhf(p.cn);
+                    const float d_o = p.dh * tcn;
+                    const float dc = p.dh * p.go * (1.f - tcn * tcn) + p.dc;
+                    const float df = dc * p.cp, di = dc * p.gg, dg = dc * p.gi;
+                    dc_out[g * HP + u] = dc * p.gf;
+                    z = make_float4(di * p.gi * (1.f - p.gi), df * p.gf * (1.f - p.gf), d_o * p.go * (1.f - p.go),
+                                    dg * (1.f - p.gg * p.gg));
+                    float* gr = gates + g * NC + u;   // dz replaces the gate cache
+                    gr[0] = z.x;
+                    gr[HP] = z.y;
+                    gr[2 * HP] = z.z;
+                    gr[3 * HP] = z.w;
+                }
+                vals[i] = z;
+            }
+            ws_produce<ITEMS>(sm, bars, gc, img, ch, b_bytes, vals);
+            ++gc;
+            tile = nt;
+            ch = nc;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) cur[i] = nxt[i];
+        }
+    } else if (warp == wsk::MMA_WARP) {
+        if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
+        __syncwarp();
+    } else {
+        const int e = warp - wsk::MMA_WARP - 1;
+        const int q = warp & 3, half = e >> 2;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        const int K = kx + HP;
+        uint32_t it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const uint32_t a = it & 1, u = it >> 1;
+            const int64_t row = (int64_t)tile * wsk::BM + 32 * q + lane;
+            mbar_wait(&bars->accfull[a], u & 1);
+            fence_after();
+            const uint32_t tq = bars->tmem + lane_off + a * N;
+            for (int c0 = half * 8; c0 < N; c0 += 16) {
+                float v[8];
+                tmem_ld8(tq + c0, v);
+                tmem_wait_ld();
+                if (row >= rows) continue;
+#pragma unroll
+                for (int h4 = 0; h4 < 2; ++h4) {
+                    const int c = c0 + 4 * h4;
+                    const float4 val = make_float4(v[4 * h4], v[4 * h4 + 1], v[4 * h4 + 2], v[4 * h4 + 3]);
+                    if (c < kx) *reinterpret_cast<float4*>(dx + row * lddx + c) = val;
+                    else if (c < K) *reinterpret_cast<float4*>(dh_out + row * HP + (c - kx)) = val;
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->accempty[a]);
+        }
+    }
+    ws_teardown(bars, N);
+}
+
+template <int HP>
+int lstm_fwd_ws_t(int64_t rows, int kx, const float* x, int64_t ldx, const float* hp_, const float* cp,
+                  const float* img, const float* b, float* h, float* c, float* gates, cudaStream_t st) {
+    constexpr int N = 4 * HP;
+    auto k = lstm_fwd_ws_kernel<HP>;
+    const size_t smem = ws_smem_bytes(N);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int ntiles = (int)cdiv(rows, wsk::BM);
+    const int grid = ntiles < kSMs ? ntiles : kSMs;
+    note_launch();
+    k<<<grid, wsk::THREADS, smem, st>>>(rows, kx, x, ldx, hp_, cp, img, b, h, c, gates);
+    return launch_status("lstm_forward_step_ws");
+}
+
+template <int HP>
+int lstm_bwd_ws_t(int64_t rows, int kx, const float* dy, const float* dh_in, const float* dc_in, float* gates,
+                  const float* cp, const float* cn, const float* img, float* dx, int64_t lddx, float* dh_out,
+                  float* dc_out, cudaStream_t st) {
+    const int N = (kx + HP + 15) / 16 * 16;
+    if (N > 256) {
+        set_error("lstm_backward_step: kx + hp = %d exceeds 256", kx + HP);
+        return DGNN_EUNSUPPORTED;
+    }
+    auto k = lstm_bwd_ws_kernel<HP>;
+    const size_t smem = ws_smem_bytes(N);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int ntiles = (int)cdiv(rows, wsk::BM);
+    const int grid = ntiles < kSMs ? ntiles : kSMs;
+    note_launch();
+    k<<<grid, wsk::THREADS, smem, st>>>(rows, kx, N, dy, dh_in, dc_in, gates, cp, cn, img, dx, lddx, dh_out,
+                                         dc_out);
+    return launch_status("lstm_backward_step_ws");
+}
+
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" {
+
+int dgnn_lstm_forward_step_ws(int64_t rows, int32_t kx, int32_t hp, const float* x, int64_t ldx,
+                              const float* h_prev, const float* c_prev, const float* wimg, const float* bias,
+                              float* h_out, float* c_out, float* gates, void* stream) {
+    DGNN_CHECK_ARG(rows >= 0 && kx % 4 == 0 && ldx % 4 == 0, "lstm_forward_step_ws: bad sizes");
+    if (rows == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (hp) {
+        case 16: return lstm_fwd_ws_t<16>(rows, kx, x, ldx, h_prev, c_prev, wimg, bias, h_out, c_out, gates, st);
+        case 32: return lstm_fwd_ws_t<32>(rows, kx, x, ldx, h_prev, c_prev, wimg, bias, h_out, c_out, gates, st);
+        case 64: return lstm_fwd_ws_t<64>(rows, kx, x, ldx, h_prev, c_prev, wimg, bias, h_out, c_out, gates, st);
+    }
+    set_error("lstm_forward_step_ws: unsupported hp %d (use dgnn_lstm_forward_step_tc)", hp);
+    return DGNN_EUNSUPPORTED;
+}
+
+int dgnn_lstm_backward_step_ws(int64_t rows, int32_t kx, int32_t hp, const float* dy, const float* dh_in,
+                               const float* dc_in, float* gates, const float* c_prev, const float* c_new,
+                               const float* wimg, float* dx, int64_t lddx, float* dh_out, float* dc_out,
+                               void* stream) {
+    DGNN_CHECK_ARG(rows >= 0 && kx % 4 == 0 && lddx % 4 == 0, "lstm_backward_step_ws: bad sizes");
+    if (rows == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (hp) {
+        case 16: return lstm_bwd_ws_t<16>(rows, kx, dy, dh_in, dc_in, gates, c_prev, c_new, wimg, dx, lddx, dh_out, dc_out, st);
+        case 32: return lstm_bwd_ws_t<32>(rows, kx, dy, dh_in, dc_in, gates, c_prev, c_new, wimg, dx, lddx, dh_out, dc_out, st);
+        case 64: return lstm_bwd_ws_t<64>(rows, kx, dy, dh_in, dc_in, gates, c_prev, c_new, wimg, dx, lddx, dh_out, dc_out, st);
+    }
+    set_error("lstm_backward_step_ws: unsupported hp %d (use dgnn_lstm_backward_step_tc)", hp);
+    return DGNN_EUNSUPPORTED;
+}
+
+}  // extern "C"

@@ -34,6 +34,7 @@ from .materialize import Materializer, SnapshotEncoding
 from .params import DeviceParams, ParamLayout
 
 F32 = 4
+WARP_SPECIALIZED = True
 
 
 class Plan:
@@ -253,7 +254,8 @@ class Rank:
             self._mprod_forward(b, l)
             return
         if eng.tensor_cores:
-            fn, wop = "dgnn_lstm_forward_step_tc", eng.params.image(f"lstm{l}.fwd")
+            fn = "dgnn_lstm_forward_step_ws" if (eng.warp_specialized and Ly.ho <= 64) else "dgnn_lstm_forward_step_tc"
+            wop = eng.params.image(f"lstm{l}.fwd")
         else:
             fn, wop = "dgnn_lstm_forward_step", eng.params.w(f"lstm{l}.wcat")
         bias = eng.params.w(f"lstm{l}.b")
@@ -373,8 +375,9 @@ class Rank:
             dh_out = self.vm(dh_buf, ho, step % 2)
             dc_out = self.vm(dc_buf, ho, step % 2)
             if use_tc:
-                call("dgnn_lstm_backward_step_tc", NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates),
-                     ptr(c_prev), ptr(c_new), ptr(wt), ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
+                fn = "dgnn_lstm_backward_step_ws" if eng.warp_specialized else "dgnn_lstm_backward_step_tc"
+                call(fn, NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates), ptr(c_prev), ptr(c_new), ptr(wt),
+                     ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
             else:
                 call("dgnn_lstm_backward_step", NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates),
                      ptr(c_prev), ptr(c_new), ptr(wt), ptr(gates), ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
@@ -509,6 +512,8 @@ class Engine:
         # tensor_cores: LSTM gate GEMMs on tcgen05 (3xTF32); False selects the
         # SIMT fp32 kernels (kept as the measured baseline and for A/B tests)
         self.tensor_cores = bool(tensor_cores)
+        # persistent warp-specialised tcgen05 step kernels (else one CTA per tile)
+        self.warp_specialized = WARP_SPECIALIZED
         if cfg.architecture not in ("cd-gcn", "tm-gcn"):
             raise ConfigError(f"architecture {cfg.architecture!r} is outside this package's hot path")
         self.cfg = cfg

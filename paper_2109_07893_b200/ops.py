@@ -289,7 +289,7 @@ def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np
     return gw.view(kx + hp, 4 * hp).cpu().numpy(), gb.cpu().numpy()
 
 
-def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True):
+def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True, warp_specialized: bool = True):
     """fp32 device LSTM over a block (training.py:370-391).  Returns
     (ys, (h, c), cache) with a device cache for lstm_block_backward."""
     dev = _dev()
@@ -314,7 +314,7 @@ def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True):
         cn = torch.zeros(rows, hp, device=dev)
         g = torch.zeros(rows, 4 * hp, device=dev)
         if img is not None:
-            call("dgnn_lstm_forward_step_tc", rows, kx, hp, ptr(x), kx, ptr(h), ptr(c), ptr(img), ptr(bb),
+            call("dgnn_lstm_forward_step_ws" if (warp_specialized and hp <= 64) else "dgnn_lstm_forward_step_tc", rows, kx, hp, ptr(x), kx, ptr(h), ptr(c), ptr(img), ptr(bb),
                  ptr(hn), ptr(cn), ptr(g), st)
         else:
             call("dgnn_lstm_forward_step", rows, kx, hp, ptr(x), kx, ptr(h), ptr(c), ptr(wc), ptr(bb), ptr(hn),
@@ -328,7 +328,8 @@ def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True):
     return ys, (h[:, :H].double().cpu().numpy(), c[:, :H].double().cpu().numpy()), cache
 
 
-def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bool = True):
+def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bool = True,
+                        warp_specialized: bool = True):
     """fp32 device BPTT over a block (training.py:394-427)."""
     dev = _dev()
     H, hp, kx, rows = cache["H"], cache["hp"], cache["kx"], cache["rows"]
@@ -357,7 +358,8 @@ def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bo
         dc2 = torch.zeros(rows, hp, device=dev)
         if bimg is not None:
             dz.copy_(cache["g"][i])      # the tensor-core step writes dz over the gate cache
-            call("dgnn_lstm_backward_step_tc", rows, kx, hp, ptr(dy), ptr(dh), ptr(dc), ptr(dz), ptr(c_prev),
+            call("dgnn_lstm_backward_step_ws" if warp_specialized else "dgnn_lstm_backward_step_tc", rows, kx, hp,
+                 ptr(dy), ptr(dh), ptr(dc), ptr(dz), ptr(c_prev),
                  ptr(cache["c"][i]), ptr(bimg), ptr(dx), kx, ptr(dh2), ptr(dc2), st)
         else:
             call("dgnn_lstm_backward_step", rows, kx, hp, ptr(dy), ptr(dh), ptr(dc), ptr(cache["g"][i]),

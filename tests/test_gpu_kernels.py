@@ -322,3 +322,35 @@ def test_lstm_weight_grad_tc_long_reduction(hp, kx):
     assert np.abs(gw - ref).max() / scale.max() < 2e-5
     assert (np.abs(gw - ref) / scale).max() < 5e-5
     assert np.allclose(gb, dz.astype(np.float64).sum(0), rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("H", [16, 32, 64])
+def test_warp_specialized_lstm_steps_match_tc_bitwise(H):
+    """Persistent warp-specialised kernels (several tiles per CTA, both TMEM
+    buffers in use) issue the same MMAs in the same order as the one-tile
+    kernels: outputs must be bit-identical."""
+    rng = np.random.default_rng(30 + H)
+    rows, fin = 128 * 148 * 2 + 77, 2 * H
+
+    class Cell:
+        wx = rng.uniform(-0.3, 0.3, (fin, 4 * H))
+        wh = rng.uniform(-0.3, 0.3, (H, 4 * H))
+        b = rng.uniform(-0.1, 0.1, 4 * H)
+
+    ts = [0, 1]
+    xs = {t: np.maximum(rng.standard_normal((rows, fin)), 0) for t in ts}
+    st = (rng.standard_normal((rows, H)) * 0.2, rng.standard_normal((rows, H)) * 0.2)
+    ys_w, (hw, cw), cache_w = pk.lstm_block_forward(Cell, st, ts, xs, warp_specialized=True)
+    ys_t, (ht, ct), cache_t = pk.lstm_block_forward(Cell, st, ts, xs, warp_specialized=False)
+    for t in ts:
+        assert np.array_equal(ys_w[t], ys_t[t])
+    assert np.array_equal(cw, ct)
+    dys = {t: rng.standard_normal((rows, H)) for t in ts}
+    dst = (rng.standard_normal((rows, H)), rng.standard_normal((rows, H)))
+    dxw, dsw, dcw = pk.lstm_block_backward(Cell, ts, cache_w, dys, dst, warp_specialized=True)
+    dxt, dst_t, dct = pk.lstm_block_backward(Cell, ts, cache_t, dys, dst, warp_specialized=False)
+    for t in ts:
+        assert np.array_equal(dxw[t], dxt[t])
+    assert np.array_equal(dsw[0], dst_t[0]) and np.array_equal(dsw[1], dst_t[1])
+    for k in dcw:
+        assert np.array_equal(dcw[k], dct[k])
