@@ -169,34 +169,56 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_fwd_ws_kernel(
     const uint32_t b_bytes = 2 * N * 64;
 
     if (warp < wsk::NPROD) {
+        // cp.async the raw fp32 chunk straight into the (swizzled) hi tile,
+        // LA chunks ahead, then split it in place: deep memory-level
+        // parallelism without holding the data in registers.
+        constexpr int LA = wsk::STAGES - 1;
         const int ptid = threadIdx.x;
-        auto fetch = [&](int tile, int ch, float4 (&v)[ITEMS]) {
+        const int my_tiles = blockIdx.x < ntiles ? (int)cdiv(ntiles - blockIdx.x, gridDim.x) : 0;
+        const uint32_t G = (uint32_t)my_tiles * nch;
+        auto issue = [&](uint32_t g) {
+            const int tile = blockIdx.x + (int)(g / nch) * gridDim.x;
+            const int ch = (int)(g % nch);
+            const int s = g % wsk::STAGES;
+            const uint32_t j = g / wsk::STAGES;
+            if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
+            if (ptid == 0) {
+                mbar_arrive_expect_tx(&bars->full_b[s], b_bytes);
+                bulk_g2s(sm.b(s), reinterpret_cast<const char*>(img) + (size_t)ch * b_bytes, b_bytes,
+                         &bars->full_b[s]);
+            }
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const int idx = ptid + 128 * i;
-                const int64_t g = (int64_t)tile * wsk::BM + (idx >> 2);
-                const int k = ch * wsk::KC + 4 * (idx & 3);
-                float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (g < rows && k < K)
-                    val = k < kx ? __ldg(reinterpret_cast<const float4*>(x + g * ldx + k))
-                                 : __ldg(reinterpret_cast<const float4*>(hprev + g * HP + (k - kx)));
-                v[i] = val;
+                const int r = idx >> 2, q = idx & 3;
+                const int64_t gr = (int64_t)tile * wsk::BM + r;
+                const int k = ch * wsk::KC + 4 * q;
+                const bool ok = gr < rows && k < K;
+                const float* src = !ok ? x : (k < kx ? x + gr * ldx + k : hprev + gr * HP + (k - kx));
+                cp_async16(sm.a_hi(s) + sw64(r, q), src, ok ? 16u : 0u);
             }
         };
-        float4 cur[ITEMS], nxt[ITEMS];
-        uint32_t gc = 0;
-        int tile = blockIdx.x, ch = 0;
-        if (tile < ntiles) fetch(tile, 0, cur);
-        while (tile < ntiles) {
-            int nt = tile, nc = ch + 1;
-            if (nc == nch) { nc = 0; nt += gridDim.x; }
-            if (nt < ntiles) fetch(nt, nc, nxt);
-            ws_produce<ITEMS>(sm, bars, gc, img, ch, b_bytes, cur);
-            ++gc;
-            tile = nt;
-            ch = nc;
+        for (uint32_t g = 0; g < (G < (uint32_t)LA ? G : (uint32_t)LA); ++g) {
+            issue(g);
+            cp_async_commit();
+        }
+        for (uint32_t g = 0; g < G; ++g) {
+            if (g + LA < G) issue(g + LA);
+            cp_async_commit();
+            cp_async_wait<LA>();
+            const int s = g % wsk::STAGES;
 #pragma unroll
-            for (int i = 0; i < ITEMS; ++i) cur[i] = nxt[i];
+            for (int i = 0; i < ITEMS; ++i) {
+                const int idx = ptid + 128 * i;
+                const uint32_t off = sw64(idx >> 2, idx & 3);
+                float4 hi, lo;
+                split4(lds128(sm.a_hi(s) + off), hi, lo);
+                sts128(sm.a_hi(s) + off, hi);
+                sts128(sm.a_lo(s) + off, lo);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if ((ptid & 31) == 0) mbar_arrive(&bars->full_a[s]);
         }
     } else if (warp == wsk::MMA_WARP) {
         if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
