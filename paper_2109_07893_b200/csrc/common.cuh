@@ -47,7 +47,23 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-__device__ __forceinline__ float sigmoidf_acc(float x) { return 1.0f / (1.0f + expf(-x)); }
+// LSTM gate activations, shared by every LSTM kernel (SIMT, tensor-core,
+// warp-specialised) so their results stay bitwise equal.  MUFU ex2/rcp:
+// a few ulp relative for sigmoid, <= ~1e-7 absolute for tanh -- the same
+// order as the tensor-core accumulation rounding, far inside the 1e-4
+// parity budget -- at a quarter of the instructions of expf + IEEE divide.
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float act_sigmoid(float x) { return rcp_approx(1.0f + ex2_approx(-1.4426950408889634f * x)); }
+__device__ __forceinline__ float act_tanh(float x) { return fmaf(2.0f, act_sigmoid(2.0f * x), -1.0f); }
 
 // device-wide exclusive scan (in place), implemented in graph.cu
 size_t scan_workspace_bytes(int64_t n);

@@ -101,13 +101,13 @@ __global__ void __launch_bounds__(256) lstm_fwd_kernel(int64_t rows, int kx, con
         float hv[2], cv[2], gi[2], gf[2], go[2], gg[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            gi[j] = sigmoidf_acc(acc[i][0 + j] + bz[0 + j]);
-            gf[j] = sigmoidf_acc(acc[i][2 + j] + bz[2 + j]);
-            go[j] = sigmoidf_acc(acc[i][4 + j] + bz[4 + j]);
-            gg[j] = tanhf(acc[i][6 + j] + bz[6 + j]);
+            gi[j] = act_sigmoid(acc[i][0 + j] + bz[0 + j]);
+            gf[j] = act_sigmoid(acc[i][2 + j] + bz[2 + j]);
+            go[j] = act_sigmoid(acc[i][4 + j] + bz[4 + j]);
+            gg[j] = act_tanh(acc[i][6 + j] + bz[6 + j]);
             const float c_old = j == 0 ? cp.x : cp.y;
             cv[j] = gf[j] * c_old + gi[j] * gg[j];
-            hv[j] = go[j] * tanhf(cv[j]);
+            hv[j] = go[j] * act_tanh(cv[j]);
         }
         st2(hout + g * HP + u0, hv[0], hv[1]);
         st2(cout + g * HP + u0, cv[0], cv[1]);
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) lstm_bwd_kernel(int64_t rows, int kx, con
             const float* gr = gates + g * C::NC + u;
             const float gi = gr[0], gf = gr[HP], go = gr[2 * HP], gg = gr[3 * HP];
             const float cp = cprev[g * HP + u], cn = cnew[g * HP + u];
-            const float tc = tanhf(cn);
+            const float tc = act_tanh(cn);
             const float dh = (dy ? dy[g * HP + u] : 0.f) + dh_in[g * HP + u];
             const float d_o = dh * tc;
             const float dc = dh * go * (1.f - tc * tc) + dc_in[g * HP + u];

@@ -265,12 +265,12 @@ __global__ void __launch_bounds__(256, (HP <= 64 ? 2 : 1)) lstm_fwd_tc_kernel(
         *reinterpret_cast<float4*>(cp + 4) = __ldg(reinterpret_cast<const float4*>(cprev + row * HP + u0 + 4));
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            gi[j] = sigmoidf_acc(z[0][j] + __ldg(bias + 0 * HP + u0 + j));
-            gf[j] = sigmoidf_acc(z[1][j] + __ldg(bias + 1 * HP + u0 + j));
-            go[j] = sigmoidf_acc(z[2][j] + __ldg(bias + 2 * HP + u0 + j));
-            gg[j] = tanhf(z[3][j] + __ldg(bias + 3 * HP + u0 + j));
+            gi[j] = act_sigmoid(z[0][j] + __ldg(bias + 0 * HP + u0 + j));
+            gf[j] = act_sigmoid(z[1][j] + __ldg(bias + 1 * HP + u0 + j));
+            go[j] = act_sigmoid(z[2][j] + __ldg(bias + 2 * HP + u0 + j));
+            gg[j] = act_tanh(z[3][j] + __ldg(bias + 3 * HP + u0 + j));
             cv[j] = gf[j] * cp[j] + gi[j] * gg[j];
-            hv[j] = go[j] * tanhf(cv[j]);
+            hv[j] = go[j] * act_tanh(cv[j]);
         }
         float4* ho = reinterpret_cast<float4*>(hout + row * HP + u0);
         float4* co = reinterpret_cast<float4*>(cout + row * HP + u0);
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(256, 2) lstm_bwd_tc_kernel(
             const int64_t g = row0 + (idx >> 2);
             if (g >= rows) return make_float4(0.f, 0.f, 0.f, 0.f);
             const int u = 4 * ch + (idx & 3);
-            const float tcn = tanhf(p.cn);
+            const float tcn = act_tanh(p.cn);
             const float d_o = p.dh * tcn;
             const float dc = p.dh * p.go * (1.f - tcn * tcn) + p.dc;
             const float df = dc * p.cp, di = dc * p.gg, dg = dc * p.gi;

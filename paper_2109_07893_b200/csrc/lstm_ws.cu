@@ -26,12 +26,32 @@ namespace wsk {
 constexpr int BM = 128;
 constexpr int KC = 16;
 constexpr int A_TILE = BM * 64;
-constexpr int NPROD = 4;
-constexpr int MMA_WARP = NPROD;
-constexpr int NEPI = 8;
-constexpr int THREADS = 32 * (NPROD + 1 + NEPI);
 constexpr int STAGES = 4;
+// Bottleneck probe (scripts/ws_probe.cu builds with -DDGNN_WS_PROBE=mask):
+// 1 skip MMAs, 2 zero-fill activations (no HBM reads), 4 skip weight copies,
+// 8 epilogue without cell math / stores, 16 without stores, 32 without cell
+// math.  Always 0 in the library.
+#ifndef DGNN_WS_PROBE
+#define DGNN_WS_PROBE 0
+#endif
+constexpr int PROBE = DGNN_WS_PROBE;
 }  // namespace wsk
+
+// Warp roles: NP producer warps, one MMA warp, NE epilogue warps (a multiple
+// of 4 so every TMEM lane quarter has an owner).
+template <int NP, int NE>
+struct WsRoles {
+    static constexpr int NPROD = NP;
+    static constexpr int MMA_WARP = NP;
+    static constexpr int NEPI = NE;
+    static constexpr int THREADS = 32 * (NP + 1 + NE);
+    static constexpr int NPT = 32 * NP;   // producer threads
+};
+// forward: heavy cell epilogue -- 16 epilogue warps (each a quarter of the
+// units of its TMEM lane quarter) when every warp still gets >= 8 units
+template <int HP>
+using FwdRoles = WsRoles<4, (HP >= 32 ? 16 : 8)>;
+using BwdRoles = WsRoles<8, 4>;   // heavy dz producer, store-only epilogue
 
 __host__ __device__ constexpr int ws_tmem_cols(int n2) {
     return n2 <= 32 ? 32 : (n2 <= 64 ? 64 : (n2 <= 128 ? 128 : (n2 <= 256 ? 256 : 512)));
@@ -55,6 +75,7 @@ inline size_t ws_smem_bytes(int n) {
     return (size_t)wsk::STAGES * (2 * wsk::A_TILE + 2 * n * 64) + 1024 + sizeof(WsBars) + 64;
 }
 
+template <class R>
 __device__ __forceinline__ WsBars* ws_setup(WsSmem& sm, int n) {
     extern __shared__ uint8_t ws_smem_raw[];
     const uint32_t raw = smem_u32(ws_smem_raw);
@@ -63,16 +84,16 @@ __device__ __forceinline__ WsBars* ws_setup(WsSmem& sm, int n) {
     sm.stage = 2 * wsk::A_TILE + 2 * n * 64;
     WsBars* bars = reinterpret_cast<WsBars*>(ws_smem_raw + pad + wsk::STAGES * sm.stage);
     const int warp = threadIdx.x >> 5;
-    if (warp == wsk::MMA_WARP) tmem_alloc(&bars->tmem, ws_tmem_cols(2 * n));
+    if (warp == R::MMA_WARP) tmem_alloc(&bars->tmem, ws_tmem_cols(2 * n));
     if (threadIdx.x == 0) {
         for (int s = 0; s < wsk::STAGES; ++s) {
-            mbar_init(&bars->full_a[s], wsk::NPROD);
+            mbar_init(&bars->full_a[s], R::NPROD);
             mbar_init(&bars->full_b[s], 1);
             mbar_init(&bars->empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->accfull[a], 1);
-            mbar_init(&bars->accempty[a], wsk::NEPI);
+            mbar_init(&bars->accempty[a], R::NEPI);
         }
         fence_mbar_init();
     }
@@ -82,10 +103,11 @@ __device__ __forceinline__ WsBars* ws_setup(WsSmem& sm, int n) {
     return bars;
 }
 
+template <class R>
 __device__ __forceinline__ void ws_teardown(WsBars* bars, int n) {
     fence_before();
     __syncthreads();
-    if ((threadIdx.x >> 5) == wsk::MMA_WARP) tmem_dealloc(bars->tmem, ws_tmem_cols(2 * n));
+    if ((threadIdx.x >> 5) == R::MMA_WARP) tmem_dealloc(bars->tmem, ws_tmem_cols(2 * n));
 }
 
 // MMA issuer: for every tile of this CTA, all K chunks into accumulator a.
@@ -111,6 +133,7 @@ __device__ __forceinline__ void ws_mma_loop(const WsSmem& sm, WsBars* bars, int 
                     const uint32_t idesc = idesc_tf32(wsk::BM, nn);
                     const uint64_t bhi = sdesc(sm.b(s) + n0 * 64 + 32 * kk, 512, kSW64);
                     const uint64_t blo = sdesc(sm.b(s) + n * 64 + n0 * 64 + 32 * kk, 512, kSW64);
+                    if (wsk::PROBE & 1) continue;
                     mma_tf32(d + n0, ahi, bhi, idesc, (ch == 0 && kk == 0) ? 0u : 1u);
                     mma_tf32(d + n0, ahi, blo, idesc, 1u);
                     mma_tf32(d + n0, alo, bhi, idesc, 1u);
@@ -124,11 +147,11 @@ __device__ __forceinline__ void ws_mma_loop(const WsSmem& sm, WsBars* bars, int 
 
 // Producer side of one chunk: wait for the stage, launch the weight copy,
 // store the activation split.  `vals[i]` holds the 4 fp32 of item
-// ptid + 128 i (row item / 4, column group item % 4).
-template <int ITEMS>
+// ptid + NPT i (row item / 4, column group item % 4).
+template <class R, int ITEMS>
 __device__ __forceinline__ void ws_produce(const WsSmem& sm, WsBars* bars, uint32_t gc, const float* img, int ch,
                                            uint32_t b_bytes, const float4 (&vals)[ITEMS]) {
-    const int ptid = threadIdx.x;   // producers are threads 0 .. 127
+    const int ptid = threadIdx.x;   // producers are threads 0 .. NPT-1
     const int s = gc % wsk::STAGES;
     const uint32_t j = gc / wsk::STAGES;
     if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
@@ -138,7 +161,7 @@ __device__ __forceinline__ void ws_produce(const WsSmem& sm, WsBars* bars, uint3
     }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const int idx = ptid + 128 * i;
+        const int idx = ptid + R::NPT * i;
         const int r = idx >> 2, q = idx & 3;
         float4 hi, lo;
         split4(vals[i], hi, lo);
@@ -154,21 +177,22 @@ __device__ __forceinline__ void ws_produce(const WsSmem& sm, WsBars* bars, uint3
 // forward
 
 template <int HP>
-__global__ void __launch_bounds__(wsk::THREADS, 1) lstm_fwd_ws_kernel(
+__global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
     int64_t rows, int kx, const float* __restrict__ x, int64_t ldx, const float* __restrict__ hprev,
     const float* __restrict__ cprev, const float* __restrict__ img, const float* __restrict__ bias,
     float* __restrict__ hout, float* __restrict__ cout, float* __restrict__ gates) {
     constexpr int N = 4 * HP;
-    constexpr int ITEMS = wsk::BM * 4 / (wsk::NPROD * 32);   // 4
+    using R = FwdRoles<HP>;
+    constexpr int ITEMS = wsk::BM * 4 / R::NPT;   // 4
     WsSmem sm;
-    WsBars* bars = ws_setup(sm, N);
+    WsBars* bars = ws_setup<R>(sm, N);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int K = kx + HP;
     const int nch = (K + wsk::KC - 1) / wsk::KC;
     const uint32_t b_bytes = 2 * N * 64;
 
-    if (warp < wsk::NPROD) {
+    if (warp < R::NPROD) {
         // cp.async the raw fp32 chunk straight into the (swizzled) hi tile,
         // LA chunks ahead, then split it in place: deep memory-level
         // parallelism without holding the data in registers.
@@ -183,33 +207,38 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_fwd_ws_kernel(
             const uint32_t j = g / wsk::STAGES;
             if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
             if (ptid == 0) {
-                mbar_arrive_expect_tx(&bars->full_b[s], b_bytes);
-                bulk_g2s(sm.b(s), reinterpret_cast<const char*>(img) + (size_t)ch * b_bytes, b_bytes,
-                         &bars->full_b[s]);
+                if (wsk::PROBE & 4) {
+                    mbar_arrive(&bars->full_b[s]);
+                } else {
+                    mbar_arrive_expect_tx(&bars->full_b[s], b_bytes);
+                    bulk_g2s(sm.b(s), reinterpret_cast<const char*>(img) + (size_t)ch * b_bytes, b_bytes,
+                             &bars->full_b[s]);
+                }
             }
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int idx = ptid + 128 * i;
+                const int idx = ptid + R::NPT * i;
                 const int r = idx >> 2, q = idx & 3;
                 const int64_t gr = (int64_t)tile * wsk::BM + r;
                 const int k = ch * wsk::KC + 4 * q;
-                const bool ok = gr < rows && k < K;
+                const bool ok = gr < rows && k < K && !(wsk::PROBE & 2);
                 const float* src = !ok ? x : (k < kx ? x + gr * ldx + k : hprev + gr * HP + (k - kx));
                 cp_async16(sm.a_hi(s) + sw64(r, q), src, ok ? 16u : 0u);
             }
         };
-        for (uint32_t g = 0; g < (G < (uint32_t)LA ? G : (uint32_t)LA); ++g) {
-            issue(g);
+        for (uint32_t g = 0; g < (uint32_t)LA; ++g) {
+            if (g < G) issue(g);
             cp_async_commit();
         }
+        // Split chunk g before waiting for the stage chunk g + LA reuses:
+        // that wait is on the MMAs of chunk g - 1, and holding the split of
+        // an already-landed chunk behind it would serialise MMA and producer.
         for (uint32_t g = 0; g < G; ++g) {
-            if (g + LA < G) issue(g + LA);
-            cp_async_commit();
-            cp_async_wait<LA>();
+            cp_async_wait<LA - 1>();
             const int s = g % wsk::STAGES;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int idx = ptid + 128 * i;
+                const int idx = ptid + R::NPT * i;
                 const uint32_t off = sw64(idx >> 2, idx & 3);
                 float4 hi, lo;
                 split4(lds128(sm.a_hi(s) + off), hi, lo);
@@ -219,24 +248,27 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_fwd_ws_kernel(
             fence_async_smem();
             __syncwarp();
             if ((ptid & 31) == 0) mbar_arrive(&bars->full_a[s]);
+            if (g + LA < G) issue(g + LA);
+            cp_async_commit();
         }
-    } else if (warp == wsk::MMA_WARP) {
+    } else if (warp == R::MMA_WARP) {
         if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
         __syncwarp();
     } else {
-        const int e = warp - wsk::MMA_WARP - 1;
-        const int q = warp & 3, half = e >> 2;
+        const int e = warp - R::MMA_WARP - 1;
+        constexpr int UPW = HP / (R::NEPI / 4);   // units per epilogue warp
+        const int q = warp & 3, part = e >> 2;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const uint32_t a = it & 1, u = it >> 1;
             const int64_t row = (int64_t)tile * wsk::BM + 32 * q + lane;
             const bool valid = row < rows;
-            float cp[HP / 2];
+            float cp[UPW];
 #pragma unroll
-            for (int i = 0; i < HP / 8; ++i) {
+            for (int i = 0; i < UPW / 4; ++i) {
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (valid) v = __ldg(reinterpret_cast<const float4*>(cprev + row * HP + half * (HP / 2) + 4 * i));
+                if (valid) v = __ldg(reinterpret_cast<const float4*>(cprev + row * HP + part * UPW + 4 * i));
                 cp[4 * i] = v.x;
                 cp[4 * i + 1] = v.y;
                 cp[4 * i + 2] = v.z;
@@ -246,22 +278,34 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_fwd_ws_kernel(
             fence_after();
             const uint32_t tq = bars->tmem + lane_off + a * N;
 #pragma unroll
-            for (int g8 = 0; g8 < HP / 16; ++g8) {
-                const int u0 = half * (HP / 2) + 8 * g8;
+            for (int g8 = 0; g8 < UPW / 8; ++g8) {
+                const int u0 = part * UPW + 8 * g8;
                 float z[4][8];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) tmem_ld8(tq + g * HP + u0, z[g]);
                 tmem_wait_ld();
-                if (!valid) continue;
+                if (!valid || (wsk::PROBE & 8)) continue;
                 float hv[8], cv[8], gi[8], gf[8], go[8], gg[8];
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
-                    gi[jj] = sigmoidf_acc(z[0][jj] + __ldg(bias + 0 * HP + u0 + jj));
-                    gf[jj] = sigmoidf_acc(z[1][jj] + __ldg(bias + 1 * HP + u0 + jj));
-                    go[jj] = sigmoidf_acc(z[2][jj] + __ldg(bias + 2 * HP + u0 + jj));
-                    gg[jj] = tanhf(z[3][jj] + __ldg(bias + 3 * HP + u0 + jj));
+                    if (wsk::PROBE & 32) {   // probe: stores without the cell math
+                        gi[jj] = z[0][jj]; gf[jj] = z[1][jj]; go[jj] = z[2][jj]; gg[jj] = z[3][jj];
+                        cv[jj] = z[0][jj] + cp[8 * g8 + jj]; hv[jj] = z[1][jj];
+                        continue;
+                    }
+                    gi[jj] = act_sigmoid(z[0][jj] + __ldg(bias + 0 * HP + u0 + jj));
+                    gf[jj] = act_sigmoid(z[1][jj] + __ldg(bias + 1 * HP + u0 + jj));
+                    go[jj] = act_sigmoid(z[2][jj] + __ldg(bias + 2 * HP + u0 + jj));
+                    gg[jj] = act_tanh(z[3][jj] + __ldg(bias + 3 * HP + u0 + jj));
                     cv[jj] = gf[jj] * cp[8 * g8 + jj] + gi[jj] * gg[jj];
-                    hv[jj] = go[jj] * tanhf(cv[jj]);
+                    hv[jj] = go[jj] * act_tanh(cv[jj]);
+                }
+                if (wsk::PROBE & 16) {   // probe: cell math without the stores
+                    float acc = 0.f;
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) acc += hv[jj] + cv[jj] + gi[jj] + gf[jj] + go[jj] + gg[jj];
+                    if (acc == 12345.f) hout[row] = acc;
+                    continue;
                 }
                 float4* ho = reinterpret_cast<float4*>(hout + row * HP + u0);
                 float4* co = reinterpret_cast<float4*>(cout + row * HP + u0);
@@ -285,39 +329,40 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_fwd_ws_kernel(
             if (lane == 0) mbar_arrive(&bars->accempty[a]);
         }
     }
-    ws_teardown(bars, N);
+    ws_teardown<R>(bars, N);
 }
 
 // ---------------------------------------------------------------------------
 // backward: producers compute dz (unit-major K chunk = 4 units x 4 gates)
 
 template <int HP>
-__global__ void __launch_bounds__(wsk::THREADS, 1) lstm_bwd_ws_kernel(
+__global__ void __launch_bounds__(BwdRoles::THREADS, 1) lstm_bwd_ws_kernel(
     int64_t rows, int kx, int N, const float* __restrict__ dy, const float* __restrict__ dh_in,
     const float* __restrict__ dc_in, float* gates, const float* __restrict__ cprev, const float* __restrict__ cnew,
     const float* __restrict__ img, float* __restrict__ dx, int64_t lddx, float* __restrict__ dh_out,
     float* __restrict__ dc_out) {
     constexpr int NC = 4 * HP;
-    constexpr int ITEMS = wsk::BM * 4 / (wsk::NPROD * 32);   // 4 (row, unit) items per producer thread
+    using R = BwdRoles;
+    constexpr int ITEMS = wsk::BM * 4 / R::NPT;   // (row, unit) items per producer thread
     WsSmem sm;
-    WsBars* bars = ws_setup(sm, N);
+    WsBars* bars = ws_setup<R>(sm, N);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int nch = HP / 4;
     const uint32_t b_bytes = 2 * N * 64;
 
-    if (warp < wsk::NPROD) {
+    if (warp < R::NPROD) {
         const int ptid = threadIdx.x;
         struct Cell {
-            float gi, gf, go, gg, cp, cn, dh, dc;
+            float gi, gf, go, gg, cp, cn, dh, dy, dc;   // raw loads only: no arithmetic before use
         };
         auto fetch = [&](int tile, int ch, Cell (&v)[ITEMS]) {
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int idx = ptid + 128 * i;
+                const int idx = ptid + R::NPT * i;
                 const int64_t g = (int64_t)tile * wsk::BM + (idx >> 2);
                 const int u = 4 * ch + (idx & 3);
-                Cell p{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                Cell p{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 if (g < rows) {
                     const float* gr = gates + g * NC + u;
                     const int64_t o = g * HP + u;
@@ -327,37 +372,44 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_bwd_ws_kernel(
                     p.gg = gr[3 * HP];
                     p.cp = __ldg(cprev + o);
                     p.cn = __ldg(cnew + o);
-                    p.dh = (dy ? __ldg(dy + o) : 0.f) + __ldg(dh_in + o);
+                    p.dh = __ldg(dh_in + o);
+                    if (dy) p.dy = __ldg(dy + o);
                     p.dc = __ldg(dc_in + o);
                 }
                 v[i] = p;
             }
         };
-        Cell cur[ITEMS], nxt[ITEMS];
-        float4 vals[ITEMS];
-        uint32_t gc = 0;
-        int tile = blockIdx.x, ch = 0;
-        if (tile < ntiles) fetch(tile, 0, cur);
-        while (tile < ntiles) {
-            int nt = tile, nc = ch + 1;
-            if (nc == nch) { nc = 0; nt += gridDim.x; }
-            if (nt < ntiles) fetch(nt, nc, nxt);
+        // Three register buffers, two chunks of loads in flight while the
+        // third is turned into dz; the loop is unrolled by three so every
+        // buffer keeps a fixed role (no register moves that would wait on
+        // outstanding loads).
+        const int my_tiles = blockIdx.x < ntiles ? (int)cdiv(ntiles - blockIdx.x, gridDim.x) : 0;
+        const uint32_t G = (uint32_t)my_tiles * nch;
+        auto fetch_g = [&](uint32_t g, Cell (&v)[ITEMS]) {
+            fetch(blockIdx.x + (int)(g / nch) * gridDim.x, (int)(g % nch), v);
+        };
+        auto step = [&](uint32_t g, Cell (&cur)[ITEMS], Cell (&fb)[ITEMS]) {
+            if (g + 2 < G) fetch_g(g + 2, fb);
+            const int tile = blockIdx.x + (int)(g / nch) * gridDim.x;
+            const int ch = (int)(g % nch);
+            float4 vals[ITEMS];
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int idx = ptid + 128 * i;
-                const int64_t g = (int64_t)tile * wsk::BM + (idx >> 2);
+                const int idx = ptid + R::NPT * i;
+                const int64_t row = (int64_t)tile * wsk::BM + (idx >> 2);
                 const int u = 4 * ch + (idx & 3);
                 const Cell& p = cur[i];
                 float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (g < rows) {
-                    const float tcn = tanhf(p.cn);
-                    const float d_o = p.dh * tcn;
-                    const float dc = p.dh * p.go * (1.f - tcn * tcn) + p.dc;
+                if (row < rows) {
+                    const float dhv = p.dy + p.dh;
+                    const float tcn = act_tanh(p.cn);
+                    const float d_o = dhv * tcn;
+                    const float dc = dhv * p.go * (1.f - tcn * tcn) + p.dc;
                     const float df = dc * p.cp, di = dc * p.gg, dg = dc * p.gi;
-                    dc_out[g * HP + u] = dc * p.gf;
+                    dc_out[row * HP + u] = dc * p.gf;
                     z = make_float4(di * p.gi * (1.f - p.gi), df * p.gf * (1.f - p.gf), d_o * p.go * (1.f - p.go),
                                     dg * (1.f - p.gg * p.gg));
-                    float* gr = gates + g * NC + u;   // dz replaces the gate cache
+                    float* gr = gates + row * NC + u;   // dz replaces the gate cache
                     gr[0] = z.x;
                     gr[HP] = z.y;
                     gr[2 * HP] = z.z;
@@ -365,18 +417,21 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_bwd_ws_kernel(
                 }
                 vals[i] = z;
             }
-            ws_produce<ITEMS>(sm, bars, gc, img, ch, b_bytes, vals);
-            ++gc;
-            tile = nt;
-            ch = nc;
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i) cur[i] = nxt[i];
+            ws_produce<R, ITEMS>(sm, bars, g, img, ch, b_bytes, vals);
+        };
+        Cell b0[ITEMS], b1[ITEMS], b2[ITEMS];
+        if (G > 0) fetch_g(0, b0);
+        if (G > 1) fetch_g(1, b1);
+        for (uint32_t g = 0; g < G; g += 3) {
+            step(g, b0, b2);
+            if (g + 1 < G) step(g + 1, b1, b0);
+            if (g + 2 < G) step(g + 2, b2, b1);
         }
-    } else if (warp == wsk::MMA_WARP) {
+    } else if (warp == R::MMA_WARP) {
         if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
         __syncwarp();
     } else {
-        const int e = warp - wsk::MMA_WARP - 1;
+        const int e = warp - R::MMA_WARP - 1;
         const int q = warp & 3, half = e >> 2;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
         const int K = kx + HP;
@@ -387,7 +442,7 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_bwd_ws_kernel(
             mbar_wait(&bars->accfull[a], u & 1);
             fence_after();
             const uint32_t tq = bars->tmem + lane_off + a * N;
-            for (int c0 = half * 8; c0 < N; c0 += 16) {
+            for (int c0 = half * 8; c0 < N; c0 += 2 * R::NEPI) {
                 float v[8];
                 tmem_ld8(tq + c0, v);
                 tmem_wait_ld();
@@ -405,7 +460,7 @@ __global__ void __launch_bounds__(wsk::THREADS, 1) lstm_bwd_ws_kernel(
             if (lane == 0) mbar_arrive(&bars->accempty[a]);
         }
     }
-    ws_teardown(bars, N);
+    ws_teardown<R>(bars, N);
 }
 
 template <int HP>
@@ -418,7 +473,7 @@ int lstm_fwd_ws_t(int64_t rows, int kx, const float* x, int64_t ldx, const float
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int grid = ntiles < kSMs ? ntiles : kSMs;
     note_launch();
-    k<<<grid, wsk::THREADS, smem, st>>>(rows, kx, x, ldx, hp_, cp, img, b, h, c, gates);
+    k<<<grid, FwdRoles<HP>::THREADS, smem, st>>>(rows, kx, x, ldx, hp_, cp, img, b, h, c, gates);
     return launch_status("lstm_forward_step_ws");
 }
 
@@ -437,7 +492,7 @@ int lstm_bwd_ws_t(int64_t rows, int kx, const float* dy, const float* dh_in, con
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int grid = ntiles < kSMs ? ntiles : kSMs;
     note_launch();
-    k<<<grid, wsk::THREADS, smem, st>>>(rows, kx, N, dy, dh_in, dc_in, gates, cp, cn, img, dx, lddx, dh_out,
+    k<<<grid, BwdRoles::THREADS, smem, st>>>(rows, kx, N, dy, dh_in, dc_in, gates, cp, cn, img, dx, lddx, dh_out,
                                          dc_out);
     return launch_status("lstm_backward_step_ws");
 }
