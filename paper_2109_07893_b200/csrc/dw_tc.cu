@@ -7,25 +7,60 @@
 // Both operands are staged MN-major straight from their row-major HBM
 // layout (a 128-byte row segment of 32 columns is one swizzle-atom row), so
 // nothing is transposed: A = dz^T (M = 4*HP gate columns, one or two M=128
-// tiles), B = xcat^T (N = kx + HP rounded to 16), K = rows.  3xTF32 split as in
-// lstm_tc.cu.  One persistent CTA per SM owns a contiguous row range.
+// tiles), B = xcat^T (N = kx + HP rounded to 32), K = rows.  3xTF32 split as
+// in lstm_tc.cu.  One persistent CTA per SM owns a contiguous row range.
+//
+// Warp-specialised (same scheme as lstm_ws.cu):
+//   warps 0..3  loaders: cp.async the raw fp32 rows of a stage straight into
+//               the swizzled hi tiles as soon as its slot is free, completion
+//               tracked by landed[s] (cp.async.mbarrier.arrive);
+//   warps 4..11 converters: split each landed stage in place (hi, lo), fold
+//               dz into fp64 column sums (db), arrive full[s] -- never
+//               blocked behind the slot-reuse wait;
+//   warp 12     MMA issuer: 2 x mt x 3 MMAs per 16-row stage;
+//   warps 13..16 epilogue: promotion of each finished accumulation period.
 //
 // tcgen05 fp32 accumulation truncates, so a TMEM accumulator only lives for
 // DW_PERIOD rows; then it is promoted (fp32, round-to-nearest) into the CTA's
-// own slot in global memory (L2 resident) and restarted.  The CTA slots are
-// reduced in fp64 in fixed order by a second kernel: deterministic.
+// own slot in global memory (L2 resident, [N][M] so the promotion reductions
+// are coalesced) and restarted.  Two accumulators when 2 mt N <= 512 TMEM
+// columns, else one (the MMA then waits for the promotion).  The CTA slots
+// are reduced in fp64 in fixed order by a second kernel: deterministic.
 #include "common.cuh"
 #include "tc.cuh"
 
 namespace dgnn {
 using namespace tc;
 
-constexpr int DW_ROWS = 16;      // reduction rows per stage = two 8-row K groups
+constexpr int DW_ROWS = 16;      // reduction rows per stage = two 8-row K steps
 constexpr int DW_PERIOD = 512;   // rows per TMEM accumulation period
-constexpr int DW_STAGES = 3;
+constexpr int DW_MAX_STAGES = 4;
+constexpr int DW_NLOAD = 4, DW_NCONV = 8, DW_NPROD = DW_NLOAD + DW_NCONV, DW_MMA_WARP = DW_NPROD, DW_NEPI = 4;
+constexpr int DW_THREADS = 32 * (DW_NPROD + 1 + DW_NEPI);
+constexpr int DW_SMEM_MAX = 232448;
+// Bottleneck probe (scripts/dw_probe.cu, -DDGNN_DW_PROBE=mask): 1 skip MMAs,
+// 2 zero-fill operands (no HBM reads), 4 promotion without the slot update,
+// 8 producers without the tf32 split.  Always 0 in the library.
+#ifndef DGNN_DW_PROBE
+#define DGNN_DW_PROBE 0
+#endif
+constexpr int DW_PROBE = DGNN_DW_PROBE;
+#if DGNN_DW_PROBE & 16
+// probe 16: per-CTA cycles each role spends blocked on its barriers
+__device__ unsigned long long dw_prof[kSMs * 8];
+#endif
+__device__ __forceinline__ void dw_wait(uint64_t* bar, uint32_t parity, long long& acc) {
+    if (DW_PROBE & 16) {
+        const long long t = clock64();
+        mbar_wait(bar, parity);
+        acc += clock64() - t;
+    } else {
+        mbar_wait(bar, parity);
+    }
+}
 
 struct DwShape {
-    int M, mtile, mt, N, atoms_a, atoms_b, a_half, b_half, stage, tmem_cols;
+    int M, mtile, mt, N, atoms_a, atoms_b, a_half, b_half, stage, acc_cols, nacc, tmem_cols, stages;
 };
 
 __host__ __device__ inline DwShape dw_shape(int hp, int kx) {
@@ -39,12 +74,21 @@ __host__ __device__ inline DwShape dw_shape(int hp, int kx) {
     s.a_half = 4 * s.atoms_a * 512;   // hi (or lo) part: 4 K groups (of 4 rows) x atoms x 512 B
     s.b_half = 4 * s.atoms_b * 512;
     s.stage = 2 * s.a_half + 2 * s.b_half;
-    const int cols = s.mt * s.N;
+    s.acc_cols = s.mt * s.N;
+    s.nacc = 2 * s.acc_cols <= 512 ? 2 : 1;
+    const int cols = s.nacc * s.acc_cols;
     s.tmem_cols = cols <= 32 ? 32 : (cols <= 64 ? 64 : (cols <= 128 ? 128 : (cols <= 256 ? 256 : 512)));
+    s.stages = (DW_SMEM_MAX - 1024 - 256) / s.stage;
+    if (s.stages > DW_MAX_STAGES) s.stages = DW_MAX_STAGES;
     return s;
 }
 
-inline size_t dw_smem_bytes(const DwShape& s) { return (size_t)DW_STAGES * s.stage + 1024 + 128; }
+inline size_t dw_smem_bytes(const DwShape& s) { return (size_t)s.stages * s.stage + 1024 + 256; }
+
+struct DwBars {
+    uint64_t landed[DW_MAX_STAGES], full[DW_MAX_STAGES], empty[DW_MAX_STAGES], accfull[2], accempty[2];
+    uint32_t tmem;
+};
 
 // MN-major tf32 operands must use SWIZZLE_128B_BASE32B (CUTLASS
 // Layout_MN_SW128_32B_Atom): a 512-byte atom holds 4 K rows x 32 MN elements
@@ -58,35 +102,45 @@ __device__ __forceinline__ uint32_t mn_off(int r, int c, int atoms) {
 }
 
 template <int HP>
-__global__ void __launch_bounds__(256, 1) lstm_dw_tc_kernel(int64_t rows, int64_t np, int kx,
-                                                            const float* __restrict__ x, int64_t ldx,
-                                                            const float* __restrict__ y,
-                                                            const float* __restrict__ h0,
-                                                            const float* __restrict__ dz,
-                                                            float* __restrict__ slots, double* __restrict__ dbs) {
+__global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows, int64_t np, int kx,
+                                                                   const float* __restrict__ x, int64_t ldx,
+                                                                   const float* __restrict__ y,
+                                                                   const float* __restrict__ h0,
+                                                                   const float* __restrict__ dz,
+                                                                   float* __restrict__ slots,
+                                                                   double* __restrict__ dbs) {
     constexpr int M = 4 * HP;
-    constexpr int AV = (DW_ROWS * M / 4) / 256;      // A float4 items per thread per stage
+    constexpr int NLT = 32 * DW_NLOAD, NCT = 32 * DW_NCONV;   // loader / converter threads
+    constexpr int LA_ITEMS = DW_ROWS * (M / 4) / NLT;    // A float4 items per loader thread per stage
+    constexpr int LB_ITEMS = (DW_ROWS * 64 + NLT - 1) / NLT;   // B items (N <= 256)
+    constexpr int CA_ITEMS = DW_ROWS * (M / 4) / NCT;    // per converter thread
+    constexpr int CB_ITEMS = (DW_ROWS * 64 + NCT - 1) / NCT;
     const DwShape S = dw_shape(HP, kx);
     const int K = kx + HP;
-    const int BVEC = DW_ROWS * S.N / 4;              // B float4 items per stage
-    constexpr int BMAX = (DW_ROWS * 256 / 4 + 255) / 256;
+    const int BVEC = DW_ROWS * S.N / 4;
 
     extern __shared__ uint8_t dw_smem_raw[];
     const uint32_t raw = smem_u32(dw_smem_raw);
     uint8_t* base = dw_smem_raw + ((1024 - (raw & 1023)) & 1023);
     const uint32_t sb = smem_u32(base);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + DW_STAGES * S.stage);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + DW_STAGES);
-    const int tid = threadIdx.x;
-    if (tid < 32) tmem_alloc(tslot, S.tmem_cols);
-    if (tid == 32) {
-        for (int i = 0; i < DW_STAGES; ++i) mbar_init(&bars[i], 1);
+    DwBars* bars = reinterpret_cast<DwBars*>(base + S.stages * S.stage);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == DW_MMA_WARP) tmem_alloc(&bars->tmem, S.tmem_cols);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S.stages; ++i) {
+            mbar_init(&bars->landed[i], 32 * DW_NLOAD);
+            mbar_init(&bars->full[i], DW_NCONV);
+            mbar_init(&bars->empty[i], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->accfull[a], 1);
+            mbar_init(&bars->accempty[a], DW_NEPI);
+        }
         fence_mbar_init();
     }
     fence_before();
     __syncthreads();
     fence_after();
-    const uint32_t tmem = *tslot;
 
     // contiguous row range of this CTA (multiple of 16)
     const int64_t per = cdiv(cdiv(rows, gridDim.x), DW_ROWS) * DW_ROWS;
@@ -94,146 +148,220 @@ __global__ void __launch_bounds__(256, 1) lstm_dw_tc_kernel(int64_t rows, int64_
     const int64_t r_end = min(rows, r_begin + per);
     const int nst = r_end > r_begin ? (int)cdiv(r_end - r_begin, DW_ROWS) : 0;
     const int period_st = DW_PERIOD / DW_ROWS;
-    float* slot = slots + (size_t)blockIdx.x * M * S.N;
-
-    float4 ca[AV], na[AV], cb[BMAX], nb[BMAX];
+    const int nper = (nst + period_st - 1) / period_st;
+    float* slot = slots + (size_t)blockIdx.x * M * S.N;   // [N][M]
     double dbacc[4] = {0.0, 0.0, 0.0, 0.0};
-    auto fetch = [&](int st, float4* va, float4* vb) {
-        const int64_t r0 = r_begin + (int64_t)st * DW_ROWS;
-#pragma unroll
-        for (int i = 0; i < AV; ++i) {
-            const int idx = tid + 256 * i;
-            const int r = idx / (M / 4), c = 4 * (idx % (M / 4));
-            const int64_t g = r0 + r;
-            va[i] = g < r_end ? __ldg(reinterpret_cast<const float4*>(dz + g * M + c))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int i = 0; i < BMAX; ++i) {
-            const int idx = tid + 256 * i;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (idx < BVEC) {
-                const int r = idx / (S.N / 4), c = 4 * (idx % (S.N / 4));
-                const int64_t g = r0 + r;
-                if (g < r_end && c < K) {
-                    if (c < kx) v = __ldg(reinterpret_cast<const float4*>(x + g * ldx + c));
-                    else if (g >= np) v = __ldg(reinterpret_cast<const float4*>(y + (g - np) * HP + (c - kx)));
-                    else v = __ldg(reinterpret_cast<const float4*>(h0 + g * HP + (c - kx)));
-                }
-            }
-            vb[i] = v;
-        }
-    };
-    if (nst > 0) fetch(0, ca, cb);
+    long long wacc0 = 0, wacc1 = 0;
+    const long long t_start = clock64();
 
-    const int w = tid >> 5, lane = tid & 31, q = w & 3, half = w >> 2;
-    for (int st = 0; st < nst; ++st) {
-        const int s = st % DW_STAGES;
-        if (st + 1 < nst) fetch(st + 1, na, nb);
-        if (st >= DW_STAGES) mbar_wait(&bars[s], ((st - DW_STAGES) / DW_STAGES) & 1);
-        const uint32_t a_hi = sb + s * S.stage, a_lo = a_hi + S.a_half;
-        const uint32_t b_hi = a_lo + S.a_half, b_lo = b_hi + S.b_half;
+    if (warp < DW_NLOAD) {
+        const int lt = threadIdx.x;
+        int arow[LA_ITEMS], brow[LB_ITEMS], bcol[LB_ITEMS], acol[LA_ITEMS];
+        uint32_t aoff[LA_ITEMS], boff[LB_ITEMS];
 #pragma unroll
-        for (int i = 0; i < AV; ++i) {
-            const int idx = tid + 256 * i;
-            const int r = idx / (M / 4), c = 4 * (idx % (M / 4));
-            float4 hi, lo;
-            split4(ca[i], hi, lo);
-            const uint32_t o = mn_off(r, c, S.atoms_a);
-            sts128(a_hi + o, hi);
-            sts128(a_lo + o, lo);
-            dbacc[0] += ca[i].x;
-            dbacc[1] += ca[i].y;
-            dbacc[2] += ca[i].z;
-            dbacc[3] += ca[i].w;
+        for (int i = 0; i < LA_ITEMS; ++i) {
+            const int idx = lt + 32 * DW_NLOAD * i;
+            arow[i] = idx / (M / 4);
+            acol[i] = 4 * (idx % (M / 4));
+            aoff[i] = mn_off(arow[i], acol[i], S.atoms_a);
         }
 #pragma unroll
-        for (int i = 0; i < BMAX; ++i) {
-            const int idx = tid + 256 * i;
-            if (idx < BVEC) {
-                const int r = idx / (S.N / 4), c = 4 * (idx % (S.N / 4));
-                float4 hi, lo;
-                split4(cb[i], hi, lo);
-                const uint32_t o = mn_off(r, c, S.atoms_b);
-                sts128(b_hi + o, hi);
-                sts128(b_lo + o, lo);
+        for (int i = 0; i < LB_ITEMS; ++i) {
+            const int idx = lt + 32 * DW_NLOAD * i;
+            brow[i] = idx < BVEC ? idx / (S.N / 4) : -1;
+            bcol[i] = idx < BVEC ? 4 * (idx % (S.N / 4)) : 0;
+            boff[i] = idx < BVEC ? mn_off(brow[i], bcol[i], S.atoms_b) : 0u;
+        }
+        for (int g = 0; g < nst; ++g) {
+            const int s = g % S.stages;
+            const int j = g / S.stages;
+            if (j >= 1) dw_wait(&bars->empty[s], (j - 1) & 1, wacc0);
+            const int64_t r0 = r_begin + (int64_t)g * DW_ROWS;
+            const uint32_t a_hi = sb + s * S.stage, b_hi = a_hi + 2 * S.a_half;
+#pragma unroll
+            for (int i = 0; i < LA_ITEMS; ++i) {
+                const int64_t gr = r0 + arow[i];
+                const bool ok = gr < r_end && !(DW_PROBE & 2);
+                cp_async16(a_hi + aoff[i], ok ? dz + gr * M + acol[i] : dz, ok ? 16u : 0u);
             }
-        }
-        fence_async_smem();
-        __syncthreads();
-        const bool first = (st % period_st) == 0;
-        if (tid == 0) {
-            fence_after();
-            const uint32_t idesc = idesc_tf32_mn(S.mtile, S.N);
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-                const uint64_t bh = sdesc_mn(b_hi + 2 * kk * S.atoms_b * 512, 512, S.atoms_b * 512, kSW128B32);
-                const uint64_t bl = sdesc_mn(b_lo + 2 * kk * S.atoms_b * 512, 512, S.atoms_b * 512, kSW128B32);
-                for (int m = 0; m < S.mt; ++m) {
-                    const uint32_t aoff = (2 * kk * S.atoms_a + m * (S.mtile / 32)) * 512;
-                    const uint64_t ah = sdesc_mn(a_hi + aoff, 512, S.atoms_a * 512, kSW128B32);
-                    const uint64_t al = sdesc_mn(a_lo + aoff, 512, S.atoms_a * 512, kSW128B32);
-                    const uint32_t d = tmem + m * S.N;
-                    mma_tf32(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
-                    mma_tf32(d, ah, bl, idesc, 1u);
-                    mma_tf32(d, al, bh, idesc, 1u);
+            for (int i = 0; i < LB_ITEMS; ++i) {
+                if (brow[i] >= 0) {
+                    const int64_t gr = r0 + brow[i];
+                    const int c = bcol[i];
+                    const float* src = x;
+                    const bool ok = gr < r_end && c < K && !(DW_PROBE & 2);
+                    if (ok) {
+                        if (c < kx) src = x + gr * ldx + c;
+                        else if (gr >= np) src = y + (gr - np) * HP + (c - kx);
+                        else src = h0 + gr * HP + (c - kx);
+                    }
+                    cp_async16(b_hi + boff[i], src, ok ? 16u : 0u);
                 }
             }
-            commit(&bars[s]);
+            cp_async_mbar_arrive(&bars->landed[s]);
         }
-        const bool end_of_period = ((st + 1) % period_st) == 0 || st + 1 == nst;
-        if (end_of_period) {
-            // promotion: TMEM period sum -> fp32 slot (round to nearest)
-            mbar_wait(&bars[s], (st / DW_STAGES) & 1);
+        cp_async_wait<0>();
+    } else if (warp < DW_NPROD) {
+        const int ct = threadIdx.x - 32 * DW_NLOAD;
+        const int acol = 4 * (ct % (M / 4));   // 32 * DW_NCONV is a multiple of M / 4
+        uint32_t aoff[CA_ITEMS], boff[CB_ITEMS];
+#pragma unroll
+        for (int i = 0; i < CA_ITEMS; ++i) aoff[i] = mn_off((ct + 32 * DW_NCONV * i) / (M / 4), acol, S.atoms_a);
+#pragma unroll
+        for (int i = 0; i < CB_ITEMS; ++i) {
+            const int idx = ct + 32 * DW_NCONV * i;
+            boff[i] = idx < BVEC ? mn_off(idx / (S.N / 4), 4 * (idx % (S.N / 4)), S.atoms_b) : 0xFFFFFFFFu;
+        }
+        for (int g = 0; g < nst; ++g) {
+            const int s = g % S.stages;
+            dw_wait(&bars->landed[s], (g / S.stages) & 1, wacc0);
+            const uint32_t a_hi = sb + s * S.stage, a_lo = a_hi + S.a_half;
+            const uint32_t b_hi = a_lo + S.a_half, b_lo = b_hi + S.b_half;
+            // all shared loads first (the asm accessors keep program order),
+            // then split + stores: one smem latency per stage, not per item
+            float4 va[CA_ITEMS], vb[CB_ITEMS];
+#pragma unroll
+            for (int i = 0; i < CA_ITEMS; ++i) va[i] = lds128(a_hi + aoff[i]);
+#pragma unroll
+            for (int i = 0; i < CB_ITEMS; ++i)
+                if (boff[i] != 0xFFFFFFFFu) vb[i] = lds128(b_hi + boff[i]);
+#pragma unroll
+            for (int i = 0; i < CA_ITEMS * !(DW_PROBE & 8); ++i) {
+                float4 hi, lo;
+                split4(va[i], hi, lo);
+                sts128(a_hi + aoff[i], hi);
+                sts128(a_lo + aoff[i], lo);
+            }
+#pragma unroll
+            for (int i = 0; i < CB_ITEMS * !(DW_PROBE & 8); ++i) {
+                if (boff[i] != 0xFFFFFFFFu) {
+                    float4 hi, lo;
+                    split4(vb[i], hi, lo);
+                    sts128(b_hi + boff[i], hi);
+                    sts128(b_lo + boff[i], lo);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < CA_ITEMS; ++i) {
+                dbacc[0] += va[i].x;
+                dbacc[1] += va[i].y;
+                dbacc[2] += va[i].z;
+                dbacc[3] += va[i].w;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->full[s]);
+        }
+    } else if (warp == DW_MMA_WARP) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_tf32_mn(S.mtile, S.N);
+            int g = 0;
+            for (int p = 0; p < nper; ++p) {
+                const int a = S.nacc == 2 ? (p & 1) : 0;
+                const int u = S.nacc == 2 ? (p >> 1) : p;   // use count of accumulator a
+                if (u >= 1) dw_wait(&bars->accempty[a], (u - 1) & 1, wacc1);
+                fence_after();
+                const uint32_t dbase = bars->tmem + a * S.acc_cols;
+                const int g_end = min(nst, (p + 1) * period_st);
+                for (bool first = true; g < g_end; ++g, first = false) {
+                    const int s = g % S.stages;
+                    dw_wait(&bars->full[s], (g / S.stages) & 1, wacc0);
+                    fence_after();
+                    const uint32_t a_hi = sb + s * S.stage, a_lo = a_hi + S.a_half;
+                    const uint32_t b_hi = a_lo + S.a_half, b_lo = b_hi + S.b_half;
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const uint64_t bh = sdesc_mn(b_hi + 2 * kk * S.atoms_b * 512, 512, S.atoms_b * 512, kSW128B32);
+                        const uint64_t bl = sdesc_mn(b_lo + 2 * kk * S.atoms_b * 512, 512, S.atoms_b * 512, kSW128B32);
+                        for (int m = 0; m < S.mt; ++m) {
+                            if (DW_PROBE & 1) break;
+                            const uint32_t aoff = (2 * kk * S.atoms_a + m * (S.mtile / 32)) * 512;
+                            const uint64_t ah = sdesc_mn(a_hi + aoff, 512, S.atoms_a * 512, kSW128B32);
+                            const uint64_t al = sdesc_mn(a_lo + aoff, 512, S.atoms_a * 512, kSW128B32);
+                            const uint32_t d = dbase + m * S.N;
+                            mma_tf32(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
+                            mma_tf32(d, ah, bl, idesc, 1u);
+                            mma_tf32(d, al, bh, idesc, 1u);
+                        }
+                    }
+                    commit(&bars->empty[s]);
+                }
+                commit(&bars->accfull[a]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // promotion: TMEM period sum -> fp32 slot[k][j] (round to nearest);
+        // DW_NEPI / 4 warps share a TMEM lane quarter and split the columns
+        constexpr int WPQ = DW_NEPI / 4, CS = 8 * WPQ;   // column stride of one warp
+        const int e = warp - DW_MMA_WARP - 1;
+        const int q = warp & 3, half = e >> 2;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        for (int p = 0; p < nper; ++p) {
+            const int a = S.nacc == 2 ? (p & 1) : 0;
+            const int u = S.nacc == 2 ? (p >> 1) : p;
+            dw_wait(&bars->accfull[a], u & 1, wacc0);
             fence_after();
-            const bool first_period = st < period_st;
             for (int m = 0; m < S.mt; ++m) {
                 const int j = m * S.mtile + 32 * q + lane;
-                for (int c0 = half * 8; c0 < S.N; c0 += 16) {
-                    float v[8];
-                    tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + m * S.N + c0, v);
+                const bool jok = 32 * q + lane < S.mtile;
+                // four 8-column chunks per TMEM wait; the slot update is a
+                // fire-and-forget reduction (RED.ADD, coalesced over j), so
+                // the accumulator is released after the TMEM reads alone.
+                // Each slot element is only ever updated by this thread, in
+                // period order: the fp32 sum sequence is fixed.
+                constexpr int GR = 4;
+                for (int c0 = half * 8; c0 < S.N; c0 += CS * GR) {
+                    float v[GR][8];
+#pragma unroll
+                    for (int ci = 0; ci < GR; ++ci)
+                        if (c0 + CS * ci < S.N) tmem_ld8(bars->tmem + lane_off + a * S.acc_cols + m * S.N + c0 + CS * ci, v[ci]);
                     tmem_wait_ld();
-                    if (32 * q + lane < S.mtile) {
-                        float4* o = reinterpret_cast<float4*>(slot + (size_t)j * S.N + c0);
-                        float4 a = make_float4(v[0], v[1], v[2], v[3]), b = make_float4(v[4], v[5], v[6], v[7]);
-                        if (!first_period) {
-                            const float4 p0 = o[0], p1 = o[1];
-                            a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
-                            b.x += p1.x; b.y += p1.y; b.z += p1.z; b.w += p1.w;
-                        }
-                        o[0] = a;
-                        o[1] = b;
+                    if (jok && !(DW_PROBE & 4)) {
+#pragma unroll
+                        for (int ci = 0; ci < GR; ++ci)
+#pragma unroll
+                            for (int t = 0; t < 8; ++t)
+                                if (c0 + CS * ci < S.N) atomicAdd(slot + (size_t)(c0 + CS * ci + t) * M + j, v[ci][t]);
                     }
                 }
             }
             fence_before();
-            __syncthreads();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->accempty[a]);
         }
-#pragma unroll
-        for (int i = 0; i < AV; ++i) ca[i] = na[i];
-#pragma unroll
-        for (int i = 0; i < BMAX; ++i) cb[i] = nb[i];
     }
-    // db partial: threads sharing a column group combine in fixed order
-    __shared__ double dbred[256][4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) dbred[tid][j] = dbacc[j];
+#if DGNN_DW_PROBE & 16
+    if (lane == 0 && (warp == 0 || warp == DW_NLOAD || warp == DW_MMA_WARP || warp == DW_MMA_WARP + 1)) {
+        const int k = warp == 0 ? 0 : (warp == DW_NLOAD ? 1 : (warp == DW_MMA_WARP ? 2 : 4));
+        dw_prof[blockIdx.x * 8 + k] = wacc0;
+        if (warp == DW_MMA_WARP) dw_prof[blockIdx.x * 8 + 3] = wacc1;
+        if (warp == 0) dw_prof[blockIdx.x * 8 + 5] = clock64() - t_start;
+    }
+#endif
+    fence_before();
     __syncthreads();
-    if (tid < M / 4) {
-        double s4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int t = tid; t < 256; t += M / 4)
-            for (int j = 0; j < 4; ++j) s4[j] += dbred[t][j];
-        for (int j = 0; j < 4; ++j) dbs[(size_t)blockIdx.x * M + 4 * tid + j] = s4[j];
+    // db partial: producer threads sharing a column group combine in fixed
+    // order (the stage ring is free now)
+    double* dbred = reinterpret_cast<double*>(base);
+    if (warp >= DW_NLOAD && warp < DW_NPROD) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dbred[(threadIdx.x - 32 * DW_NLOAD) * 4 + t] = dbacc[t];
     }
-    if (nst == 0) {   // empty range: publish zeros
-        for (int i = tid; i < M * S.N; i += 256) slot[i] = 0.f;
+    __syncthreads();
+    if (threadIdx.x < M / 4) {
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int t = threadIdx.x; t < NCT; t += M / 4)
+            for (int jj = 0; jj < 4; ++jj) s4[jj] += dbred[t * 4 + jj];
+        for (int jj = 0; jj < 4; ++jj) dbs[(size_t)blockIdx.x * M + 4 * threadIdx.x + jj] = s4[jj];
     }
     fence_before();
     __syncthreads();
-    if (tid < 32) tmem_dealloc(tmem, S.tmem_cols);
+    if (warp == DW_MMA_WARP) tmem_dealloc(bars->tmem, S.tmem_cols);
 }
 
-// gw[k][j] += sum_cta slot[cta][j][k] ; gb[j] += sum_cta dbs[cta][j]   (fp64, fixed order)
+// gw[k][j] += sum_cta slot[cta][k][j] ; gb[j] += sum_cta dbs[cta][j]   (fp64, fixed order)
 __global__ void dw_reduce_kernel(int nct, int M, int N, int K, const float* __restrict__ slots,
                                  const double* __restrict__ dbs, double* __restrict__ gw, int64_t ldg,
                                  double* __restrict__ gb) {
@@ -241,7 +369,7 @@ __global__ void dw_reduce_kernel(int nct, int M, int N, int K, const float* __re
     if (i < (int64_t)M * K) {
         const int k = (int)(i / M), j = (int)(i % M);
         double s = 0.0;
-        for (int c = 0; c < nct; ++c) s += (double)slots[((size_t)c * M + j) * N + k];
+        for (int c = 0; c < nct; ++c) s += (double)slots[((size_t)c * N + k) * M + j];
         gw[(int64_t)k * ldg + j] += s;
     } else if (i < (int64_t)M * K + M && gb) {
         const int j = (int)(i - (int64_t)M * K);
@@ -255,7 +383,7 @@ template <int HP>
 int lstm_dw_tc_t(int64_t rows, int64_t np, int kx, const float* x, int64_t ldx, const float* y, const float* h0,
                  const float* dz, double* gw, double* gb, void* ws, size_t ws_bytes, cudaStream_t st) {
     const DwShape S = dw_shape(HP, kx);
-    if (S.mt * S.N > 512 || S.N > 256) {
+    if (S.acc_cols > 512 || S.N > 256 || S.stages < 3) {
         set_error("lstm_weight_grad_tc: kx + hp = %d too wide", kx + HP);
         return DGNN_EUNSUPPORTED;
     }
@@ -267,11 +395,13 @@ int lstm_dw_tc_t(int64_t rows, int64_t np, int kx, const float* x, int64_t ldx, 
     }
     float* slots = reinterpret_cast<float*>(ws);
     double* dbs = reinterpret_cast<double*>(slots + (size_t)grid * S.M * S.N);
+    // slots accumulate period sums by reduction: start from zero
+    cudaMemsetAsync(slots, 0, (size_t)grid * S.M * S.N * sizeof(float), st);
     auto k = lstm_dw_tc_kernel<HP>;
     const size_t smem = dw_smem_bytes(S);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     note_launch();
-    k<<<grid, 256, smem, st>>>(rows, np, kx, x, ldx, y, h0, dz, slots, dbs);
+    k<<<grid, DW_THREADS, smem, st>>>(rows, np, kx, x, ldx, y, h0, dz, slots, dbs);
     const int K = kx + HP;
     const int64_t tot = (int64_t)S.M * K + S.M;
     note_launch();

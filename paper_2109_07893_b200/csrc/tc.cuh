@@ -140,11 +140,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// tf32 split: hi = round-to-nearest tf32, lo = exact remainder
+// tf32 split: hi = round-to-nearest-away tf32, lo = exact remainder.  The
+// integer form equals cvt.rna.tf32.f32 for every finite input below 2^128
+// (operands here are activations and gradients) in two ALU ops instead of
+// the four sm_100 spends on cvt.rna.
 __device__ __forceinline__ float tf32_hi(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void split4(const float4& v, float4& hi, float4& lo) {
@@ -161,6 +162,11 @@ __device__ __forceinline__ void split4(const float4& v, float4& hi, float4& lo) 
 // 16-byte async global->shared copy; src_bytes = 0 zero-fills (out of range)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+// arrive on `bar` once all prior cp.async of this thread have landed (the
+// barrier's expected count includes this arrival)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
