@@ -126,10 +126,15 @@ int dgnn_spmm_f32(int32_t n, const int32_t* rowptr, const int32_t* col, const fl
  *   skip:  r = relu([s, q])  (width fp + hp)        (cd-gcn)
  *   plain: r = relu(q)       (width hp)             (tm-gcn)
  * s_out (nullable) keeps s for the backward.  fp in {4,16,32,64,128}
- * (4 only without aggregation), hp in {16,32,64,128}. */
+ * (4 only without aggregation), hp in {16,32,64,128}.  fp, hp <= 64 (fp >= 16)
+ * run the tcgen05 instance (gather warps + 3xTF32 transform), the rest the
+ * SIMT kernel. */
 int dgnn_gcn_forward(int32_t n, const int32_t* rowptr, const int32_t* col, const float* val,
                      dgnn_frame x, int32_t fp, const float* w, int32_t hp, int skip,
                      dgnn_frame s_out, dgnn_frame r_out, void* stream);
+
+/* Selects the K3 instance: 1 (default) tcgen05 where available, 0 SIMT. */
+void dgnn_set_gcn_tensor_cores(int on);
 
 /* K4 row part (training.py:347-350, 359-367):
  *   dpre = dr (.) [r > 0];  skip: ds = dpre[:, :fp] + dpre[:, fp:] * w^T

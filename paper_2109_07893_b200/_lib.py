@@ -39,6 +39,7 @@ _SIGS = {
     "dgnn_spmm_f64": (c_int, [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, P]),
     "dgnn_spmm_f32": (c_int, [c_int32, P, P, P, Frame, c_int32, Frame, P]),
     "dgnn_gcn_forward": (c_int, [c_int32, P, P, P, Frame, c_int32, P, c_int32, c_int, Frame, Frame, P]),
+    "dgnn_set_gcn_tensor_cores": (None, [c_int]),
     "dgnn_gcn_backward_rows": (c_int, [c_int32, Frame, Frame, c_int32, P, c_int32, c_int, Frame, P]),
     "dgnn_gcn_weight_grad_workspace": (c_size_t, [c_int32, c_int32]),
     "dgnn_gcn_weight_grad": (c_int, [c_int32, Frame, Frame, Frame, c_int32, c_int32, c_int, P, P,

@@ -192,6 +192,10 @@ __global__ void __launch_bounds__(256) gcn_bwd_rows_kernel(int32_t n, dgnn_frame
     }
 }
 
+// tcgen05 instance of K3 (gcn_tc.cu); -1 when the shape has none
+int gcn_fwd_tc(int fp, int hp, bool skip, bool agg, int32_t n, const int32_t* rp, const int32_t* col,
+               const float* val, dgnn_frame x, const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st);
+
 }  // namespace dgnn
 
 using namespace dgnn;
@@ -295,6 +299,12 @@ int gcn_bwd_fp(int32_t fp, int32_t hp, int32_t n, dgnn_frame dr, dgnn_frame r, c
 
 extern "C" {
 
+// K3 engine selection: tcgen05 instance where one exists (default) or the
+// SIMT kernel (A/B and strict-tolerance tests); dgnn_set_gcn_tensor_cores.
+static int dgnn_gcn_tensor_cores = 1;
+
+void dgnn_set_gcn_tensor_cores(int on) { dgnn_gcn_tensor_cores = on != 0; }
+
 int dgnn_spmm_f32(int32_t n, const int32_t* rowptr, const int32_t* col, const float* val, dgnn_frame x,
                   int32_t f, dgnn_frame out, void* stream) {
     DGNN_CHECK_ARG(n >= 0, "spmm_f32: negative size");
@@ -318,6 +328,10 @@ int dgnn_gcn_forward(int32_t n, const int32_t* rowptr, const int32_t* col, const
     if (n == 0) return DGNN_OK;
     cudaStream_t st = as_stream(stream);
     const bool agg = rowptr != nullptr;
+    if (dgnn_gcn_tensor_cores) {
+        const int rc = gcn_fwd_tc(fp, hp, skip != 0, agg, n, rowptr, col, val, x, w, s_out, r_out, st);
+        if (rc >= 0) return rc;
+    }
     if (skip) {
         return agg ? gcn_fwd_fp<true, true>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st)
                    : gcn_fwd_fp<true, false>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st);

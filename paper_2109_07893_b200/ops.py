@@ -274,6 +274,31 @@ def tc_gemm(a: np.ndarray, w: np.ndarray) -> np.ndarray:
     return out.double().cpu().numpy()
 
 
+def gcn_forward(n: int, rowptr: np.ndarray | None, col: np.ndarray | None, val: np.ndarray | None,
+                x: np.ndarray, w: np.ndarray, skip: bool, tensor_cores: bool = True):
+    """Test hook of K3 `dgnn_gcn_forward`: s = (A x if rowptr is given else x),
+    r = relu([s, s w]) (skip) | relu(s w); fp32.  Returns (s, r)."""
+    dev = _dev()
+    fp, hp = w.shape
+    xd = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(dev)
+    wd = torch.from_numpy(np.ascontiguousarray(w, np.float32)).to(dev)
+    rw = fp + hp if skip else hp
+    s_out = torch.full((n, fp), np.nan, dtype=torch.float32, device=dev)
+    r_out = torch.full((n, rw), np.nan, dtype=torch.float32, device=dev)
+    st = _lib.stream_handle()
+    agg = rowptr is not None
+    rp = _i32(rowptr, dev) if agg else None
+    cd = _i32(col if len(col) else np.zeros(1), dev) if agg else None
+    vd = torch.from_numpy(np.ascontiguousarray(val if len(val) else np.zeros(1), np.float32)).to(dev) if agg else None
+    call("dgnn_set_gcn_tensor_cores", int(tensor_cores))
+    try:
+        call("dgnn_gcn_forward", n, ptr(rp), ptr(cd), ptr(vd), _lib.frame(xd, fp), fp, ptr(wd), hp, int(skip),
+             _lib.frame(s_out, fp), _lib.frame(r_out, rw), st)
+    finally:
+        call("dgnn_set_gcn_tensor_cores", 1)
+    return s_out.cpu().numpy(), r_out.cpu().numpy()
+
+
 def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np.ndarray, np_rows: int):
     """Tensor-core block weight gradient (test hook of dgnn_lstm_weight_grad_tc):
     returns (sum_r xcat[r]^T dz[r]  as (kx+hp) x 4hp, sum_r dz[r]) in fp64."""

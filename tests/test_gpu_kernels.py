@@ -354,3 +354,42 @@ def test_warp_specialized_lstm_steps_match_tc_bitwise(H):
     assert np.array_equal(dsw[0], dst_t[0]) and np.array_equal(dsw[1], dst_t[1])
     for k in dcw:
         assert np.array_equal(dcw[k], dct[k])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fp,hp,skip,agg", [(64, 64, True, True), (32, 16, False, True), (16, 64, True, True),
+                                            (64, 32, False, True), (64, 64, True, False)])
+def test_gcn_forward_tensor_cores(fp, hp, skip, agg):
+    """K3 tcgen05 instance (gather warps + 3xTF32 transform) against fp64:
+    ragged last tile, empty rows, and a hub row whose tile overflows the
+    staged-index capacity (global-index path).  The aggregation s is the
+    same fp32 FMA sequence as the SIMT kernel: bitwise equal."""
+    from paper_2109_07893_b200.ops import gcn_forward
+    rng = np.random.default_rng(fp * 7 + hp + skip)
+    n = 5000 + 37
+    deg = rng.integers(0, 4, size=n)
+    deg[1234] = 3000
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, size=rows.size).astype(np.int32)
+    val = rng.uniform(-1, 1, size=rows.size).astype(np.float32)
+    rowptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    x = rng.standard_normal((n, fp)).astype(np.float32)
+    w = (rng.standard_normal((fp, hp)) * 0.2).astype(np.float32)
+    args = (rowptr, cols, val) if agg else (None, None, None)
+    s, r = gcn_forward(n, *args, x, w, skip)
+    s2, r2 = gcn_forward(n, *args, x, w, skip, tensor_cores=False)
+    assert np.array_equal(s, s2)
+    if agg:
+        ref_s = np.zeros((n, fp))
+        np.add.at(ref_s, rows, val.astype(np.float64)[:, None] * x.astype(np.float64)[cols])
+    else:
+        ref_s = x.astype(np.float64)
+    sc = np.abs(ref_s).max()
+    assert np.abs(s - ref_s).max() <= 1e-5 * sc
+    q = s.astype(np.float64) @ w.astype(np.float64)
+    qs = (np.abs(s).astype(np.float64) @ np.abs(w).astype(np.float64)).max()
+    got_q = r[:, fp:] if skip else r
+    assert np.abs(got_q - np.maximum(q, 0)).max() <= 2e-6 * qs
+    if skip:
+        assert np.array_equal(r[:, :fp], np.maximum(s, 0))
+    assert np.abs((r2[:, fp:] if skip else r2) - got_q).max() <= 2e-6 * qs

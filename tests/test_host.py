@@ -18,7 +18,7 @@ from helpers import product_graph
 
 def header_symbols():
     text = (ROOT / "include" / "dgnn_b200.h").read_text()
-    return sorted(set(re.findall(r"^(?:int|size_t|long long|const char\*)\s+(dgnn_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|size_t|long long|const char\*)\s+(dgnn_\w+)\(", text, re.M)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
