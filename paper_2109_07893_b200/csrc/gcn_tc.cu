@@ -48,6 +48,7 @@ struct GtcBars {
     uint64_t full[gtc::ASTAGES], empty[gtc::ASTAGES], ifull[gtc::ISTAGES], iempty[gtc::ISTAGES], accfull[2],
         accempty[2];
     uint32_t tmem;
+    int32_t claim[gtc::ASTAGES];   // row-chunk claim counters (monotonic)
 };
 
 struct GtcIdx {            // one index stage
@@ -79,7 +80,6 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     using L = GtcLayout<FP, HP>;
     constexpr int G = FP / 4;              // lanes per row
     constexpr int RW = 32 / G;             // rows per warp pass
-    constexpr int NGROUPS = gtc::NGATHER * RW;
     extern __shared__ uint8_t gtc_smem_raw[];
     const uint32_t raw = smem_u32(gtc_smem_raw);
     uint8_t* base = gtc_smem_raw + ((1024 - (raw & 1023)) & 1023);
@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
         for (int s = 0; s < gtc::ASTAGES; ++s) {
             mbar_init(&bars->full[s], gtc::NGATHER);
             mbar_init(&bars->empty[s], 1);
+            bars->claim[s] = 0;
         }
         for (int s = 0; s < gtc::ISTAGES; ++s) {
             mbar_init(&bars->ifull[s], 1);
@@ -123,13 +124,13 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     fence_after();
 
     if (warp < gtc::NGATHER) {
-        const int grp = warp * RW + lane / G, gl = lane % G;
+        const int sub = lane / G, gl = lane % G;
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const int s = it % gtc::ASTAGES, si = it % gtc::ISTAGES;
             const GtcIdx& ix = idx[si];
-            if (AGG) mbar_wait(&bars->ifull[si], (it / gtc::ISTAGES) & 1);
-            if (it >= gtc::ASTAGES) mbar_wait(&bars->empty[s], ((it / gtc::ASTAGES) - 1) & 1);
+            if (AGG) mbar_wait_sleep(&bars->ifull[si], (it / gtc::ISTAGES) & 1);
+            if (it >= gtc::ASTAGES) mbar_wait_sleep(&bars->empty[s], ((it / gtc::ASTAGES) - 1) & 1);
             const uint32_t a_hi = sb + s * L::A_STAGE, a_lo = a_hi + L::A_HALF;
             const bool spill = AGG && ix.spill;
             // two rows per lane group per pass, the first four edges of both
@@ -149,8 +150,19 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 }
                 for (; e < ee; ++e) fma4(acc, vs[e], xrow(cs[e]));
             };
-            for (int r = grp; r < gtc::BM; r += 2 * NGROUPS) {
-                const int rb = r + NGROUPS;
+            // Row chunks (2 RW rows: two rows per lane group) are claimed
+            // dynamically, so warps that drew short rows take more of them
+            // and the tile completes together.  Every warp makes exactly one
+            // failing claim per tile, so use k of stage s starts its claims
+            // at k (NCHUNK + NGATHER): the counter never needs a reset.
+            constexpr int CROWS = 2 * RW, NCHUNK = gtc::BM / CROWS;
+            const int cbase = (int)(it / gtc::ASTAGES) * (NCHUNK + gtc::NGATHER);
+            for (;;) {
+                int chunk = 0;
+                if (lane == 0) chunk = atomicAdd(&bars->claim[s], 1) - cbase;
+                chunk = __shfl_sync(0xffffffffu, chunk, 0);
+                if (chunk >= NCHUNK) break;
+                const int r = chunk * CROWS + sub, rb = r + RW;
                 const int64_t row_a = (int64_t)tile * gtc::BM + r, row_b = (int64_t)tile * gtc::BM + rb;
                 const bool oka = row_a < n, okb = rb < gtc::BM && row_b < n;
                 float4 acc_a = make_float4(0.f, 0.f, 0.f, 0.f), acc_b = acc_a;
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             uint32_t it = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int si = it % gtc::ISTAGES;
-                if (it >= gtc::ISTAGES) mbar_wait(&bars->iempty[si], ((it / gtc::ISTAGES) - 1) & 1);
+                if (it >= gtc::ISTAGES) mbar_wait_sleep(&bars->iempty[si], ((it / gtc::ISTAGES) - 1) & 1);
                 GtcIdx& ix = idx[si];
                 const int64_t r0 = (int64_t)tile * gtc::BM;
                 const int nr = (int)min((int64_t)gtc::BM, (int64_t)n - r0);
@@ -240,8 +252,8 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int s = it % gtc::ASTAGES;
                 const uint32_t a = it & 1, u = it >> 1;
-                if (u >= 1) mbar_wait(&bars->accempty[a], (u - 1) & 1);
-                mbar_wait(&bars->full[s], (it / gtc::ASTAGES) & 1);
+                if (u >= 1) mbar_wait_sleep(&bars->accempty[a], (u - 1) & 1);
+                mbar_wait_sleep(&bars->full[s], (it / gtc::ASTAGES) & 1);
                 fence_after();
                 const uint32_t d = bars->tmem + a * HP;
                 const uint32_t a_hi = sb + s * L::A_STAGE, a_lo = a_hi + L::A_HALF;
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const uint32_t a = it & 1, u = it >> 1;
-            mbar_wait(&bars->accfull[a], u & 1);
+            mbar_wait_sleep(&bars->accfull[a], u & 1);
             fence_after();
 #pragma unroll
             for (int c0 = 0; c0 < HP; c0 += 8) {
