@@ -152,11 +152,25 @@ int dgnn_gcn_weight_grad(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, i
 
 /* ---------------- temporal stage (K5/K6/K7) ----------------------------- */
 
+/* Cache layouts.  x, h (h_prev, h_out), dy, dh and dx are row-major.  The
+ * per-step caches c (c_prev, c_out, c_new), gates / dz and dc are
+ * TILE-BLOCKED over the step's `rows`: element (r, j) of an n x w array is
+ * at  (r & ~127) w + (j / 4) 4 tr + (r & 127) 4 + (j % 4),
+ * tr = min(128, n - (r & ~127))  -- 4-column groups of 128-row tiles stored
+ * contiguously, so each warp access of these caches is 512 contiguous bytes.
+ * A step's array occupies exactly n w floats.  dgnn_tile_block /
+ * dgnn_tile_unblock convert. */
+
+/* row-major (steps x n) x w  <->  tile-blocked per step of n rows */
+int dgnn_tile_block(int64_t steps, int64_t n, int32_t w, const float* src, float* dst, void* stream);
+int dgnn_tile_unblock(int64_t steps, int64_t n, int32_t w, const float* src, float* dst, void* stream);
+
 /* K5 -- one LSTM step over `rows` vertex rows (training.py:370-391):
  *   z = [x | h_prev] * wcat + b,  wcat: (kx + hp) x 4hp, gate blocks [i|f|o|g]
  *   c = f c_prev + i g,  h = o tanh(c)
- * x rows have kx (= padded fin) columns at stride ldx; h/c rows stride hp;
- * gates (nullable) caches [i|f|o|g] at stride 4hp.  hp in {16,32,64,128}. */
+ * x rows have kx (= padded fin) columns at stride ldx; h rows stride hp;
+ * c_prev / c_out tile-blocked (rows x hp); gates (nullable) caches [i|f|o|g],
+ * tile-blocked rows x 4hp.  hp in {16,32,64,128}. */
 int dgnn_lstm_forward_step(int64_t rows, int32_t kx, int32_t hp, const float* x, int64_t ldx,
                            const float* h_prev, const float* c_prev, const float* wcat,
                            const float* bias, float* h_out, float* c_out, float* gates,
@@ -215,7 +229,8 @@ int dgnn_lstm_backward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float
  *   gwcat[k][j] += sum_r xcat[r][k] dz[r][j],  gb[j] += sum_r dz[r][j]
  * over rows r = t*np + v of the block (rows = bsize*np), with
  * xcat[r] = [x[r] (kx cols, ld ldx) | h_prev] and h_prev = h_out[r - np]
- * (t > 0) or h0[v] (t = 0).  dz: rows x 4hp.  Operands MN-major straight
+ * (t > 0) or h0[v] (t = 0).  dz: bsize steps of np x 4hp, each tile-blocked
+ * (the backward step's in-place output).  Operands MN-major straight
  * from HBM, 3xTF32, TMEM accumulation restarted every 512 rows and promoted
  * to per-CTA fp32 slots, fp64 fixed-order final reduction.  hp in
  * {32, 64}, kx + hp <= 256. */
@@ -229,7 +244,8 @@ int dgnn_lstm_weight_grad_tc(int64_t rows, int64_t np, int32_t kx, int32_t hp, c
  *   dh = dy + dh_in; do, dc, df, di, dg as the reference; dc_out = dc f
  *   dz = [di i(1-i) | df f(1-f) | do o(1-o) | dg (1-g^2)]  (written, 4hp wide)
  *   [dx | dh_out] = dz * wcat^T   using wcat_t (4hp x (kx+hp), row-major)
- * dy == NULL means zero.  dz may alias gates (in-place). */
+ * dy == NULL means zero.  dz may alias gates (in-place).  gates, dz, c_prev,
+ * c_new, dc_in, dc_out tile-blocked; dy, dh_in, dh_out, dx row-major. */
 int dgnn_lstm_backward_step(int64_t rows, int32_t kx, int32_t hp, const float* dy,
                             const float* dh_in, const float* dc_in, const float* gates,
                             const float* c_prev, const float* c_new, const float* wcat_t,

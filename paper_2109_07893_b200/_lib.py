@@ -44,6 +44,8 @@ _SIGS = {
     "dgnn_gcn_weight_grad_workspace": (c_size_t, [c_int32, c_int32]),
     "dgnn_gcn_weight_grad": (c_int, [c_int32, Frame, Frame, Frame, c_int32, c_int32, c_int, P, P,
                                      c_size_t, P]),
+    "dgnn_tile_block": (c_int, [c_int64, c_int64, c_int32, P, P, P]),
+    "dgnn_tile_unblock": (c_int, [c_int64, c_int64, c_int32, P, P, P]),
     "dgnn_lstm_forward_step": (c_int, [c_int64, c_int32, c_int32, P, c_int64, P, P, P, P, P, P, P, P]),
     "dgnn_tc_weight_image_bytes": (c_size_t, [c_int32, c_int32]),
     "dgnn_tc_weight_image": (c_int, [c_int32, c_int32, P, c_int64, P, P]),

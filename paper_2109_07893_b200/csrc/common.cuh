@@ -29,6 +29,21 @@ __device__ __forceinline__ T* frame_row(const dgnn_frame& f, int64_t i) {
     return reinterpret_cast<T*>(f.ptr) + s * f.slab_stride + r * f.ld;
 }
 
+// ---- tile-blocked layout of the LSTM step caches -----------------------
+// The per-step cell state c, the gate cache (overwritten in place by dz) and
+// the cell-state gradient dc are stored "tile-blocked": rows in tiles of 128,
+// columns in groups of 4, and each (tile, group) block -- 4 floats of the
+// tile's rows -- contiguous.  Every producer and consumer of these caches
+// holds one row per lane, so a warp's float4 access covers 512 contiguous
+// bytes instead of 32 rows x 16 B.  Compact: the last tile of a step only
+// holds its own rows, so a step of n rows x W floats occupies n W floats.
+// (h stays row-major: the next layer gathers it by vertex.)
+__host__ __device__ __forceinline__ int64_t tb_off(int64_t row, int col, int w, int64_t n) {
+    const int64_t t0 = row & ~(int64_t)127;
+    const int64_t tr = n - t0 < 128 ? n - t0 : 128;
+    return t0 * w + (int64_t)(col >> 2) * 4 * tr + (row - t0) * 4 + (col & 3);
+}
+
 // ---- warp helpers -------------------------------------------------------
 __device__ __forceinline__ int warp_inclusive_scan(int v) {
     const int lane = threadIdx.x & 31;

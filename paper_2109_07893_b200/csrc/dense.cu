@@ -186,11 +186,44 @@ __global__ void axpy_kernel(int64_t n, float coef, const float* __restrict__ y, 
     z[i] = init ? t : z[i] + t;
 }
 
+// row-major <-> tile-blocked (common.cuh tb_off), one float per thread
+template <bool TO_BLOCKED>
+__global__ void tile_block_kernel(int64_t total, int64_t n, int w, const float* __restrict__ src,
+                                  float* __restrict__ dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int64_t step_elems = n * w;
+    const int64_t t = i / step_elems, rem = i - t * step_elems;
+    const int64_t r = rem / w;
+    const int j = (int)(rem - r * w);
+    const int64_t b = t * step_elems + tb_off(r, j, w, n);
+    if (TO_BLOCKED) dst[b] = src[i];
+    else dst[i] = src[b];
+}
+
 }  // namespace dgnn
 
 using namespace dgnn;
 
 extern "C" {
+
+int dgnn_tile_block(int64_t steps, int64_t n, int32_t w, const float* src, float* dst, void* stream) {
+    DGNN_CHECK_ARG(steps >= 0 && n >= 0 && w > 0 && w % 4 == 0, "tile_block: bad sizes");
+    const int64_t total = steps * n * w;
+    if (total == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    tile_block_kernel<true><<<(unsigned)cdiv(total, 256), 256, 0, as_stream(stream)>>>(total, n, w, src, dst);
+    return launch_status("tile_block");
+}
+
+int dgnn_tile_unblock(int64_t steps, int64_t n, int32_t w, const float* src, float* dst, void* stream) {
+    DGNN_CHECK_ARG(steps >= 0 && n >= 0 && w > 0 && w % 4 == 0, "tile_unblock: bad sizes");
+    const int64_t total = steps * n * w;
+    if (total == 0) return DGNN_OK;
+    ::dgnn::note_launch();
+    tile_block_kernel<false><<<(unsigned)cdiv(total, 256), 256, 0, as_stream(stream)>>>(total, n, w, src, dst);
+    return launch_status("tile_unblock");
+}
 
 size_t dgnn_gemm_tn_workspace(int32_t m, int32_t n) { return tn_workspace_bytes(m, n); }
 

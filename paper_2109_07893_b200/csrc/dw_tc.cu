@@ -11,14 +11,14 @@
 // in lstm_tc.cu.  One persistent CTA per SM owns a contiguous row range.
 //
 // Warp-specialised (same scheme as lstm_ws.cu):
-//   warps 0..3  loaders: cp.async the raw fp32 rows of a stage straight into
+//   warps 0..7  loaders: cp.async the raw fp32 rows of a stage straight into
 //               the swizzled hi tiles as soon as its slot is free, completion
 //               tracked by landed[s] (cp.async.mbarrier.arrive);
-//   warps 4..11 converters: split each landed stage in place (hi, lo), fold
+//   warps 8..15 converters: split each landed stage in place (hi, lo), fold
 //               dz into fp64 column sums (db), arrive full[s] -- never
 //               blocked behind the slot-reuse wait;
-//   warp 12     MMA issuer: 2 x mt x 3 MMAs per 16-row stage;
-//   warps 13..16 epilogue: promotion of each finished accumulation period.
+//   warp 16     MMA issuer: 2 x mt x 3 MMAs per 16-row stage;
+//   warps 17..20 epilogue: promotion of each finished accumulation period.
 //
 // tcgen05 fp32 accumulation truncates, so a TMEM accumulator only lives for
 // DW_PERIOD rows; then it is promoted (fp32, round-to-nearest) into the CTA's
@@ -35,7 +35,7 @@ using namespace tc;
 constexpr int DW_ROWS = 16;      // reduction rows per stage = two 8-row K steps
 constexpr int DW_PERIOD = 512;   // rows per TMEM accumulation period
 constexpr int DW_MAX_STAGES = 4;
-constexpr int DW_NLOAD = 4, DW_NCONV = 8, DW_NPROD = DW_NLOAD + DW_NCONV, DW_MMA_WARP = DW_NPROD, DW_NEPI = 4;
+constexpr int DW_NLOAD = 8, DW_NCONV = 8, DW_NPROD = DW_NLOAD + DW_NCONV, DW_MMA_WARP = DW_NPROD, DW_NEPI = 4;
 constexpr int DW_THREADS = 32 * (DW_NPROD + 1 + DW_NEPI);
 constexpr int DW_SMEM_MAX = 232448;
 // Bottleneck probe (scripts/dw_probe.cu, -DDGNN_DW_PROBE=mask): 1 skip MMAs,
@@ -160,9 +160,11 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
         uint32_t aoff[LA_ITEMS], boff[LB_ITEMS];
 #pragma unroll
         for (int i = 0; i < LA_ITEMS; ++i) {
+            // consecutive lanes take consecutive rows of one 4-column group:
+            // 16 rows x 16 B contiguous in the tile-blocked dz
             const int idx = lt + 32 * DW_NLOAD * i;
-            arow[i] = idx / (M / 4);
-            acol[i] = 4 * (idx % (M / 4));
+            arow[i] = idx % DW_ROWS;
+            acol[i] = 4 * (idx / DW_ROWS);
             aoff[i] = mn_off(arow[i], acol[i], S.atoms_a);
         }
 #pragma unroll
@@ -172,17 +174,34 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
             bcol[i] = idx < BVEC ? 4 * (idx % (S.N / 4)) : 0;
             boff[i] = idx < BVEC ? mn_off(brow[i], bcol[i], S.atoms_b) : 0u;
         }
+        // dz is tile-blocked per step (common.cuh tb_off, rows r = t np + v).
+        // Every A item of this thread is the same stage row (lt % 16), so the
+        // row part of the address is formed once per stage from an
+        // incrementally tracked (t, v); items add their column block.
+        int64_t ct = r_begin / np, cv = r_begin - ct * np + (lt % DW_ROWS);
+        while (cv >= np) {
+            cv -= np;
+            ++ct;
+        }
         for (int g = 0; g < nst; ++g) {
             const int s = g % S.stages;
             const int j = g / S.stages;
             if (j >= 1) dw_wait(&bars->empty[s], (j - 1) & 1, wacc0);
             const int64_t r0 = r_begin + (int64_t)g * DW_ROWS;
             const uint32_t a_hi = sb + s * S.stage, b_hi = a_hi + 2 * S.a_half;
+            {
+                const int64_t v0 = cv & ~(int64_t)127;
+                const int64_t tr = min((int64_t)128, np - v0);
+                const float* rowp = dz + (ct * np + v0) * M + (cv - v0) * 4;   // tb_off(cv, 0, M, np)
+                const bool ok = r0 + arow[0] < r_end && !(DW_PROBE & 2);
 #pragma unroll
-            for (int i = 0; i < LA_ITEMS; ++i) {
-                const int64_t gr = r0 + arow[i];
-                const bool ok = gr < r_end && !(DW_PROBE & 2);
-                cp_async16(a_hi + aoff[i], ok ? dz + gr * M + acol[i] : dz, ok ? 16u : 0u);
+                for (int i = 0; i < LA_ITEMS; ++i)
+                    cp_async16(a_hi + aoff[i], ok ? rowp + (int64_t)acol[i] * tr : dz, ok ? 16u : 0u);
+                cv += DW_ROWS;
+                while (cv >= np) {
+                    cv -= np;
+                    ++ct;
+                }
             }
 #pragma unroll
             for (int i = 0; i < LB_ITEMS; ++i) {

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) lstm_fwd_kernel(int64_t rows, int kx, con
     for (int i = 0; i < C::RPT; ++i) {
         const int64_t g = row0 + rg * C::RPT + i;
         if (g >= rows) continue;
-        const float2 cp = ld2(cprev + g * HP + u0);
+        const float2 cp = ld2(cprev + tb_off(g, u0, HP, rows));
         float hv[2], cv[2], gi[2], gf[2], go[2], gg[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -110,13 +110,12 @@ __global__ void __launch_bounds__(256) lstm_fwd_kernel(int64_t rows, int kx, con
             hv[j] = go[j] * act_tanh(cv[j]);
         }
         st2(hout + g * HP + u0, hv[0], hv[1]);
-        st2(cout + g * HP + u0, cv[0], cv[1]);
+        st2(cout + tb_off(g, u0, HP, rows), cv[0], cv[1]);
         if (gates) {
-            float* gr = gates + g * C::NC + u0;
-            st2(gr + 0 * HP, gi[0], gi[1]);
-            st2(gr + 1 * HP, gf[0], gf[1]);
-            st2(gr + 2 * HP, go[0], go[1]);
-            st2(gr + 3 * HP, gg[0], gg[1]);
+            st2(gates + tb_off(g, 0 * HP + u0, C::NC, rows), gi[0], gi[1]);
+            st2(gates + tb_off(g, 1 * HP + u0, C::NC, rows), gf[0], gf[1]);
+            st2(gates + tb_off(g, 2 * HP + u0, C::NC, rows), go[0], go[1]);
+            st2(gates + tb_off(g, 3 * HP + u0, C::NC, rows), gg[0], gg[1]);
         }
     }
 }
@@ -157,24 +156,24 @@ __global__ void __launch_bounds__(256) lstm_bwd_kernel(int64_t rows, int kx, con
         const int64_t g = row0 + r;
         float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
         if (g < rows) {
-            const float* gr = gates + g * C::NC + u;
-            const float gi = gr[0], gf = gr[HP], go = gr[2 * HP], gg = gr[3 * HP];
-            const float cp = cprev[g * HP + u], cn = cnew[g * HP + u];
+            const float gi = gates[tb_off(g, u, C::NC, rows)], gf = gates[tb_off(g, HP + u, C::NC, rows)],
+                        go = gates[tb_off(g, 2 * HP + u, C::NC, rows)], gg = gates[tb_off(g, 3 * HP + u, C::NC, rows)];
+            const int64_t o = tb_off(g, u, HP, rows);
+            const float cp = cprev[o], cn = cnew[o];
             const float tc = act_tanh(cn);
             const float dh = (dy ? dy[g * HP + u] : 0.f) + dh_in[g * HP + u];
             const float d_o = dh * tc;
-            const float dc = dh * go * (1.f - tc * tc) + dc_in[g * HP + u];
+            const float dc = dh * go * (1.f - tc * tc) + dc_in[o];
             const float df = dc * cp, di = dc * gg, dg = dc * gi;
-            dc_out[g * HP + u] = dc * gf;
+            dc_out[o] = dc * gf;
             z0 = di * gi * (1.f - gi);
             z1 = df * gf * (1.f - gf);
             z2 = d_o * go * (1.f - go);
             z3 = dg * (1.f - gg * gg);
-            float* dzr = dz + g * C::NC + u;
-            dzr[0] = z0;
-            dzr[HP] = z1;
-            dzr[2 * HP] = z2;
-            dzr[3 * HP] = z3;
+            dz[tb_off(g, u, C::NC, rows)] = z0;
+            dz[tb_off(g, HP + u, C::NC, rows)] = z1;
+            dz[tb_off(g, 2 * HP + u, C::NC, rows)] = z2;
+            dz[tb_off(g, 3 * HP + u, C::NC, rows)] = z3;
         }
         dzs[(0 * HP + u) * C::BM + r] = z0;
         dzs[(1 * HP + u) * C::BM + r] = z1;

@@ -261,8 +261,9 @@ __global__ void __launch_bounds__(256, (HP <= 64 ? 2 : 1)) lstm_fwd_tc_kernel(
         tmem_wait_ld();
         if (row >= rows) continue;
         float cp[8], hv[8], cv[8], gi[8], gf[8], go[8], gg[8];
-        *reinterpret_cast<float4*>(cp) = __ldg(reinterpret_cast<const float4*>(cprev + row * HP + u0));
-        *reinterpret_cast<float4*>(cp + 4) = __ldg(reinterpret_cast<const float4*>(cprev + row * HP + u0 + 4));
+        *reinterpret_cast<float4*>(cp) = __ldg(reinterpret_cast<const float4*>(cprev + tb_off(row, u0, HP, rows)));
+        *reinterpret_cast<float4*>(cp + 4) =
+            __ldg(reinterpret_cast<const float4*>(cprev + tb_off(row, u0 + 4, HP, rows)));
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             gi[j] = act_sigmoid(z[0][j] + __ldg(bias + 0 * HP + u0 + j));
@@ -273,19 +274,18 @@ __global__ void __launch_bounds__(256, (HP <= 64 ? 2 : 1)) lstm_fwd_tc_kernel(
             hv[j] = go[j] * act_tanh(cv[j]);
         }
         float4* ho = reinterpret_cast<float4*>(hout + row * HP + u0);
-        float4* co = reinterpret_cast<float4*>(cout + row * HP + u0);
         ho[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
         ho[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
-        co[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-        co[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+        *reinterpret_cast<float4*>(cout + tb_off(row, u0, HP, rows)) = make_float4(cv[0], cv[1], cv[2], cv[3]);
+        *reinterpret_cast<float4*>(cout + tb_off(row, u0 + 4, HP, rows)) = make_float4(cv[4], cv[5], cv[6], cv[7]);
         if (gates) {
-            float* gr = gates + row * N + u0;
             float* src[4] = {gi, gf, go, gg};
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
-                float4* o = reinterpret_cast<float4*>(gr + g * HP);
-                o[0] = make_float4(src[g][0], src[g][1], src[g][2], src[g][3]);
-                o[1] = make_float4(src[g][4], src[g][5], src[g][6], src[g][7]);
+                *reinterpret_cast<float4*>(gates + tb_off(row, g * HP + u0, N, rows)) =
+                    make_float4(src[g][0], src[g][1], src[g][2], src[g][3]);
+                *reinterpret_cast<float4*>(gates + tb_off(row, g * HP + u0 + 4, N, rows)) =
+                    make_float4(src[g][4], src[g][5], src[g][6], src[g][7]);
             }
         }
     }
@@ -315,16 +315,15 @@ __global__ void __launch_bounds__(256, 2) lstm_bwd_tc_kernel(
             const int u = 4 * ch + (idx & 3);
             Cell p{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (g < rows) {
-                const float* gr = gates + g * NC + u;
-                const int64_t o = g * HP + u;
-                p.gi = gr[0];
-                p.gf = gr[HP];
-                p.go = gr[2 * HP];
-                p.gg = gr[3 * HP];
-                p.cp = __ldg(cprev + o);
-                p.cn = __ldg(cnew + o);
+                const int64_t o = g * HP + u, ob = tb_off(g, u, HP, rows);
+                p.gi = gates[tb_off(g, u, NC, rows)];
+                p.gf = gates[tb_off(g, HP + u, NC, rows)];
+                p.go = gates[tb_off(g, 2 * HP + u, NC, rows)];
+                p.gg = gates[tb_off(g, 3 * HP + u, NC, rows)];
+                p.cp = __ldg(cprev + ob);
+                p.cn = __ldg(cnew + ob);
                 p.dh = (dy ? __ldg(dy + o) : 0.f) + __ldg(dh_in + o);
-                p.dc = __ldg(dc_in + o);
+                p.dc = __ldg(dc_in + ob);
             }
             return p;
         },
@@ -336,16 +335,16 @@ __global__ void __launch_bounds__(256, 2) lstm_bwd_tc_kernel(
             const float d_o = p.dh * tcn;
             const float dc = p.dh * p.go * (1.f - tcn * tcn) + p.dc;
             const float df = dc * p.cp, di = dc * p.gg, dg = dc * p.gi;
-            dc_out[g * HP + u] = dc * p.gf;
+            dc_out[tb_off(g, u, HP, rows)] = dc * p.gf;
             const float z0 = di * p.gi * (1.f - p.gi);
             const float z1 = df * p.gf * (1.f - p.gf);
             const float z2 = d_o * p.go * (1.f - p.go);
             const float z3 = dg * (1.f - p.gg * p.gg);
-            float* gr = gates + g * NC + u;   // dz replaces the gate cache (training.py:413-421)
-            gr[0] = z0;
-            gr[HP] = z1;
-            gr[2 * HP] = z2;
-            gr[3 * HP] = z3;
+            // dz replaces the gate cache (training.py:413-421)
+            gates[tb_off(g, u, NC, rows)] = z0;
+            gates[tb_off(g, HP + u, NC, rows)] = z1;
+            gates[tb_off(g, 2 * HP + u, NC, rows)] = z2;
+            gates[tb_off(g, 3 * HP + u, NC, rows)] = z3;
             return make_float4(z0, z1, z2, z3);
         });
     const int K = kx + HP;

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
 #pragma unroll
             for (int i = 0; i < UPW / 4; ++i) {
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (valid) v = __ldg(reinterpret_cast<const float4*>(cprev + row * HP + part * UPW + 4 * i));
+                if (valid) v = __ldg(reinterpret_cast<const float4*>(cprev + tb_off(row, part * UPW + 4 * i, HP, rows)));
                 cp[4 * i] = v.x;
                 cp[4 * i + 1] = v.y;
                 cp[4 * i + 2] = v.z;
@@ -308,19 +308,20 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
                     continue;
                 }
                 float4* ho = reinterpret_cast<float4*>(hout + row * HP + u0);
-                float4* co = reinterpret_cast<float4*>(cout + row * HP + u0);
                 ho[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
                 ho[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
-                co[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-                co[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+                // c and the gate cache are tile-blocked: 512 B per warp store
+                *reinterpret_cast<float4*>(cout + tb_off(row, u0, HP, rows)) = make_float4(cv[0], cv[1], cv[2], cv[3]);
+                *reinterpret_cast<float4*>(cout + tb_off(row, u0 + 4, HP, rows)) =
+                    make_float4(cv[4], cv[5], cv[6], cv[7]);
                 if (gates) {
-                    float* gr = gates + row * N + u0;
                     const float* src[4] = {gi, gf, go, gg};
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
-                        float4* o = reinterpret_cast<float4*>(gr + g * HP);
-                        o[0] = make_float4(src[g][0], src[g][1], src[g][2], src[g][3]);
-                        o[1] = make_float4(src[g][4], src[g][5], src[g][6], src[g][7]);
+                        *reinterpret_cast<float4*>(gates + tb_off(row, g * HP + u0, N, rows)) =
+                            make_float4(src[g][0], src[g][1], src[g][2], src[g][3]);
+                        *reinterpret_cast<float4*>(gates + tb_off(row, g * HP + u0 + 4, N, rows)) =
+                            make_float4(src[g][4], src[g][5], src[g][6], src[g][7]);
                     }
                 }
             }
@@ -364,17 +365,16 @@ __global__ void __launch_bounds__(BwdRoles::THREADS, 1) lstm_bwd_ws_kernel(
                 const int u = 4 * ch + (idx & 3);
                 Cell p{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 if (g < rows) {
-                    const float* gr = gates + g * NC + u;
-                    const int64_t o = g * HP + u;
-                    p.gi = gr[0];
-                    p.gf = gr[HP];
-                    p.go = gr[2 * HP];
-                    p.gg = gr[3 * HP];
-                    p.cp = __ldg(cprev + o);
-                    p.cn = __ldg(cnew + o);
+                    const int64_t o = g * HP + u, ob = tb_off(g, u, HP, rows);
+                    p.gi = gates[tb_off(g, u, NC, rows)];
+                    p.gf = gates[tb_off(g, HP + u, NC, rows)];
+                    p.go = gates[tb_off(g, 2 * HP + u, NC, rows)];
+                    p.gg = gates[tb_off(g, 3 * HP + u, NC, rows)];
+                    p.cp = __ldg(cprev + ob);
+                    p.cn = __ldg(cnew + ob);
                     p.dh = __ldg(dh_in + o);
                     if (dy) p.dy = __ldg(dy + o);
-                    p.dc = __ldg(dc_in + o);
+                    p.dc = __ldg(dc_in + ob);
                 }
                 v[i] = p;
             }
@@ -406,14 +406,14 @@ __global__ void __launch_bounds__(BwdRoles::THREADS, 1) lstm_bwd_ws_kernel(
                     const float d_o = dhv * tcn;
                     const float dc = dhv * p.go * (1.f - tcn * tcn) + p.dc;
                     const float df = dc * p.cp, di = dc * p.gg, dg = dc * p.gi;
-                    dc_out[row * HP + u] = dc * p.gf;
+                    dc_out[tb_off(row, u, HP, rows)] = dc * p.gf;
                     z = make_float4(di * p.gi * (1.f - p.gi), df * p.gf * (1.f - p.gf), d_o * p.go * (1.f - p.go),
                                     dg * (1.f - p.gg * p.gg));
-                    float* gr = gates + row * NC + u;   // dz replaces the gate cache
-                    gr[0] = z.x;
-                    gr[HP] = z.y;
-                    gr[2 * HP] = z.z;
-                    gr[3 * HP] = z.w;
+                    // dz replaces the gate cache
+                    gates[tb_off(row, u, NC, rows)] = z.x;
+                    gates[tb_off(row, HP + u, NC, rows)] = z.y;
+                    gates[tb_off(row, 2 * HP + u, NC, rows)] = z.z;
+                    gates[tb_off(row, 3 * HP + u, NC, rows)] = z.w;
                 }
                 vals[i] = z;
             }

@@ -394,13 +394,19 @@ class Rank:
             return
         ws = self.ws_tn
         K4 = 4 * ho
-        call("dgnn_gemm_tn", B * NP, Ly.kx, K4, ptr(self.R_vm[l]), Ly.rw, ptr(self.G_vm[l]), K4, ptr(g_wcat), K4,
+        # the split-K SIMT GEMM reads dz row-major: unblock the tile-blocked cache
+        need = B * NP * K4
+        if getattr(self, "dz_rows", None) is None or self.dz_rows.numel() < need:
+            self.dz_rows = torch.empty(need, dtype=torch.float32, device=self.G_vm[l].device)
+        dz = self.dz_rows
+        call("dgnn_tile_unblock", B, NP, K4, ptr(self.G_vm[l]), ptr(dz), st)
+        call("dgnn_gemm_tn", B * NP, Ly.kx, K4, ptr(self.R_vm[l]), Ly.rw, ptr(dz), K4, ptr(g_wcat), K4,
              ptr(g_b), ptr(ws), ws.numel(), st)
         g_wh = g_wcat[Ly.kx:]
         if B > 1:
-            call("dgnn_gemm_tn", (B - 1) * NP, ho, K4, ptr(self.Y_vm[l]), ho, ptr(self.vm(self.G_vm[l], K4, 1)),
+            call("dgnn_gemm_tn", (B - 1) * NP, ho, K4, ptr(self.Y_vm[l]), ho, ptr(self.vm(dz, K4, 1)),
                  K4, ptr(g_wh), K4, None, ptr(ws), ws.numel(), st)
-        call("dgnn_gemm_tn", NP, ho, K4, ptr(self.act[l][0]), ho, ptr(self.G_vm[l]), K4, ptr(g_wh), K4, None,
+        call("dgnn_gemm_tn", NP, ho, K4, ptr(self.act[l][0]), ho, ptr(dz), K4, ptr(g_wh), K4, None,
              ptr(ws), ws.numel(), st)
 
     def _mprod_backward(self, b, l):

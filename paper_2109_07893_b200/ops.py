@@ -258,6 +258,15 @@ def _lstm_weights(wx, wh, b, dev):
     return H, hp, kx, torch.from_numpy(wc).to(dev), torch.from_numpy(wct).to(dev), torch.from_numpy(bb).to(dev)
 
 
+def _tile(t: torch.Tensor, w: int, to_blocked: bool) -> torch.Tensor:
+    """rows x w row-major <-> tile-blocked (the LSTM cache layout, see
+    include/dgnn_b200.h)."""
+    out = torch.empty_like(t)
+    call("dgnn_tile_block" if to_blocked else "dgnn_tile_unblock", 1, t.shape[0], w, ptr(t), ptr(out),
+         _lib.stream_handle())
+    return out
+
+
 def tc_gemm(a: np.ndarray, w: np.ndarray) -> np.ndarray:
     """a @ w.T on the tcgen05 3xTF32 mainloop (self-test of the tensor-core
     path); a: m x k, w: n x k with n in {64, 128, 256}, k % 4 == 0."""
@@ -306,6 +315,9 @@ def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np
     rows, kx = x.shape
     hp = h0.shape[1]
     t = [torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev) for a in (x, h_out, h0, dz)]
+    blk = torch.empty_like(t[3])     # dz is tile-blocked per step of np_rows rows
+    call("dgnn_tile_block", rows // np_rows, np_rows, 4 * hp, ptr(t[3]), ptr(blk), _lib.stream_handle())
+    t[3] = blk
     gw = torch.zeros((kx + hp) * 4 * hp, dtype=torch.float64, device=dev)
     gb = torch.zeros(4 * hp, dtype=torch.float64, device=dev)
     ws = torch.empty(query("dgnn_lstm_weight_grad_tc_workspace", kx, hp), dtype=torch.uint8, device=dev)
@@ -329,7 +341,7 @@ def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True, 
     rows = h0.shape[0]
     st = _lib.stream_handle()
     h = _pad_rows(np.asarray(h0), hp, dev)
-    c = _pad_rows(np.asarray(c0), hp, dev)
+    c = _tile(_pad_rows(np.asarray(c0), hp, dev), hp, True)
     cache = {"h0": h, "c0": c, "x": [], "h": [], "c": [], "g": [], "H": H, "hp": hp, "kx": kx,
              "wc": wc, "wct": wct, "rows": rows}
     ys = {}
@@ -350,6 +362,7 @@ def lstm_block_forward(cell, state_in, ts, xs: dict, tensor_cores: bool = True, 
         cache["g"].append(g)
         h, c = hn, cn
         ys[t] = hn[:, :H].double().cpu().numpy()
+    c = _tile(c, hp, False)
     return ys, (h[:, :H].double().cpu().numpy(), c[:, :H].double().cpu().numpy()), cache
 
 
@@ -365,7 +378,7 @@ def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bo
         bimg = torch.zeros(query("dgnn_tc_weight_image_bytes", nb, 4 * hp) // 4, dtype=torch.float32, device=dev)
         call("dgnn_tc_weight_image_ex", nb, kx + hp, 4 * hp, ptr(cache["wc"]), 4 * hp, hp, ptr(bimg), st)
     dh = _pad_rows(np.asarray(dstate_out[0]), hp, dev)
-    dc = _pad_rows(np.asarray(dstate_out[1]), hp, dev)
+    dc = _tile(_pad_rows(np.asarray(dstate_out[1]), hp, dev), hp, True)
     K4 = 4 * hp
     gwc = torch.zeros((kx + hp) * K4, dtype=torch.float64, device=dev)
     gb = torch.zeros(K4, dtype=torch.float64, device=dev)
@@ -393,9 +406,10 @@ def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bo
         if bimg is not None and hp >= 32:
             dzs[i] = dz
         else:
-            call("dgnn_gemm_tn", rows, kx, K4, ptr(cache["x"][i]), kx, ptr(dz), K4, ptr(gwc), K4, ptr(gb),
+            dzr = _tile(dz, K4, False)
+            call("dgnn_gemm_tn", rows, kx, K4, ptr(cache["x"][i]), kx, ptr(dzr), K4, ptr(gwc), K4, ptr(gb),
                  ptr(ws), ws.numel(), st)
-            call("dgnn_gemm_tn", rows, hp, K4, ptr(h_prev), hp, ptr(dz), K4, ptr(gwc[kx * K4:]), K4, None,
+            call("dgnn_gemm_tn", rows, hp, K4, ptr(h_prev), hp, ptr(dzr), K4, ptr(gwc[kx * K4:]), K4, None,
                  ptr(ws), ws.numel(), st)
         fin = np.asarray(cell.wx).shape[0]
         dxs[t] = dx[:, :fin].double().cpu().numpy()
@@ -418,5 +432,6 @@ def lstm_block_backward(cell, ts, cache, dys: dict, dstate_out, tensor_cores: bo
         dwx[:, gi * H:(gi + 1) * H] = g[:fin, gi * hp:gi * hp + H]
         dwh[:, gi * H:(gi + 1) * H] = g[kx:kx + H, gi * hp:gi * hp + H]
         db[gi * H:(gi + 1) * H] = gbv[gi * hp:gi * hp + H]
+    dc = _tile(dc, hp, False)
     return dxs, (dh[:, :H].double().cpu().numpy(), dc[:, :H].double().cpu().numpy()), \
         {"wx": dwx, "wh": dwh, "b": db}
