@@ -51,6 +51,10 @@ const char* dgnn_last_error(void);
 int dgnn_abi_version(void);
 /* Number of kernels launched through this library so far (process-wide). */
 long long dgnn_launch_count(void);
+/* Keep `sms` SMs free of the persistent (one CTA per SM) kernels so that
+ * communication kernels running concurrently on another stream (NCCL P2P of
+ * the multi-GPU exchange) are scheduled at once; 0 (default) uses all 148. */
+void dgnn_set_sm_reserve(int sms);
 /* 1 if the loaded cubin targets sm_100a and a device of that class is present */
 int dgnn_device_check(int device);
 

@@ -27,6 +27,7 @@ _SIGS = {
     "dgnn_abi_version": (c_int, []),
     "dgnn_launch_count": (ctypes.c_longlong, []),
     "dgnn_device_check": (c_int, [c_int]),
+    "dgnn_set_sm_reserve": (None, [c_int]),
     "dgnn_rowptr_from_sorted_rows": (c_int, [c_int32, c_int64, P, P, P]),
     "dgnn_csr_apply_delta_workspace": (c_size_t, [c_int32]),
     "dgnn_csr_apply_delta": (c_int, [c_int32, P, P, c_int64, P, P, c_int64, P, P, P, P, c_int64, P,

@@ -406,6 +406,9 @@ int lstm_dw_tc_t(int64_t rows, int64_t np, int kx, const float* x, int64_t ldx, 
         set_error("lstm_weight_grad_tc: kx + hp = %d too wide", kx + HP);
         return DGNN_EUNSUPPORTED;
     }
+    // always one CTA per SM: the CTA row ranges (and so the fp32 period
+    // sums) must not depend on dgnn_set_sm_reserve, or results would differ
+    // between single- and multi-GPU runs
     const int grid = kSMs;
     const size_t need = (size_t)grid * S.M * S.N * sizeof(float) + (size_t)grid * S.M * sizeof(double);
     if (ws_bytes < need) {

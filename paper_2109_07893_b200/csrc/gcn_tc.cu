@@ -327,7 +327,7 @@ int gcn_fwd_tc_t(int32_t n, const int32_t* rp, const int32_t* col, const float* 
     auto k = gcn_fwd_tc_kernel<FP, HP, SKIP, AGG>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     const int ntiles = (int)cdiv(n, gtc::BM);
-    const int grid = ntiles < kSMs ? ntiles : kSMs;
+    const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
     note_launch();
     k<<<grid, gtc::THREADS, L::BYTES, st>>>(n, rp, col, val, x, w, s_out, r_out);
     return launch_status("gcn_forward (tcgen05)");

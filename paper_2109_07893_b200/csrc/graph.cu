@@ -15,6 +15,9 @@ static thread_local char g_err[1024] = "";
 static std::atomic<long long> g_launches{0};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static std::atomic<int> g_sm_reserve{0};
+int persistent_ctas() { return kSMs - g_sm_reserve.load(std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
@@ -357,6 +360,12 @@ const char* dgnn_last_error(void) { return dgnn::last_error(); }
 int dgnn_abi_version(void) { return 1; }
 
 long long dgnn_launch_count(void) { return dgnn::launch_count(); }
+
+void dgnn_set_sm_reserve(int sms) {
+    if (sms < 0) sms = 0;
+    if (sms > dgnn::kSMs / 2) sms = dgnn::kSMs / 2;
+    dgnn::g_sm_reserve.store(sms, std::memory_order_relaxed);
+}
 
 int dgnn_device_check(int device) {
     cudaDeviceProp p;

@@ -471,7 +471,7 @@ int lstm_fwd_ws_t(int64_t rows, int kx, const float* x, int64_t ldx, const float
     const size_t smem = ws_smem_bytes(N);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int ntiles = (int)cdiv(rows, wsk::BM);
-    const int grid = ntiles < kSMs ? ntiles : kSMs;
+    const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
     note_launch();
     k<<<grid, FwdRoles<HP>::THREADS, smem, st>>>(rows, kx, x, ldx, hp_, cp, img, b, h, c, gates);
     return launch_status("lstm_forward_step_ws");
@@ -490,7 +490,7 @@ int lstm_bwd_ws_t(int64_t rows, int kx, const float* dy, const float* dh_in, con
     const size_t smem = ws_smem_bytes(N);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int ntiles = (int)cdiv(rows, wsk::BM);
-    const int grid = ntiles < kSMs ? ntiles : kSMs;
+    const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
     note_launch();
     k<<<grid, BwdRoles::THREADS, smem, st>>>(rows, kx, N, dy, dh_in, dc_in, gates, cp, cn, img, dx, lddx, dh_out,
                                          dc_out);

@@ -23,6 +23,8 @@ ledgers and results line up call for call, but every phase is device work:
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -35,6 +37,10 @@ from .params import DeviceParams, ParamLayout
 
 F32 = 4
 WARP_SPECIALIZED = True
+# multi-GPU: fold the forward all-to-alls into the producing loops (P2P per slab / step)
+PIPELINED_EXCHANGE = True
+# SMs the persistent kernels leave free for the concurrent NCCL P2P kernels
+SM_RESERVE = int(os.environ.get("DGNN_SM_RESERVE", "32"))
 
 
 class Plan:
@@ -227,6 +233,50 @@ class Rank:
             self.mat.wait()
             self.graph_waited = True
 
+    def gcn_forward_pipelined(self, b, l):
+        """Multi-GPU forward GCN of layer l with the owner -> vertex-major
+        exchange folded in: every owned snapshot is computed one destination
+        row slab at a time (destination order me+1, me+2, ...), and each
+        finished slab is sent to its rank with NCCL P2P (grouped send + recv,
+        rank p sends to p+k while receiving from p-k) while the next slab is
+        computed; this rank's own slab is copied locally.  Returns the NCCL
+        works to wait on."""
+        import torch.distributed as dist
+        eng = self.eng
+        plan = eng.plan
+        P, C, NP, me = plan.P, plan.chunk, plan.NP, self.q
+        Ly = eng.layout.layers[l]
+        st = _lib.stream_handle()
+        w = eng.params.w(f"gcn{l}.w")
+        fp, rw = Ly.fp, Ly.rw
+        works = []
+        for c, t in enumerate(self.ts):
+            if l > 0:
+                self._wait_graph()
+                x_all = self.own(self.Y_own[l - 1], fp, c)
+                s = self.slots[c]
+            for k in range(P):
+                q = (me + k) % P
+                if l == 0:
+                    x = _lib.Frame(self.s1[t].data_ptr() + F32 * q * NP * fp, fp, 0, 0)
+                    rp = col = val = None
+                else:
+                    x = x_all
+                    rp, col, val = s.rowptr.data_ptr() + 4 * q * NP, ptr(s.col), ptr(s.val)
+                s_out = _lib.Frame(self.S_own[l].data_ptr() + F32 * (c * plan.N + q * NP) * fp, fp, 0, 0) \
+                    if (self.keep and l > 0) else _lib.Frame(None, 0, 0, 0)
+                dst = self.own_slab_rows(self.R_own[l], rw, c, q)
+                call("dgnn_gcn_forward", NP, rp, col, val, x, fp, ptr(w), Ly.hg, int(self.skip), s_out,
+                     _lib.Frame(dst.data_ptr(), rw, 0, 0), st)
+                if q == me:   # the backward reads the relu masks from the owner layout too
+                    self.vm(self.R_vm[l], rw, me * C + c).copy_(dst)
+                else:
+                    src = (me - k) % P
+                    ops = [dist.P2POp(dist.isend, dst, q),
+                           dist.P2POp(dist.irecv, self.vm(self.R_vm[l], rw, src * C + c), src)]
+                    works += dist.batch_isend_irecv(ops)
+        return works
+
     def gcn_forward(self, b, l):
         eng = self.eng
         Ly = eng.layout.layers[l]
@@ -245,7 +295,7 @@ class Rank:
             call("dgnn_gcn_forward", eng.plan.N, rp, col, val, x, Ly.fp, ptr(w), Ly.hg, int(self.skip),
                  s_out, self.own(self.R_own[l], Ly.rw, c), st)
 
-    def rnn_forward(self, b, l):
+    def rnn_forward(self, b, l, pipelined=False):
         eng = self.eng
         Ly = eng.layout.layers[l]
         NP, B = eng.plan.NP, eng.plan.bsize
@@ -261,6 +311,7 @@ class Rank:
         bias = eng.params.w(f"lstm{l}.b")
         h_prev, c_prev = self.act[l]
         ho = Ly.ho
+        works = []
         for i in range(B):
             x = self.vm(self.R_vm[l], Ly.rw, i)
             h_out = self.vm(self.Y_vm[l], ho, i)
@@ -269,9 +320,41 @@ class Rank:
             call(fn, NP, Ly.kx, ho, ptr(x), Ly.rw, ptr(h_prev), ptr(c_prev), ptr(wop), ptr(bias), ptr(h_out),
                  ptr(c_out), ptr(gates), st)
             h_prev, c_prev = h_out, c_out
+            if pipelined:
+                works += self._send_step_to_owner(self.Y_vm[l], self.Y_own[l], ho, i)
         if not self.keep:
             self.state[l][0].copy_(h_prev)
             self.state[l][1].copy_(c_prev)
+        return works
+
+    def _scatter_owned_step(self, own_buf, vm_buf, W, c):
+        """Owned step c, owner layout -> every rank's vertex-major step
+        me*C + c (shift pattern: send to me+k, receive from me-k)."""
+        import torch.distributed as dist
+        plan = self.eng.plan
+        P, C, me = plan.P, plan.chunk, self.q
+        self.vm(vm_buf, W, me * C + c).copy_(self.own_slab_rows(own_buf, W, c, me))
+        ops = []
+        for k in range(1, P):
+            q, src = (me + k) % P, (me - k) % P
+            ops += [dist.P2POp(dist.isend, self.own_slab_rows(own_buf, W, c, q), q),
+                    dist.P2POp(dist.irecv, self.vm(vm_buf, W, src * C + c), src)]
+        return dist.batch_isend_irecv(ops)
+
+    def _send_step_to_owner(self, vm_buf, own_buf, W, i):
+        """Vertex-major block step i (this rank's vertex chunk) -> slot
+        [me][c] of the owner layout on the step's owner; the owner receives
+        every other rank's chunk.  Overlaps the next LSTM step."""
+        import torch.distributed as dist
+        plan = self.eng.plan
+        P, C, me = plan.P, plan.chunk, self.q
+        p, c = i // C, i % C
+        rows = self.vm(vm_buf, W, i)
+        if p != me:
+            return dist.batch_isend_irecv([dist.P2POp(dist.isend, rows, p)])
+        self.own_slab_rows(own_buf, W, c, me).copy_(rows)
+        ops = [dist.P2POp(dist.irecv, self.own_slab_rows(own_buf, W, c, src), src) for src in range(P) if src != me]
+        return dist.batch_isend_irecv(ops) if ops else []
 
     def _mprod_forward(self, b, l):
         """`training.py:430-441` over the vertex chunk; trailing frames from
@@ -330,8 +413,15 @@ class Rank:
                  eng.layout.ep, eng.cfg.classes, ptr(eng.params.w("head.w")), ptr(eng.params.w("head.b")),
                  ptr(self.correct), st)
 
-    def loss_grads(self, b):
-        """`training.py:713-735`: head grads + dz seeds (owner layout)."""
+    def loss_grads(self, b, pipelined=False):
+        """`training.py:713-735`: head grads + dz seeds (owner layout); when
+        pipelined, each owned step's seeds are scattered to the vertex-major
+        buffers of every rank as soon as they are written (returns works)."""
+        works = []
+        self._loss_grads(b, works if pipelined else None)
+        return works
+
+    def _loss_grads(self, b, works):
         eng = self.eng
         Ly = eng.layout.layers[-1]
         st = _lib.stream_handle()
@@ -343,6 +433,8 @@ class Rank:
             if d is None:
                 for q in range(eng.plan.P):
                     self.own_slab_rows(self.dZ_own, Ly.ho, c, q).zero_()
+                if works is not None:
+                    works += self._scatter_owned_step(self.dZ_own, self.dY_vm, Ly.ho, c)
                 continue
             z = self.own(self.Y_own[-1], Ly.ho, c)
             call("dgnn_head_loss", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), z, ep, C, ptr(hw), ptr(hb),
@@ -352,13 +444,16 @@ class Rank:
                  self.ws_head.numel(), st)
             call("dgnn_head_scatter", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), ptr(self.dlogits), ptr(hw), ep, C,
                  dz, st)
+            if works is not None:
+                works += self._scatter_owned_step(self.dZ_own, self.dY_vm, Ly.ho, c)
 
-    def rnn_backward(self, b, l):
+    def rnn_backward(self, b, l, pipelined=False):
         eng = self.eng
         Ly = eng.layout.layers[l]
         if not self.skip:
             self._mprod_backward(b, l)
-            return
+            return []
+        works = []
         NP, B = eng.plan.NP, eng.plan.bsize
         ho = Ly.ho
         st = _lib.stream_handle()
@@ -382,6 +477,8 @@ class Rank:
                 call("dgnn_lstm_backward_step", NP, Ly.kx, ho, ptr(dy), ptr(dh_in), ptr(dc_in), ptr(gates),
                      ptr(c_prev), ptr(c_new), ptr(wt), ptr(gates), ptr(dx), Ly.rw, ptr(dh_out), ptr(dc_out), st)
             dh_in, dc_in = dh_out, dc_out
+            if pipelined:
+                works += self._send_step_to_owner(self.dR_vm[l], self.dR_own[l], Ly.rw, i)
         self.dstate[l][0].copy_(dh_in)
         self.dstate[l][1].copy_(dc_in)
         # weight gradients over every (row, step) of the block (training.py:422-424)
@@ -391,7 +488,7 @@ class Rank:
             ws = self.ws_dw
             call("dgnn_lstm_weight_grad_tc", B * NP, NP, Ly.kx, ho, ptr(self.R_vm[l]), Ly.rw, ptr(self.Y_vm[l]),
                  ptr(self.act[l][0]), ptr(self.G_vm[l]), ptr(g_wcat), ptr(g_b), ptr(ws), ws.numel(), st)
-            return
+            return works
         ws = self.ws_tn
         K4 = 4 * ho
         # the split-K SIMT GEMM reads dz row-major: unblock the tile-blocked cache
@@ -408,6 +505,7 @@ class Rank:
                  K4, ptr(g_wh), K4, None, ptr(ws), ws.numel(), st)
         call("dgnn_gemm_tn", NP, ho, K4, ptr(self.act[l][0]), ho, ptr(dz), K4, ptr(g_wh), K4, None,
              ptr(ws), ws.numel(), st)
+        return works
 
     def _mprod_backward(self, b, l):
         """`training.py:444-460` + owed trailing gradients (`dist.py:396-407`)."""
@@ -442,7 +540,11 @@ class Rank:
                 g = self.dtrail[l].pop(k)
                 call("dgnn_axpy_frame", cnt, 1.0, ptr(g), ptr(self.vm(out, Ly.rw, k - ts[0])), 0, st)
 
-    def gcn_backward(self, b, l):
+    def gcn_backward(self, b, l, pipelined=False):
+        """K4 for every owned step; when pipelined, each step's input gradient
+        (owner layout, layer l-1) is scattered to the vertex-major buffers of
+        every rank as soon as it is written (returns works)."""
+        works = []
         eng = self.eng
         Ly = eng.layout.layers[l]
         st = _lib.stream_handle()
@@ -461,6 +563,9 @@ class Rank:
                 sl = self.slots[c]
                 call("dgnn_spmm_f32", N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val), ds, Ly.fp,
                      self.own(self.dZ_own, Ly.fp, c), st)
+                if pipelined:
+                    works += self._scatter_owned_step(self.dZ_own, self.dY_vm, Ly.fp, c)
+        return works
 
 
 class LocalFabric:
@@ -542,6 +647,8 @@ class Engine:
             if dist.get_world_size() != workers:
                 raise ConfigError(f"workers={workers} but the process group has {dist.get_world_size()} ranks")
             ids = [dist.get_rank()]
+            if workers > 1 and PIPELINED_EXCHANGE:
+                _lib.lib().dgnn_set_sm_reserve(SM_RESERVE)
         else:
             ids = list(range(workers))
         self.ranks = [Rank(self, q, dev) for q in ids]
@@ -568,9 +675,32 @@ class Engine:
             msgs = plan.P * (plan.P - 1)
             comm.record_alltoall(units, msgs, phase, b, l)
 
+    def _record_xchg(self, comm, phase, b, l):
+        if comm is not None:
+            plan = self.plan
+            comm.record_alltoall(plan.bsize * plan.NP * (plan.P - 1), plan.P * (plan.P - 1), phase, b, l)
+
     def _layers_forward(self, b, phase, comm):
         layers = self.layout.layers
+        # one rank per GPU: exchanges folded into the producing loops (P2P
+        # sends of finished slabs / steps overlap the next kernel)
+        pipelined = self.fabric.distributed and self.plan.P > 1 and PIPELINED_EXCHANGE
         for l, Ly in enumerate(layers):
+            if pipelined:
+                (r,) = self.ranks
+                works = r.gcn_forward_pipelined(b, l)
+                self._record_xchg(comm, phase, b, l)
+                for w in works:
+                    w.wait()
+                if self.skip:
+                    works = r.rnn_forward(b, l, pipelined=True)
+                    self._record_xchg(comm, phase, b, l)
+                    for w in works:
+                        w.wait()
+                else:
+                    r.rnn_forward(b, l)
+                    self._xchg(lambda r: r.Z_vm[l], lambda r: r.Y_own[l], Ly.ho, comm, phase, b, l)
+                continue
             for r in self.ranks:
                 r.gcn_forward(b, l)
             self._xchg(lambda r: r.R_own[l], lambda r: r.R_vm[l], Ly.rw, comm, phase, b, l)
@@ -607,16 +737,31 @@ class Engine:
             for r in self.ranks:
                 r.begin_block(b, keep=True, ledger=transfer)
             self._layers_forward(b, "rerun", comm)
-            for r in self.ranks:
-                r.loss_grads(b)
-            for l in reversed(range(L)):
-                Ly = layers[l]
-                self._xchg(lambda r: r.dZ_own, lambda r: r.dY_vm, Ly.ho, comm, "backward", b, l)
+            pipelined = self.fabric.distributed and plan.P > 1 and PIPELINED_EXCHANGE and self.skip
+            if pipelined:
+                # backward exchanges folded into their producers, as forward
+                (r,) = self.ranks
+                works = r.loss_grads(b, pipelined=True)
+                for l in reversed(range(L)):
+                    self._record_xchg(comm, "backward", b, l)
+                    for w in works:
+                        w.wait()
+                    works = r.rnn_backward(b, l, pipelined=True)
+                    self._record_xchg(comm, "backward", b, l)
+                    for w in works:
+                        w.wait()
+                    works = r.gcn_backward(b, l, pipelined=l > 0)
+            else:
                 for r in self.ranks:
-                    r.rnn_backward(b, l)
-                self._xchg(lambda r: r.dR_vm[l], lambda r: r.dR_own[l], Ly.rw, comm, "backward", b, l)
-                for r in self.ranks:
-                    r.gcn_backward(b, l)
+                    r.loss_grads(b)
+                for l in reversed(range(L)):
+                    Ly = layers[l]
+                    self._xchg(lambda r: r.dZ_own, lambda r: r.dY_vm, Ly.ho, comm, "backward", b, l)
+                    for r in self.ranks:
+                        r.rnn_backward(b, l)
+                    self._xchg(lambda r: r.dR_vm[l], lambda r: r.dR_own[l], Ly.rw, comm, "backward", b, l)
+                    for r in self.ranks:
+                        r.gcn_backward(b, l)
             if act is not None:
                 act.free_activations(plan.bsize * 2 * L)
                 act.free_checkpoint(1.0)
