@@ -38,7 +38,13 @@ from .params import DeviceParams, ParamLayout
 F32 = 4
 WARP_SPECIALIZED = True
 # multi-GPU: fold the forward all-to-alls into the producing loops (P2P per slab / step)
-PIPELINED_EXCHANGE = True
+#   "all"  : GCN-side (owner -> vertex-major, per destination slab / owned step)
+#            and LSTM-side (vertex-major -> owner, per step) exchanges
+#   "lstm" : LSTM-side only, GCN-side as bulk all-to-alls
+#   "auto" : "all" at P = 2, bulk above: per-step gathers load one owner's
+#            links at a time and lose to NCCL's all-to-all at P = 4
+#            (405 vs 350 ms per epoch measured)            "0": bulk only
+PIPELINED_EXCHANGE = os.environ.get("DGNN_PIPELINED_EXCHANGE", "auto")
 # SMs the persistent kernels leave free for the concurrent NCCL P2P kernels
 SM_RESERVE = int(os.environ.get("DGNN_SM_RESERVE", "32"))
 
@@ -647,7 +653,7 @@ class Engine:
             if dist.get_world_size() != workers:
                 raise ConfigError(f"workers={workers} but the process group has {dist.get_world_size()} ranks")
             ids = [dist.get_rank()]
-            if workers > 1 and PIPELINED_EXCHANGE:
+            if any(self._pipelining()):
                 _lib.lib().dgnn_set_sm_reserve(SM_RESERVE)
         else:
             ids = list(range(workers))
@@ -680,34 +686,43 @@ class Engine:
             plan = self.plan
             comm.record_alltoall(plan.bsize * plan.NP * (plan.P - 1), plan.P * (plan.P - 1), phase, b, l)
 
+    def _pipelining(self):
+        """(GCN-side, LSTM-side) exchange pipelining for this run."""
+        if not (self.fabric.distributed and self.plan.P > 1) or PIPELINED_EXCHANGE == "0":
+            return False, False
+        mode = PIPELINED_EXCHANGE
+        if mode == "auto":
+            mode = "all" if self.plan.P == 2 else "0"
+        if mode == "0":
+            return False, False
+        return mode == "all", self.skip
+
+    @staticmethod
+    def _wait(works):
+        for w in works:
+            w.wait()
+
     def _layers_forward(self, b, phase, comm):
         layers = self.layout.layers
         # one rank per GPU: exchanges folded into the producing loops (P2P
         # sends of finished slabs / steps overlap the next kernel)
-        pipelined = self.fabric.distributed and self.plan.P > 1 and PIPELINED_EXCHANGE
+        pipe_gcn, pipe_lstm = self._pipelining()
         for l, Ly in enumerate(layers):
-            if pipelined:
-                (r,) = self.ranks
-                works = r.gcn_forward_pipelined(b, l)
+            if pipe_gcn:
+                self._wait(self.ranks[0].gcn_forward_pipelined(b, l))
                 self._record_xchg(comm, phase, b, l)
-                for w in works:
-                    w.wait()
-                if self.skip:
-                    works = r.rnn_forward(b, l, pipelined=True)
-                    self._record_xchg(comm, phase, b, l)
-                    for w in works:
-                        w.wait()
-                else:
+            else:
+                for r in self.ranks:
+                    r.gcn_forward(b, l)
+                self._xchg(lambda r: r.R_own[l], lambda r: r.R_vm[l], Ly.rw, comm, phase, b, l)
+            if pipe_lstm:
+                self._wait(self.ranks[0].rnn_forward(b, l, pipelined=True))
+                self._record_xchg(comm, phase, b, l)
+            else:
+                for r in self.ranks:
                     r.rnn_forward(b, l)
-                    self._xchg(lambda r: r.Z_vm[l], lambda r: r.Y_own[l], Ly.ho, comm, phase, b, l)
-                continue
-            for r in self.ranks:
-                r.gcn_forward(b, l)
-            self._xchg(lambda r: r.R_own[l], lambda r: r.R_vm[l], Ly.rw, comm, phase, b, l)
-            for r in self.ranks:
-                r.rnn_forward(b, l)
-            src = (lambda r: r.Y_vm[l]) if self.skip else (lambda r: r.Z_vm[l])
-            self._xchg(src, lambda r: r.Y_own[l], Ly.ho, comm, phase, b, l)
+                src = (lambda r: r.Y_vm[l]) if self.skip else (lambda r: r.Z_vm[l])
+                self._xchg(src, lambda r: r.Y_own[l], Ly.ho, comm, phase, b, l)
 
     def epoch(self, comm=None, transfer=None, act=None, count_total=None, reduction="mean"):
         """Forward sweep + checkpointed reverse sweep; returns (loss, flat fp64 grads)."""
@@ -737,31 +752,27 @@ class Engine:
             for r in self.ranks:
                 r.begin_block(b, keep=True, ledger=transfer)
             self._layers_forward(b, "rerun", comm)
-            pipelined = self.fabric.distributed and plan.P > 1 and PIPELINED_EXCHANGE and self.skip
-            if pipelined:
-                # backward exchanges folded into their producers, as forward
-                (r,) = self.ranks
-                works = r.loss_grads(b, pipelined=True)
-                for l in reversed(range(L)):
+            pipe_gcn, pipe_lstm = self._pipelining()
+            works = []
+            for r in self.ranks:
+                works += r.loss_grads(b, pipelined=pipe_gcn)
+            for l in reversed(range(L)):
+                Ly = layers[l]
+                if pipe_gcn:
+                    self._wait(works)
                     self._record_xchg(comm, "backward", b, l)
-                    for w in works:
-                        w.wait()
-                    works = r.rnn_backward(b, l, pipelined=True)
-                    self._record_xchg(comm, "backward", b, l)
-                    for w in works:
-                        w.wait()
-                    works = r.gcn_backward(b, l, pipelined=l > 0)
-            else:
-                for r in self.ranks:
-                    r.loss_grads(b)
-                for l in reversed(range(L)):
-                    Ly = layers[l]
+                else:
                     self._xchg(lambda r: r.dZ_own, lambda r: r.dY_vm, Ly.ho, comm, "backward", b, l)
+                if pipe_lstm:
+                    self._wait(self.ranks[0].rnn_backward(b, l, pipelined=True))
+                    self._record_xchg(comm, "backward", b, l)
+                else:
                     for r in self.ranks:
                         r.rnn_backward(b, l)
                     self._xchg(lambda r: r.dR_vm[l], lambda r: r.dR_own[l], Ly.rw, comm, "backward", b, l)
-                    for r in self.ranks:
-                        r.gcn_backward(b, l)
+                works = []
+                for r in self.ranks:
+                    works += r.gcn_backward(b, l, pipelined=pipe_gcn and l > 0)
             if act is not None:
                 act.free_activations(plan.bsize * 2 * L)
                 act.free_checkpoint(1.0)
