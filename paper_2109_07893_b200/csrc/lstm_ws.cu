@@ -431,29 +431,47 @@ __global__ void __launch_bounds__(BwdRoles::THREADS, 1) lstm_bwd_ws_kernel(
         if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
         __syncwarp();
     } else {
+        // One warp per TMEM lane quarter.  [dx | dh] rows go out through a
+        // per-warp shared-memory transpose, 32 columns at a time: each warp
+        // store then covers 4 rows x 128 contiguous bytes instead of 32 rows
+        // x 16 B.
+        static_assert(R::NEPI == 4, "one epilogue warp per lane quarter");
         const int e = warp - R::MMA_WARP - 1;
-        const int q = warp & 3, half = e >> 2;
+        const int q = warp & 3;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        const uint32_t ebuf = sm.base + wsk::STAGES * sm.stage + 1024 + e * 4096;
         const int K = kx + HP;
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const uint32_t a = it & 1, u = it >> 1;
-            const int64_t row = (int64_t)tile * wsk::BM + 32 * q + lane;
             mbar_wait(&bars->accfull[a], u & 1);
             fence_after();
             const uint32_t tq = bars->tmem + lane_off + a * N;
-            for (int c0 = half * 8; c0 < N; c0 += 2 * R::NEPI) {
-                float v[8];
-                tmem_ld8(tq + c0, v);
-                tmem_wait_ld();
-                if (row >= rows) continue;
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                float v[4][8];
 #pragma unroll
-                for (int h4 = 0; h4 < 2; ++h4) {
-                    const int c = c0 + 4 * h4;
-                    const float4 val = make_float4(v[4 * h4], v[4 * h4 + 1], v[4 * h4 + 2], v[4 * h4 + 3]);
-                    if (c < kx) *reinterpret_cast<float4*>(dx + row * lddx + c) = val;
-                    else if (c < K) *reinterpret_cast<float4*>(dh_out + row * HP + (c - kx)) = val;
+                for (int j = 0; j < 4; ++j)
+                    if (c0 + 8 * j < N) tmem_ld8(tq + c0 + 8 * j, v[j]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        sts128(ebuf + lane * 128 + ((((2 * j + h) ^ (lane & 7))) << 4),
+                               make_float4(v[j][4 * h], v[j][4 * h + 1], v[j][4 * h + 2], v[j][4 * h + 3]));
+                __syncwarp();
+#pragma unroll
+                for (int r0 = 0; r0 < 32; r0 += 4) {
+                    const int r = r0 + (lane >> 3), ch = lane & 7;
+                    const float4 val = lds128(ebuf + r * 128 + ((ch ^ (r & 7)) << 4));
+                    const int64_t row = (int64_t)tile * wsk::BM + 32 * q + r;
+                    const int c = c0 + 4 * ch;
+                    if (row < rows) {
+                        if (c < kx) *reinterpret_cast<float4*>(dx + row * lddx + c) = val;
+                        else if (c < K) *reinterpret_cast<float4*>(dh_out + row * HP + (c - kx)) = val;
+                    }
                 }
+                __syncwarp();
             }
             fence_before();
             __syncwarp();
@@ -487,7 +505,7 @@ int lstm_bwd_ws_t(int64_t rows, int kx, const float* dy, const float* dh_in, con
         return DGNN_EUNSUPPORTED;
     }
     auto k = lstm_bwd_ws_kernel<HP>;
-    const size_t smem = ws_smem_bytes(N);
+    const size_t smem = ws_smem_bytes(N) + 1024 + BwdRoles::NEPI * 4096;   // + epilogue transpose buffers
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
