@@ -26,7 +26,7 @@ namespace wsk {
 constexpr int BM = 128;
 constexpr int KC = 16;
 constexpr int A_TILE = BM * 64;
-constexpr int STAGES = 4;
+constexpr int MAX_STAGES = 4;
 // Bottleneck probe (scripts/ws_probe.cu builds with -DDGNN_WS_PROBE=mask):
 // 1 skip MMAs, 2 zero-fill activations (no HBM reads), 4 skip weight copies,
 // 8 epilogue without cell math / stores, 16 without stores, 32 without cell
@@ -39,26 +39,31 @@ constexpr int PROBE = DGNN_WS_PROBE;
 
 // Warp roles: NP producer warps, one MMA warp, NE epilogue warps (a multiple
 // of 4 so every TMEM lane quarter has an owner).
-template <int NP, int NE>
+template <int NP, int NE, int ST = 4, int EXTRA = 0>
 struct WsRoles {
     static constexpr int NPROD = NP;
     static constexpr int MMA_WARP = NP;
     static constexpr int NEPI = NE;
-    static constexpr int THREADS = 32 * (NP + 1 + NE);
+    static constexpr int STAGES = ST;                    // A/B smem ring depth
+    static constexpr int EXTRA_WARP = NP + 1 + NE;       // first warp after the epilogue
+    static constexpr int THREADS = 32 * (NP + 1 + NE + EXTRA);
     static constexpr int NPT = 32 * NP;   // producer threads
 };
 // forward: heavy cell epilogue -- 16 epilogue warps (each a quarter of the
 // units of its TMEM lane quarter) when every warp still gets >= 8 units
 template <int HP>
 using FwdRoles = WsRoles<4, (HP >= 32 ? 16 : 8)>;
-using BwdRoles = WsRoles<8, 4>;   // heavy dz producer, store-only epilogue
+// backward: 8 dz-producer warps fed from shared memory by one loader warp
+// (the extra warp), 3-stage A/B ring to leave room for the raw input ring
+using BwdRoles = WsRoles<8, 4, 3, 1>;
 
 __host__ __device__ constexpr int ws_tmem_cols(int n2) {
     return n2 <= 32 ? 32 : (n2 <= 64 ? 64 : (n2 <= 128 ? 128 : (n2 <= 256 ? 256 : 512)));
 }
 
 struct WsBars {
-    uint64_t full_a[wsk::STAGES], full_b[wsk::STAGES], empty[wsk::STAGES], accfull[2], accempty[2];
+    uint64_t full_a[wsk::MAX_STAGES], full_b[wsk::MAX_STAGES], empty[wsk::MAX_STAGES], accfull[2], accempty[2];
+    uint64_t raw_full[wsk::MAX_STAGES], raw_empty[wsk::MAX_STAGES];   // backward input ring
     uint32_t tmem;
 };
 
@@ -71,8 +76,9 @@ struct WsSmem {
     __device__ uint32_t b(int s) const { return base + s * stage + 2 * wsk::A_TILE; }
 };
 
+template <class R>
 inline size_t ws_smem_bytes(int n) {
-    return (size_t)wsk::STAGES * (2 * wsk::A_TILE + 2 * n * 64) + 1024 + sizeof(WsBars) + 64;
+    return (size_t)R::STAGES * (2 * wsk::A_TILE + 2 * n * 64) + 1024 + sizeof(WsBars) + 64;
 }
 
 template <class R>
@@ -82,11 +88,11 @@ __device__ __forceinline__ WsBars* ws_setup(WsSmem& sm, int n) {
     const uint32_t pad = (1024 - (raw & 1023)) & 1023;
     sm.base = raw + pad;
     sm.stage = 2 * wsk::A_TILE + 2 * n * 64;
-    WsBars* bars = reinterpret_cast<WsBars*>(ws_smem_raw + pad + wsk::STAGES * sm.stage);
+    WsBars* bars = reinterpret_cast<WsBars*>(ws_smem_raw + pad + R::STAGES * sm.stage);
     const int warp = threadIdx.x >> 5;
     if (warp == R::MMA_WARP) tmem_alloc(&bars->tmem, ws_tmem_cols(2 * n));
     if (threadIdx.x == 0) {
-        for (int s = 0; s < wsk::STAGES; ++s) {
+        for (int s = 0; s < R::STAGES; ++s) {
             mbar_init(&bars->full_a[s], R::NPROD);
             mbar_init(&bars->full_b[s], 1);
             mbar_init(&bars->empty[s], 1);
@@ -111,6 +117,7 @@ __device__ __forceinline__ void ws_teardown(WsBars* bars, int n) {
 }
 
 // MMA issuer: for every tile of this CTA, all K chunks into accumulator a.
+template <class R>
 __device__ __forceinline__ void ws_mma_loop(const WsSmem& sm, WsBars* bars, int n, int ntiles, int nch) {
     uint32_t gc = 0, it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -119,8 +126,8 @@ __device__ __forceinline__ void ws_mma_loop(const WsSmem& sm, WsBars* bars, int 
         fence_after();
         const uint32_t d = bars->tmem + a * n;
         for (int ch = 0; ch < nch; ++ch, ++gc) {
-            const int s = gc % wsk::STAGES;
-            const uint32_t j = gc / wsk::STAGES;
+            const int s = gc % R::STAGES;
+            const uint32_t j = gc / R::STAGES;
             mbar_wait(&bars->full_a[s], j & 1);
             mbar_wait(&bars->full_b[s], j & 1);
             fence_after();
@@ -152,8 +159,8 @@ template <class R, int ITEMS>
 __device__ __forceinline__ void ws_produce(const WsSmem& sm, WsBars* bars, uint32_t gc, const float* img, int ch,
                                            uint32_t b_bytes, const float4 (&vals)[ITEMS]) {
     const int ptid = threadIdx.x;   // producers are threads 0 .. NPT-1
-    const int s = gc % wsk::STAGES;
-    const uint32_t j = gc / wsk::STAGES;
+    const int s = gc % R::STAGES;
+    const uint32_t j = gc / R::STAGES;
     if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
     if (ptid == 0) {
         mbar_arrive_expect_tx(&bars->full_b[s], b_bytes);
@@ -196,15 +203,15 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
         // cp.async the raw fp32 chunk straight into the (swizzled) hi tile,
         // LA chunks ahead, then split it in place: deep memory-level
         // parallelism without holding the data in registers.
-        constexpr int LA = wsk::STAGES - 1;
+        constexpr int LA = R::STAGES - 1;
         const int ptid = threadIdx.x;
         const int my_tiles = blockIdx.x < ntiles ? (int)cdiv(ntiles - blockIdx.x, gridDim.x) : 0;
         const uint32_t G = (uint32_t)my_tiles * nch;
         auto issue = [&](uint32_t g) {
             const int tile = blockIdx.x + (int)(g / nch) * gridDim.x;
             const int ch = (int)(g % nch);
-            const int s = g % wsk::STAGES;
-            const uint32_t j = g / wsk::STAGES;
+            const int s = g % R::STAGES;
+            const uint32_t j = g / R::STAGES;
             if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
             if (ptid == 0) {
                 if (wsk::PROBE & 4) {
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
         // an already-landed chunk behind it would serialise MMA and producer.
         for (uint32_t g = 0; g < G; ++g) {
             cp_async_wait<LA - 1>();
-            const int s = g % wsk::STAGES;
+            const int s = g % R::STAGES;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const int idx = ptid + R::NPT * i;
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
             cp_async_commit();
         }
     } else if (warp == R::MMA_WARP) {
-        if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
+        if (lane == 0) ws_mma_loop<R>(sm, bars, N, ntiles, nch);
         __syncwarp();
     } else {
         const int e = warp - R::MMA_WARP - 1;
@@ -352,63 +359,80 @@ __global__ void __launch_bounds__(BwdRoles::THREADS, 1) lstm_bwd_ws_kernel(
     const int nch = HP / 4;
     const uint32_t b_bytes = 2 * N * 64;
 
-    if (warp < R::NPROD) {
-        const int ptid = threadIdx.x;
-        struct Cell {
-            float gi, gf, go, gg, cp, cn, dh, dy, dc;   // raw loads only: no arithmetic before use
-        };
-        auto fetch = [&](int tile, int ch, Cell (&v)[ITEMS]) {
+    // raw input ring: per chunk (tile, 4 units) the 7 tile-blocked arrays
+    // (gates i/f/o/g, c_prev, c_new, dc_in: one contiguous tr x 16 B block
+    // each, bulk-copied) and the row-major dh_in / dy pieces (cp.async)
+    constexpr int RAWF = wsk::BM * 4 * 9;              // floats per slot
+    const int RSLOTS = N > 192 ? 3 : 4;                 // what fits next to the A/B ring
+    constexpr int O_CP = 4 * 512, O_CN = 5 * 512, O_DC = 6 * 512, O_DH = 7 * 512, O_DY = 8 * 512;
+    const uint32_t raw0 = sm.base + R::STAGES * sm.stage + 1024 + R::NEPI * 4096;
+    const float* rawf = reinterpret_cast<const float*>(
+        reinterpret_cast<const uint8_t*>(bars) + (raw0 - smem_u32(bars)));
+    const int my_tiles = blockIdx.x < ntiles ? (int)cdiv(ntiles - blockIdx.x, gridDim.x) : 0;
+    const uint32_t G = (uint32_t)my_tiles * nch;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RSLOTS; ++i) {
+            mbar_init(&bars->raw_full[i], 33);             // 32 cp.async lanes + the expect_tx arrival
+            mbar_init(&bars->raw_empty[i], R::NPROD);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == R::EXTRA_WARP) {
+        // loader: stays up to RSLOTS chunks ahead of the dz producers
+        for (uint32_t g = 0; g < G; ++g) {
+            const int tile = blockIdx.x + (int)(g / nch) * gridDim.x, ch = (int)(g % nch);
+            const int slot = g % RSLOTS;
+            const uint32_t j = g / RSLOTS;
+            if (j >= 1) mbar_wait_sleep(&bars->raw_empty[slot], (j - 1) & 1);
+            const uint32_t rb = raw0 + slot * RAWF * 4;
+            const int64_t t0 = (int64_t)tile * wsk::BM;
+            const int tr = (int)min((int64_t)wsk::BM, rows - t0);
+            const uint32_t blk = (uint32_t)tr * 16;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bars->raw_full[slot], 7 * blk);
 #pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const int idx = ptid + R::NPT * i;
-                const int64_t g = (int64_t)tile * wsk::BM + (idx >> 2);
-                const int u = 4 * ch + (idx & 3);
-                Cell p{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                if (g < rows) {
-                    const int64_t o = g * HP + u, ob = tb_off(g, u, HP, rows);
-                    p.gi = gates[tb_off(g, u, NC, rows)];
-                    p.gf = gates[tb_off(g, HP + u, NC, rows)];
-                    p.go = gates[tb_off(g, 2 * HP + u, NC, rows)];
-                    p.gg = gates[tb_off(g, 3 * HP + u, NC, rows)];
-                    p.cp = __ldg(cprev + ob);
-                    p.cn = __ldg(cnew + ob);
-                    p.dh = __ldg(dh_in + o);
-                    if (dy) p.dy = __ldg(dy + o);
-                    p.dc = __ldg(dc_in + ob);
-                }
-                v[i] = p;
+                for (int gg = 0; gg < 4; ++gg)
+                    bulk_g2s(rb + gg * 2048, gates + tb_off(t0, gg * HP + 4 * ch, NC, rows), blk, &bars->raw_full[slot]);
+                bulk_g2s(rb + O_CP * 4, cprev + tb_off(t0, 4 * ch, HP, rows), blk, &bars->raw_full[slot]);
+                bulk_g2s(rb + O_CN * 4, cnew + tb_off(t0, 4 * ch, HP, rows), blk, &bars->raw_full[slot]);
+                bulk_g2s(rb + O_DC * 4, dc_in + tb_off(t0, 4 * ch, HP, rows), blk, &bars->raw_full[slot]);
             }
-        };
-        // Three register buffers, two chunks of loads in flight while the
-        // third is turned into dz; the loop is unrolled by three so every
-        // buffer keeps a fixed role (no register moves that would wait on
-        // outstanding loads).
-        const int my_tiles = blockIdx.x < ntiles ? (int)cdiv(ntiles - blockIdx.x, gridDim.x) : 0;
-        const uint32_t G = (uint32_t)my_tiles * nch;
-        auto fetch_g = [&](uint32_t g, Cell (&v)[ITEMS]) {
-            fetch(blockIdx.x + (int)(g / nch) * gridDim.x, (int)(g % nch), v);
-        };
-        auto step = [&](uint32_t g, Cell (&cur)[ITEMS], Cell (&fb)[ITEMS]) {
-            if (g + 2 < G) fetch_g(g + 2, fb);
-            const int tile = blockIdx.x + (int)(g / nch) * gridDim.x;
-            const int ch = (int)(g % nch);
+#pragma unroll
+            for (int r = lane; r < wsk::BM; r += 32) {
+                const int64_t row = t0 + r;
+                const bool ok = r < tr;
+                cp_async16(rb + (O_DH + 4 * r) * 4, ok ? dh_in + row * HP + 4 * ch : dh_in, ok ? 16u : 0u);
+                cp_async16(rb + (O_DY + 4 * r) * 4, (ok && dy) ? dy + row * HP + 4 * ch : dh_in, (ok && dy) ? 16u : 0u);
+            }
+            cp_async_mbar_arrive(&bars->raw_full[slot]);
+        }
+        cp_async_wait<0>();
+    } else if (warp < R::NPROD) {
+        const int ptid = threadIdx.x;
+        for (uint32_t g = 0; g < G; ++g) {
+            const int tile = blockIdx.x + (int)(g / nch) * gridDim.x, ch = (int)(g % nch);
+            const int slot = g % RSLOTS;
+            mbar_wait(&bars->raw_full[slot], (g / RSLOTS) & 1);
+            const float* rw = rawf + slot * RAWF;
             float4 vals[ITEMS];
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int idx = ptid + R::NPT * i;
+                const int idx = ptid + R::NPT * i;   // = 4 r + uu: the slot's [r][uu] order
                 const int64_t row = (int64_t)tile * wsk::BM + (idx >> 2);
                 const int u = 4 * ch + (idx & 3);
-                const Cell& p = cur[i];
                 float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (row < rows) {
-                    const float dhv = p.dy + p.dh;
-                    const float tcn = act_tanh(p.cn);
+                    const float gi = rw[idx], gf = rw[512 + idx], go = rw[1024 + idx], gg = rw[1536 + idx];
+                    const float cpv = rw[O_CP + idx], cn = rw[O_CN + idx], dcv = rw[O_DC + idx];
+                    const float dhv = rw[O_DY + idx] + rw[O_DH + idx];
+                    const float tcn = act_tanh(cn);
                     const float d_o = dhv * tcn;
-                    const float dc = dhv * p.go * (1.f - tcn * tcn) + p.dc;
-                    const float df = dc * p.cp, di = dc * p.gg, dg = dc * p.gi;
-                    dc_out[tb_off(row, u, HP, rows)] = dc * p.gf;
-                    z = make_float4(di * p.gi * (1.f - p.gi), df * p.gf * (1.f - p.gf), d_o * p.go * (1.f - p.go),
-                                    dg * (1.f - p.gg * p.gg));
+                    const float dc = dhv * go * (1.f - tcn * tcn) + dcv;
+                    const float df = dc * cpv, di = dc * gg, dg = dc * gi;
+                    dc_out[tb_off(row, u, HP, rows)] = dc * gf;
+                    z = make_float4(di * gi * (1.f - gi), df * gf * (1.f - gf), d_o * go * (1.f - go), dg * (1.f - gg * gg));
                     // dz replaces the gate cache
                     gates[tb_off(row, u, NC, rows)] = z.x;
                     gates[tb_off(row, HP + u, NC, rows)] = z.y;
@@ -417,18 +441,12 @@ __global__ void __launch_bounds__(BwdRoles::THREADS, 1) lstm_bwd_ws_kernel(
                 }
                 vals[i] = z;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->raw_empty[slot]);
             ws_produce<R, ITEMS>(sm, bars, g, img, ch, b_bytes, vals);
-        };
-        Cell b0[ITEMS], b1[ITEMS], b2[ITEMS];
-        if (G > 0) fetch_g(0, b0);
-        if (G > 1) fetch_g(1, b1);
-        for (uint32_t g = 0; g < G; g += 3) {
-            step(g, b0, b2);
-            if (g + 1 < G) step(g + 1, b1, b0);
-            if (g + 2 < G) step(g + 2, b2, b1);
         }
     } else if (warp == R::MMA_WARP) {
-        if (lane == 0) ws_mma_loop(sm, bars, N, ntiles, nch);
+        if (lane == 0) ws_mma_loop<R>(sm, bars, N, ntiles, nch);
         __syncwarp();
     } else {
         // One warp per TMEM lane quarter.  [dx | dh] rows go out through a
@@ -439,7 +457,7 @@ __global__ void __launch_bounds__(BwdRoles::THREADS, 1) lstm_bwd_ws_kernel(
         const int e = warp - R::MMA_WARP - 1;
         const int q = warp & 3;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-        const uint32_t ebuf = sm.base + wsk::STAGES * sm.stage + 1024 + e * 4096;
+        const uint32_t ebuf = sm.base + R::STAGES * sm.stage + 1024 + e * 4096;
         const int K = kx + HP;
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -486,7 +504,7 @@ int lstm_fwd_ws_t(int64_t rows, int kx, const float* x, int64_t ldx, const float
                   const float* img, const float* b, float* h, float* c, float* gates, cudaStream_t st) {
     constexpr int N = 4 * HP;
     auto k = lstm_fwd_ws_kernel<HP>;
-    const size_t smem = ws_smem_bytes(N);
+    const size_t smem = ws_smem_bytes<FwdRoles<HP>>(N);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
@@ -505,7 +523,9 @@ int lstm_bwd_ws_t(int64_t rows, int kx, const float* dy, const float* dh_in, con
         return DGNN_EUNSUPPORTED;
     }
     auto k = lstm_bwd_ws_kernel<HP>;
-    const size_t smem = ws_smem_bytes(N) + 1024 + BwdRoles::NEPI * 4096;   // + epilogue transpose buffers
+    // + epilogue transpose buffers + the raw input ring (18 KB slots)
+    const size_t smem = ws_smem_bytes<BwdRoles>(N) + 1024 + BwdRoles::NEPI * 4096 +
+                        (size_t)(N > 192 ? 3 : 4) * wsk::BM * 4 * 9 * 4;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
