@@ -9,11 +9,15 @@ from __future__ import annotations
 
 import ctypes
 from ctypes import c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_void_p
+import os
 from pathlib import Path
 
 from .errors import CorruptDeltaError, DeviceError, InputError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdgnn_b200.so"
+# bottleneck-probe builds (scripts/*probe*) substitute a variant library
+if os.environ.get("DGNN_LIB_PATH"):
+    LIB_PATH = Path(os.environ["DGNN_LIB_PATH"])
 
 
 class Frame(ctypes.Structure):

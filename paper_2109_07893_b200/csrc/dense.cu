@@ -12,6 +12,12 @@ namespace dgnn {
 
 constexpr int TN_BM = 64, TN_BN = 64, TN_BR = 16;
 
+// tcgen05 GCN weight gradient (gcn_dw_tc.cu) and the K3/K4 engine switch (spmm.cu)
+size_t gcn_dw_tc_workspace(int fp, int hp);
+int gcn_dw_tc(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int fp, int hp, int skip, double* gw, void* ws,
+              size_t ws_bytes, cudaStream_t st);
+int gcn_tensor_cores_on();
+
 // Loaders map (row r, column c) of the logical A / B operands to memory; c is
 // always a multiple of 4 and the 4 columns are contiguous.
 struct PlainLoader {
@@ -234,11 +240,19 @@ int dgnn_gemm_tn(int64_t rows, int32_t m, int32_t n, const float* a, int64_t lda
                   as_stream(stream), "gemm_tn");
 }
 
-size_t dgnn_gcn_weight_grad_workspace(int32_t fp, int32_t hp) { return tn_workspace_bytes(fp, hp); }
+size_t dgnn_gcn_weight_grad_workspace(int32_t fp, int32_t hp) {
+    const size_t a = tn_workspace_bytes(fp, hp), b = gcn_dw_tc_workspace(fp, hp);
+    return a > b ? a : b;
+}
 
 int dgnn_gcn_weight_grad(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int32_t fp, int32_t hp, int skip,
                          double* gw, void* ws, size_t ws_bytes, void* stream) {
     DGNN_CHECK_ARG(fp % 4 == 0 && hp % 4 == 0, "gcn_weight_grad: widths must be x4");
+    if (n <= 0) return DGNN_OK;
+    if (gcn_tensor_cores_on()) {
+        const int rc = gcn_dw_tc(n, s, dr, r, fp, hp, skip, gw, ws, ws_bytes, as_stream(stream));
+        if (rc >= 0) return rc;
+    }
     const int off = skip ? fp : 0;
     return tn_run((int64_t)n, fp, hp, FrameLoader{s, 0, fp}, MaskedFrameLoader{dr, r, off, hp}, gw, hp, nullptr,
                   ws, ws_bytes, as_stream(stream), "gcn_weight_grad");

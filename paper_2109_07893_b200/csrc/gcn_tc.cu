@@ -23,6 +23,13 @@
 //
 // Persistent grid (one CTA per SM), 2-stage A ring, 3-stage index ring,
 // 2 TMEM accumulators.  FP in {16, 32, 64}, HP in {16, 32, 64}.
+//
+// BWD instance (K4 rows, training.py:347-350, 359-367): the same pipeline
+// computes ds = dpre[:, :F] (skip) + dq W^T with dpre = dr (.) [r > 0] and
+// dq = dpre[:, F:] (skip) | dpre (plain): the gather warps load dq rows
+// (masked on the fly, no aggregation) as the K-major A tile (K = hidden),
+// the W image holds B[f][h] = W[f][h] (N = F), and the epilogue adds the
+// skip term dpre[:, :F] in its row-contiguous store pass.
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -37,6 +44,13 @@ __device__ __forceinline__ void fma4(float4& a, float s, const float4& b) {
 }
 
 namespace gtc {
+// BWD bottleneck probe (scripts/gtb_probe.sh builds with -DDGNN_GTB_PROBE=mask):
+// 1 epilogue without the skip-term loads, 2 gathers without the mask loads,
+// 4 epilogue without global stores, 8 gathers without any HBM load.
+#ifndef DGNN_GTB_PROBE
+#define DGNN_GTB_PROBE 0
+#endif
+constexpr int PROBE = DGNN_GTB_PROBE;
 constexpr int BM = 128;
 constexpr int NGATHER = 20, IDX_WARP = 20, MMA_WARP = 21, EPI0 = 22, NEPI = 4;
 constexpr int THREADS = 32 * (EPI0 + NEPI);
@@ -46,7 +60,7 @@ constexpr int ECAP = 1024;   // edges per tile staged in shared memory (else rea
 
 struct GtcBars {
     uint64_t full[gtc::ASTAGES], empty[gtc::ASTAGES], ifull[gtc::ISTAGES], iempty[gtc::ISTAGES], accfull[2],
-        accempty[2];
+        accempty[2], skipready[2], skipfree[2];
     uint32_t tmem;
     int32_t claim[gtc::ASTAGES];   // row-chunk claim counters (monotonic)
 };
@@ -73,11 +87,15 @@ struct GtcLayout {
     static constexpr int TMEM_COLS = 2 * HP <= 32 ? 32 : (2 * HP <= 64 ? 64 : 128);
 };
 
-template <int FP, int HP, bool SKIP, bool AGG>
+template <int FP, int HP, bool SKIP, bool AGG, bool BWD>
 __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const float* __restrict__ val,
-    dgnn_frame x, const float* __restrict__ w, dgnn_frame s_out, dgnn_frame r_out) {
+    dgnn_frame x, const float* __restrict__ w, dgnn_frame s_out, dgnn_frame r_out, dgnn_frame mk) {
+    static_assert(!(BWD && AGG), "the backward instance has no aggregation");
     using L = GtcLayout<FP, HP>;
+    // BWD: x = dr, mk = r (mask source), r_out = ds; dq sits at column
+    // offset F (= HP) of dr / r in the skip layer
+    constexpr int DQ_OFF = (BWD && SKIP) ? HP : 0;
     constexpr int G = FP / 4;              // lanes per row
     constexpr int RW = 32 / G;             // rows per warp pass
     extern __shared__ uint8_t gtc_smem_raw[];
@@ -89,12 +107,14 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (int)cdiv(n, gtc::BM);
 
-    // W image: B[j][k] = W[k][j], tf32 hi / lo, SW64 K-major chunks of 16 k
+    // W image: B[j][k] = W[k][j] (forward; BWD: W[j][k]), tf32 hi / lo, SW64
+    // K-major chunks of 16 k
     for (int i = threadIdx.x; i < HP * FP / 4; i += gtc::THREADS) {
         const int j = i / (FP / 4), k4 = i % (FP / 4);
         const int k = 4 * k4;
-        const float4 v = make_float4(w[(k + 0) * HP + j], w[(k + 1) * HP + j], w[(k + 2) * HP + j],
-                                     w[(k + 3) * HP + j]);
+        const float4 v = BWD ? *reinterpret_cast<const float4*>(w + j * FP + k)
+                             : make_float4(w[(k + 0) * HP + j], w[(k + 1) * HP + j], w[(k + 2) * HP + j],
+                                           w[(k + 3) * HP + j]);
         float4 hi, lo;
         split4(v, hi, lo);
         const uint32_t o = (uint32_t)((k / 16) * HP * 64) + sw64(j, (k % 16) / 4);
@@ -115,6 +135,8 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->accfull[a], 1);
             mbar_init(&bars->accempty[a], gtc::NEPI);
+            mbar_init(&bars->skipready[a], 32 * gtc::NGATHER);
+            mbar_init(&bars->skipfree[a], gtc::NEPI);
         }
         fence_mbar_init();
     }
@@ -133,6 +155,10 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             if (it >= gtc::ASTAGES) mbar_wait_sleep(&bars->empty[s], ((it / gtc::ASTAGES) - 1) & 1);
             const uint32_t a_hi = sb + s * L::A_STAGE, a_lo = a_hi + L::A_HALF;
             const bool spill = AGG && ix.spill;
+            // BWD skip: the skip term dpre[:, :F] of this tile's rows goes to ds
+            // now; the epilogue adds q on top (RED) once skipready[it & 1]
+            // completes.  skipfree keeps the gathers at most one tile ahead of it.
+            if (BWD && SKIP && it >= 2) mbar_wait_sleep(&bars->skipfree[it & 1], ((it >> 1) - 1) & 1);
             // two rows per lane group per pass, the first four edges of both
             // in flight together (mean degree is ~2: most rows are one batch)
             const int32_t* cs = spill ? col + ix.ebase : ix.col;
@@ -186,6 +212,29 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                     }
                     if (eea - ea > 4) tail(acc_a, ea + 4, eea);
                     if (eeb - eb > 4) tail(acc_b, eb + 4, eeb);
+                } else if constexpr (BWD) {
+                    auto dqrow = [&](int64_t row) {
+                        if (gtc::PROBE & 8) return make_float4(1.f, 0.f, 1.f, 0.f);
+                        const float4 g = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(x, row) + DQ_OFF) + gl);
+                        const float4 m = (gtc::PROBE & 2) ? g : __ldg(reinterpret_cast<const float4*>(frame_row<const float>(mk, row) + DQ_OFF) + gl);
+                        return make_float4(m.x > 0.f ? g.x : 0.f, m.y > 0.f ? g.y : 0.f, m.z > 0.f ? g.z : 0.f,
+                                           m.w > 0.f ? g.w : 0.f);
+                    };
+                    if (oka) acc_a = dqrow(row_a);
+                    if (okb) acc_b = dqrow(row_b);
+                    if constexpr (SKIP) {
+                        auto skip_chunk = [&](int64_t row, int c) {
+                            const float4 g = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(x, row)) + c);
+                            const float4 m = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(mk, row)) + c);
+                            reinterpret_cast<float4*>(frame_row<float>(r_out, row))[c] =
+                                make_float4(m.x > 0.f ? g.x : 0.f, m.y > 0.f ? g.y : 0.f, m.z > 0.f ? g.z : 0.f,
+                                            m.w > 0.f ? g.w : 0.f);
+                        };
+                        for (int c = gl; c < HP / 4; c += G) {
+                            if (oka) skip_chunk(row_a, c);
+                            if (okb) skip_chunk(row_b, c);
+                        }
+                    }
                 } else {
                     if (oka) acc_a = xrow((int)row_a);
                     if (okb) acc_b = xrow((int)row_b);
@@ -196,7 +245,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                     if (rr >= gtc::BM) break;
                     const int64_t row = h ? row_b : row_a;
                     const float4 acc = h ? acc_b : acc_a;
-                    if (h ? okb : oka) {
+                    if (!BWD && (h ? okb : oka)) {
                         if (s_out.ptr) reinterpret_cast<float4*>(frame_row<float>(s_out, row))[gl] = acc;
                         if (SKIP)
                             reinterpret_cast<float4*>(frame_row<float>(r_out, row))[gl] = make_float4(
@@ -211,6 +260,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 }
             }
             fence_async_smem();
+            if (BWD && SKIP) mbar_arrive(&bars->skipready[it & 1]);   // every lane: releases its ds stores
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&bars->full[s]);
@@ -295,24 +345,34 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 for (int h = 0; h < 2; ++h) {
                     const int c = c0 / 4 + h;
                     sts128(buf + lane * HP * 4 + ((c ^ (lane & 7) % CPR) << 4),
-                           make_float4(fmaxf(v[4 * h], 0.f), fmaxf(v[4 * h + 1], 0.f), fmaxf(v[4 * h + 2], 0.f),
-                                       fmaxf(v[4 * h + 3], 0.f)));
+                           BWD ? make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3])
+                               : make_float4(fmaxf(v[4 * h], 0.f), fmaxf(v[4 * h + 1], 0.f),
+                                             fmaxf(v[4 * h + 2], 0.f), fmaxf(v[4 * h + 3], 0.f)));
                 }
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->accempty[a]);
+            if (BWD && SKIP) mbar_wait_sleep(&bars->skipready[a], u & 1);
             // row-contiguous stores: 32 / CPR rows per warp instruction
             constexpr int RPI = 32 / CPR;
             const int rr = lane / CPR, c = lane % CPR;
-#pragma unroll 4
+#pragma unroll(BWD ? 8 : 4)
             for (int r0 = 0; r0 < 32; r0 += RPI) {
                 const int r = r0 + rr;
                 const int64_t row = (int64_t)tile * gtc::BM + 32 * q + r;
                 const float4 vv = lds128(buf + r * HP * 4 + ((c ^ (r & 7) % CPR) << 4));
-                if (row < n) reinterpret_cast<float4*>(frame_row<float>(r_out, row) + (SKIP ? FP : 0))[c] = vv;
+                if (row < n) {
+                    float* dst = frame_row<float>(r_out, row) + (BWD ? 0 : (SKIP ? FP : 0)) + 4 * c;
+                    if (BWD && SKIP) {
+                        if (!(gtc::PROBE & 4)) red_add4(dst, vv);   // ds = dpre[:, :F] (gathers) + q
+                    } else {
+                        *reinterpret_cast<float4*>(dst) = vv;
+                    }
+                }
             }
             __syncwarp();
+            if (BWD && SKIP && lane == 0) mbar_arrive(&bars->skipfree[a]);
         }
     }
     fence_before();
@@ -320,17 +380,17 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     if (warp == gtc::MMA_WARP) tmem_dealloc(bars->tmem, L::TMEM_COLS);
 }
 
-template <int FP, int HP, bool SKIP, bool AGG>
+template <int FP, int HP, bool SKIP, bool AGG, bool BWD = false>
 int gcn_fwd_tc_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x, const float* w,
-                 dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+                 dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st, dgnn_frame mk = dgnn_frame{}) {
     using L = GtcLayout<FP, HP>;
-    auto k = gcn_fwd_tc_kernel<FP, HP, SKIP, AGG>;
+    auto k = gcn_fwd_tc_kernel<FP, HP, SKIP, AGG, BWD>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     const int ntiles = (int)cdiv(n, gtc::BM);
     const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
     note_launch();
-    k<<<grid, gtc::THREADS, L::BYTES, st>>>(n, rp, col, val, x, w, s_out, r_out);
-    return launch_status("gcn_forward (tcgen05)");
+    k<<<grid, gtc::THREADS, L::BYTES, st>>>(n, rp, col, val, x, w, s_out, r_out, mk);
+    return launch_status(BWD ? "gcn_backward_rows (tcgen05)" : "gcn_forward (tcgen05)");
 }
 
 // dispatch used by dgnn_gcn_forward; returns -1 when the shape has no
@@ -348,6 +408,22 @@ int gcn_fwd_tc(int fp, int hp, bool skip, bool agg, int32_t n, const int32_t* rp
     GTC_CASE(32, 16) GTC_CASE(32, 32) GTC_CASE(32, 64)
     GTC_CASE(64, 16) GTC_CASE(64, 32) GTC_CASE(64, 64)
 #undef GTC_CASE
+    return -1;
+}
+
+// K4 rows on tcgen05: fp = F (MMA N), hp = hidden (MMA K); -1 when the
+// shape has no instance (the caller then uses the SIMT kernel)
+int gcn_bwd_tc(int fp, int hp, bool skip, int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame ds,
+               cudaStream_t st) {
+    const dgnn_frame none{};
+#define GTB_CASE(F, H)                                                                                         \
+    if (fp == F && hp == H)                                                                                    \
+        return skip ? gcn_fwd_tc_t<H, F, true, false, true>(n, nullptr, nullptr, nullptr, dr, w, none, ds, st, r) \
+                    : gcn_fwd_tc_t<H, F, false, false, true>(n, nullptr, nullptr, nullptr, dr, w, none, ds, st, r);
+    GTB_CASE(16, 16) GTB_CASE(16, 32) GTB_CASE(16, 64)
+    GTB_CASE(32, 16) GTB_CASE(32, 32) GTB_CASE(32, 64)
+    GTB_CASE(64, 16) GTB_CASE(64, 32) GTB_CASE(64, 64)
+#undef GTB_CASE
     return -1;
 }
 

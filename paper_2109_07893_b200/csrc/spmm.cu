@@ -195,6 +195,8 @@ __global__ void __launch_bounds__(256) gcn_bwd_rows_kernel(int32_t n, dgnn_frame
 // tcgen05 instance of K3 (gcn_tc.cu); -1 when the shape has none
 int gcn_fwd_tc(int fp, int hp, bool skip, bool agg, int32_t n, const int32_t* rp, const int32_t* col,
                const float* val, dgnn_frame x, const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st);
+int gcn_bwd_tc(int fp, int hp, bool skip, int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame ds,
+               cudaStream_t st);
 
 }  // namespace dgnn
 
@@ -305,6 +307,14 @@ static int dgnn_gcn_tensor_cores = 1;
 
 void dgnn_set_gcn_tensor_cores(int on) { dgnn_gcn_tensor_cores = on != 0; }
 
+}  // extern "C"
+
+namespace dgnn {
+int gcn_tensor_cores_on() { return dgnn_gcn_tensor_cores; }
+}  // namespace dgnn
+
+extern "C" {
+
 int dgnn_spmm_f32(int32_t n, const int32_t* rowptr, const int32_t* col, const float* val, dgnn_frame x,
                   int32_t f, dgnn_frame out, void* stream) {
     DGNN_CHECK_ARG(n >= 0, "spmm_f32: negative size");
@@ -345,6 +355,10 @@ int dgnn_gcn_backward_rows(int32_t n, dgnn_frame dr, dgnn_frame r, int32_t fp, c
     DGNN_CHECK_ARG(n >= 0, "gcn_backward_rows: negative size");
     if (n == 0) return DGNN_OK;
     cudaStream_t st = as_stream(stream);
+    if (dgnn_gcn_tensor_cores) {
+        const int rc = gcn_bwd_tc(fp, hp, skip != 0, n, dr, r, w, ds, st);
+        if (rc >= 0) return rc;
+    }
     return skip ? gcn_bwd_fp<true>(fp, hp, n, dr, r, w, ds, st) : gcn_bwd_fp<false>(fp, hp, n, dr, r, w, ds, st);
 }
 

@@ -308,6 +308,49 @@ def gcn_forward(n: int, rowptr: np.ndarray | None, col: np.ndarray | None, val: 
     return s_out.cpu().numpy(), r_out.cpu().numpy()
 
 
+def gcn_backward(dr: np.ndarray, r: np.ndarray, s: np.ndarray, w: np.ndarray, skip: bool,
+                 tensor_cores: bool = True, slabs: int = 0, rows_ds: bool = True):
+    """Test hook of K4's row part and weight gradient (`dgnn_gcn_backward_rows`,
+    `dgnn_gcn_weight_grad`, training.py:347-350, 359-367): with dpre =
+    dr (.) [r > 0] and dq = dpre[:, F:] (skip) | dpre, returns (ds, gw) =
+    (dpre[:, :F] + dq w^T (skip) | dq w^T, s^T dq) -- ds None when rows_ds is
+    False.  `slabs` > 0 passes the inputs as split (owner-layout) frames."""
+    dev = _dev()
+    n = dr.shape[0]
+    fp, hp = w.shape
+    rw = dr.shape[1]
+
+    def dev_frame(a, wdt):
+        t = torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev)
+        if slabs <= 0:
+            return t, _lib.frame(t, wdt)
+        rps = -(-n // slabs)
+        buf = torch.full((slabs, rps + 3, wdt), np.nan, dtype=torch.float32, device=dev)
+        for q in range(slabs):
+            part = t[q * rps:(q + 1) * rps]
+            buf[q, :part.shape[0]] = part
+        return buf, _lib.frame(buf, wdt, rps, (rps + 3) * wdt)
+
+    keep = []
+    drd, fdr = dev_frame(dr, rw)
+    rd, fr = dev_frame(r, rw)
+    sd, fs = dev_frame(s, fp)
+    keep += [drd, rd, sd]
+    wd = torch.from_numpy(np.ascontiguousarray(w, np.float32)).to(dev)
+    ds = torch.full((n, fp), np.nan, dtype=torch.float32, device=dev)
+    gw = torch.zeros(fp * hp, dtype=torch.float64, device=dev)
+    ws = torch.empty(query("dgnn_gcn_weight_grad_workspace", fp, hp), dtype=torch.uint8, device=dev)
+    st = _lib.stream_handle()
+    call("dgnn_set_gcn_tensor_cores", int(tensor_cores))
+    try:
+        call("dgnn_gcn_weight_grad", n, fs, fdr, fr, fp, hp, int(skip), ptr(gw), ptr(ws), ws.numel(), st)
+        if rows_ds:
+            call("dgnn_gcn_backward_rows", n, fdr, fr, fp, ptr(wd), hp, int(skip), _lib.frame(ds, fp), st)
+    finally:
+        call("dgnn_set_gcn_tensor_cores", 1)
+    return (ds.cpu().numpy() if rows_ds else None), gw.view(fp, hp).cpu().numpy()
+
+
 def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np.ndarray, np_rows: int):
     """Tensor-core block weight gradient (test hook of dgnn_lstm_weight_grad_tc):
     returns (sum_r xcat[r]^T dz[r]  as (kx+hp) x 4hp, sum_r dz[r]) in fp64."""

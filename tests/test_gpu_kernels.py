@@ -393,3 +393,40 @@ def test_gcn_forward_tensor_cores(fp, hp, skip, agg):
     if skip:
         assert np.array_equal(r[:, :fp], np.maximum(s, 0))
     assert np.abs((r2[:, fp:] if skip else r2) - got_q).max() <= 2e-6 * qs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fp,hp,skip,slabs,n", [(64, 64, True, 0, 70001), (4, 64, True, 0, 20011),
+                                                (32, 16, False, 0, 9000), (64, 64, True, 2, 30002),
+                                                (16, 32, True, 4, 5003), (64, 128, False, 0, 3000)])
+def test_gcn_backward_tensor_cores(fp, hp, skip, slabs, n):
+    """K4 rows (tcgen05 BWD instance of K3) and the tcgen05 GCN weight
+    gradient against fp64: masked dq, skip term, ragged tails, split
+    owner-layout frames, long reductions (period promotion), and the SIMT
+    kernels on the same inputs."""
+    from paper_2109_07893_b200.ops import gcn_backward
+    rng = np.random.default_rng(fp + 3 * hp + n)
+    rw = fp + hp if skip else hp
+    dr = rng.standard_normal((n, rw)).astype(np.float32)
+    r = np.maximum(rng.standard_normal((n, rw)), 0).astype(np.float32)
+    s = rng.standard_normal((n, fp)).astype(np.float32)
+    w = (rng.standard_normal((fp, hp)) * 0.2).astype(np.float32)
+    rows_ds = fp >= 16
+    ds, gw = gcn_backward(dr, r, s, w, skip, slabs=slabs, rows_ds=rows_ds)
+    ds2, gw2 = gcn_backward(dr, r, s, w, skip, tensor_cores=False, rows_ds=rows_ds)
+    dpre = dr.astype(np.float64) * (r > 0)
+    dq = dpre[:, fp:] if skip else dpre
+    ref_gw = s.astype(np.float64).T @ dq
+    scale = np.abs(s).astype(np.float64).T @ np.abs(dq)
+    assert np.all(np.abs(gw - ref_gw) <= 2e-6 * scale + 1e-9), np.abs(gw - ref_gw).max()
+    assert np.all(np.abs(gw2 - ref_gw) <= 2e-6 * scale + 1e-9)
+    if rows_ds:
+        ref_ds = dq @ w.astype(np.float64).T + (dpre[:, :fp] if skip else 0.0)
+        sc = (np.abs(dq) @ np.abs(w.astype(np.float64)).T).max() + 1.0
+        assert np.abs(ds - ref_ds).max() <= 2e-6 * sc
+        assert np.abs(ds2 - ref_ds).max() <= 2e-6 * sc
+    # deterministic: the same inputs give bitwise the same results
+    ds3, gw3 = gcn_backward(dr, r, s, w, skip, slabs=slabs, rows_ds=rows_ds)
+    assert np.array_equal(gw, gw3)
+    if rows_ds:
+        assert np.array_equal(ds, ds3)
