@@ -210,7 +210,7 @@ def run_ours(args):
                    "dgnn_lstm_forward_step_ws", "dgnn_lstm_backward_step_ws",
                    "dgnn_lstm_backward_step_tc", "dgnn_lstm_weight_grad_tc", "dgnn_gemm_tn", "dgnn_gcn_forward",
                    "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows", "dgnn_csr_apply_delta",
-                   "dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_head_loss", "dgnn_head_grad",
+                   "dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_head_loss", "dgnn_head_grad", "dgnn_head_loss_grad",
                    "dgnn_head_scatter"]
     timer = _lib.KernelTimer(timed_names)
     clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_rank{rank}.csv"

@@ -292,6 +292,14 @@ int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_fram
                    int32_t c, const double* dlogits, double* ghw, double* ghb, void* workspace,
                    size_t workspace_bytes, void* stream);
 
+/* K8 fused (training.py:698-735, 2 classes): head_loss and head_grad in one
+ * pass over the pairs -- loss_pp and dlogits as dgnn_head_loss, ghw / ghb
+ * accumulated as dgnn_head_grad (deterministic fixed-order reduction).
+ * Workspace from dgnn_head_grad_workspace. */
+int dgnn_head_loss_grad(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y, dgnn_frame z,
+                        int32_t ep, int32_t c, const float* hw, const float* hb, double scale, double* loss_pp,
+                        int32_t n_partials, double* dlogits, double* ghw, double* ghb, void* ws, size_t ws_bytes,
+                        void* stream);
 /* dz seeds (training.py:732-734) as a gather over the vertex->slot
  * incidence (ascending slot order = the np.add.at order):
  *   dz[x] = sum_{slot s of x} dlogits[s/2] . hw[side(s)]^T ; zero rows elsewhere. */

@@ -75,6 +75,8 @@ _SIGS = {
                                P, P]),
     "dgnn_head_grad_workspace": (c_size_t, [c_int32, c_int32]),
     "dgnn_head_grad": (c_int, [c_int64, P, P, Frame, c_int32, c_int32, P, P, P, P, c_size_t, P]),
+    "dgnn_head_loss_grad": (c_int, [c_int64, P, P, P, Frame, c_int32, c_int32, P, P, c_double, P, c_int32, P, P, P,
+                                    P, c_size_t, P]),
     "dgnn_head_scatter": (c_int, [c_int32, P, P, P, P, c_int32, c_int32, Frame, P]),
     "dgnn_head_predict": (c_int, [c_int64, P, P, P, Frame, c_int32, c_int32, P, P, P, P]),
     "dgnn_sum_f64": (c_int, [c_int64, P, P, c_int, P]),

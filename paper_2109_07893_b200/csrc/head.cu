@@ -214,6 +214,155 @@ int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const dou
     return launch_status("head_scatter");
 }
 
+
+// Fused head loss + head-parameter gradient (one pass over the labelled
+// pairs, training.py:698-735).  LP = EP / 8 lanes per pair (8 embedding
+// dims each), 32 / LP pairs per warp in flight.  Logits are reduced over the
+// group in a fixed butterfly and taken from the group leader, which does
+// the fp64 softmax CE, writes loss_pp and dlogits (the scatter kernel reads
+// them) and broadcasts dl to its group; every lane folds a * dl into fp64
+// accumulators of its 8 dims (u and v side).  Pairs are assigned statically
+// (fixed grid), groups / warps / CTAs are combined in fixed order and the
+// per-CTA partials are reduced by head_lg_reduce_kernel: deterministic.
+constexpr int kHeadCtas = kSMs;
+
+template <int EP>
+__global__ void __launch_bounds__(256) head_loss_grad_kernel(int64_t npairs, const int32_t* __restrict__ u,
+                                                             const int32_t* __restrict__ v,
+                                                             const int32_t* __restrict__ y, dgnn_frame z, int C,
+                                                             const float* __restrict__ hw,
+                                                             const float* __restrict__ hb, double scale,
+                                                             double* __restrict__ loss_pp,
+                                                             double* __restrict__ dlogits,
+                                                             double* __restrict__ part) {
+    constexpr int LP = EP / 8;                 // lanes per pair
+    constexpr int ROWS = 2 * EP + 1;           // head.w rows (u side, v side) + bias
+    __shared__ float hws[2 * EP * kMaxClasses];
+    __shared__ double red[8][ROWS * 2];        // per-warp partials (C <= 2 staged here; see below)
+    for (int i = threadIdx.x; i < 2 * EP * C; i += blockDim.x) hws[i] = hw[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gl = lane % LP, grp = lane / LP;
+    const unsigned gmask = (LP == 32 ? 0xffffffffu : (((1u << LP) - 1u) << (grp * LP)));
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LP;
+    const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / LP;
+    const int k0 = 8 * gl;
+    double acc_u[8][2], acc_v[8][2], acc_b[2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc_u[j][0] = acc_u[j][1] = acc_v[j][0] = acc_v[j][1] = 0.0;
+    acc_b[0] = acc_b[1] = 0.0;
+    for (int64_t p = gid; p < npairs; p += ngroups) {
+        const float4* zu = reinterpret_cast<const float4*>(frame_row<const float>(z, u[p]) + k0);
+        const float4* zv = reinterpret_cast<const float4*>(frame_row<const float>(z, v[p]) + k0);
+        const float4 a0 = zu[0], a1 = zu[1], b0 = zv[0], b1 = zv[1];
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        float lg[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            float t = 0.f;
+            if (c < C) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) t += a[j] * hws[(k0 + j) * C + c] + b[j] * hws[(EP + k0 + j) * C + c];
+            }
+#pragma unroll
+            for (int o = LP / 2; o > 0; o >>= 1) t += __shfl_xor_sync(gmask, t, o);
+            lg[c] = __shfl_sync(gmask, t, grp * LP);   // the leader's value: one rounding for the group
+        }
+        double dl[2] = {0.0, 0.0};
+        if (gl == 0) {
+            const double l0 = (double)(lg[0] + hb[0]), l1 = (double)(lg[1] + hb[1]);
+            const double mx = l0 > l1 ? l0 : l1;
+            const double lz = log(exp(l0 - mx) + exp(l1 - mx));
+            const int lab = y[p];
+            loss_pp[p] = -(((lab ? l1 : l0) - mx) - lz);
+            dl[0] = (exp((l0 - mx) - lz) - (lab == 0 ? 1.0 : 0.0)) * scale;
+            dl[1] = (exp((l1 - mx) - lz) - (lab == 1 ? 1.0 : 0.0)) * scale;
+            dlogits[p * 2] = dl[0];
+            dlogits[p * 2 + 1] = dl[1];
+            acc_b[0] += dl[0];
+            acc_b[1] += dl[1];
+        }
+        dl[0] = __shfl_sync(gmask, dl[0], grp * LP);
+        dl[1] = __shfl_sync(gmask, dl[1], grp * LP);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                acc_u[j][c] += (double)a[j] * dl[c];
+                acc_v[j][c] += (double)b[j] * dl[c];
+            }
+    }
+    // groups of a warp -> group 0 (fixed order: group g adds group g + span)
+#pragma unroll
+    for (int span = 16; span >= LP; span >>= 1) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                acc_u[j][c] += __shfl_down_sync(0xffffffffu, acc_u[j][c], span);
+                acc_v[j][c] += __shfl_down_sync(0xffffffffu, acc_v[j][c], span);
+            }
+        acc_b[0] += __shfl_down_sync(0xffffffffu, acc_b[0], span);
+        acc_b[1] += __shfl_down_sync(0xffffffffu, acc_b[1], span);
+    }
+    if (lane < LP) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                red[warp][(k0 + j) * 2 + c] = acc_u[j][c];
+                red[warp][(EP + k0 + j) * 2 + c] = acc_v[j][c];
+            }
+        if (lane == 0) {
+            red[warp][2 * EP * 2] = acc_b[0];
+            red[warp][2 * EP * 2 + 1] = acc_b[1];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ROWS * 2; i += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w][i];
+        part[(int64_t)blockIdx.x * ROWS * 2 + i] = t;
+    }
+}
+
+// ghw[k][c] (k < 2 ep) / ghb[c] += sum over CTAs of part (fixed tree)
+__global__ void __launch_bounds__(128) head_lg_reduce_kernel(int nct, int outs, int ep,
+                                                             const double* __restrict__ part,
+                                                             double* __restrict__ ghw, double* __restrict__ ghb) {
+    __shared__ double sh[128];
+    const int i = blockIdx.x;   // output index: row k = i / 2, class c = i % 2
+    double t = 0.0;
+    for (int b = threadIdx.x; b < nct; b += 128) t += part[(int64_t)b * outs + i];
+    sh[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = 64; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int k = i / 2, c = i % 2;
+        if (k < 2 * ep) ghw[k * 2 + c] += sh[0];
+        else ghb[c] += sh[0];
+    }
+}
+
+template <int EP>
+int head_loss_grad_t(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y, dgnn_frame z,
+                     const float* hw, const float* hb, double scale, double* loss_pp, double* dlogits, double* ghw,
+                     double* ghb, double* part, cudaStream_t st) {
+    int64_t blocks = cdiv(npairs, 256 / (EP / 8));
+    blocks = blocks > kHeadCtas ? kHeadCtas : (blocks < 1 ? 1 : blocks);
+    note_launch();
+    head_loss_grad_kernel<EP><<<(unsigned)blocks, 256, 0, st>>>(npairs, u, v, y, z, 2, hw, hb, scale, loss_pp,
+                                                                 dlogits, part);
+    const int outs = (2 * EP + 1) * 2;
+    note_launch();
+    head_lg_reduce_kernel<<<(unsigned)outs, 128, 0, st>>>((int)blocks, outs, EP, part, ghw, ghb);
+    return launch_status("head_loss_grad");
+}
+
 }  // namespace dgnn
 
 using namespace dgnn;
@@ -270,6 +419,29 @@ int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_fram
     ::dgnn::note_launch();
     head_grad_reduce_kernel<<<(unsigned)cdiv(outs, 256), 256, 0, st>>>((int)nch, ep, c, part, ghw, ghb);
     return launch_status("head_grad");
+}
+
+int dgnn_head_loss_grad(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y, dgnn_frame z,
+                        int32_t ep, int32_t c, const float* hw, const float* hb, double scale, double* loss_pp,
+                        int32_t n_partials, double* dlogits, double* ghw, double* ghb, void* ws, size_t ws_bytes,
+                        void* stream) {
+    DGNN_CHECK_ARG(c == 2, "head_loss_grad: the fused kernel serves the 2-class link predictor");
+    DGNN_CHECK_ARG(n_partials >= npairs, "head_loss_grad: per-pair loss buffer too small");
+    if (ws_bytes < dgnn_head_grad_workspace(ep, c)) {
+        set_error("head_loss_grad: workspace too small");
+        return DGNN_EWORKSPACE;
+    }
+    if (npairs == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    double* part = reinterpret_cast<double*>(ws);
+    switch (ep) {
+        case 16: return head_loss_grad_t<16>(npairs, u, v, y, z, hw, hb, scale, loss_pp, dlogits, ghw, ghb, part, st);
+        case 32: return head_loss_grad_t<32>(npairs, u, v, y, z, hw, hb, scale, loss_pp, dlogits, ghw, ghb, part, st);
+        case 64: return head_loss_grad_t<64>(npairs, u, v, y, z, hw, hb, scale, loss_pp, dlogits, ghw, ghb, part, st);
+        case 128: return head_loss_grad_t<128>(npairs, u, v, y, z, hw, hb, scale, loss_pp, dlogits, ghw, ghb, part, st);
+    }
+    set_error("head_loss_grad: unsupported width %d", ep);
+    return DGNN_EUNSUPPORTED;
 }
 
 int dgnn_head_scatter(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot, const double* dlogits,

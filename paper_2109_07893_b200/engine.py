@@ -204,6 +204,9 @@ class Rank:
         mx = max([v["n"] for d in self.lab.values() for v in d.values()] + [1])
         self.loss_pp = torch.zeros(mx, dtype=torch.float64, device=self.dev)
         self.dlogits = torch.zeros(mx * eng.cfg.classes, dtype=torch.float64, device=self.dev)
+        # per-timestep loss sums, written by the backward's fused head kernel
+        # and summed in timestep order at the end of the epoch
+        self.loss_t = torch.zeros(eng.plan.T, dtype=torch.float64, device=self.dev)
 
     # ---------------------------------------------------------------- phases
     def reset_state(self):
@@ -219,6 +222,8 @@ class Rank:
             self.dtrail = [dict() for _ in self.eng.layout.layers]
         self.pi = {}
         self.loss_acc.zero_()
+        if hasattr(self, "loss_t"):
+            self.loss_t.zero_()
         self.correct.zero_()
 
     def begin_block(self, b, keep, ledger=None, count_bytes=True):
@@ -443,11 +448,20 @@ class Rank:
                     works += self._scatter_owned_step(self.dZ_own, self.dY_vm, Ly.ho, c)
                 continue
             z = self.own(self.Y_own[-1], Ly.ho, c)
-            call("dgnn_head_loss", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), z, ep, C, ptr(hw), ptr(hb),
-                 eng.scale, ptr(self.loss_pp), self.loss_pp.numel(), ptr(self.dlogits), st)
-            call("dgnn_head_grad", d["n"], ptr(d["u"]), ptr(d["v"]), z, ep, C, ptr(self.dlogits),
-                 ptr(eng.params.gw("head.w")), ptr(eng.params.gw("head.b")), ptr(self.ws_head),
-                 self.ws_head.numel(), st)
+            if C == 2:
+                # loss + head gradient in one pass; the loss of the step is
+                # kept (the forward sweep does not recompute it)
+                call("dgnn_head_loss_grad", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), z, ep, C, ptr(hw),
+                     ptr(hb), eng.scale, ptr(self.loss_pp), self.loss_pp.numel(), ptr(self.dlogits),
+                     ptr(eng.params.gw("head.w")), ptr(eng.params.gw("head.b")), ptr(self.ws_head),
+                     self.ws_head.numel(), st)
+                call("dgnn_sum_f64", d["n"], ptr(self.loss_pp), self.loss_t.data_ptr() + 8 * t, 0, st)
+            else:
+                call("dgnn_head_loss", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), z, ep, C, ptr(hw),
+                     ptr(hb), eng.scale, ptr(self.loss_pp), self.loss_pp.numel(), ptr(self.dlogits), st)
+                call("dgnn_head_grad", d["n"], ptr(d["u"]), ptr(d["v"]), z, ep, C, ptr(self.dlogits),
+                     ptr(eng.params.gw("head.w")), ptr(eng.params.gw("head.b")), ptr(self.ws_head),
+                     self.ws_head.numel(), st)
             call("dgnn_head_scatter", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), ptr(self.dlogits), ptr(hw), ep, C,
                  dz, st)
             if works is not None:
@@ -742,7 +756,8 @@ class Engine:
                 r.begin_block(b, keep=False, ledger=transfer)
             self._layers_forward(b, "forward", comm)
             for r in self.ranks:
-                r.block_loss(b)
+                if self.cfg.classes != 2:
+                    r.block_loss(b)
                 r.store_pi(b)
             if act is not None:
                 act.alloc_checkpoint(1.0)
@@ -780,6 +795,9 @@ class Engine:
         self.params.g.copy_(grads)
         if comm is not None:
             comm.record_allreduce(self.layout.count, plan.P)
+        if self.cfg.classes == 2:
+            for r in self.ranks:   # per-timestep sums in timestep order
+                call("dgnn_sum_f64", plan.T, ptr(r.loss_t), ptr(r.loss_acc), 0, _lib.stream_handle())
         loss_dev = self.fabric.allreduce([sum_ranks([r.loss_acc for r in self.ranks])])
         return loss_dev, grads
 
