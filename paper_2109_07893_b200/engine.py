@@ -47,6 +47,15 @@ WARP_SPECIALIZED = True
 PIPELINED_EXCHANGE = os.environ.get("DGNN_PIPELINED_EXCHANGE", "auto")
 # SMs the persistent kernels leave free for the concurrent NCCL P2P kernels
 SM_RESERVE = int(os.environ.get("DGNN_SM_RESERVE", "32"))
+# multi-GPU cd-gcn: cut the GCN between its sparse aggregation (snapshot
+# owner) and its dense transform + ReLU (vertex owner).  The exchanges then
+# carry s = Ahat y (F wide) instead of r = relu([s, s W]) (F + H wide) and
+# ds instead of dr, and layer 0 -- whose aggregation s1 is input-static --
+# needs no exchange at all: every rank keeps s1 of its vertex chunk.  Same
+# arithmetic per row; 41% less all-to-all volume at the bench shape.  The
+# CommLedger still records the reference's schedule (dist.py:548-574);
+# `Engine.bytes_moved` counts what actually crossed the fabric.
+SPLIT_GCN = os.environ.get("DGNN_SPLIT_GCN", "1")
 
 
 class Plan:
@@ -101,6 +110,13 @@ class Rank:
         self.Y_own = [_zeros(P * C * NP * Ly.ho, device=dev) for Ly in layers]
         self.S_own = [None] + [_zeros(C * N * Ly.fp, device=dev) for Ly in layers[1:]]
         same = P == 1
+        self.split = eng.split
+        if self.split:
+            # S_own is in the owner layout [P][C][NP][fp] (all-to-all ready)
+            self.S_vm = [None] + [_zeros(B * NP * Ly.fp, device=dev) for Ly in layers[1:]]
+            self.dS_vm = [None] + [_zeros(B * NP * Ly.fp, device=dev) for Ly in layers[1:]]
+            self.dS_own = [None] + [_zeros(P * C * NP * Ly.fp, device=dev) for Ly in layers[1:]]
+            self.s1v = {}   # s1[t] rows of this rank's vertex chunk, every t
         self.R_vm = self.R_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
         self.Y_vm = self.Y_own if same else [_zeros(B * NP * Ly.ho, device=dev) for Ly in layers]
         wmax = max(Ly.ho for Ly in layers)
@@ -174,7 +190,8 @@ class Rank:
         prep = Materializer(eng.enc, self.dev, slots=1, resident=False, with_f64=True)
         x64 = torch.zeros(N * max(2, fin), dtype=torch.float64, device=self.dev)
         s64 = torch.zeros(N * fin, dtype=torch.float64, device=self.dev)
-        for t in plan.owned(self.q):
+        owned_t = set(plan.owned(self.q))
+        for t in (range(plan.T) if self.split else plan.owned(self.q)):
             slot = prep.materialize([t], ledger=None, count_bytes=False)[0]
             prep.wait()
             if feats_host is None:     # degree features of the (raw) graph, dtdg.py:255-266
@@ -185,7 +202,11 @@ class Rank:
                  ptr(s64), fin, st)
             out = _zeros(N * fp0, device=self.dev)
             call("dgnn_cast_f64_to_f32_frame", N, fin, ptr(s64), fin, frame(out, fp0), st)
-            self.s1[t] = out
+            if self.split:
+                NP = plan.NP
+                self.s1v[t] = out[self.q * NP * fp0:(self.q + 1) * NP * fp0].clone()
+            if t in owned_t:
+                self.s1[t] = out
         prep.check()
         del prep
         owned = set(plan.owned(self.q))
@@ -305,6 +326,68 @@ class Rank:
             s_out = self.plain(self.S_own[l], Ly.fp, c) if (self.keep and l > 0) else _lib.Frame(None, 0, 0, 0)
             call("dgnn_gcn_forward", eng.plan.N, rp, col, val, x, Ly.fp, ptr(w), Ly.hg, int(self.skip),
                  s_out, self.own(self.R_own[l], Ly.rw, c), st)
+
+    # ----------------------------------------------- split GCN (P > 1, cd-gcn)
+    def gcn_aggregate(self, b, l):
+        """Owner side of the split GCN: s = Ahat_t y_t for every owned step,
+        into the owner layout (the all-to-all source); bitwise the s of K3."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        st = _lib.stream_handle()
+        self._wait_graph()
+        for c, t in enumerate(self.ts):
+            s = self.slots[c]
+            call("dgnn_spmm_f32", eng.plan.N, ptr(s.rowptr), ptr(s.col), ptr(s.val),
+                 self.own(self.Y_own[l - 1], Ly.fp, c), Ly.fp, self.own(self.S_own[l], Ly.fp, c), st)
+
+    def _split_input(self, l, i):
+        NP = self.eng.plan.NP
+        Ly = self.eng.layout.layers[l]
+        if l == 0:
+            t = self.eng.plan.block_steps(self.b)[i]
+            return _lib.Frame(self.s1v[t].data_ptr(), Ly.fp, 0, 0)
+        return _lib.Frame(self.S_vm[l].data_ptr() + F32 * i * NP * Ly.fp, Ly.fp, 0, 0)
+
+    def gcn_dense_forward(self, b, l):
+        """Vertex side of the split GCN: r = relu([s, s W]) for every block
+        step of this rank's vertex chunk (K3 without aggregation)."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        NP = eng.plan.NP
+        st = _lib.stream_handle()
+        w = eng.params.w(f"gcn{l}.w")
+        for i in range(eng.plan.bsize):
+            r_out = _lib.Frame(self.R_vm[l].data_ptr() + F32 * i * NP * Ly.rw, Ly.rw, 0, 0)
+            call("dgnn_gcn_forward", NP, None, None, None, self._split_input(l, i), Ly.fp, ptr(w), Ly.hg,
+                 int(self.skip), _lib.Frame(None, 0, 0, 0), r_out, st)
+
+    def gcn_dense_backward(self, b, l):
+        """Vertex side of the split GCN backward: dW += s^T dq and (l > 0)
+        ds = dpre[:, :F] + dq W^T for every block step of the vertex chunk."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        NP = eng.plan.NP
+        st = _lib.stream_handle()
+        w = eng.params.w(f"gcn{l}.w")
+        gw = eng.params.gw(f"gcn{l}.w")
+        for i in range(eng.plan.bsize):
+            dr = _lib.Frame(self.dR_vm[l].data_ptr() + F32 * i * NP * Ly.rw, Ly.rw, 0, 0)
+            r = _lib.Frame(self.R_vm[l].data_ptr() + F32 * i * NP * Ly.rw, Ly.rw, 0, 0)
+            call("dgnn_gcn_weight_grad", NP, self._split_input(l, i), dr, r, Ly.fp, Ly.hg, int(self.skip), ptr(gw),
+                 ptr(self.ws_tn), self.ws_tn.numel(), st)
+            if l > 0:
+                ds = _lib.Frame(self.dS_vm[l].data_ptr() + F32 * i * NP * Ly.fp, Ly.fp, 0, 0)
+                call("dgnn_gcn_backward_rows", NP, dr, r, Ly.fp, ptr(w), Ly.hg, int(self.skip), ds, st)
+
+    def gcn_transpose_aggregate(self, b, l):
+        """Owner side of the split GCN backward: dy_{l-1} = Ahat_t^T ds_t."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        st = _lib.stream_handle()
+        for c, t in enumerate(self.ts):
+            sl = self.slots[c]
+            call("dgnn_spmm_f32", eng.plan.N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val),
+                 self.own(self.dS_own[l], Ly.fp, c), Ly.fp, self.own(self.dZ_own, Ly.fp, c), st)
 
     def rnn_forward(self, b, l, pipelined=False):
         eng = self.eng
@@ -659,6 +742,8 @@ class Engine:
         self.resident = resident
         self.enc = encoding if encoding is not None else SnapshotEncoding(graph)
         self.fabric = fabric or LocalFabric()
+        self.split = self.skip and self.plan.P > 1 and SPLIT_GCN == "1"
+        self.bytes_moved = 0      # bytes that crossed the fabric (all ranks of this process)
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.params = DeviceParams(self.layout, dev)
@@ -690,6 +775,7 @@ class Engine:
         plan = self.plan
         count = plan.chunk * plan.NP * W
         self.fabric.exchange(self.ranks, src, dst, count)
+        self.bytes_moved += F32 * count * (plan.P - 1) * len(self.ranks)
         if comm is not None:
             units = plan.bsize * plan.NP * (plan.P - 1)
             msgs = plan.P * (plan.P - 1)
@@ -702,6 +788,8 @@ class Engine:
 
     def _pipelining(self):
         """(GCN-side, LSTM-side) exchange pipelining for this run."""
+        if self.split:
+            return False, False
         if not (self.fabric.distributed and self.plan.P > 1) or PIPELINED_EXCHANGE == "0":
             return False, False
         mode = PIPELINED_EXCHANGE
@@ -722,7 +810,16 @@ class Engine:
         # sends of finished slabs / steps overlap the next kernel)
         pipe_gcn, pipe_lstm = self._pipelining()
         for l, Ly in enumerate(layers):
-            if pipe_gcn:
+            if self.split:
+                if l == 0:
+                    self._record_xchg(comm, phase, b, l)     # s1 is local: nothing moves
+                else:
+                    for r in self.ranks:
+                        r.gcn_aggregate(b, l)
+                    self._xchg(lambda r: r.S_own[l], lambda r: r.S_vm[l], Ly.fp, comm, phase, b, l)
+                for r in self.ranks:
+                    r.gcn_dense_forward(b, l)
+            elif pipe_gcn:
                 self._wait(self.ranks[0].gcn_forward_pipelined(b, l))
                 self._record_xchg(comm, phase, b, l)
             else:
@@ -778,6 +875,17 @@ class Engine:
                     self._record_xchg(comm, "backward", b, l)
                 else:
                     self._xchg(lambda r: r.dZ_own, lambda r: r.dY_vm, Ly.ho, comm, "backward", b, l)
+                if self.split:
+                    for r in self.ranks:
+                        r.rnn_backward(b, l)
+                        r.gcn_dense_backward(b, l)
+                    if l == 0:
+                        self._record_xchg(comm, "backward", b, l)
+                    else:
+                        self._xchg(lambda r: r.dS_vm[l], lambda r: r.dS_own[l], layers[l].fp, comm, "backward", b, l)
+                        for r in self.ranks:
+                            r.gcn_transpose_aggregate(b, l)
+                    continue
                 if pipe_lstm:
                     self._wait(self.ranks[0].rnn_backward(b, l, pipelined=True))
                     self._record_xchg(comm, "backward", b, l)
