@@ -212,6 +212,8 @@ def run_ours(args):
                    "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows", "dgnn_csr_apply_delta",
                    "dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_head_loss", "dgnn_head_grad", "dgnn_head_loss_grad",
                    "dgnn_head_scatter"]
+    if args.timeline:   # every C-ABI call, for the per-stream idle breakdown
+        timed_names = list(_lib._SIGS.keys()) if hasattr(_lib, "_SIGS") else timed_names
     timer = _lib.KernelTimer(timed_names)
     clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_rank{rank}.csv"
                           if (ROOT / "gpurun_out").exists() else None)
@@ -230,6 +232,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     _lib.set_timer(None)
     launches = _lib.launch_count() - launches0
+    timeline = timer.gaps(e0) if args.timeline else None
     if P > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -337,6 +340,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "prep_seconds": prep_s,
+            "timeline": timeline,
         }
         print(json.dumps(line))
     if P > 1:
@@ -419,6 +423,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--timeline", action="store_true", help="per-stream busy / idle breakdown (diagnostic)")
     ap.add_argument("--cpu-scale", type=int, default=128)
     ap.add_argument("--cpu-scale-ref", type=int, default=256)
     args = ap.parse_args()

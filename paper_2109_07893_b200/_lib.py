@@ -119,12 +119,35 @@ class KernelTimer:
         self.names = set(names)
         self.records = {}      # name -> list of (start, end, args)
         self._streams = {}
+        self.order = []        # (stream handle, name, start, end) in issue order
 
     def stream(self, handle):
         import torch
         if handle not in self._streams:
             self._streams[handle] = torch.cuda.ExternalStream(handle)
         return self._streams[handle]
+
+    def gaps(self, t0, top: int = 8):
+        """Per stream: busy ms inside the recorded calls, idle ms between
+        consecutive calls (waits on other streams / the fabric / the host),
+        and the calls preceded by the largest total idle time.  `t0` is an
+        event recorded at the start of the timed region."""
+        import torch
+        torch.cuda.synchronize()
+        out = {}
+        last = {}
+        for st, name, e0, e1 in self.order:
+            d = out.setdefault(str(st), {"busy_ms": 0.0, "idle_ms": 0.0, "idle_before": {}})
+            d["busy_ms"] += e0.elapsed_time(e1)
+            prev = last.get(st)
+            idle = prev.elapsed_time(e0) if prev is not None else t0.elapsed_time(e0)
+            if idle > 0:
+                d["idle_ms"] += idle
+                d["idle_before"][name] = d["idle_before"].get(name, 0.0) + idle
+            last[st] = e1
+        for d in out.values():
+            d["idle_before"] = dict(sorted(d["idle_before"].items(), key=lambda kv: -kv[1])[:top])
+        return out
 
     def durations(self):
         """name -> list of (ms, args); synchronises."""
@@ -156,6 +179,7 @@ def call(name: str, *args) -> None:
         rc = getattr(lib(), name)(*args)
         e1.record(s)
         t.records.setdefault(name, []).append((e0, e1, args))
+        t.order.append((args[-1], name, e0, e1))
     else:
         rc = getattr(lib(), name)(*args)
     if rc:

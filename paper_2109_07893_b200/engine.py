@@ -102,7 +102,9 @@ class Rank:
         plan, layers = eng.plan, eng.layout.layers
         P, C, B, N, NP = plan.P, plan.chunk, plan.bsize, plan.N, plan.NP
         dev = self.dev
-        self.mat = Materializer(eng.enc, dev, slots=C, resident=eng.resident)
+        self.mat = Materializer(eng.enc, dev, slots=C, resident=eng.resident, sets=2)
+        self.prefetched = {}     # block -> (slots, ready event) rebuilt ahead of its pass
+        self.set_turn = 0
         self.skip = eng.skip
         L = len(layers)
         # snapshot-major (owner layout) and vertex-major buffers
@@ -247,12 +249,31 @@ class Rank:
             self.loss_t.zero_()
         self.correct.zero_()
 
-    def begin_block(self, b, keep, ledger=None, count_bytes=True):
+    def begin_block(self, b, keep, ledger=None, count_bytes=True, next_b=None):
         """`dist.py:301-318`: stream the owned chunk through the codec and pick
-        the carried state (forward sweep) or pi_{b-1} (checkpoint rerun)."""
+        the carried state (forward sweep) or pi_{b-1} (checkpoint rerun).
+        `next_b`: the block of the following pass, whose graph is rebuilt on
+        the graph stream (into the other slot set) while this block computes."""
         self.b, self.keep = b, keep
         self.ts = self.eng.plan.steps_of(self.q, b)
-        self.slots = self.mat.materialize(self.ts, ledger=ledger, count_bytes=count_bytes)
+        # everything enqueued so far (the previous block) is done with the
+        # slot set that block used two passes ago
+        released = torch.cuda.Event()
+        released.record(torch.cuda.current_stream(self.dev))
+        if b in self.prefetched:
+            self.slots, self.ready_ev = self.prefetched.pop(b)
+            self.mat.account(self.ts, ledger, count_bytes)
+        else:
+            self.set_turn ^= 1
+            self.slots = self.mat.materialize(self.ts, ledger=ledger, count_bytes=count_bytes,
+                                              set_idx=self.set_turn, after=released)
+            self.ready_ev = self.mat.ready
+        if next_b is not None and len(self.eng.plan.steps_of(self.q, next_b)):
+            self.set_turn ^= 1
+            nts = self.eng.plan.steps_of(self.q, next_b)
+            slots = self.mat.materialize(nts, ledger=None, count_bytes=False, set_idx=self.set_turn,
+                                         after=released)
+            self.prefetched[next_b] = (slots, self.mat.ready)
         self.graph_waited = False
         if self.skip:
             if keep:
@@ -262,7 +283,7 @@ class Rank:
 
     def _wait_graph(self):
         if not self.graph_waited:
-            self.mat.wait()
+            torch.cuda.current_stream(self.dev).wait_event(self.ready_ev)
             self.graph_waited = True
 
     def gcn_forward_pipelined(self, b, l):
@@ -348,6 +369,55 @@ class Rank:
             return _lib.Frame(self.s1v[t].data_ptr(), Ly.fp, 0, 0)
         return _lib.Frame(self.S_vm[l].data_ptr() + F32 * i * NP * Ly.fp, Ly.fp, 0, 0)
 
+    def gcn_aggregate_step(self, l, c):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        self._wait_graph()
+        s = self.slots[c]
+        call("dgnn_spmm_f32", eng.plan.N, ptr(s.rowptr), ptr(s.col), ptr(s.val),
+             self.own(self.Y_own[l - 1], Ly.fp, c), Ly.fp, self.own(self.S_own[l], Ly.fp, c),
+             _lib.stream_handle())
+
+    def gcn_dense_step(self, l, i):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        NP = eng.plan.NP
+        r_out = _lib.Frame(self.R_vm[l].data_ptr() + F32 * i * NP * Ly.rw, Ly.rw, 0, 0)
+        call("dgnn_gcn_forward", NP, None, None, None, self._split_input(l, i), Ly.fp,
+             ptr(eng.params.w(f"gcn{l}.w")), Ly.hg, int(self.skip), _lib.Frame(None, 0, 0, 0), r_out,
+             _lib.stream_handle())
+
+    def gcn_dense_backward_step(self, l, i):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        NP = eng.plan.NP
+        st = _lib.stream_handle()
+        dr = _lib.Frame(self.dR_vm[l].data_ptr() + F32 * i * NP * Ly.rw, Ly.rw, 0, 0)
+        r = _lib.Frame(self.R_vm[l].data_ptr() + F32 * i * NP * Ly.rw, Ly.rw, 0, 0)
+        call("dgnn_gcn_weight_grad", NP, self._split_input(l, i), dr, r, Ly.fp, Ly.hg, int(self.skip),
+             ptr(eng.params.gw(f"gcn{l}.w")), ptr(self.ws_tn), self.ws_tn.numel(), st)
+        if l > 0:
+            ds = _lib.Frame(self.dS_vm[l].data_ptr() + F32 * i * NP * Ly.fp, Ly.fp, 0, 0)
+            call("dgnn_gcn_backward_rows", NP, dr, r, Ly.fp, ptr(eng.params.w(f"gcn{l}.w")), Ly.hg,
+                 int(self.skip), ds, st)
+
+    def gcn_transpose_aggregate_step(self, l, c):
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        sl = self.slots[c]
+        call("dgnn_spmm_f32", eng.plan.N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val),
+             self.own(self.dS_own[l], Ly.fp, c), Ly.fp, self.own(self.dZ_own, Ly.fp, c), _lib.stream_handle())
+
+    def xchg_owned_step(self, own_buf, vm_buf, W, c):
+        """All-to-all of owned step c alone: slab q of the owner layout ->
+        vertex-major step p*C + c on rank q (async; returns the work)."""
+        import torch.distributed as dist
+        plan = self.eng.plan
+        P, C = plan.P, plan.chunk
+        ins = [self.own_slab_rows(own_buf, W, c, q) for q in range(P)]
+        outs = [self.vm(vm_buf, W, p * C + c) for p in range(P)]
+        return [dist.all_to_all(outs, ins, async_op=True)]
+
     def gcn_dense_forward(self, b, l):
         """Vertex side of the split GCN: r = relu([s, s W]) for every block
         step of this rank's vertex chunk (K3 without aggregation)."""
@@ -389,7 +459,7 @@ class Rank:
             call("dgnn_spmm_f32", eng.plan.N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val),
                  self.own(self.dS_own[l], Ly.fp, c), Ly.fp, self.own(self.dZ_own, Ly.fp, c), st)
 
-    def rnn_forward(self, b, l, pipelined=False):
+    def rnn_forward(self, b, l, pipelined=False, before_step=None):
         eng = self.eng
         Ly = eng.layout.layers[l]
         NP, B = eng.plan.NP, eng.plan.bsize
@@ -407,6 +477,8 @@ class Rank:
         ho = Ly.ho
         works = []
         for i in range(B):
+            if before_step is not None:
+                before_step(i)
             x = self.vm(self.R_vm[l], Ly.rw, i)
             h_out = self.vm(self.Y_vm[l], ho, i)
             c_out = self.vm(self.C_vm[l], ho, i) if self.keep else self.vm(self.cbuf[l], ho, i % 2)
@@ -515,6 +587,38 @@ class Rank:
         self._loss_grads(b, works if pipelined else None)
         return works
 
+    def loss_grads_split(self, b):
+        """Head seeds of every owned step (reverse order), each followed by
+        the all-to-all of that step alone; returns {c: works}."""
+        eng = self.eng
+        Ly = eng.layout.layers[-1]
+        out = {}
+        for c in reversed(range(len(self.ts))):
+            self._head_step(c, self.ts[c])
+            out[c] = self.xchg_owned_step(self.dZ_own, self.dY_vm, Ly.ho, c)
+        return out
+
+    def _head_step(self, c, t):
+        eng = self.eng
+        Ly = eng.layout.layers[-1]
+        st = _lib.stream_handle()
+        ep, C = eng.layout.ep, eng.cfg.classes
+        hw, hb = eng.params.w("head.w"), eng.params.w("head.b")
+        d = self.lab["train"].get(t)
+        dz = self.own(self.dZ_own, Ly.ho, c)
+        if d is None:
+            for q in range(eng.plan.P):
+                self.own_slab_rows(self.dZ_own, Ly.ho, c, q).zero_()
+            return
+        z = self.own(self.Y_own[-1], Ly.ho, c)
+        call("dgnn_head_loss_grad", d["n"], ptr(d["u"]), ptr(d["v"]), ptr(d["y"]), z, ep, C, ptr(hw),
+             ptr(hb), eng.scale, ptr(self.loss_pp), self.loss_pp.numel(), ptr(self.dlogits),
+             ptr(eng.params.gw("head.w")), ptr(eng.params.gw("head.b")), ptr(self.ws_head),
+             self.ws_head.numel(), st)
+        call("dgnn_sum_f64", d["n"], ptr(self.loss_pp), self.loss_t.data_ptr() + 8 * t, 0, st)
+        call("dgnn_head_scatter", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), ptr(self.dlogits), ptr(hw), ep, C,
+             dz, st)
+
     def _loss_grads(self, b, works):
         eng = self.eng
         Ly = eng.layout.layers[-1]
@@ -550,7 +654,7 @@ class Rank:
             if works is not None:
                 works += self._scatter_owned_step(self.dZ_own, self.dY_vm, Ly.ho, c)
 
-    def rnn_backward(self, b, l, pipelined=False):
+    def rnn_backward(self, b, l, pipelined=False, after_step=None, before_step=None):
         eng = self.eng
         Ly = eng.layout.layers[l]
         if not self.skip:
@@ -565,6 +669,8 @@ class Rank:
         dh_buf, dc_buf = self.dcarry[l]
         dh_in, dc_in = self.dstate[l]
         for step, i in enumerate(reversed(range(B))):
+            if before_step is not None:
+                before_step(i)
             dy = self.vm(self.dY_vm, ho, i)
             gates = self.vm(self.G_vm[l], 4 * ho, i)
             c_prev = self.vm(self.C_vm[l], ho, i - 1) if i > 0 else self.act[l][1]
@@ -582,6 +688,8 @@ class Rank:
             dh_in, dc_in = dh_out, dc_out
             if pipelined:
                 works += self._send_step_to_owner(self.dR_vm[l], self.dR_own[l], Ly.rw, i)
+            if after_step is not None:
+                works += after_step(i) or []
         self.dstate[l][0].copy_(dh_in)
         self.dstate[l][1].copy_(dc_in)
         # weight gradients over every (row, step) of the block (training.py:422-424)
@@ -743,6 +851,11 @@ class Engine:
         self.enc = encoding if encoding is not None else SnapshotEncoding(graph)
         self.fabric = fabric or LocalFabric()
         self.split = self.skip and self.plan.P > 1 and SPLIT_GCN == "1"
+        # one rank per GPU: per-step exchanges overlapping the split GCN / LSTM
+        # (measured, N = 2: 247 vs 260 ms per epoch; N = 4: 304 vs 264 -- at
+        # P > 2 the bulk all-to-alls win, so "auto" pipelines only at P = 2)
+        self.split_pipe = (self.split and self.fabric.distributed and cfg.classes == 2
+                           and (PIPELINED_EXCHANGE == "all" or (PIPELINED_EXCHANGE == "auto" and self.plan.P == 2)))
         self.bytes_moved = 0      # bytes that crossed the fabric (all ranks of this process)
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
@@ -752,7 +865,7 @@ class Engine:
             if dist.get_world_size() != workers:
                 raise ConfigError(f"workers={workers} but the process group has {dist.get_world_size()} ranks")
             ids = [dist.get_rank()]
-            if any(self._pipelining()):
+            if any(self._pipelining()) or self.split_pipe:
                 _lib.lib().dgnn_set_sm_reserve(SM_RESERVE)
         else:
             ids = list(range(workers))
@@ -804,12 +917,83 @@ class Engine:
         for w in works:
             w.wait()
 
+    def _moved(self, W):
+        plan = self.plan
+        self.bytes_moved += F32 * plan.chunk * plan.NP * W * (plan.P - 1)
+
+    def _split_layer_forward_pipelined(self, b, l, phase, comm):
+        """Split GCN + LSTM of layer l with per-step exchanges: owned step c's
+        s goes out (all-to-all of that step alone) as soon as its SpMM is
+        done, the dense transform + LSTM of block step i waits only for the
+        exchange carrying it, and each finished h step is sent to its owner
+        while the next step computes."""
+        (r,) = self.ranks
+        Ly = self.layout.layers[l]
+        C = self.plan.chunk
+        sw = []
+        if l > 0:
+            for c in range(C):
+                r.gcn_aggregate_step(l, c)
+                sw.append(r.xchg_owned_step(r.S_own[l], r.S_vm[l], Ly.fp, c))
+            self._moved(Ly.fp)
+        self._record_xchg(comm, phase, b, l)
+
+        def before(i):
+            if l > 0:
+                self._wait(sw[i % C])
+            r.gcn_dense_step(l, i)
+
+        works = r.rnn_forward(b, l, pipelined=True, before_step=before)
+        self._wait(works)
+        self._moved(Ly.ho)
+        self._record_xchg(comm, phase, b, l)
+
+    def _split_backward_pipelined(self, b, comm):
+        """Reverse sweep of block b with per-step exchanges: the head seeds of
+        each owned step (reverse step order) go out as soon as they are
+        written; per layer, the LSTM backward of block step i waits only for
+        the exchange carrying its dy, its dense GCN backward (dW, ds) follows
+        at once and ds is sent to the step's owner while the next step
+        computes; the owner's transpose SpMM of each owned step then feeds the
+        next layer's seeds the same way."""
+        (r,) = self.ranks
+        layers = self.layout.layers
+        C = self.plan.chunk
+        dyw = r.loss_grads_split(b)
+        self._moved(layers[-1].ho)
+        for l in reversed(range(len(layers))):
+            Ly = layers[l]
+            self._record_xchg(comm, "backward", b, l)
+
+            def before(i, dyw=dyw):
+                self._wait(dyw[i % C])
+
+            def after(i, l=l, Ly=Ly):
+                r.gcn_dense_backward_step(l, i)
+                if l > 0:
+                    return r._send_step_to_owner(r.dS_vm[l], r.dS_own[l], Ly.fp, i)
+                return []
+
+            works = r.rnn_backward(b, l, before_step=before, after_step=after)
+            self._wait(works)
+            self._record_xchg(comm, "backward", b, l)
+            if l > 0:
+                self._moved(Ly.fp)
+                dyw = {}
+                for c in reversed(range(C)):
+                    r.gcn_transpose_aggregate_step(l, c)
+                    dyw[c] = r.xchg_owned_step(r.dZ_own, r.dY_vm, Ly.fp, c)
+                self._moved(Ly.fp)
+
     def _layers_forward(self, b, phase, comm):
         layers = self.layout.layers
         # one rank per GPU: exchanges folded into the producing loops (P2P
         # sends of finished slabs / steps overlap the next kernel)
         pipe_gcn, pipe_lstm = self._pipelining()
         for l, Ly in enumerate(layers):
+            if self.split_pipe:
+                self._split_layer_forward_pipelined(b, l, phase, comm)
+                continue
             if self.split:
                 if l == 0:
                     self._record_xchg(comm, phase, b, l)     # s1 is local: nothing moves
@@ -850,7 +1034,7 @@ class Engine:
         self.params.zero_grad()
         for b in range(plan.nblk):
             for r in self.ranks:
-                r.begin_block(b, keep=False, ledger=transfer)
+                r.begin_block(b, keep=False, ledger=transfer, next_b=b + 1 if b + 1 < plan.nblk else b)
             self._layers_forward(b, "forward", comm)
             for r in self.ranks:
                 if self.cfg.classes != 2:
@@ -862,8 +1046,16 @@ class Engine:
             if act is not None:
                 act.alloc_activations(plan.bsize * 2 * L)
             for r in self.ranks:
-                r.begin_block(b, keep=True, ledger=transfer)
+                # the last rerun prefetches block 0 again: the next pass (the
+                # next epoch's forward sweep, or an evaluation) starts there
+                r.begin_block(b, keep=True, ledger=transfer, next_b=b - 1 if b > 0 else 0)
             self._layers_forward(b, "rerun", comm)
+            if self.split_pipe:
+                self._split_backward_pipelined(b, comm)
+                if act is not None:
+                    act.free_activations(plan.bsize * 2 * L)
+                    act.free_checkpoint(1.0)
+                continue
             pipe_gcn, pipe_lstm = self._pipelining()
             works = []
             for r in self.ranks:
@@ -923,7 +1115,8 @@ class Engine:
             r.reset_state()
         for b in range(plan.nblk):
             for r in self.ranks:
-                r.begin_block(b, keep=False, ledger=None, count_bytes=False)
+                r.begin_block(b, keep=False, ledger=None, count_bytes=False,
+                              next_b=b + 1 if b + 1 < plan.nblk else None)
             self._layers_forward(b, "eval", None)
             for r in self.ranks:
                 r.predict(b)
@@ -944,7 +1137,8 @@ class Engine:
             r.reset_state()
         for b in range(plan.nblk):
             for r in self.ranks:
-                r.begin_block(b, keep=False, ledger=None, count_bytes=False)
+                r.begin_block(b, keep=False, ledger=None, count_bytes=False,
+                              next_b=b + 1 if b + 1 < plan.nblk else None)
             self._layers_forward(b, "eval", None)
             for r in self.ranks:
                 for c, t in enumerate(r.ts):

@@ -202,7 +202,7 @@ class Materializer:
     """Device-side rebuild of the snapshots a rank owns, chunk by chunk."""
 
     def __init__(self, enc: SnapshotEncoding, device, slots: int, resident: bool = False,
-                 with_f64: bool = False):
+                 with_f64: bool = False, sets: int = 1):
         self.enc = enc
         self.device = torch.device(device)
         n = enc.n
@@ -236,21 +236,33 @@ class Materializer:
         self.ws_lap = torch.empty(query("dgnn_laplacian_workspace", n), dtype=torch.uint8,
                                   device=self.device)
         self.status = torch.zeros(4, **i32)
-        self.slots = []
-        for _ in range(slots):
-            self.slots.append(LapSlot(
-                torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
-                torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
-                torch.empty(cap_h, **f64) if with_f64 else None,
-                torch.empty(cap_h, **f64) if with_f64 else None))
+        # `sets` independent slot sets: with two, the next block's graph is
+        # rebuilt on the graph stream while the current block computes
+        self.sets = []
+        for _ in range(sets):
+            self.sets.append([])
+            self.slots = self.sets[-1]
+            for _ in range(slots):
+                self.slots.append(LapSlot(
+                    torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
+                    torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
+                    torch.empty(cap_h, **f64) if with_f64 else None,
+                    torch.empty(cap_h, **f64) if with_f64 else None))
+        self.slots = self.sets[0]
+        self.ready_sets = [torch.cuda.Event() for _ in range(sets)]
         self.bytes_h2d = 0
         self.bytes_full_equiv = 0
         self.ready = torch.cuda.Event()
 
-    def materialize(self, ts, ledger=None, count_bytes: bool = True):
-        """Rebuild Ahat_t for the contiguous run `ts` into slots 0..len(ts)-1.
-        Returns the slots; `self.ready` is recorded on the graph stream."""
+    def materialize(self, ts, ledger=None, count_bytes: bool = True, set_idx: int = 0, after=None):
+        """Rebuild Ahat_t for the contiguous run `ts` into slots 0..len(ts)-1
+        of slot set `set_idx`.  Returns the slots; the set's ready event (and
+        `self.ready`) is recorded on the graph stream.  `after`: an event
+        marking the end of the set's previous consumers (default: everything
+        already enqueued on the current stream)."""
         enc = self.enc
+        self.slots = self.sets[set_idx]
+        self.ready = self.ready_sets[set_idx]
         if len(ts) > len(self.slots):
             raise InputError("chunk longer than the materialiser's slot count")
         plan = enc.chunk(ts)
@@ -274,15 +286,14 @@ class Materializer:
                     vo, vc = plan.val_range
                     self.vals_dev[:vc].copy_(enc.vals[vo:vo + vc], non_blocking=True)
             gs.wait_stream(cs)
-        if count_bytes:
-            self.bytes_h2d += enc.chunk_bytes(ts)
-            self.bytes_full_equiv += enc.full_bytes(ts)
-        if ledger is not None:
-            enc.charge(ledger, ts)
+        self.account(ts, ledger, count_bytes)
         cur = 0
         voff = vbase
-        # slots are overwritten: wait for every consumer already enqueued on the compute stream
-        gs.wait_stream(torch.cuda.current_stream(self.device))
+        # slots are overwritten: wait for their consumers on the compute stream
+        if after is not None:
+            gs.wait_event(after)
+        else:
+            gs.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(gs):
             for i, t in enumerate(ts):
                 m = int(enc.nnz[t])
@@ -320,6 +331,16 @@ class Materializer:
                 s.a_rowptr, s.a_t_rowptr, s.t = a_rowptr, self.at_rowptr, t
             self.ready.record(gs)
         return self.slots[:len(ts)]
+
+    def account(self, ts, ledger=None, count_bytes: bool = True):
+        """Charge one streaming pass of `ts` (reference-equivalent ledger
+        counters, real H2D bytes).  Called when a pass consumes a chunk; a
+        chunk rebuilt ahead of its pass is charged by that pass."""
+        if count_bytes:
+            self.bytes_h2d += self.enc.chunk_bytes(ts)
+            self.bytes_full_equiv += self.enc.full_bytes(ts)
+        if ledger is not None:
+            self.enc.charge(ledger, ts)
 
     def wait(self, stream=None):
         (stream or torch.cuda.current_stream(self.device)).wait_event(self.ready)
