@@ -388,7 +388,8 @@ __global__ void dw_reduce_kernel(int nct, int M, int N, int K, const float* __re
     if (i < (int64_t)M * K) {
         const int k = (int)(i / M), j = (int)(i % M);
         double s = 0.0;
-        for (int c = 0; c < nct; ++c) s += (double)slots[((size_t)c * N + k) * M + j];
+#pragma unroll 16
+        for (int c = 0; c < nct; ++c) s += (double)__ldg(slots + ((size_t)c * N + k) * M + j);
         gw[(int64_t)k * ldg + j] += s;
     } else if (i < (int64_t)M * K + M && gb) {
         const int j = (int)(i - (int64_t)M * K);

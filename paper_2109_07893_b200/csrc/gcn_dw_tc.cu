@@ -264,7 +264,8 @@ __global__ void gdw_reduce_kernel(int nct, int ma, int n, int fp, int hp, const 
     if (i >= (int64_t)fp * hp) return;
     const int f = (int)(i / hp), h = (int)(i % hp);
     double s = 0.0;
-    for (int c = 0; c < nct; ++c) s += (double)slots[((size_t)c * n + f) * ma + h];
+#pragma unroll 16
+    for (int c = 0; c < nct; ++c) s += (double)__ldg(slots + ((size_t)c * n + f) * ma + h);
     gw[i] += s;
 }
 

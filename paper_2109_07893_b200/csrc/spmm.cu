@@ -66,6 +66,38 @@ __global__ void __launch_bounds__(256) spmm_f32_kernel(int32_t n, const int32_t*
         st4(frame_row<float>(out, row) + 4 * gl, gather_row(row, rp, col, val, x, gl));
 }
 
+// K3 for the 4-wide first layer (s = s1 rows, no aggregation): HP / 4 lanes
+// per row, each computing one float4 of q = s W in the same fmaf order as
+// gcn_fwd_kernel (bitwise equal) and storing it coalesced (a row-per-lane
+// layout would scatter 32 rows per store instruction).
+template <int HP, bool SKIP>
+__global__ void __launch_bounds__(256) gcn_fwd_narrow_kernel(int32_t n, dgnn_frame x, const float* __restrict__ w,
+                                                             dgnn_frame s_out, dgnn_frame r_out) {
+    constexpr int LPR = HP / 4 >= 32 ? 32 : HP / 4, RPW = 32 / LPR, QV = HP / (4 * LPR);
+    __shared__ float4 wsm4[HP];   // 4 x HP
+    for (int i = threadIdx.x; i < HP; i += blockDim.x) wsm4[i] = reinterpret_cast<const float4*>(w)[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, sub = lane / LPR, gl = lane % LPR;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = warp * RPW + sub; row < n; row += nwarps * RPW) {
+        const float4 sv = ldg4(frame_row<const float>(x, row));
+        float* rr = frame_row<float>(r_out, row);
+#pragma unroll
+        for (int i = 0; i < QV; ++i) {
+            const int c4 = gl + LPR * i;
+            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) fma4(q, comp(sv, kk), wsm4[kk * (HP / 4) + c4]);
+            st4(rr + (SKIP ? 4 : 0) + 4 * c4, relu4(q));
+        }
+        if (gl == 0) {
+            if (s_out.ptr) st4(frame_row<float>(s_out, row), sv);
+            if (SKIP) st4(rr, relu4(sv));
+        }
+    }
+}
+
 // K3: s = Ahat x (or x), q = s W, r = relu([s, q]) | relu(q)
 template <int FP, int HP, bool SKIP, bool AGG>
 __global__ void __launch_bounds__(256) gcn_fwd_kernel(int32_t n, const int32_t* __restrict__ rp,
@@ -197,6 +229,8 @@ int gcn_fwd_tc(int fp, int hp, bool skip, bool agg, int32_t n, const int32_t* rp
                const float* val, dgnn_frame x, const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st);
 int gcn_bwd_tc(int fp, int hp, bool skip, int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame ds,
                cudaStream_t st);
+int spmm_gather(int f, int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x,
+                dgnn_frame out, cudaStream_t st);
 
 }  // namespace dgnn
 
@@ -218,6 +252,14 @@ int spmm_f32_t(int32_t n, const int32_t* rp, const int32_t* col, const float* va
 template <int FP, int HP, bool SKIP, bool AGG>
 int gcn_fwd_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x, const float* w,
               dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+    if constexpr (FP == 4 && !AGG) {
+        constexpr int LPR = HP / 4 >= 32 ? 32 : HP / 4, RPW = 32 / LPR;
+        int64_t blocks = cdiv(cdiv(n, RPW), 8);
+        blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+        ::dgnn::note_launch();
+        gcn_fwd_narrow_kernel<HP, SKIP><<<(unsigned)blocks, 256, 0, st>>>(n, x, w, s_out, r_out);
+        return launch_status("gcn_forward (narrow)");
+    }
     constexpr int RW = 32 / (FP / 4);
     const size_t smem = (size_t)FP * HP * sizeof(float);
     auto k = gcn_fwd_kernel<FP, HP, SKIP, AGG>;
@@ -320,6 +362,10 @@ int dgnn_spmm_f32(int32_t n, const int32_t* rowptr, const int32_t* col, const fl
     DGNN_CHECK_ARG(n >= 0, "spmm_f32: negative size");
     if (n == 0) return DGNN_OK;
     cudaStream_t st = as_stream(stream);
+    if (dgnn_gcn_tensor_cores) {   // the K3 gather pipeline (bitwise the same sums)
+        const int rc = spmm_gather(f, n, rowptr, col, val, x, out, st);
+        if (rc >= 0) return rc;
+    }
     switch (f) {
         case 4: return spmm_f32_t<4>(n, rowptr, col, val, x, out, st);
         case 16: return spmm_f32_t<16>(n, rowptr, col, val, x, out, st);

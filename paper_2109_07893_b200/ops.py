@@ -308,6 +308,25 @@ def gcn_forward(n: int, rowptr: np.ndarray | None, col: np.ndarray | None, val: 
     return s_out.cpu().numpy(), r_out.cpu().numpy()
 
 
+def spmm_f32(rowptr: np.ndarray, col: np.ndarray, val: np.ndarray, x: np.ndarray, tensor_cores: bool = True):
+    """Test hook of `dgnn_spmm_f32` (fp32 CSR SpMM, core.py:142-152 order):
+    the K3 gather pipeline (default) or the SIMT kernel."""
+    dev = _dev()
+    n, f = rowptr.shape[0] - 1, x.shape[1]
+    xd = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(dev)
+    out = torch.full((n, f), np.nan, dtype=torch.float32, device=dev)
+    rp = _i32(rowptr, dev)
+    cd = _i32(col if len(col) else np.zeros(1), dev)
+    vd = torch.from_numpy(np.ascontiguousarray(val if len(val) else np.zeros(1), np.float32)).to(dev)
+    call("dgnn_set_gcn_tensor_cores", int(tensor_cores))
+    try:
+        call("dgnn_spmm_f32", n, ptr(rp), ptr(cd), ptr(vd), _lib.frame(xd, f), f, _lib.frame(out, f),
+             _lib.stream_handle())
+    finally:
+        call("dgnn_set_gcn_tensor_cores", 1)
+    return out.cpu().numpy()
+
+
 def gcn_backward(dr: np.ndarray, r: np.ndarray, s: np.ndarray, w: np.ndarray, skip: bool,
                  tensor_cores: bool = True, slabs: int = 0, rows_ds: bool = True):
     """Test hook of K4's row part and weight gradient (`dgnn_gcn_backward_rows`,

@@ -43,3 +43,31 @@ for fp, hp, skip in ((64, 64, True), (4, 64, True)):
             byts = 4 * n * ((fp + 2 * hp) if what == "dw" else (2 * rw + fp))
             print(f"fp={fp} hp={hp} tc={tc} {what}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s", flush=True)
 call("dgnn_set_gcn_tensor_cores", 1)
+
+# SpMM: gather pipeline (tcgen05 flag on) vs SIMT, avg degree ~1.6 (bench shape)
+rng = np.random.default_rng(0)
+nnz = int(1.62 * n)
+rows = np.sort(rng.integers(0, n, size=nnz))
+cols = rng.integers(0, n, size=nnz).astype(np.int32)
+rp = torch.from_numpy(np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n))]).astype(np.int32)).to(dev)
+cd = torch.from_numpy(cols).to(dev)
+vd = torch.rand(nnz, device=dev)
+for f in (64,):
+    x = torch.randn(n, f, device=dev)
+    out = torch.empty(n, f, device=dev)
+    for tc in (1, 0):
+        call("dgnn_set_gcn_tensor_cores", tc)
+        run = lambda: call("dgnn_spmm_f32", n, ptr(rp), ptr(cd), ptr(vd), _lib.frame(x, f), f, _lib.frame(out, f), st)
+        for _ in range(3):
+            run()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(20):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 20 * 1e3
+        byts = 4 * (n + 1) + 8 * nnz + 4 * f * nnz + 4 * n * f
+        print(f"spmm f={f} tc={tc}: {us:.1f} us  {byts / us / 1e3:.0f} GB/s (gather-incl.)", flush=True)
+call("dgnn_set_gcn_tensor_cores", 1)

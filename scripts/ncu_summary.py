@@ -58,6 +58,10 @@ def launches(tag: str) -> str:
         a[1] += d.get("gpu__time_duration.sum", 0.0)
         a[2] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
     total = sum(a[1] for a in agg.values())
+    import json
+    (ROOT / "profiles" / f"{tag}_traffic.json").write_text(json.dumps(
+        {name: {"launches": n, "avg_us": t / n / 1e3, "dram_bytes_per_launch": b / n}
+         for name, (n, t, b) in agg.items()}, indent=1, sort_keys=True) + "\n")
     lines = [f"# {tag}: launch list of one timed epoch (bench.py --steps 1 --warmup 1)", "",
              "`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
              "--clock-control none` over exactly the launches of the timed epoch. ncu serialises "

@@ -13,7 +13,7 @@ PY
 echo "launches per epoch: $N"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s $N -c $N --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo launches rc=$?
-for k in lstm_fwd_ws_kernel lstm_bwd_ws_kernel lstm_dw_tc_kernel gcn_fwd_kernel; do
+for k in lstm_fwd_ws_kernel lstm_bwd_ws_kernel lstm_dw_tc_kernel gcn_fwd_tc_kernel gcn_dw_tc_kernel head_loss_grad_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 6 -c 1 -o gpurun_out/full_$k $CMD \
       > gpurun_out/ncu_full_$k.log 2>&1; echo full $k rc=$?
 done

@@ -358,7 +358,8 @@ def test_warp_specialized_lstm_steps_match_tc_bitwise(H):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("fp,hp,skip,agg", [(64, 64, True, True), (32, 16, False, True), (16, 64, True, True),
-                                            (64, 32, False, True), (64, 64, True, False)])
+                                            (64, 32, False, True), (64, 64, True, False), (4, 64, True, False),
+                                            (4, 32, False, False)])
 def test_gcn_forward_tensor_cores(fp, hp, skip, agg):
     """K3 tcgen05 instance (gather warps + 3xTF32 transform) against fp64:
     ragged last tile, empty rows, and a hub row whose tile overflows the
@@ -430,3 +431,27 @@ def test_gcn_backward_tensor_cores(fp, hp, skip, slabs, n):
     assert np.array_equal(gw, gw3)
     if rows_ds:
         assert np.array_equal(ds, ds3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("f", [16, 32, 64])
+def test_spmm_f32_gather_pipeline_bitwise(f):
+    """dgnn_spmm_f32 on the K3 gather pipeline (aggregation-only instance)
+    is bitwise the SIMT kernel: same fp32 FMA chain per row in edge order;
+    empty rows, a hub row past the staged-index capacity, ragged tail."""
+    from paper_2109_07893_b200.ops import spmm_f32
+    rng = np.random.default_rng(f)
+    n = 148 * 128 * 5 + 13          # several tiles per persistent CTA
+    deg = rng.integers(0, 5, size=n)
+    deg[4321] = 2500
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, size=rows.size).astype(np.int32)
+    val = rng.uniform(-1, 1, size=rows.size).astype(np.float32)
+    rowptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    x = rng.standard_normal((n, f)).astype(np.float32)
+    a = spmm_f32(rowptr, cols, val, x)
+    b = spmm_f32(rowptr, cols, val, x, tensor_cores=False)
+    assert np.array_equal(a, b)
+    ref = np.zeros((n, f))
+    np.add.at(ref, rows, val.astype(np.float64)[:, None] * x.astype(np.float64)[cols])
+    assert np.abs(a - ref).max() <= 1e-5 * np.abs(ref).max()
