@@ -87,14 +87,11 @@ struct GtcLayout {
     static constexpr int TMEM_COLS = 2 * HP <= 32 ? 32 : (2 * HP <= 64 ? 64 : 128);
 };
 
-template <int FP, int HP, bool SKIP, bool AGG, bool BWD, bool SONLY = false>
+template <int FP, int HP, bool SKIP, bool AGG, bool BWD>
 __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const float* __restrict__ val,
     dgnn_frame x, const float* __restrict__ w, dgnn_frame s_out, dgnn_frame r_out, dgnn_frame mk) {
     static_assert(!(BWD && AGG), "the backward instance has no aggregation");
-    // SONLY: aggregation only (s = Ahat x into s_out, the SpMM of dgnn_spmm_f32):
-    // the gather warps and the index ring run, the tensor-core half idles
-    static_assert(!SONLY || (AGG && !SKIP && !BWD), "SONLY is a plain aggregation");
     using L = GtcLayout<FP, HP>;
     // BWD: x = dr, mk = r (mask source), r_out = ds; dq sits at column
     // offset F (= HP) of dr / r in the skip layer
@@ -112,7 +109,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
 
     // W image: B[j][k] = W[k][j] (forward; BWD: W[j][k]), tf32 hi / lo, SW64
     // K-major chunks of 16 k
-    for (int i = threadIdx.x; i < (SONLY ? 0 : HP * FP / 4); i += gtc::THREADS) {
+    for (int i = threadIdx.x; i < HP * FP / 4; i += gtc::THREADS) {
         const int j = i / (FP / 4), k4 = i % (FP / 4);
         const int k = 4 * k4;
         const float4 v = BWD ? *reinterpret_cast<const float4*>(w + j * FP + k)
@@ -157,7 +154,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             const int s = it % gtc::ASTAGES, si = it % gtc::ISTAGES;
             const GtcIdx& ix = idx[si];
             if (AGG) mbar_wait_sleep(&bars->ifull[si], (it / gtc::ISTAGES) & 1);
-            if (!SONLY && it >= gtc::ASTAGES) mbar_wait_sleep(&bars->empty[s], ((it / gtc::ASTAGES) - 1) & 1);
+            if (it >= gtc::ASTAGES) mbar_wait_sleep(&bars->empty[s], ((it / gtc::ASTAGES) - 1) & 1);
             const uint32_t a_hi = sb + s * L::A_STAGE, a_lo = a_hi + L::A_HALF;
             const bool spill = AGG && ix.spill;
             // BWD skip: the skip term dpre[:, :F] of this tile's rows goes to ds
@@ -185,13 +182,11 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             // dynamically, so warps that drew short rows take more of them
             // and the tile completes together.  Every warp makes exactly one
             // failing claim per tile, so use k of stage s starts its claims
-            // at k (NCHUNK + NGATHER): the counter never needs a reset.  The
-            // stage's barrier ring keeps warps from running a use ahead: the A
-            // ring (empty[s]) normally, the index ring in the aggregation-only
-            // instance (no A ring).
+            // at k (NCHUNK + NGATHER): the counter never needs a reset (the
+            // A ring's empty[s] keeps every warp within one use of stage s).
             constexpr int CROWS = 2 * RW, NCHUNK = gtc::BM / CROWS;
-            const int cslot = SONLY ? si : s;
-            const int cbase = (int)(it / (SONLY ? gtc::ISTAGES : gtc::ASTAGES)) * (NCHUNK + gtc::NGATHER);
+            const int cslot = s;
+            const int cbase = (int)(it / gtc::ASTAGES) * (NCHUNK + gtc::NGATHER);
             for (;;) {
                 int chunk = 0;
                 if (lane == 0) chunk = atomicAdd(&bars->claim[cslot], 1) - cbase;
@@ -260,7 +255,6 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                             reinterpret_cast<float4*>(frame_row<float>(r_out, row))[gl] = make_float4(
                                 fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
                     }
-                    if (SONLY) continue;
                     float4 hi, lo;
                     split4(acc, hi, lo);
                     const int k = 4 * gl;
@@ -273,7 +267,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             if (BWD && SKIP) mbar_arrive(&bars->skipready[it & 1]);   // every lane: releases its ds stores
             __syncwarp();
             if (lane == 0) {
-                if (!SONLY) mbar_arrive(&bars->full[s]);
+                mbar_arrive(&bars->full[s]);
                 if (AGG) mbar_arrive(&bars->iempty[si]);
             }
         }
@@ -305,8 +299,6 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 if (lane == 0) mbar_arrive(&bars->ifull[si]);   // release: the stores above happen-before
             }
         }
-    } else if (SONLY) {
-        // no tensor-core work
     } else if (warp == gtc::MMA_WARP) {
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(gtc::BM, HP);
@@ -392,11 +384,11 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     if (warp == gtc::MMA_WARP) tmem_dealloc(bars->tmem, L::TMEM_COLS);
 }
 
-template <int FP, int HP, bool SKIP, bool AGG, bool BWD = false, bool SONLY = false>
+template <int FP, int HP, bool SKIP, bool AGG, bool BWD = false>
 int gcn_fwd_tc_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x, const float* w,
                  dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st, dgnn_frame mk = dgnn_frame{}) {
     using L = GtcLayout<FP, HP>;
-    auto k = gcn_fwd_tc_kernel<FP, HP, SKIP, AGG, BWD, SONLY>;
+    auto k = gcn_fwd_tc_kernel<FP, HP, SKIP, AGG, BWD>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     const int ntiles = (int)cdiv(n, gtc::BM);
     const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();
@@ -436,18 +428,6 @@ int gcn_bwd_tc(int fp, int hp, bool skip, int32_t n, dgnn_frame dr, dgnn_frame r
     GTB_CASE(32, 16) GTB_CASE(32, 32) GTB_CASE(32, 64)
     GTB_CASE(64, 16) GTB_CASE(64, 32) GTB_CASE(64, 64)
 #undef GTB_CASE
-    return -1;
-}
-
-// SpMM (dgnn_spmm_f32) on the K3 gather pipeline; -1 when the width has none
-int spmm_gather(int f, int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x,
-                dgnn_frame out, cudaStream_t st) {
-    const dgnn_frame none{};
-    switch (f) {
-        case 16: return gcn_fwd_tc_t<16, 16, false, true, false, true>(n, rp, col, val, x, nullptr, out, none, st);
-        case 32: return gcn_fwd_tc_t<32, 16, false, true, false, true>(n, rp, col, val, x, nullptr, out, none, st);
-        case 64: return gcn_fwd_tc_t<64, 16, false, true, false, true>(n, rp, col, val, x, nullptr, out, none, st);
-    }
     return -1;
 }
 

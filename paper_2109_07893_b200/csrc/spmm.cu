@@ -229,8 +229,7 @@ int gcn_fwd_tc(int fp, int hp, bool skip, bool agg, int32_t n, const int32_t* rp
                const float* val, dgnn_frame x, const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st);
 int gcn_bwd_tc(int fp, int hp, bool skip, int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame ds,
                cudaStream_t st);
-int spmm_gather(int f, int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x,
-                dgnn_frame out, cudaStream_t st);
+
 
 }  // namespace dgnn
 
@@ -362,10 +361,6 @@ int dgnn_spmm_f32(int32_t n, const int32_t* rowptr, const int32_t* col, const fl
     DGNN_CHECK_ARG(n >= 0, "spmm_f32: negative size");
     if (n == 0) return DGNN_OK;
     cudaStream_t st = as_stream(stream);
-    if (dgnn_gcn_tensor_cores) {   // the K3 gather pipeline (bitwise the same sums)
-        const int rc = spmm_gather(f, n, rowptr, col, val, x, out, st);
-        if (rc >= 0) return rc;
-    }
     switch (f) {
         case 4: return spmm_f32_t<4>(n, rowptr, col, val, x, out, st);
         case 16: return spmm_f32_t<16>(n, rowptr, col, val, x, out, st);

@@ -435,10 +435,10 @@ def test_gcn_backward_tensor_cores(fp, hp, skip, slabs, n):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("f", [16, 32, 64])
-def test_spmm_f32_gather_pipeline_bitwise(f):
-    """dgnn_spmm_f32 on the K3 gather pipeline (aggregation-only instance)
-    is bitwise the SIMT kernel: same fp32 FMA chain per row in edge order;
-    empty rows, a hub row past the staged-index capacity, ragged tail."""
+def test_spmm_f32_large(f):
+    """dgnn_spmm_f32 (K4 aggregation) at several rows per warp: run-to-run
+    bitwise reproducible and within fp32 rounding of the fp64 sum; empty
+    rows, a hub row, ragged tail."""
     from paper_2109_07893_b200.ops import spmm_f32
     rng = np.random.default_rng(f)
     n = 148 * 128 * 5 + 13          # several tiles per persistent CTA
