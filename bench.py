@@ -35,13 +35,35 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-N_PER_GPU = 750_000
-EDGES_PER_GPU = 468_750
-T = 32
-HIDDEN = 64
-CHURN = 0.10
+# workloads: c2 = BASELINE configs[1] (the default, the headline line);
+# c3 = configs[2] (TM-GCN, banded M-product, AMLSim-style graph), run with
+# --config c3 for the DESIGN table (strong scaling: the whole graph is split
+# over the GPUs)
+CONFIGS = {
+    "c2": dict(arch="cd-gcn", n=750_000, m=468_750, T=32, hidden=64, churn=0.10, nblk=4, gen="churn",
+               scaling="weak",
+               workload="configs[1] Epinions-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=64, "
+                        "N=750k/GPU, T=32, 468,750 edges/snapshot/GPU (15M/GPU total), 10% churn"),
+    "c3": dict(arch="tm-gcn", n=1_000_000, m=2_000_000, T=64, hidden=32, churn=0.02, nblk=8, gen="aml",
+               scaling="strong",
+               workload="configs[2] TM-GCN (plain GCN + banded M-product, window 2) hidden=32 on an "
+                        "AMLSim-style transaction graph: N=1M, T=64, 2M edges/snapshot (128M total), "
+                        "heavy-tailed degrees, 2% churn"),
+}
+CFG = CONFIGS["c2"]
+N_PER_GPU = CFG["n"]
+EDGES_PER_GPU = CFG["m"]
+T = CFG["T"]
+HIDDEN = CFG["hidden"]
+CHURN = CFG["churn"]
 THETA = 0.10
-NBLK = 4
+NBLK = CFG["nblk"]
+
+
+def select_config(name):
+    global CFG, N_PER_GPU, EDGES_PER_GPU, T, HIDDEN, CHURN, NBLK
+    CFG = CONFIGS[name]
+    N_PER_GPU, EDGES_PER_GPU, T, HIDDEN, CHURN, NBLK = (CFG[k] for k in ("n", "m", "T", "hidden", "churn", "nblk"))
 METRIC = "training epoch time and edges·snapshots/sec at 1/2/4/8 B200; SpMM HBM GB/s"
 
 
@@ -113,12 +135,17 @@ class ClockSampler:
 # workload
 
 
+def scale_of(P: int) -> int:
+    return P if CFG["scaling"] == "weak" else 1
+
+
 def make_workload(P: int, seed: int = 1):
     import paper_2109_07893_b200 as pk
-    from paper_2109_07893_b200.synth import churn_graph, sample_pairs_fast
-    n = N_PER_GPU * P
-    g = churn_graph(n, T, EDGES_PER_GPU * P, CHURN, seed=seed)
-    cfg = pk.ModelConfig("cd-gcn", in_features=2, hidden_features=HIDDEN, embed_features=HIDDEN)
+    from paper_2109_07893_b200.synth import aml_graph, churn_graph, sample_pairs_fast
+    n = N_PER_GPU * scale_of(P)
+    gen = churn_graph if CFG["gen"] == "churn" else aml_graph
+    g = gen(n, T, EDGES_PER_GPU * scale_of(P), CHURN, seed=seed)
+    cfg = pk.ModelConfig(CFG["arch"], in_features=2, hidden_features=HIDDEN, embed_features=HIDDEN)
     data = pk.prepare_training_data(cfg, g)
     train, _ = sample_pairs_fast(g, THETA, seed + 1000003)
     params = pk.init_params(cfg, 0)
@@ -242,11 +269,14 @@ def run_ours(args):
     cfg, g, data, train, params = make_workload(P)
     prep_s = time.time() - t0
     fabric = NcclFabric() if P > 1 else LocalFabric()
-    eng = Engine(cfg, g, P, NBLK, resident=True, fabric=fabric)
+    eng = Engine(cfg, data.graph, P, NBLK, resident=True, fabric=fabric,
+                 m_matrix=None if data.m_matrix is None else np.asarray(data.m_matrix.matrix),
+                 feats_host=None if cfg.architecture == "cd-gcn"
+                 else [np.asarray(f, np.float64) for f in data.feats.frames])
     eng.set_labels(train.by_time, None)
     eng.params.load(params)
     count = train.total_pairs()
-    total_es = int(sum(s.nnz for s in g.snapshots))     # whole job: edge*snapshots per epoch
+    total_es = int(sum(s.nnz for s in g.snapshots))     # whole job: edge*snapshots per epoch (raw graph)
 
     def step():
         loss_dev, grads = eng.epoch(None, None, None, count, "mean")
@@ -325,7 +355,7 @@ def run_ours(args):
     # SpMM (fused GCN forward with aggregation, layer 1) HBM rate
     spmm = None
     sl = [(d, a) for d, a in durs.get("dgnn_gcn_forward", []) if a[1] is not None]
-    if sl:
+    if sl and cfg.architecture == "cd-gcn":
         r0 = eng.ranks[0]
         nnz_mean = float(np.mean(eng.enc.nnz_hat))
         Ly = eng.layout.layers[1]
@@ -389,12 +419,11 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": total_es / (ms / 1e3), "unit": "edge*snapshots/s", "n_gpus": P,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (fp64 graph values / master weights)",
+            "scaling": CFG["scaling"], "vs_baseline": None, "dtype": "fp32 (fp64 graph values / master weights)",
             "data": "synthetic exact-churn dynamic graph, random-init weights",
-            "config": {"workload": "configs[1] Epinions-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=64, "
-                                   "N=750k/GPU, T=32, 468,750 edges/snapshot/GPU (15M/GPU total), 10% churn",
-                       "model": "cd-gcn", "num_vertices": N_PER_GPU * P, "num_timesteps": T,
-                       "edges_per_snapshot": EDGES_PER_GPU * P, "hidden": HIDDEN, "nblk": NBLK,
+            "config": {"workload": CFG["workload"],
+                       "model": CFG["arch"], "num_vertices": N_PER_GPU * scale_of(P), "num_timesteps": T,
+                       "edges_per_snapshot": EDGES_PER_GPU * scale_of(P), "hidden": HIDDEN, "nblk": NBLK,
                        "theta": THETA, "train_pairs": count, "parallelism": f"snapshot-partitioned x{P}",
                        "l2": "inputs larger than L2 (per-epoch working set ~tens of GB)",
                        "graph_in_timed_region": "delta-encoded graph resident in HBM, CSR/Laplacian "
@@ -431,9 +460,10 @@ def cpu_baseline(sample_scale: int = 128, threads: bool = True, steps: int = 1, 
     import dtgnn_oracle as O
     from paper_2109_07893_b200.synth import churn_keys
     n, m = cpu_sample(sample_scale)
-    keys = churn_keys(n, T, m, CHURN, seed=1)
+    from paper_2109_07893_b200.synth import aml_keys
+    keys = (churn_keys if CFG["gen"] == "churn" else aml_keys)(n, T, m, CHURN, seed=1)
     snaps = [O.Coo(n, k // n, k % n, np.ones(k.shape[0])) for k in keys]
-    cfg = O.Cfg("cd-gcn", 2, HIDDEN, HIDDEN)
+    cfg = O.Cfg(CFG["arch"], 2, HIDDEN, HIDDEN)
     Pp = O.prepare(cfg, snaps)
     train, _ = O.sample_labels(snaps, THETA, 1 + 1000003)
     params = O.init_params(cfg, 0)
@@ -460,9 +490,9 @@ def cpu_baseline(sample_scale: int = 128, threads: bool = True, steps: int = 1, 
     return {"value": es / dt, "unit": "edge*snapshots/s", "cores": workers, "kind": "port",
             "seconds_per_epoch": dt, "cpu_utilisation": util, "host_cpus": cores,
             "sample": f"oracle port (numpy fp64 restatement of dtgnn distributed_epoch, threads scheduler, "
-                      f"P={workers}) + Adam on the configs[1] shape scaled 1/{sample_scale}: N={n}, T={T}, "
-                      f"{m} edges/snapshot, 10% churn, cd-gcn H={HIDDEN}, nblk={NBLK}; metric is linear in "
-                      f"N and nnz"}
+                      f"P={workers}) + Adam on the {CFG['workload'].split(':')[0]} shape scaled 1/{sample_scale}: "
+                      f"N={n}, T={T}, {m} edges/snapshot, {CHURN:.0%} churn, {CFG['arch']} H={HIDDEN}, "
+                      f"nblk={NBLK}; metric is linear in N and nnz"}
 
 
 def run_reference(args):
@@ -473,10 +503,9 @@ def run_reference(args):
     cb = cpu_baseline(sample_scale=args.cpu_scale_ref, threads=True, steps=args.steps, warmup=args.warmup)
     line = {"metric": METRIC, "value": cb["value"], "unit": "edge*snapshots/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_epoch"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+            "higher_is_better": True, "scaling": CFG["scaling"], "vs_baseline": None, "dtype": "fp64",
             "data": "synthetic exact-churn dynamic graph, random-init weights",
-            "config": {"workload": "configs[1] Epinions-scale cd-gcn hidden=64 (CPU sample, see cpu_baseline)",
-                       "model": "cd-gcn"},
+            "config": {"workload": CFG["workload"] + " (CPU sample, see cpu_baseline)", "model": CFG["arch"]},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "edge*snapshots/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -494,7 +523,10 @@ def main():
     ap.add_argument("--timeline", action="store_true", help="per-stream busy / idle breakdown (diagnostic)")
     ap.add_argument("--cpu-scale", type=int, default=128)
     ap.add_argument("--cpu-scale-ref", type=int, default=256)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2",
+                    help="workload (c2: the headline configs[1] line; c3: TM-GCN configs[2])")
     args = ap.parse_args()
+    select_config(args.config)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -24,12 +24,14 @@ import numpy as np
 from .graph import DynamicGraph, SparseMatrix
 
 
-def _draw_absent(rng, space: int, count: int, taken_sorted: np.ndarray) -> np.ndarray:
-    """`count` distinct keys from [0, space) not in `taken_sorted`, in draw order."""
+def _draw_absent(rng, space: int, count: int, taken_sorted: np.ndarray, sampler=None) -> np.ndarray:
+    """`count` distinct keys from [0, space) not in `taken_sorted`, in draw
+    order; `sampler(rng, size)` draws candidate keys (default: uniform)."""
     got = np.zeros(0, dtype=np.int64)
     while got.shape[0] < count:
         need = count - got.shape[0]
-        cand = rng.integers(0, space, size=max(64, 2 * need + 16), dtype=np.int64)
+        size = max(64, 2 * need + 16)
+        cand = sampler(rng, size) if sampler is not None else rng.integers(0, space, size=size, dtype=np.int64)
         _, first = np.unique(cand, return_index=True)
         cand = cand[np.sort(first)]                      # distinct, draw order kept
         if taken_sorted.size:
@@ -61,6 +63,43 @@ def churn_keys(num_vertices: int, num_timesteps: int, edges_per_snapshot: int,
         cur = np.sort(np.concatenate([cur[keep], ins]))
         out.append(cur)
     return out
+
+
+def aml_keys(num_vertices: int, num_timesteps: int, edges_per_snapshot: int, churn: float, seed: int,
+             gamma: float = 2.5) -> list:
+    """AMLSim-style transaction graph (BASELINE configs[2]): account degrees
+    are heavy-tailed -- both endpoints are drawn by rank r = floor(n u^gamma)
+    (u uniform; gamma = 2.5 gives the top 1% of accounts ~16% of the edges
+    and hubs ~1000x the mean degree) through a seeded random relabelling -- and transactions
+    persist: each step replaces `churn` of the edges with new draws from the
+    same distribution.  Sorted int64 key arrays, one per timestep."""
+    n, m = int(num_vertices), int(edges_per_snapshot)
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n).astype(np.int64)
+
+    def sampler(rng, size):
+        ru = np.minimum((n * rng.random(size) ** gamma).astype(np.int64), n - 1)
+        rv = np.minimum((n * rng.random(size) ** gamma).astype(np.int64), n - 1)
+        return perm[ru] * n + perm[rv]
+
+    cur = np.sort(_draw_absent(rng, n * n, m, np.zeros(0, np.int64), sampler))
+    out = [cur]
+    k = int(round(churn * m))
+    for _ in range(1, num_timesteps):
+        drop = rng.choice(cur.shape[0], size=k, replace=False)
+        keep = np.ones(cur.shape[0], dtype=bool)
+        keep[drop] = False
+        ins = _draw_absent(rng, n * n, k, cur, sampler)
+        cur = np.sort(np.concatenate([cur[keep], ins]))
+        out.append(cur)
+    return out
+
+
+def aml_graph(num_vertices: int, num_timesteps: int, edges_per_snapshot: int, churn: float, seed: int,
+              gamma: float = 2.5) -> DynamicGraph:
+    n = int(num_vertices)
+    return DynamicGraph(n, [SparseMatrix.from_canonical(n, k // n, k % n, None)
+                            for k in aml_keys(n, num_timesteps, edges_per_snapshot, churn, seed, gamma)])
 
 
 def churn_graph(num_vertices: int, num_timesteps: int, edges_per_snapshot: int,
