@@ -56,6 +56,10 @@ SM_RESERVE = int(os.environ.get("DGNN_SM_RESERVE", "32"))
 # CommLedger still records the reference's schedule (dist.py:548-574);
 # `Engine.bytes_moved` counts what actually crossed the fabric.
 SPLIT_GCN = os.environ.get("DGNN_SPLIT_GCN", "1")
+# multi-GPU exchange transport of the split GCN: "peer" = copy-engine pushes
+# into symmetric (NVLink peer) memory, per block, overlapping compute;
+# "nccl" = NCCL all-to-alls (bulk, or per step at P = 2)
+EXCHANGE = os.environ.get("DGNN_EXCHANGE", "peer")
 
 
 class Plan:
@@ -109,21 +113,25 @@ class Rank:
         L = len(layers)
         # snapshot-major (owner layout) and vertex-major buffers
         self.R_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
-        self.Y_own = [_zeros(P * C * NP * Ly.ho, device=dev) for Ly in layers]
+        # receive buffers of the peer (copy-engine) exchange live in one
+        # symmetric allocation, same offsets on every rank
+        peer = eng.peer
+        recv = (lambda n: peer.alloc(n)) if peer is not None else (lambda n: _zeros(n, device=dev))
+        self.Y_own = [recv(P * C * NP * Ly.ho) for Ly in layers]
         self.S_own = [None] + [_zeros(C * N * Ly.fp, device=dev) for Ly in layers[1:]]
         same = P == 1
         self.split = eng.split
         if self.split:
             # S_own is in the owner layout [P][C][NP][fp] (all-to-all ready)
-            self.S_vm = [None] + [_zeros(B * NP * Ly.fp, device=dev) for Ly in layers[1:]]
+            self.S_vm = [None] + [recv(B * NP * Ly.fp) for Ly in layers[1:]]
             self.dS_vm = [None] + [_zeros(B * NP * Ly.fp, device=dev) for Ly in layers[1:]]
-            self.dS_own = [None] + [_zeros(P * C * NP * Ly.fp, device=dev) for Ly in layers[1:]]
+            self.dS_own = [None] + [recv(P * C * NP * Ly.fp) for Ly in layers[1:]]
             self.s1v = {}   # s1[t] rows of this rank's vertex chunk, every t
         self.R_vm = self.R_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
         self.Y_vm = self.Y_own if same else [_zeros(B * NP * Ly.ho, device=dev) for Ly in layers]
         wmax = max(Ly.ho for Ly in layers)
         self.dZ_own = _zeros(P * C * NP * wmax, device=dev)
-        self.dY_vm = self.dZ_own if same else _zeros(B * NP * wmax, device=dev)
+        self.dY_vm = self.dZ_own if same else recv(B * NP * wmax)
         self.dR_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
         self.dR_vm = self.dR_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
         self.dS = _zeros(N * max(Ly.fp for Ly in layers), device=dev)
@@ -459,7 +467,7 @@ class Rank:
             call("dgnn_spmm_f32", eng.plan.N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val),
                  self.own(self.dS_own[l], Ly.fp, c), Ly.fp, self.own(self.dZ_own, Ly.fp, c), st)
 
-    def rnn_forward(self, b, l, pipelined=False, before_step=None):
+    def rnn_forward(self, b, l, pipelined=False, before_step=None, after_step=None):
         eng = self.eng
         Ly = eng.layout.layers[l]
         NP, B = eng.plan.NP, eng.plan.bsize
@@ -488,6 +496,8 @@ class Rank:
             h_prev, c_prev = h_out, c_out
             if pipelined:
                 works += self._send_step_to_owner(self.Y_vm[l], self.Y_own[l], ho, i)
+            if after_step is not None:
+                after_step(i)
         if not self.keep:
             self.state[l][0].copy_(h_prev)
             self.state[l][1].copy_(c_prev)
@@ -851,10 +861,23 @@ class Engine:
         self.enc = encoding if encoding is not None else SnapshotEncoding(graph)
         self.fabric = fabric or LocalFabric()
         self.split = self.skip and self.plan.P > 1 and SPLIT_GCN == "1"
+        # one rank per GPU, split GCN: blocks pushed by the copy engines into
+        # peer memory as soon as they are produced (peer.py)
+        self.peer = None
+        if (self.split and self.fabric.distributed and EXCHANGE == "peer" and cfg.classes == 2):
+            from .peer import PeerExchange
+            lay = ParamLayout(cfg)
+            Pn, Cn, Bn, NPn = self.plan.P, self.plan.chunk, self.plan.bsize, self.plan.NP
+            wmax = max(Ly.ho for Ly in lay.layers)
+            need = sum(Pn * Cn * NPn * Ly.ho + 64 for Ly in lay.layers)
+            need += sum(Bn * NPn * Ly.fp + Pn * Cn * NPn * Ly.fp + 128 for Ly in lay.layers[1:])
+            need += Bn * NPn * wmax + 64
+            self.peer = PeerExchange(torch.device(device) if device is not None else
+                                     torch.device("cuda", torch.cuda.current_device()), need)
         # one rank per GPU: per-step exchanges overlapping the split GCN / LSTM
         # (measured, N = 2: 247 vs 260 ms per epoch; N = 4: 304 vs 264 -- at
         # P > 2 the bulk all-to-alls win, so "auto" pipelines only at P = 2)
-        self.split_pipe = (self.split and self.fabric.distributed and cfg.classes == 2
+        self.split_pipe = (self.split and self.fabric.distributed and cfg.classes == 2 and self.peer is None
                            and (PIPELINED_EXCHANGE == "all" or (PIPELINED_EXCHANGE == "auto" and self.plan.P == 2)))
         self.bytes_moved = 0      # bytes that crossed the fabric (all ranks of this process)
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -948,6 +971,107 @@ class Engine:
         self._moved(Ly.ho)
         self._record_xchg(comm, phase, b, l)
 
+    # ------------------------------------------- peer (copy-engine) exchanges
+    def _ch(self, kind, l, i):
+        """Signal channel of block step i of exchange `kind` at layer l
+        (channel 0 is the barrier)."""
+        L, B = len(self.layout.layers), self.plan.bsize
+        return 1 + (kind * L + l) * B + i
+
+    def _peer_layer_forward(self, b, l, phase, comm):
+        """Layer l of a forward pass with per-block pushes: the owner waits for
+        every rank's h block of an owned step, aggregates it and pushes the
+        s blocks out; each vertex rank waits for the s block of a step right
+        before its dense transform + LSTM step, and pushes the finished h
+        block to the step's owner."""
+        (r,) = self.ranks
+        peer, plan = self.peer, self.plan
+        Ly = self.layout.layers[l]
+        P, C, me = plan.P, plan.chunk, r.q
+        Y, S = 0, 1
+        if l > 0:
+            prev = self.layout.layers[l - 1]
+            for c in range(C):
+                j = me * C + c
+                for q in range(P):
+                    peer.wait(q, self._ch(Y, l - 1, j))
+                r.gcn_aggregate_step(l, c)
+                for k in range(P):
+                    q = (me + k) % P
+                    peer.push(r.own_slab_rows(r.S_own[l], Ly.fp, c, q), r.vm(r.S_vm[l], Ly.fp, j), q,
+                              self._ch(S, l, j))
+            self.bytes_moved += F32 * C * plan.NP * Ly.fp * (P - 1)
+        self._record_xchg(comm, phase, b, l)
+
+        def before(i):
+            if l > 0:
+                peer.wait(i // C, self._ch(S, l, i))
+            r.gcn_dense_step(l, i)
+
+        def after(i):
+            p, c = i // C, i % C
+            peer.push(r.vm(r.Y_vm[l], Ly.ho, i), r.own_slab_rows(r.Y_own[l], Ly.ho, c, me), p, self._ch(Y, l, i))
+
+        r.rnn_forward(b, l, before_step=before, after_step=after)
+        self.bytes_moved += F32 * C * plan.NP * Ly.ho * (P - 1)
+        self._record_xchg(comm, phase, b, l)
+        if l == len(self.layout.layers) - 1:
+            # the head reads Y_own of the last layer: wait for every h block
+            for c in range(C):
+                for q in range(P):
+                    peer.wait(q, self._ch(Y, l, me * C + c))
+            peer.drain()
+
+    def _peer_backward(self, b, comm):
+        """Reverse sweep of block b with per-block pushes (dy seeds from the
+        owner, ds back to the owner after each LSTM + dense backward step,
+        transpose SpMMs of owned steps feeding the next layer's seeds)."""
+        (r,) = self.ranks
+        peer, plan = self.peer, self.plan
+        layers = self.layout.layers
+        P, C, me = plan.P, plan.chunk, r.q
+        DY, DS = 2, 3
+        top = layers[-1]
+        for c in reversed(range(C)):
+            j = me * C + c
+            r._head_step(c, r.ts[c])
+            for k in range(P):
+                q = (me + k) % P
+                peer.push(r.own_slab_rows(r.dZ_own, top.ho, c, q), r.vm(r.dY_vm, top.ho, j), q,
+                          self._ch(DY, len(layers) - 1, j))
+        self.bytes_moved += F32 * C * plan.NP * top.ho * (P - 1)
+        for l in reversed(range(len(layers))):
+            Ly = layers[l]
+            self._record_xchg(comm, "backward", b, l)
+
+            def before(i, l=l, Ly=Ly):
+                peer.wait(i // C, self._ch(DY, l, i))
+
+            def after(i, l=l, Ly=Ly):
+                r.gcn_dense_backward_step(l, i)
+                if l > 0:
+                    p, c = i // C, i % C
+                    peer.push(r.vm(r.dS_vm[l], Ly.fp, i), r.own_slab_rows(r.dS_own[l], Ly.fp, c, me), p,
+                              self._ch(DS, l, i))
+                return []
+
+            r.rnn_backward(b, l, before_step=before, after_step=after)
+            self._record_xchg(comm, "backward", b, l)
+            if l > 0:
+                self.bytes_moved += F32 * C * plan.NP * Ly.fp * (P - 1)
+                peer.drain()          # dZ_own is about to be rewritten: its seed pushes must be out
+                for c in reversed(range(C)):
+                    j = me * C + c
+                    for q in range(P):
+                        peer.wait(q, self._ch(DS, l, j))
+                    r.gcn_transpose_aggregate_step(l, c)
+                    for k in range(P):
+                        q = (me + k) % P
+                        peer.push(r.own_slab_rows(r.dZ_own, Ly.fp, c, q), r.vm(r.dY_vm, Ly.fp, j), q,
+                                  self._ch(DY, l - 1, j))
+                self.bytes_moved += F32 * C * plan.NP * Ly.fp * (P - 1)
+        peer.drain()
+
     def _split_backward_pipelined(self, b, comm):
         """Reverse sweep of block b with per-step exchanges: the head seeds of
         each owned step (reverse step order) go out as soon as they are
@@ -990,7 +1114,12 @@ class Engine:
         # one rank per GPU: exchanges folded into the producing loops (P2P
         # sends of finished slabs / steps overlap the next kernel)
         pipe_gcn, pipe_lstm = self._pipelining()
+        if self.peer is not None:
+            self.peer.barrier()
         for l, Ly in enumerate(layers):
+            if self.peer is not None:
+                self._peer_layer_forward(b, l, phase, comm)
+                continue
             if self.split_pipe:
                 self._split_layer_forward_pipelined(b, l, phase, comm)
                 continue
@@ -1050,8 +1179,11 @@ class Engine:
                 # next epoch's forward sweep, or an evaluation) starts there
                 r.begin_block(b, keep=True, ledger=transfer, next_b=b - 1 if b > 0 else 0)
             self._layers_forward(b, "rerun", comm)
-            if self.split_pipe:
-                self._split_backward_pipelined(b, comm)
+            if self.split_pipe or self.peer is not None:
+                if self.peer is not None:
+                    self._peer_backward(b, comm)
+                else:
+                    self._split_backward_pipelined(b, comm)
                 if act is not None:
                     act.free_activations(plan.bsize * 2 * L)
                     act.free_checkpoint(1.0)
