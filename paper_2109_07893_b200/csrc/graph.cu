@@ -188,11 +188,21 @@ __global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ col, in
     if (e < nnz) atomicAdd(&cnt[col[e]], 1);
 }
 
+// Rows longer than kLongRow (heavy-tailed graphs: hub accounts) are handed
+// to warp-per-row kernels through a device list, so one thread never walks
+// thousands of entries while the rest of the grid idles.
+constexpr int kLongRow = 64;
+
 __global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ rp,
                                          const int32_t* __restrict__ col, const double* __restrict__ val,
-                                         int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval) {
+                                         int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval,
+                                         int32_t* __restrict__ long_rows, int32_t* long_count) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= n) return;
+    if (rp[r + 1] - rp[r] > kLongRow) {
+        long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
+        return;
+    }
     for (int e = rp[r]; e < rp[r + 1]; ++e) {
         const int pos = atomicAdd(&cursor[col[e]], 1);
         tcol[pos] = (int32_t)r;
@@ -200,7 +210,25 @@ __global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ 
     }
 }
 
+__global__ void transpose_scatter_long_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                              const double* __restrict__ val, int32_t* cursor,
+                                              int32_t* __restrict__ tcol, double* __restrict__ tval,
+                                              const int32_t* __restrict__ long_rows,
+                                              const int32_t* __restrict__ long_count) {
+    const int lane = threadIdx.x & 31;
+    const int cnt = *long_count;
+    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < cnt; li += (gridDim.x * blockDim.x) >> 5) {
+        const int r = long_rows[li];
+        for (int e = rp[r] + lane; e < rp[r + 1]; e += 32) {
+            const int pos = atomicAdd(&cursor[col[e]], 1);
+            tcol[pos] = r;
+            if (val) tval[pos] = val[e];
+        }
+    }
+}
+
 constexpr int kSmallSeg = 32;
+constexpr int kBitonicMax = 16384;   // long segments sorted in shared memory up to this length
 
 // Short segments: one thread sorts its column in registers/local memory.
 __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp,
@@ -228,21 +256,64 @@ __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp
     }
 }
 
-// Long segments: one block per segment, rank = #smaller keys (keys are distinct rows).
-__global__ void seg_sort_large_kernel(const int32_t* __restrict__ trp, const int32_t* __restrict__ src_col,
-                                      const double* __restrict__ src_val, int32_t* __restrict__ dst_col,
-                                      double* __restrict__ dst_val, const int32_t* __restrict__ long_list,
-                                      const int32_t* __restrict__ long_count) {
+// Long segments: one block per segment.  Up to kBitonicMax entries: a
+// bitonic sort of (row, source index) pairs in shared memory (padded to a
+// power of two with INT_MAX keys), O(d log^2 d).  Longer ones: rank = #smaller
+// keys (keys are distinct rows), O(d^2) -- a fallback for extreme hubs.
+__global__ void __launch_bounds__(1024) seg_sort_large_kernel(const int32_t* __restrict__ trp,
+                                                              const int32_t* __restrict__ src_col,
+                                                              const double* __restrict__ src_val,
+                                                              int32_t* __restrict__ dst_col,
+                                                              double* __restrict__ dst_val,
+                                                              const int32_t* __restrict__ long_list,
+                                                              const int32_t* __restrict__ long_count) {
+    extern __shared__ int32_t ssort[];   // [kBitonicMax] keys | [kBitonicMax] source index
+    int32_t* skey = ssort;
+    int32_t* sidx = ssort + kBitonicMax;
     const int cnt = *long_count;
     for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
         const int c = long_list[li];
         const int b = trp[c], e = trp[c + 1], d = e - b;
-        for (int i = threadIdx.x; i < d; i += blockDim.x) {
-            const int k = src_col[b + i];
-            int rank = 0;
-            for (int j = 0; j < d; ++j) rank += src_col[b + j] < k;
-            dst_col[b + rank] = k;
-            if (dst_val) dst_val[b + rank] = src_val[b + i];
+        if (d <= kBitonicMax) {
+            int p2 = 1;
+            while (p2 < d) p2 <<= 1;
+            for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+                skey[i] = i < d ? src_col[b + i] : INT_MAX;
+                sidx[i] = b + i;
+            }
+            __syncthreads();
+            for (int k = 2; k <= p2; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+                        const int ij = i ^ j;
+                        if (ij > i) {
+                            const bool up = (i & k) == 0;
+                            const int a0 = skey[i], a1 = skey[ij];
+                            if ((a0 > a1) == up) {
+                                skey[i] = a1;
+                                skey[ij] = a0;
+                                const int t = sidx[i];
+                                sidx[i] = sidx[ij];
+                                sidx[ij] = t;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int i = threadIdx.x; i < d; i += blockDim.x) {
+                dst_col[b + i] = skey[i];
+                if (dst_val) dst_val[b + i] = src_val[sidx[i]];
+            }
+            __syncthreads();
+        } else {
+            for (int i = threadIdx.x; i < d; i += blockDim.x) {
+                const int k = src_col[b + i];
+                int rank = 0;
+                for (int j = 0; j < d; ++j) rank += src_col[b + j] < k;
+                dst_col[b + rank] = k;
+                if (dst_val) dst_val[b + rank] = src_val[b + i];
+            }
         }
     }
 }
@@ -269,10 +340,15 @@ __device__ __forceinline__ double lap_value(int64_t r, int c, double a, const do
 
 __global__ void lap_count_kernel(int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
                                  const double* __restrict__ mval, const double* __restrict__ is, int transposed,
-                                 int32_t* __restrict__ cnt) {
+                                 int32_t* __restrict__ cnt, int32_t* __restrict__ long_rows,
+                                 int32_t* long_count) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r > n) return;
     if (r == n) { cnt[n] = 0; return; }
+    if (mrp[r + 1] - mrp[r] > kLongRow) {
+        long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
+        return;
+    }
     int k = 0;
     bool diag = false;
     for (int e = mrp[r]; e < mrp[r + 1]; ++e) {
@@ -291,6 +367,7 @@ __global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, con
                                  float* __restrict__ o32, double* __restrict__ o64, int64_t cap) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= n) return;
+    if (mrp[r + 1] - mrp[r] > kLongRow) return;   // lap_write_long_kernel
     int64_t pos = orp[r];
     bool diag_done = false;
     auto emit = [&](int c, double v) {
@@ -312,6 +389,91 @@ __global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, con
         emit(c, lap_value(r, c, a, is, transposed));
     }
     if (!diag_done) emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
+}
+
+// Warp-per-row versions for the long rows.  Entries of a row are sorted by
+// column; the identity term of a row without a stored diagonal is inserted
+// before its first column > r.  Output order and values are the thread
+// kernels' exactly.
+__global__ void lap_count_long_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+                                      const double* __restrict__ mval, const double* __restrict__ is,
+                                      int transposed, int32_t* __restrict__ cnt,
+                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
+    const int lane = threadIdx.x & 31;
+    const int nl = *long_count;
+    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+        const int r = long_rows[li];
+        int k = 0;
+        bool diag = false;
+        for (int e0 = mrp[r]; e0 < mrp[r + 1]; e0 += 32) {
+            const int e = e0 + lane;
+            bool nz = false, isd = false;
+            if (e < mrp[r + 1]) {
+                const int c = mcol[e];
+                isd = c == r;
+                nz = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
+            }
+            k += __popc(__ballot_sync(0xffffffffu, nz));
+            diag |= __any_sync(0xffffffffu, isd);
+        }
+        if (lane == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
+    }
+}
+
+__global__ void lap_write_long_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+                                      const double* __restrict__ mval, const double* __restrict__ is,
+                                      int transposed, const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
+                                      float* __restrict__ o32, double* __restrict__ o64, int64_t cap,
+                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int nl = *long_count;
+    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+        const int r = long_rows[li];
+        const int rb = mrp[r], re = mrp[r + 1];
+        // insertion of the identity term: before the first column > r when no
+        // column == r is stored (the thread kernel's diag_done logic)
+        bool has_diag = false;
+        int before = 0, nzb = 0;   // stored entries with column < r, and how many of them are nonzero
+        for (int e0 = rb; e0 < re; e0 += 32) {
+            const int e = e0 + lane;
+            const int c = e < re ? mcol[e] : INT_MAX;
+            has_diag |= __any_sync(0xffffffffu, c == r);
+            before += __popc(__ballot_sync(0xffffffffu, c < r));
+            const bool nzl = c < r && lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
+            nzb += __popc(__ballot_sync(0xffffffffu, nzl));
+        }
+        const double dv = has_diag ? 0.0 : lap_value(r, r, 0.0, is, transposed);
+        const int dshift = (!has_diag && dv != 0.0) ? 1 : 0;
+        int64_t pos = orp[r];
+        for (int e0 = rb; e0 < re; e0 += 32) {
+            const int e = e0 + lane;
+            double v = 0.0;
+            int c = 0;
+            if (e < re) {
+                c = mcol[e];
+                v = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed);
+            }
+            const unsigned nzm = __ballot_sync(0xffffffffu, v != 0.0);
+            const int idx = e - rb;   // entry index within the row
+            const int64_t p = pos + __popc(nzm & lt) + (idx >= before ? dshift : 0);
+            if (v != 0.0 && p < cap) {
+                ocol[p] = c;
+                o32[p] = (float)v;
+                if (o64) o64[p] = v;
+            }
+            pos += __popc(nzm);
+        }
+        if (lane == 0 && dshift) {
+            // position: every nonzero stored entry with column < r precedes it
+            const int64_t p = orp[r] + nzb;
+            if (p < cap) {
+                ocol[p] = r;
+                o32[p] = (float)dv;
+                if (o64) o64[p] = dv;
+            }
+        }
+    }
 }
 
 __global__ void degree_kernel(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ trp,
@@ -416,9 +578,10 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
 }
 
 size_t dgnn_csr_transpose_workspace(int32_t n) {
-    // cursor[n] (reused as the hub-column list after the scatter) + counter + scan;
-    // the nnz-sized scatter staging is passed separately (stage_col / stage_val)
-    return (size_t)round64((int64_t)n + 1) * sizeof(int32_t) + 64 * sizeof(int32_t) +
+    // cursor[n] (reused as the hub-column list after the scatter) + counter +
+    // long-row list [n] + counter + scan; the nnz-sized scatter staging is
+    // passed separately (stage_col / stage_val)
+    return 2 * ((size_t)round64((int64_t)n + 1) * sizeof(int32_t) + 64 * sizeof(int32_t)) +
            scan_workspace_bytes((int64_t)n + 1);
 }
 
@@ -437,9 +600,12 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     cudaStream_t st = as_stream(stream);
     int32_t* cursor = reinterpret_cast<int32_t*>(ws);
     int32_t* long_count = cursor + round64((int64_t)n + 1);
-    void* sws = long_count + 64;
-    size_t sws_bytes = ws_bytes - (size_t)round64((int64_t)n + 1) * sizeof(int32_t) - 64 * sizeof(int32_t);
+    int32_t* long_rows = long_count + 64;
+    int32_t* long_rows_count = long_rows + round64((int64_t)n + 1);
+    void* sws = long_rows_count + 64;
+    size_t sws_bytes = ws_bytes - 2 * ((size_t)round64((int64_t)n + 1) * sizeof(int32_t) + 64 * sizeof(int32_t));
     cudaMemsetAsync(long_count, 0, sizeof(int32_t), st);
+    cudaMemsetAsync(long_rows_count, 0, sizeof(int32_t), st);
     ::dgnn::note_launch();
     zero_i32_kernel<<<(unsigned)cdiv((int64_t)n + 1, 256), 256, 0, st>>>(t_rowptr, (int64_t)n + 1);
     if (nnz) {
@@ -451,18 +617,25 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     cudaMemcpyAsync(cursor, t_rowptr, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
     ::dgnn::note_launch();
     transpose_scatter_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, rowptr, col, val, cursor, stage_col,
-                                                                      stage_val);
+                                                                      stage_val, long_rows, long_rows_count);
+    ::dgnn::note_launch();
+    transpose_scatter_long_kernel<<<kSMs, 256, 0, st>>>(rowptr, col, val, cursor, stage_col, stage_val, long_rows,
+                                                        long_rows_count);
     ::dgnn::note_launch();
     seg_sort_small_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, t_rowptr, stage_col, stage_val, t_col,
                                                                    val ? t_val : nullptr, cursor, long_count);
     ::dgnn::note_launch();
-    seg_sort_large_kernel<<<kSMs, 256, 0, st>>>(t_rowptr, stage_col, stage_val, t_col, val ? t_val : nullptr,
-                                                cursor, long_count);
+    const int sort_smem = 2 * kBitonicMax * (int)sizeof(int32_t);
+    cudaFuncSetAttribute(seg_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem);
+    seg_sort_large_kernel<<<kSMs, 1024, sort_smem, st>>>(t_rowptr, stage_col, stage_val, t_col,
+                                                         val ? t_val : nullptr, cursor, long_count);
     return launch_status("csr_transpose");
 }
 
 size_t dgnn_laplacian_workspace(int32_t n) {
-    return (size_t)round64(n) * sizeof(double) + scan_workspace_bytes((int64_t)n + 1);
+    // is[n] | long-row list [n] + counter | scan
+    return (size_t)round64(n) * sizeof(double) + (size_t)round64((int64_t)n + 1) * sizeof(int32_t) +
+           64 * sizeof(int32_t) + scan_workspace_bytes((int64_t)n + 1);
 }
 
 int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, const int32_t* m_col,
@@ -476,18 +649,29 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     }
     cudaStream_t st = as_stream(stream);
     double* is = reinterpret_cast<double*>(ws);
-    void* sws = is + round64(n);
-    size_t sws_bytes = ws_bytes - (size_t)round64(n) * sizeof(double);
+    int32_t* long_rows = reinterpret_cast<int32_t*>(is + round64(n));
+    int32_t* long_count = long_rows + round64((int64_t)n + 1);
+    void* sws = long_count + 64;
+    size_t sws_bytes = ws_bytes - (size_t)round64(n) * sizeof(double) -
+                       (size_t)round64((int64_t)n + 1) * sizeof(int32_t) - 64 * sizeof(int32_t);
     const unsigned g = (unsigned)cdiv((int64_t)n + 1, 128);
+    cudaMemsetAsync(long_count, 0, sizeof(int32_t), st);
     ::dgnn::note_launch();
     inv_sqrt_deg_kernel<<<g, 128, 0, st>>>(n, a_rowptr, is);
     ::dgnn::note_launch();
-    lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr);
+    lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
+                                        long_count);
+    ::dgnn::note_launch();
+    lap_count_long_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
+                                                long_count);
     int rc = exclusive_scan_i32(out_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
     if (rc) return rc;
     ::dgnn::note_launch();
     lap_write_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
                                         out_val32, out_val64, out_cap);
+    ::dgnn::note_launch();
+    lap_write_long_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
+                                                out_val32, out_val64, out_cap, long_rows, long_count);
     return launch_status("laplacian");
 }
 

@@ -455,3 +455,37 @@ def test_spmm_f32_large(f):
     ref = np.zeros((n, f))
     np.add.at(ref, rows, val.astype(np.float64)[:, None] * x.astype(np.float64)[cols])
     assert np.abs(a - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+def test_laplacian_and_transpose_heavy_tailed_bit_exact(oracle):
+    """Hub rows (> 64 entries: warp-per-row count / write / scatter, with and
+    without a stored diagonal, entries on both sides of it, zero products
+    elided) and hub columns (bitonic shared-memory sort, and one past its
+    16384-entry capacity: the rank fallback) against the oracle, bit-exact."""
+    rng = np.random.default_rng(11)
+    n = 20000
+    parts_r, parts_c = [rng.integers(0, n, 30000)], [rng.integers(0, n, 30000)]
+    for h in (5, 77, 12345):                       # hub rows
+        parts_r.append(np.full(3000, h))
+        parts_c.append(rng.permutation(n)[:3000])
+    parts_r.append(np.array([77]))                  # row 77 stores its diagonal
+    parts_c.append(np.array([77]))
+    parts_r.append(rng.permutation(n)[:17000])      # a column past the bitonic capacity
+    parts_c.append(np.full(17000, 9))
+    parts_r.append(rng.permutation(n)[:5000])       # a bitonic column
+    parts_c.append(np.full(5000, 4242))
+    rows, cols = np.concatenate(parts_r), np.concatenate(parts_c)
+    vals = rng.standard_normal(rows.shape[0])
+    vals[rng.random(rows.shape[0]) < 0.01] = 0.0    # explicit zeros vanish
+    a = pk.SparseMatrix.from_entries(n, rows, cols, vals)
+    oa = oracle.Coo(n, a.rows, a.cols, a.vals)
+    ref = oracle.laplacian(oa)
+    got = pk.normalize_laplacian(a)
+    assert np.array_equal(got.rows, ref.rows) and np.array_equal(got.cols, ref.cols)
+    assert np.array_equal(got.vals, ref.vals)
+    from paper_2109_07893_b200.ops import normalize_laplacian_transpose
+    lt = normalize_laplacian_transpose(a)
+    assert lt == pk.SparseMatrix.from_entries(n, ref.cols, ref.rows, ref.vals)
+    g = rng.standard_normal((n, 3))
+    assert np.array_equal(pk.spmm_transpose(a, g), oracle.spmm_t(oa, g))
