@@ -136,6 +136,8 @@ static int rowptr_launch(int32_t n, int64_t nnz, const int32_t* rows, int32_t* r
 
 // ---------------------------------------------------------------------------
 // K1: delta apply (delta.py:126-146), one thread per row, two-pointer merge
+// (rows longer than kMergeLong: a warp each, delta_merge_long_kernel)
+constexpr int kMergeLong = 64;
 
 __global__ void delta_count_kernel(int32_t n, const int32_t* __restrict__ orp,
                                    const int32_t* __restrict__ drp, const int32_t* __restrict__ irp,
@@ -150,9 +152,14 @@ __global__ void delta_merge_kernel(int32_t n, const int32_t* __restrict__ orp,
                                    const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
                                    const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
                                    const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
-                                   int32_t* __restrict__ ncol, int64_t cap, int32_t* status) {
+                                   int32_t* __restrict__ ncol, int64_t cap, int32_t* status,
+                                   int32_t* __restrict__ long_rows, int32_t* long_count) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= n) return;
+    if ((orp[r + 1] - orp[r]) + (irp[r + 1] - irp[r]) > kMergeLong) {   // delta_merge_long_kernel
+        long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
+        return;
+    }
     int di = drp[r];
     const int de = drp[r + 1];
     int ii = irp[r];
@@ -173,6 +180,64 @@ __global__ void delta_merge_kernel(int32_t n, const int32_t* __restrict__ orp,
     while (ii < ie) { if (pos < end) ncol[pos] = icol[ii]; ++pos; ++ii; }
     if (pos != (int64_t)nrp[r + 1]) ++bad;
     if (bad) atomicAdd(status, bad);
+}
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Long rows (hubs): one warp per row, every entry placed independently by
+// binary search -- an old entry c lands at (#old before it) - (#deletes < c)
+// + (#inserts < c), an insert at (#old < c) - (#deletes < c) + its index.
+// Same output as the two-pointer merge for a consistent delta; the same
+// inconsistencies (deleting an absent entry, inserting a present one) are
+// counted into `status`.
+__global__ void delta_merge_long_kernel(const int32_t* __restrict__ orp, const int32_t* __restrict__ ocol,
+                                        const int32_t* __restrict__ drp, const int32_t* __restrict__ dcol,
+                                        const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+                                        const int32_t* __restrict__ nrp, int32_t* __restrict__ ncol, int64_t cap,
+                                        int32_t* status, const int32_t* __restrict__ long_rows,
+                                        const int32_t* __restrict__ long_count) {
+    const int lane = threadIdx.x & 31;
+    const int nl = *long_count;
+    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+        const int r = long_rows[li];
+        const int o0 = orp[r], no = orp[r + 1] - o0;
+        const int d0 = drp[r], nd = drp[r + 1] - d0;
+        const int i0 = irp[r], ni = irp[r + 1] - i0;
+        const int64_t base = nrp[r], end = min((int64_t)nrp[r + 1], cap);
+        int bad = 0;
+        for (int k = lane; k < no; k += 32) {
+            const int c = ocol[o0 + k];
+            const int kd = lower_bound_i32(dcol + d0, nd, c);
+            if (kd < nd && dcol[d0 + kd] == c) continue;            // deleted
+            const int ki = lower_bound_i32(icol + i0, ni, c);
+            if (ki < ni && icol[i0 + ki] == c) ++bad;               // insertion overlaps the common set
+            const int64_t p = base + k - kd + ki;
+            if (p < end) ncol[p] = c;
+        }
+        for (int k = lane; k < ni; k += 32) {
+            const int c = icol[i0 + k];
+            const int ko = lower_bound_i32(ocol + o0, no, c);
+            const int kd = lower_bound_i32(dcol + d0, nd, c);
+            const int64_t p = base + ko - kd + k;
+            if (p < end) ncol[p] = c;
+        }
+        for (int k = lane; k < nd; k += 32) {                      // deletions must exist
+            const int c = dcol[d0 + k];
+            const int ko = lower_bound_i32(ocol + o0, no, c);
+            if (!(ko < no && ocol[o0 + ko] == c)) ++bad;
+        }
+        if (lane == 0 && (int64_t)no - nd + ni != (int64_t)nrp[r + 1] - base) ++bad;
+        bad = warp_sum(bad);
+        if (lane == 0 && bad) atomicAdd(status, bad);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -545,7 +610,9 @@ int dgnn_rowptr_from_sorted_rows(int32_t n, int64_t nnz, const int32_t* rows, in
 }
 
 size_t dgnn_csr_apply_delta_workspace(int32_t n) {
-    return 2 * (size_t)round64((int64_t)n + 1) * sizeof(int32_t) + scan_workspace_bytes((int64_t)n + 1);
+    // delete / insert rowptrs, long-row list + counter, scan
+    return 3 * (size_t)round64((int64_t)n + 1) * sizeof(int32_t) + 64 * sizeof(int32_t) +
+           scan_workspace_bytes((int64_t)n + 1);
 }
 
 int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* old_col, int64_t n_del,
@@ -561,8 +628,11 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
     cudaStream_t st = as_stream(stream);
     int32_t* drp = reinterpret_cast<int32_t*>(ws);
     int32_t* irp = drp + round64((int64_t)n + 1);
-    void* sws = irp + round64((int64_t)n + 1);
-    size_t sws_bytes = ws_bytes - 2 * (size_t)round64((int64_t)n + 1) * sizeof(int32_t);
+    int32_t* long_rows = irp + round64((int64_t)n + 1);
+    int32_t* long_count = long_rows + round64((int64_t)n + 1);
+    void* sws = long_count + 64;
+    size_t sws_bytes = ws_bytes - 3 * (size_t)round64((int64_t)n + 1) * sizeof(int32_t) - 64 * sizeof(int32_t);
+    cudaMemsetAsync(long_count, 0, sizeof(int32_t), st);
     int rc = rowptr_launch(n, n_del, del_row, drp, st);
     if (!rc) rc = rowptr_launch(n, n_ins, ins_row, irp, st);
     if (rc) return rc;
@@ -573,7 +643,11 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
     if (rc) return rc;
     ::dgnn::note_launch();
     delta_merge_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, old_rowptr, old_col, drp, del_col, irp,
-                                                               ins_col, new_rowptr, new_col, new_cap, status);
+                                                               ins_col, new_rowptr, new_col, new_cap, status,
+                                                               long_rows, long_count);
+    ::dgnn::note_launch();
+    delta_merge_long_kernel<<<kSMs, 256, 0, st>>>(old_rowptr, old_col, drp, del_col, irp, ins_col, new_rowptr,
+                                                  new_col, new_cap, status, long_rows, long_count);
     return launch_status("csr_apply_delta");
 }
 

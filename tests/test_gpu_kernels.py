@@ -489,3 +489,31 @@ def test_laplacian_and_transpose_heavy_tailed_bit_exact(oracle):
     assert lt == pk.SparseMatrix.from_entries(n, ref.cols, ref.rows, ref.vals)
     g = rng.standard_normal((n, 3))
     assert np.array_equal(pk.spmm_transpose(a, g), oracle.spmm_t(oa, g))
+
+
+@pytest.mark.gpu
+def test_apply_hub_rows_round_trip_and_corruption():
+    """Rows longer than 64 entries go through the warp-per-row merge: round
+    trips through diff / apply on hub rows, and the corrupt-delta checks
+    (delete absent, insert present) still fire on them."""
+    rng = np.random.default_rng(5)
+    n = 3000
+
+    def hubby():
+        r = np.concatenate([rng.integers(0, n, 4000), np.full(900, 17), np.full(300, 2999)])
+        c = np.concatenate([rng.integers(0, n, 4000), rng.permutation(n)[:900], rng.permutation(n)[:300]])
+        return pk.SparseMatrix.from_entries(n, r, c, rng.choice([1.0, 0.5, -2.0], r.shape[0]))
+
+    for _ in range(3):
+        a, b = hubby(), hubby()
+        assert pk.apply(a, pk.diff(a, b)) == b
+    a = hubby()
+    hub_cols = a.cols[a.rows == 17]
+    absent = np.setdiff1d(np.arange(n), hub_cols)[:1]
+    bad = pk.SnapshotDelta(n, np.array([[17, absent[0]]]), np.zeros((0, 2), np.int64), a.vals)
+    with pytest.raises(pk.CorruptDeltaError):
+        pk.apply(a, bad)
+    bad = pk.SnapshotDelta(n, np.zeros((0, 2), np.int64), np.array([[17, hub_cols[5]]]),
+                           np.concatenate([a.vals, [1.0]]))
+    with pytest.raises(pk.CorruptDeltaError):
+        pk.apply(a, bad)
