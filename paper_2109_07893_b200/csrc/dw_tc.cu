@@ -33,7 +33,10 @@ namespace dgnn {
 using namespace tc;
 
 constexpr int DW_ROWS = 16;      // reduction rows per stage = two 8-row K steps
-constexpr int DW_PERIOD = 512;   // rows per TMEM accumulation period
+#ifndef DGNN_DW_PERIOD
+#define DGNN_DW_PERIOD 512
+#endif
+constexpr int DW_PERIOD = DGNN_DW_PERIOD;   // rows per TMEM accumulation period
 constexpr int DW_MAX_STAGES = 4;
 constexpr int DW_NLOAD = 8, DW_NCONV = 8, DW_NPROD = DW_NLOAD + DW_NCONV, DW_MMA_WARP = DW_NPROD, DW_NEPI = 4;
 constexpr int DW_THREADS = 32 * (DW_NPROD + 1 + DW_NEPI);
