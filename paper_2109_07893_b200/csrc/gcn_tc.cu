@@ -8,18 +8,17 @@
 // FMAs and is L1-bound at ~22% of HBM.  Here the transform runs on the
 // tensor cores, so the SM only gathers:
 //
-//   warps 0..15  gather: per 128-row tile, one lane group (FP/4 lanes, a
-//                float4 each) per row, 4 rows per lane group in flight;
-//                neighbour rows are fetched with the row's indices read
-//                from shared memory, s / relu(s) stored
+//   warps 0..19  gather: per 128-row tile, one lane group (FP/4 lanes, a
+//                float4 each) per row; neighbour rows are fetched with the
+//                row's indices read from shared memory, s / relu(s) stored
 //                straight from registers (coalesced), and s is split to tf32
 //                hi/lo into the SW64 K-major A tile;
-//   warp 16      index loader: stages the tile's rowptr slice and its
+//   warp 20      index loader: stages the tile's rowptr slice and its
 //                col/val range into shared memory two tiles ahead, so the
 //                gather issues the x loads after one latency, not three;
-//   warp 17      MMA issuer (one lane): 3xTF32, M = 128, N = HP, K = FP,
+//   warp 21      MMA issuer (one lane): 3xTF32, M = 128, N = HP, K = FP,
 //                W (hi/lo, K-major) resident in shared memory;
-//   warps 18..21 epilogue: TMEM -> ReLU -> per-warp shared-memory transpose
+//   warps 22..25 epilogue: TMEM -> ReLU -> per-warp shared-memory transpose
 //                -> row-contiguous stores of relu(q).
 //
 // Persistent grid (one CTA per SM), 2-stage A ring, 3-stage index ring,
@@ -53,7 +52,7 @@ namespace gtc {
 #endif
 constexpr int PROBE = DGNN_GTB_PROBE;
 constexpr int BM = 128;
-constexpr int NGATHER = 16, IDX_WARP = 16, MMA_WARP = 17, EPI0 = 18, NEPI = 4;
+constexpr int NGATHER = 20, IDX_WARP = 20, MMA_WARP = 21, EPI0 = 22, NEPI = 4;
 constexpr int THREADS = 32 * (EPI0 + NEPI);
 constexpr int ASTAGES = 2, ISTAGES = 3;
 constexpr int ECAP = 1024;   // edges per tile staged in shared memory (else read from global)
@@ -179,16 +178,13 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 }
                 for (; e < ee; ++e) fma4(acc, vs[e], xrow(cs[e]));
             };
-            // Row chunks (RPG RW rows: RPG rows per lane group) are claimed
+            // Row chunks (2 RW rows: two rows per lane group) are claimed
             // dynamically, so warps that drew short rows take more of them
             // and the tile completes together.  Every warp makes exactly one
             // failing claim per tile, so use k of stage s starts its claims
             // at k (NCHUNK + NGATHER): the counter never needs a reset (the
             // A ring's empty[s] keeps every warp within one use of stage s).
-            // Aggregation: 4 rows per lane group with their first 2 edges in
-            // flight together (mean degree ~1.6: most rows are one batch).
-            constexpr int RPG = AGG ? 4 : 2, NE = 2;
-            constexpr int CROWS = RPG * RW, NCHUNK = gtc::BM / CROWS;
+            constexpr int CROWS = 2 * RW, NCHUNK = gtc::BM / CROWS;
             const int cslot = s;
             const int cbase = (int)(it / gtc::ASTAGES) * (NCHUNK + gtc::NGATHER);
             for (;;) {
@@ -196,82 +192,73 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 if (lane == 0) chunk = atomicAdd(&bars->claim[cslot], 1) - cbase;
                 chunk = __shfl_sync(0xffffffffu, chunk, 0);
                 if (chunk >= NCHUNK) break;
-                int rr[RPG];
-                int64_t row[RPG];
-                bool ok[RPG];
-                float4 acc[RPG];
-#pragma unroll
-                for (int h = 0; h < RPG; ++h) {
-                    rr[h] = chunk * CROWS + sub + h * RW;
-                    row[h] = (int64_t)tile * gtc::BM + rr[h];
-                    ok[h] = rr[h] < gtc::BM && row[h] < n;
-                    acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
+                const int r = chunk * CROWS + sub, rb = r + RW;
+                const int64_t row_a = (int64_t)tile * gtc::BM + r, row_b = (int64_t)tile * gtc::BM + rb;
+                const bool oka = row_a < n, okb = rb < gtc::BM && row_b < n;
+                float4 acc_a = make_float4(0.f, 0.f, 0.f, 0.f), acc_b = acc_a;
                 if constexpr (AGG) {
-                    int eb[RPG], ee[RPG];
-                    float4 xv[RPG][NE];
-                    float wv[RPG][NE];
+                    const int ea = oka ? ix.rp[r] : 0, eea = oka ? ix.rp[r + 1] : 0;
+                    const int eb = okb ? ix.rp[rb] : 0, eeb = okb ? ix.rp[rb + 1] : 0;
+                    float4 xa[4], xb[4];
+                    float wa[4], wb[4];
 #pragma unroll
-                    for (int h = 0; h < RPG; ++h) {
-                        eb[h] = ok[h] ? ix.rp[rr[h]] : 0;
-                        ee[h] = ok[h] ? ix.rp[rr[h] + 1] : 0;
-#pragma unroll
-                        for (int j = 0; j < NE; ++j) {
-                            const bool in = eb[h] + j < ee[h];
-                            wv[h][j] = in ? vs[eb[h] + j] : 0.f;
-                            xv[h][j] = in ? xrow(cs[eb[h] + j]) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
+                    for (int j = 0; j < 4; ++j) {
+                        const bool ja = ea + j < eea, jb = eb + j < eeb;
+                        wa[j] = ja ? vs[ea + j] : 0.f;
+                        wb[j] = jb ? vs[eb + j] : 0.f;
+                        xa[j] = ja ? xrow(cs[ea + j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        xb[j] = jb ? xrow(cs[eb + j]) : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
-                    for (int h = 0; h < RPG; ++h) {
-#pragma unroll
-                        for (int j = 0; j < NE; ++j) fma4(acc[h], wv[h][j], xv[h][j]);
-                        if (ee[h] - eb[h] > NE) tail(acc[h], eb[h] + NE, ee[h]);
+                    for (int j = 0; j < 4; ++j) {
+                        fma4(acc_a, wa[j], xa[j]);
+                        fma4(acc_b, wb[j], xb[j]);
                     }
+                    if (eea - ea > 4) tail(acc_a, ea + 4, eea);
+                    if (eeb - eb > 4) tail(acc_b, eb + 4, eeb);
                 } else if constexpr (BWD) {
-                    auto dqrow = [&](int64_t rw) {
+                    auto dqrow = [&](int64_t row) {
                         if (gtc::PROBE & 8) return make_float4(1.f, 0.f, 1.f, 0.f);
-                        const float4 g = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(x, rw) + DQ_OFF) + gl);
-                        const float4 m = (gtc::PROBE & 2) ? g : __ldg(reinterpret_cast<const float4*>(frame_row<const float>(mk, rw) + DQ_OFF) + gl);
+                        const float4 g = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(x, row) + DQ_OFF) + gl);
+                        const float4 m = (gtc::PROBE & 2) ? g : __ldg(reinterpret_cast<const float4*>(frame_row<const float>(mk, row) + DQ_OFF) + gl);
                         return make_float4(m.x > 0.f ? g.x : 0.f, m.y > 0.f ? g.y : 0.f, m.z > 0.f ? g.z : 0.f,
                                            m.w > 0.f ? g.w : 0.f);
                     };
-#pragma unroll
-                    for (int h = 0; h < RPG; ++h)
-                        if (ok[h]) acc[h] = dqrow(row[h]);
+                    if (oka) acc_a = dqrow(row_a);
+                    if (okb) acc_b = dqrow(row_b);
                     if constexpr (SKIP) {
-                        auto skip_chunk = [&](int64_t rw, int c) {
-                            const float4 g = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(x, rw)) + c);
-                            const float4 m = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(mk, rw)) + c);
-                            reinterpret_cast<float4*>(frame_row<float>(r_out, rw))[c] =
+                        auto skip_chunk = [&](int64_t row, int c) {
+                            const float4 g = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(x, row)) + c);
+                            const float4 m = __ldg(reinterpret_cast<const float4*>(frame_row<const float>(mk, row)) + c);
+                            reinterpret_cast<float4*>(frame_row<float>(r_out, row))[c] =
                                 make_float4(m.x > 0.f ? g.x : 0.f, m.y > 0.f ? g.y : 0.f, m.z > 0.f ? g.z : 0.f,
                                             m.w > 0.f ? g.w : 0.f);
                         };
                         for (int c = gl; c < HP / 4; c += G) {
-#pragma unroll
-                            for (int h = 0; h < RPG; ++h)
-                                if (ok[h]) skip_chunk(row[h], c);
+                            if (oka) skip_chunk(row_a, c);
+                            if (okb) skip_chunk(row_b, c);
                         }
                     }
                 } else {
-#pragma unroll
-                    for (int h = 0; h < RPG; ++h)
-                        if (ok[h]) acc[h] = xrow((int)row[h]);
+                    if (oka) acc_a = xrow((int)row_a);
+                    if (okb) acc_b = xrow((int)row_b);
                 }
 #pragma unroll
-                for (int h = 0; h < RPG; ++h) {
-                    if (rr[h] >= gtc::BM) break;
-                    if (!BWD && ok[h]) {
-                        if (s_out.ptr) reinterpret_cast<float4*>(frame_row<float>(s_out, row[h]))[gl] = acc[h];
+                for (int h = 0; h < 2; ++h) {
+                    const int rr = h ? rb : r;
+                    if (rr >= gtc::BM) break;
+                    const int64_t row = h ? row_b : row_a;
+                    const float4 acc = h ? acc_b : acc_a;
+                    if (!BWD && (h ? okb : oka)) {
+                        if (s_out.ptr) reinterpret_cast<float4*>(frame_row<float>(s_out, row))[gl] = acc;
                         if (SKIP)
-                            reinterpret_cast<float4*>(frame_row<float>(r_out, row[h]))[gl] = make_float4(
-                                fmaxf(acc[h].x, 0.f), fmaxf(acc[h].y, 0.f), fmaxf(acc[h].z, 0.f),
-                                fmaxf(acc[h].w, 0.f));
+                            reinterpret_cast<float4*>(frame_row<float>(r_out, row))[gl] = make_float4(
+                                fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
                     }
                     float4 hi, lo;
-                    split4(acc[h], hi, lo);
+                    split4(acc, hi, lo);
                     const int k = 4 * gl;
-                    const uint32_t o = (uint32_t)((k / 16) * gtc::BM * 64) + sw64(rr[h], (k % 16) / 4);
+                    const uint32_t o = (uint32_t)((k / 16) * gtc::BM * 64) + sw64(rr, (k % 16) / 4);
                     sts128(a_hi + o, hi);
                     sts128(a_lo + o, lo);
                 }
