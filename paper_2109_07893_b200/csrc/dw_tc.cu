@@ -383,22 +383,25 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
     if (warp == DW_MMA_WARP) tmem_dealloc(bars->tmem, S.tmem_cols);
 }
 
-// gw[k][j] += sum_cta slot[cta][k][j] ; gb[j] += sum_cta dbs[cta][j]   (fp64, fixed order)
+// gw[k][j] += sum_cta slot[cta][k][j] ; gb[j] += sum_cta dbs[cta][j]   (fp64, fixed
+// order: one warp per output, lane l sums CTAs l, l + 32, ... then a fixed butterfly)
 __global__ void dw_reduce_kernel(int nct, int M, int N, int K, const float* __restrict__ slots,
                                  const double* __restrict__ dbs, double* __restrict__ gw, int64_t ldg,
                                  double* __restrict__ gb) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i < (int64_t)M * K) {
         const int k = (int)(i / M), j = (int)(i % M);
         double s = 0.0;
-#pragma unroll 16
-        for (int c = 0; c < nct; ++c) s += (double)__ldg(slots + ((size_t)c * N + k) * M + j);
-        gw[(int64_t)k * ldg + j] += s;
+        for (int c = lane; c < nct; c += 32) s += (double)__ldg(slots + ((size_t)c * N + k) * M + j);
+        s = warp_sum(s);
+        if (lane == 0) gw[(int64_t)k * ldg + j] += s;
     } else if (i < (int64_t)M * K + M && gb) {
         const int j = (int)(i - (int64_t)M * K);
         double s = 0.0;
-        for (int c = 0; c < nct; ++c) s += dbs[(size_t)c * M + j];
-        gb[j] += s;
+        for (int c = lane; c < nct; c += 32) s += dbs[(size_t)c * M + j];
+        s = warp_sum(s);
+        if (lane == 0) gb[j] += s;
     }
 }
 
@@ -431,7 +434,7 @@ int lstm_dw_tc_t(int64_t rows, int64_t np, int kx, const float* x, int64_t ldx, 
     const int K = kx + HP;
     const int64_t tot = (int64_t)S.M * K + S.M;
     note_launch();
-    dw_reduce_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(grid, S.M, S.N, K, slots, dbs, gw, S.M, gb);
+    dw_reduce_kernel<<<(unsigned)cdiv(tot * 32, 256), 256, 0, st>>>(grid, S.M, S.N, K, slots, dbs, gw, S.M, gb);
     return launch_status("lstm_weight_grad_tc");
 }
 

@@ -257,16 +257,18 @@ __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows
     if (warp == gdw::MMA_WARP) tmem_dealloc(bars->tmem, S.tmem_cols);
 }
 
-// gw[f][h] += sum_cta slot[cta][f][h]   (fp64, fixed order)
+// gw[f][h] += sum_cta slot[cta][f][h]   (fp64, fixed order: one warp per
+// output, lane l sums slots l, l + 32, ... in order, then a fixed butterfly)
 __global__ void gdw_reduce_kernel(int nct, int ma, int n, int fp, int hp, const float* __restrict__ slots,
                                   double* __restrict__ gw) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= (int64_t)fp * hp) return;
     const int f = (int)(i / hp), h = (int)(i % hp);
     double s = 0.0;
-#pragma unroll 16
-    for (int c = 0; c < nct; ++c) s += (double)__ldg(slots + ((size_t)c * n + f) * ma + h);
-    gw[i] += s;
+    for (int c = lane; c < nct; c += 32) s += (double)__ldg(slots + ((size_t)c * n + f) * ma + h);
+    s = warp_sum(s);
+    if (lane == 0) gw[i] += s;
 }
 
 size_t gcn_dw_tc_workspace(int fp, int hp) {
@@ -307,7 +309,7 @@ int gcn_dw_tc(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int fp, int 
         gcn_dw_tc_kernel<128><<<grid, gdw::THREADS, smem, st>>>(n, fp, hp, off, s, dr, r, slots);
     }
     note_launch();
-    gdw_reduce_kernel<<<(unsigned)cdiv((int64_t)fp * hp, 256), 256, 0, st>>>(grid, ma, S.N, fp, hp, slots, gw);
+    gdw_reduce_kernel<<<(unsigned)cdiv((int64_t)fp * hp * 32, 256), 256, 0, st>>>(grid, ma, S.N, fp, hp, slots, gw);
     return launch_status("gcn_weight_grad (tcgen05)");
 }
 
