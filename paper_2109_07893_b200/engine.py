@@ -132,7 +132,6 @@ class Rank:
         wmax = max(Ly.ho for Ly in layers)
         self.dZ_own = _zeros(P * C * NP * wmax, device=dev)
         self.dY_vm = self.dZ_own if same else recv(B * NP * wmax)
-        self.dZ2_own = _zeros(P * C * NP * wmax, device=dev) if peer is not None else self.dZ_own
         self.dR_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
         self.dR_vm = self.dR_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
         self.dS = _zeros(N * max(Ly.fp for Ly in layers), device=dev)
@@ -415,7 +414,7 @@ class Rank:
         Ly = eng.layout.layers[l]
         sl = self.slots[c]
         call("dgnn_spmm_f32", eng.plan.N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val),
-             self.own(self.dS_own[l], Ly.fp, c), Ly.fp, self.own(self.dZ2_own, Ly.fp, c), _lib.stream_handle())
+             self.own(self.dS_own[l], Ly.fp, c), Ly.fp, self.own(self.dZ_own, Ly.fp, c), _lib.stream_handle())
 
     def xchg_owned_step(self, own_buf, vm_buf, W, c):
         """All-to-all of owned step c alone: slab q of the owner layout ->
@@ -886,8 +885,6 @@ class Engine:
         self.split_pipe = (self.split and self.fabric.distributed and cfg.classes == 2 and self.peer is None
                            and (PIPELINED_EXCHANGE == "all" or (PIPELINED_EXCHANGE == "auto" and self.plan.P == 2)))
         self.bytes_moved = 0      # bytes that crossed the fabric (all ranks of this process)
-        self._aggregated = {}     # peer transport: layer -> owner aggregation already done in the loop below
-        self._seeded = {}         # peer transport: block -> head seeds pushed during the rerun
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.params = DeviceParams(self.layout, dev)
@@ -986,39 +983,30 @@ class Engine:
         L, B = len(self.layout.layers), self.plan.bsize
         return 1 + (kind * L + l) * B + i
 
-    PEER_LAG = 1   # owner-side work for step j runs after the local step j + PEER_LAG
-
     def _peer_layer_forward(self, b, l, phase, comm):
-        """Layer l of a forward pass with per-block pushes.  Each vertex rank
-        waits for the s block of a step right before its dense transform +
-        LSTM step and pushes the finished h block to the step's owner.  The
-        owner-side work that consumes those h blocks -- the next layer's
-        aggregation of an owned step (then its s pushes), or in the rerun the
-        head of an owned step (then its dy seed pushes) -- is interleaved into
-        this loop as soon as every rank is PEER_LAG steps past that step, so
-        no pass starts with a pipeline bubble."""
+        """Layer l of a forward pass with per-block pushes: the owner waits for
+        every rank's h block of an owned step, aggregates it and pushes the
+        s blocks out; each vertex rank waits for the s block of a step right
+        before its dense transform + LSTM step, and pushes the finished h
+        block to the step's owner."""
         (r,) = self.ranks
         peer, plan = self.peer, self.plan
-        layers = self.layout.layers
-        Ly = layers[l]
-        P, C, B, me = plan.P, plan.chunk, plan.bsize, r.q
-        Y, S, DY = 0, 1, 2
-        last = l == len(layers) - 1
-        if l > 0 and not self._aggregated.get(l, False):
+        Ly = self.layout.layers[l]
+        P, C, me = plan.P, plan.chunk, r.q
+        Y, S = 0, 1
+        if l > 0:
+            prev = self.layout.layers[l - 1]
             for c in range(C):
-                self._peer_aggregate(r, l, c)
-        self._aggregated[l] = False
+                j = me * C + c
+                for q in range(P):
+                    peer.wait(q, self._ch(Y, l - 1, j))
+                r.gcn_aggregate_step(l, c)
+                for k in range(P):
+                    q = (me + k) % P
+                    peer.push(r.own_slab_rows(r.S_own[l], Ly.fp, c, q), r.vm(r.S_vm[l], Ly.fp, j), q,
+                              self._ch(S, l, j))
+            self.bytes_moved += F32 * C * plan.NP * Ly.fp * (P - 1)
         self._record_xchg(comm, phase, b, l)
-        owned = list(range(C))            # owned steps c (block step me*C + c) still to consume
-
-        def consume(c):
-            j = me * C + c
-            for q in range(P):
-                peer.wait(q, self._ch(Y, l, j))
-            if not last:
-                self._peer_aggregate(r, l + 1, c, waited=True)
-            elif phase == "rerun":
-                self._peer_seed(r, c)
 
         def before(i):
             if l > 0:
@@ -1028,101 +1016,65 @@ class Engine:
         def after(i):
             p, c = i // C, i % C
             peer.push(r.vm(r.Y_vm[l], Ly.ho, i), r.own_slab_rows(r.Y_own[l], Ly.ho, c, me), p, self._ch(Y, l, i))
-            while owned and me * C + owned[0] + self.PEER_LAG <= i:
-                consume(owned.pop(0))
 
         r.rnn_forward(b, l, before_step=before, after_step=after)
-        while owned:
-            consume(owned.pop(0))
-        if not last:
-            self._aggregated[l + 1] = True
-        elif phase == "rerun":
-            self._seeded[b] = True
-            self.bytes_moved += F32 * C * plan.NP * Ly.ho * (P - 1)
         self.bytes_moved += F32 * C * plan.NP * Ly.ho * (P - 1)
         self._record_xchg(comm, phase, b, l)
-        if last:
+        if l == len(self.layout.layers) - 1:
+            # the head reads Y_own of the last layer: wait for every h block
+            for c in range(C):
+                for q in range(P):
+                    peer.wait(q, self._ch(Y, l, me * C + c))
             peer.drain()
 
-    def _peer_aggregate(self, r, l, c, waited=False):
-        """Owner: s of owned step c at layer l (waits for every rank's h block
-        of layer l - 1 unless the caller did), pushed to every vertex rank."""
-        peer, plan = self.peer, self.plan
-        Ly = self.layout.layers[l]
-        P, C, me = plan.P, plan.chunk, r.q
-        j = me * C + c
-        if not waited:
-            for q in range(P):
-                peer.wait(q, self._ch(0, l - 1, j))
-        r.gcn_aggregate_step(l, c)
-        for k in range(P):
-            q = (me + k) % P
-            peer.push(r.own_slab_rows(r.S_own[l], Ly.fp, c, q), r.vm(r.S_vm[l], Ly.fp, j), q, self._ch(1, l, j))
-        self.bytes_moved += F32 * plan.NP * Ly.fp * (P - 1)
-
-    def _peer_seed(self, r, c):
-        """Owner: head loss / gradient / dy seeds of owned step c, pushed."""
-        peer, plan = self.peer, self.plan
-        top = self.layout.layers[-1]
-        P, C, me = plan.P, plan.chunk, r.q
-        j = me * C + c
-        r._head_step(c, r.ts[c])
-        for k in range(P):
-            q = (me + k) % P
-            peer.push(r.own_slab_rows(r.dZ_own, top.ho, c, q), r.vm(r.dY_vm, top.ho, j), q,
-                      self._ch(2, len(self.layout.layers) - 1, j))
-
     def _peer_backward(self, b, comm):
-        """Reverse sweep of block b with per-block pushes: dy seeds from the
-        owner (pushed during the rerun), ds back to the owner after each LSTM
-        + dense backward step, and the owner's transpose SpMM of an owned step
-        interleaved into the loop as soon as every rank is PEER_LAG steps past
-        it, its dy pushed to the vertex ranks for the layer below."""
+        """Reverse sweep of block b with per-block pushes (dy seeds from the
+        owner, ds back to the owner after each LSTM + dense backward step,
+        transpose SpMMs of owned steps feeding the next layer's seeds)."""
         (r,) = self.ranks
         peer, plan = self.peer, self.plan
         layers = self.layout.layers
-        P, C, B, me = plan.P, plan.chunk, plan.bsize, r.q
+        P, C, me = plan.P, plan.chunk, r.q
         DY, DS = 2, 3
-        if not self._seeded.pop(b, False):
-            for c in reversed(range(C)):
-                self._peer_seed(r, c)
-            self.bytes_moved += F32 * C * plan.NP * layers[-1].ho * (P - 1)
+        top = layers[-1]
+        for c in reversed(range(C)):
+            j = me * C + c
+            r._head_step(c, r.ts[c])
+            for k in range(P):
+                q = (me + k) % P
+                peer.push(r.own_slab_rows(r.dZ_own, top.ho, c, q), r.vm(r.dY_vm, top.ho, j), q,
+                          self._ch(DY, len(layers) - 1, j))
+        self.bytes_moved += F32 * C * plan.NP * top.ho * (P - 1)
         for l in reversed(range(len(layers))):
             Ly = layers[l]
             self._record_xchg(comm, "backward", b, l)
-            owned = list(reversed(range(C)))
 
-            def consume(c, l=l, Ly=Ly):
-                j = me * C + c
-                for q in range(P):
-                    peer.wait(q, self._ch(DS, l, j))
-                r.gcn_transpose_aggregate_step(l, c)        # into dZ2_own: the seeds' buffer may still be read
-                for k in range(P):
-                    q = (me + k) % P
-                    peer.push(r.own_slab_rows(r.dZ2_own, Ly.fp, c, q), r.vm(r.dY_vm, Ly.fp, j), q,
-                              self._ch(DY, l - 1, j))
-
-            def before(i, l=l):
+            def before(i, l=l, Ly=Ly):
                 peer.wait(i // C, self._ch(DY, l, i))
 
-            def after(i, l=l, Ly=Ly, owned=owned, consume=consume):
+            def after(i, l=l, Ly=Ly):
                 r.gcn_dense_backward_step(l, i)
                 if l > 0:
                     p, c = i // C, i % C
                     peer.push(r.vm(r.dS_vm[l], Ly.fp, i), r.own_slab_rows(r.dS_own[l], Ly.fp, c, me), p,
                               self._ch(DS, l, i))
-                    while owned and me * C + owned[0] - self.PEER_LAG >= i:
-                        consume(owned.pop(0))
                 return []
 
-            if l > 0:
-                peer.drain()   # dZ2_own of the layer above: its pushes are out before it is rewritten
             r.rnn_backward(b, l, before_step=before, after_step=after)
-            while l > 0 and owned:
-                consume(owned.pop(0))
             self._record_xchg(comm, "backward", b, l)
             if l > 0:
-                self.bytes_moved += 2 * F32 * C * plan.NP * Ly.fp * (P - 1)
+                self.bytes_moved += F32 * C * plan.NP * Ly.fp * (P - 1)
+                peer.drain()          # dZ_own is about to be rewritten: its seed pushes must be out
+                for c in reversed(range(C)):
+                    j = me * C + c
+                    for q in range(P):
+                        peer.wait(q, self._ch(DS, l, j))
+                    r.gcn_transpose_aggregate_step(l, c)
+                    for k in range(P):
+                        q = (me + k) % P
+                        peer.push(r.own_slab_rows(r.dZ_own, Ly.fp, c, q), r.vm(r.dY_vm, Ly.fp, j), q,
+                                  self._ch(DY, l - 1, j))
+                self.bytes_moved += F32 * C * plan.NP * Ly.fp * (P - 1)
         peer.drain()
 
     def _split_backward_pipelined(self, b, comm):
