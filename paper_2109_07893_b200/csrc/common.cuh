@@ -32,6 +32,15 @@ __device__ __forceinline__ T* frame_row(const dgnn_frame& f, int64_t i) {
     return reinterpret_cast<T*>(f.ptr) + s * f.slab_stride + r * f.ld;
 }
 
+// ---- hub rows of the aggregation ----------------------------------------
+// Rows with more than kHubRow stored entries (heavy-tailed graphs: hub
+// accounts) are skipped by the per-row gather loops of the SpMM / K3
+// kernels (one lane group would walk them serially while the whole tile
+// waits) and computed afterwards by hub_rows_kernel (spmm.cu): a CTA per hub
+// row, edges split over lane groups, partials reduced in a fixed tree --
+// deterministic, and the same for the tcgen05 and SIMT instances.
+constexpr int kHubRow = 256;
+
 // ---- tile-blocked layout of the LSTM step caches -----------------------
 // The per-step cell state c, the gate cache (overwritten in place by dz) and
 // the cell-state gradient dc are stored "tile-blocked": rows in tiles of 128,

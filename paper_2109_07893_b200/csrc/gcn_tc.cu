@@ -197,8 +197,10 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 const bool oka = row_a < n, okb = rb < gtc::BM && row_b < n;
                 float4 acc_a = make_float4(0.f, 0.f, 0.f, 0.f), acc_b = acc_a;
                 if constexpr (AGG) {
-                    const int ea = oka ? ix.rp[r] : 0, eea = oka ? ix.rp[r + 1] : 0;
-                    const int eb = okb ? ix.rp[rb] : 0, eeb = okb ? ix.rp[rb + 1] : 0;
+                    const int ea = oka ? ix.rp[r] : 0, eb = okb ? ix.rp[rb] : 0;
+                    int eea = oka ? ix.rp[r + 1] : 0, eeb = okb ? ix.rp[rb + 1] : 0;
+                    if (eea - ea > kHubRow) eea = ea;   // hub rows: hub_rows_kernel
+                    if (eeb - eb > kHubRow) eeb = eb;
                     float4 xa[4], xb[4];
                     float wa[4], wb[4];
 #pragma unroll

@@ -34,7 +34,8 @@ __device__ __forceinline__ float4 gather_row(int64_t row, const int32_t* __restr
                                              int gl) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     int e = rp[row];
-    const int ee = rp[row + 1];
+    int ee = rp[row + 1];
+    if (ee - e > kHubRow) ee = e;   // hub rows: hub_rows_kernel
     for (; e + 3 < ee; e += 4) {
         const int c0 = __ldg(col + e), c1 = __ldg(col + e + 1), c2 = __ldg(col + e + 2),
                   c3 = __ldg(col + e + 3);
@@ -64,6 +65,78 @@ __global__ void __launch_bounds__(256) spmm_f32_kernel(int32_t n, const int32_t*
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t row = warp * RW + sub; row < n; row += nwarps * RW)
         st4(frame_row<float>(out, row) + 4 * gl, gather_row(row, rp, col, val, x, gl));
+}
+
+// Hub rows (degree > kHubRow) of an aggregation, after the main kernel on the
+// same stream.  MODE 0: out = s (SpMM); 1: skip GCN r = [relu(s), relu(sW)]
+// (+ s_out); 2: plain GCN r = relu(sW) (+ s_out).  Each CTA scans 256 rows
+// at a time and computes each hub among them: G = F/4 lanes per edge slot,
+// 256/G slots each summing a strided share of the edges in order, slots
+// combined by a fixed tree; q_j = sum_k s_k W[k][j] in k order.
+template <int F, int H, int MODE>
+__global__ void __launch_bounds__(256) hub_rows_kernel(int32_t n, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ col,
+                                                       const float* __restrict__ val, dgnn_frame x,
+                                                       const float* __restrict__ w, dgnn_frame s_out,
+                                                       dgnn_frame r_out) {
+    constexpr int G = F / 4, EPS = 256 / G;
+    __shared__ int32_t list[256];
+    __shared__ int cnt;
+    __shared__ float4 part[EPS][G];
+    const int slot = threadIdx.x / G, gl = threadIdx.x % G;
+    for (int64_t base = (int64_t)blockIdx.x * 256; base < n; base += (int64_t)gridDim.x * 256) {
+        if (threadIdx.x == 0) cnt = 0;
+        __syncthreads();
+        const int64_t r = base + threadIdx.x;
+        if (r < n && rp[r + 1] - rp[r] > kHubRow) list[atomicAdd(&cnt, 1)] = (int32_t)r;
+        __syncthreads();
+        const int nh = cnt;
+        for (int k = 0; k < nh; ++k) {
+            const int row = list[k];
+            const int eb = rp[row], ee = rp[row + 1];
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int e = eb + slot; e < ee; e += EPS)
+                fma4(acc, __ldg(val + e), ldg4(frame_row<const float>(x, __ldg(col + e)) + 4 * gl));
+            part[slot][gl] = acc;
+            __syncthreads();
+            for (int h = EPS / 2; h > 0; h >>= 1) {
+                if (slot < h) {
+                    const float4 o = part[slot + h][gl];
+                    float4 v = part[slot][gl];
+                    v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                    part[slot][gl] = v;
+                }
+                __syncthreads();
+            }
+            if constexpr (MODE == 0) {
+                if (threadIdx.x < G) st4(frame_row<float>(r_out, row) + 4 * gl, part[0][gl]);
+            } else {
+                float* rr = frame_row<float>(r_out, row);
+                if (threadIdx.x < G) {
+                    if (s_out.ptr) st4(frame_row<float>(s_out, row) + 4 * gl, part[0][gl]);
+                    if (MODE == 1) st4(rr + 4 * gl, relu4(part[0][gl]));
+                }
+                const float* sv = reinterpret_cast<const float*>(&part[0][0]);
+                for (int j = threadIdx.x; j < H; j += blockDim.x) {
+                    float q = 0.f;
+                    for (int kk = 0; kk < F; ++kk) q = fmaf(sv[kk], __ldg(w + kk * H + j), q);
+                    rr[(MODE == 1 ? F : 0) + j] = fmaxf(q, 0.f);
+                }
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+    }
+}
+
+template <int F, int H, int MODE>
+int hub_rows_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x, const float* w,
+               dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+    int64_t blocks = cdiv(n, 256);
+    blocks = blocks > 4 * kSMs ? 4 * kSMs : (blocks < 1 ? 1 : blocks);
+    ::dgnn::note_launch();
+    hub_rows_kernel<F, H, MODE><<<(unsigned)blocks, 256, 0, st>>>(n, rp, col, val, x, w, s_out, r_out);
+    return launch_status("hub_rows");
 }
 
 // K3 for the 4-wide first layer (s = s1 rows, no aggregation): HP / 4 lanes
@@ -245,7 +318,9 @@ int spmm_f32_t(int32_t n, const int32_t* rp, const int32_t* col, const float* va
     blocks = blocks < 1 ? 1 : (blocks > 32 * kSMs ? 32 * kSMs : blocks);
     ::dgnn::note_launch();
     spmm_f32_kernel<F><<<(unsigned)blocks, 256, 0, st>>>(n, rp, col, val, x, out);
-    return launch_status("spmm_f32");
+    const int rc = launch_status("spmm_f32");
+    if (rc) return rc;
+    return hub_rows_t<F, 4, 0>(n, rp, col, val, x, nullptr, dgnn_frame{}, out, st);
 }
 
 template <int FP, int HP, bool SKIP, bool AGG>
@@ -340,6 +415,34 @@ int gcn_bwd_fp(int32_t fp, int32_t hp, int32_t n, dgnn_frame dr, dgnn_frame r, c
 
 }  // namespace
 
+// hub rows of the fused GCN forward (both instances)
+template <int F>
+int gcn_hub_rows_h(int hp, bool skip, int32_t n, const int32_t* rp, const int32_t* col, const float* val,
+                   dgnn_frame x, const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+    switch (hp) {
+#define HUB_H(H)                                                                                   \
+    case H:                                                                                        \
+        return skip ? hub_rows_t<F, H, 1>(n, rp, col, val, x, w, s_out, r_out, st)                \
+                    : hub_rows_t<F, H, 2>(n, rp, col, val, x, w, s_out, r_out, st);
+        HUB_H(16) HUB_H(32) HUB_H(64) HUB_H(128)
+#undef HUB_H
+    }
+    set_error("gcn_forward: unsupported hp %d", hp);
+    return DGNN_EUNSUPPORTED;
+}
+
+int gcn_hub_rows(int fp, int hp, bool skip, int32_t n, const int32_t* rp, const int32_t* col, const float* val,
+                 dgnn_frame x, const float* w, dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
+    switch (fp) {
+        case 16: return gcn_hub_rows_h<16>(hp, skip, n, rp, col, val, x, w, s_out, r_out, st);
+        case 32: return gcn_hub_rows_h<32>(hp, skip, n, rp, col, val, x, w, s_out, r_out, st);
+        case 64: return gcn_hub_rows_h<64>(hp, skip, n, rp, col, val, x, w, s_out, r_out, st);
+        case 128: return gcn_hub_rows_h<128>(hp, skip, n, rp, col, val, x, w, s_out, r_out, st);
+    }
+    set_error("gcn_forward: unsupported fp %d", fp);
+    return DGNN_EUNSUPPORTED;
+}
+
 extern "C" {
 
 // K3 engine selection: tcgen05 instance where one exists (default) or the
@@ -379,16 +482,18 @@ int dgnn_gcn_forward(int32_t n, const int32_t* rowptr, const int32_t* col, const
     if (n == 0) return DGNN_OK;
     cudaStream_t st = as_stream(stream);
     const bool agg = rowptr != nullptr;
-    if (dgnn_gcn_tensor_cores) {
-        const int rc = gcn_fwd_tc(fp, hp, skip != 0, agg, n, rowptr, col, val, x, w, s_out, r_out, st);
-        if (rc >= 0) return rc;
+    int rc = -1;
+    if (dgnn_gcn_tensor_cores) rc = gcn_fwd_tc(fp, hp, skip != 0, agg, n, rowptr, col, val, x, w, s_out, r_out, st);
+    if (rc < 0) {
+        if (skip)
+            rc = agg ? gcn_fwd_fp<true, true>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st)
+                     : gcn_fwd_fp<true, false>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st);
+        else
+            rc = agg ? gcn_fwd_fp<false, true>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st)
+                     : gcn_fwd_fp<false, false>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st);
     }
-    if (skip) {
-        return agg ? gcn_fwd_fp<true, true>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st)
-                   : gcn_fwd_fp<true, false>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st);
-    }
-    return agg ? gcn_fwd_fp<false, true>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st)
-               : gcn_fwd_fp<false, false>(fp, hp, n, rowptr, col, val, x, w, s_out, r_out, st);
+    if (rc || !agg) return rc;
+    return gcn_hub_rows(fp, hp, skip != 0, n, rowptr, col, val, x, w, s_out, r_out, st);
 }
 
 int dgnn_gcn_backward_rows(int32_t n, dgnn_frame dr, dgnn_frame r, int32_t fp, const float* w, int32_t hp,
