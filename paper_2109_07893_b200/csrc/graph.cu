@@ -137,7 +137,7 @@ static int rowptr_launch(int32_t n, int64_t nnz, const int32_t* rows, int32_t* r
 // ---------------------------------------------------------------------------
 // K1: delta apply (delta.py:126-146), one thread per row, two-pointer merge
 // (rows longer than kMergeLong: a warp each, delta_merge_long_kernel)
-constexpr int kMergeLong = 64;
+constexpr int kMergeLong = 16;
 
 __global__ void delta_count_kernel(int32_t n, const int32_t* __restrict__ orp,
                                    const int32_t* __restrict__ drp, const int32_t* __restrict__ irp,
@@ -256,7 +256,7 @@ __global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ col, in
 // Rows longer than kLongRow (heavy-tailed graphs: hub accounts) are handed
 // to warp-per-row kernels through a device list, so one thread never walks
 // thousands of entries while the rest of the grid idles.
-constexpr int kLongRow = 64;
+constexpr int kLongRow = 16;
 
 __global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ rp,
                                          const int32_t* __restrict__ col, const double* __restrict__ val,

@@ -211,7 +211,10 @@ class Materializer:
         f32 = dict(dtype=torch.float32, device=self.device)
         self.resident = resident
         self.copy_stream = torch.cuda.Stream(device=self.device)
-        self.graph_stream = torch.cuda.Stream(device=self.device)
+        # high priority: the rebuild kernels take SMs as soon as they free up, so
+        # a graph-bound pass (large value-carrying graphs) is not starved by
+        # the compute stream's persistent kernels
+        self.graph_stream = torch.cuda.Stream(device=self.device, priority=-1)
         # encoded input on device: everything (resident) or a chunk-sized staging area
         if resident:
             self.full_dev = enc.full.to(self.device)
