@@ -192,28 +192,31 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int key)
     return lo;
 }
 
-// Long rows (hubs): one warp per row, every entry placed independently by
+// Long rows (hubs): one CTA per row (a warp per row left a ~8000-entry hub
+// as a 250-step serial tail), every entry placed independently by
 // binary search -- an old entry c lands at (#old before it) - (#deletes < c)
 // + (#inserts < c), an insert at (#old < c) - (#deletes < c) + its index.
 // Same output as the two-pointer merge for a consistent delta; the same
 // inconsistencies (deleting an absent entry, inserting a present one) are
 // counted into `status`.
-__global__ void delta_merge_long_kernel(const int32_t* __restrict__ orp, const int32_t* __restrict__ ocol,
-                                        const int32_t* __restrict__ drp, const int32_t* __restrict__ dcol,
-                                        const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
-                                        const int32_t* __restrict__ nrp, int32_t* __restrict__ ncol, int64_t cap,
-                                        int32_t* status, const int32_t* __restrict__ long_rows,
-                                        const int32_t* __restrict__ long_count) {
-    const int lane = threadIdx.x & 31;
+constexpr int kLongThreads = 256;   // CTA size of every hub-row kernel
+constexpr int kLongCTAs = 4;        // CTAs per SM of every hub-row kernel
+
+__global__ void __launch_bounds__(kLongThreads) delta_merge_long_kernel(
+        const int32_t* __restrict__ orp, const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
+        const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+        const int32_t* __restrict__ nrp, int32_t* __restrict__ ncol, int64_t cap, int32_t* status,
+        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
+    const int tid = threadIdx.x, nt = blockDim.x;
     const int nl = *long_count;
-    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
         const int r = long_rows[li];
         const int o0 = orp[r], no = orp[r + 1] - o0;
         const int d0 = drp[r], nd = drp[r + 1] - d0;
         const int i0 = irp[r], ni = irp[r + 1] - i0;
         const int64_t base = nrp[r], end = min((int64_t)nrp[r + 1], cap);
         int bad = 0;
-        for (int k = lane; k < no; k += 32) {
+        for (int k = tid; k < no; k += nt) {
             const int c = ocol[o0 + k];
             const int kd = lower_bound_i32(dcol + d0, nd, c);
             if (kd < nd && dcol[d0 + kd] == c) continue;            // deleted
@@ -222,21 +225,20 @@ __global__ void delta_merge_long_kernel(const int32_t* __restrict__ orp, const i
             const int64_t p = base + k - kd + ki;
             if (p < end) ncol[p] = c;
         }
-        for (int k = lane; k < ni; k += 32) {
+        for (int k = tid; k < ni; k += nt) {
             const int c = icol[i0 + k];
             const int ko = lower_bound_i32(ocol + o0, no, c);
             const int kd = lower_bound_i32(dcol + d0, nd, c);
             const int64_t p = base + ko - kd + k;
             if (p < end) ncol[p] = c;
         }
-        for (int k = lane; k < nd; k += 32) {                      // deletions must exist
+        for (int k = tid; k < nd; k += nt) {                        // deletions must exist
             const int c = dcol[d0 + k];
             const int ko = lower_bound_i32(ocol + o0, no, c);
             if (!(ko < no && ocol[o0 + ko] == c)) ++bad;
         }
-        if (lane == 0 && (int64_t)no - nd + ni != (int64_t)nrp[r + 1] - base) ++bad;
-        bad = warp_sum(bad);
-        if (lane == 0 && bad) atomicAdd(status, bad);
+        if (tid == 0 && (int64_t)no - nd + ni != (int64_t)nrp[r + 1] - base) ++bad;
+        if (bad) atomicAdd(status, bad);
     }
 }
 
@@ -275,16 +277,14 @@ __global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ 
     }
 }
 
-__global__ void transpose_scatter_long_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                              const double* __restrict__ val, int32_t* cursor,
-                                              int32_t* __restrict__ tcol, double* __restrict__ tval,
-                                              const int32_t* __restrict__ long_rows,
-                                              const int32_t* __restrict__ long_count) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kLongThreads) transpose_scatter_long_kernel(
+        const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+        int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval,
+        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
     const int cnt = *long_count;
-    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < cnt; li += (gridDim.x * blockDim.x) >> 5) {
+    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {   // a CTA per hub row
         const int r = long_rows[li];
-        for (int e = rp[r] + lane; e < rp[r + 1]; e += 32) {
+        for (int e = rp[r] + threadIdx.x; e < rp[r + 1]; e += blockDim.x) {
             const int pos = atomicAdd(&cursor[col[e]], 1);
             tcol[pos] = r;
             if (val) tval[pos] = val[e];
@@ -293,18 +293,21 @@ __global__ void transpose_scatter_long_kernel(const int32_t* __restrict__ rp, co
 }
 
 constexpr int kSmallSeg = 32;
+constexpr int kRankMax = 1024;       // mid segments: rank sort of a shared-memory copy
 constexpr int kBitonicMax = 16384;   // long segments sorted in shared memory up to this length
 
 // Short segments: one thread sorts its column in registers/local memory.
 __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp,
                                       const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
                                       int32_t* __restrict__ dst_col, double* __restrict__ dst_val,
+                                      int32_t* __restrict__ mid_list, int32_t* mid_count,
                                       int32_t* __restrict__ long_list, int32_t* long_count) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= n) return;
     const int b = trp[c], e = trp[c + 1], d = e - b;
-    if (d > kSmallSeg) {                       // hub column: handed to the block-per-segment kernel
-        long_list[atomicAdd(long_count, 1)] = (int32_t)c;
+    if (d > kSmallSeg) {                       // hub column: handed to a block-per-segment kernel
+        if (d <= kRankMax) mid_list[atomicAdd(mid_count, 1)] = (int32_t)c;
+        else long_list[atomicAdd(long_count, 1)] = (int32_t)c;
         return;
     }
     int key[kSmallSeg];
@@ -318,6 +321,33 @@ __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp
     for (int i = 0; i < d; ++i) {
         dst_col[b + i] = key[i];
         if (dst_val) dst_val[b + i] = src_val[idx[i]];
+    }
+}
+
+// Mid segments (kSmallSeg < d <= kRankMax; most hub columns of a heavy-tailed
+// graph): one CTA per segment, keys staged in shared memory, each entry placed
+// at its rank = #smaller keys (keys are distinct rows, so the order is the
+// sort's).  A 1024-thread bitonic network per 40-entry column left most of
+// its threads idle behind ~20 barriers.
+__global__ void __launch_bounds__(kLongThreads) seg_sort_mid_kernel(
+        const int32_t* __restrict__ trp, const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
+        int32_t* __restrict__ dst_col, double* __restrict__ dst_val, const int32_t* __restrict__ mid_list,
+        const int32_t* __restrict__ mid_count) {
+    __shared__ int32_t skey[kRankMax];
+    const int cnt = *mid_count;
+    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+        const int c = mid_list[li];
+        const int b = trp[c], d = trp[c + 1] - b;
+        for (int i = threadIdx.x; i < d; i += blockDim.x) skey[i] = src_col[b + i];
+        __syncthreads();
+        for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            const int k = skey[i];
+            int rank = 0;
+            for (int j = 0; j < d; ++j) rank += skey[j] < k;
+            dst_col[b + rank] = k;
+            if (dst_val) dst_val[b + rank] = src_val[b + i];
+        }
+        __syncthreads();
     }
 }
 
@@ -456,80 +486,130 @@ __global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, con
     if (!diag_done) emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
 }
 
-// Warp-per-row versions for the long rows.  Entries of a row are sorted by
-// column; the identity term of a row without a stored diagonal is inserted
-// before its first column > r.  Output order and values are the thread
-// kernels' exactly.
-__global__ void lap_count_long_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
-                                      const double* __restrict__ mval, const double* __restrict__ is,
-                                      int transposed, int32_t* __restrict__ cnt,
-                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int lane = threadIdx.x & 31;
+// CTA-per-row versions for the long rows (hub rows of heavy-tailed graphs;
+// a warp per row made the largest hub a serial tail of the whole call).
+// Entries of a row are sorted by column; the identity term of a row without
+// a stored diagonal is inserted before its first column > r.  Output order
+// and values are the thread kernels' exactly.
+constexpr int kLapIlp = 4;   // entries per thread per chunk of a hub row (loads in flight)
+
+__global__ void __launch_bounds__(kLongThreads) lap_count_long_kernel(
+        const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+        const double* __restrict__ is, int transposed, int32_t* __restrict__ cnt,
+        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
     const int nl = *long_count;
-    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+    const int nt = blockDim.x;
+    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
         const int r = long_rows[li];
-        int k = 0;
-        bool diag = false;
-        for (int e0 = mrp[r]; e0 < mrp[r + 1]; e0 += 32) {
-            const int e = e0 + lane;
-            bool nz = false, isd = false;
-            if (e < mrp[r + 1]) {
-                const int c = mcol[e];
-                isd = c == r;
-                nz = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
+        const int rb = mrp[r], re = mrp[r + 1];
+        int k = 0, diag = 0;
+        for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
+            int c[kLapIlp];
+            double a[kLapIlp];
+#pragma unroll
+            for (int j = 0; j < kLapIlp; ++j) {
+                const int e = e0 + j * nt + threadIdx.x;
+                c[j] = e < re ? mcol[e] : -1;
+                a[j] = e < re && mval ? mval[e] : 1.0;
             }
-            k += __popc(__ballot_sync(0xffffffffu, nz));
-            diag |= __any_sync(0xffffffffu, isd);
+            int nz = 0, isd = 0;
+#pragma unroll
+            for (int j = 0; j < kLapIlp; ++j) {
+                isd |= c[j] == r;
+                nz += c[j] >= 0 && lap_value(r, c[j], a[j], is, transposed) != 0.0;
+            }
+            k += __syncthreads_count(nz >= 1) + __syncthreads_count(nz >= 2) + __syncthreads_count(nz >= 3) +
+                 __syncthreads_count(nz >= 4);
+            diag |= __syncthreads_or(isd);
         }
-        if (lane == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
+        if (threadIdx.x == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
     }
 }
 
-__global__ void lap_write_long_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
-                                      const double* __restrict__ mval, const double* __restrict__ is,
-                                      int transposed, const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
-                                      float* __restrict__ o32, double* __restrict__ o64, int64_t cap,
-                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kLongThreads) lap_write_long_kernel(
+        const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+        const double* __restrict__ is, int transposed, const int32_t* __restrict__ orp,
+        int32_t* __restrict__ ocol, float* __restrict__ o32, double* __restrict__ o64, int64_t cap,
+        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
+    __shared__ int s_warp[kLapIlp][kLongThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5, nt = blockDim.x;
     const unsigned lt = (1u << lane) - 1u;
     const int nl = *long_count;
-    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
         const int r = long_rows[li];
         const int rb = mrp[r], re = mrp[r + 1];
         // insertion of the identity term: before the first column > r when no
-        // column == r is stored (the thread kernel's diag_done logic)
-        bool has_diag = false;
-        int before = 0, nzb = 0;   // stored entries with column < r, and how many of them are nonzero
-        for (int e0 = rb; e0 < re; e0 += 32) {
-            const int e = e0 + lane;
-            const int c = e < re ? mcol[e] : INT_MAX;
-            has_diag |= __any_sync(0xffffffffu, c == r);
-            before += __popc(__ballot_sync(0xffffffffu, c < r));
-            const bool nzl = c < r && lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
-            nzb += __popc(__ballot_sync(0xffffffffu, nzl));
+        // column == r is stored (the thread kernel's diag_done logic).  Columns
+        // are sorted, so the entries with column < r are a prefix of the row:
+        // before = its length, nzb = its nonzero entries.
+        int has_diag = 0, before = 0, nzb = 0;
+        for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
+            int c[kLapIlp];
+            double a[kLapIlp];
+#pragma unroll
+            for (int j = 0; j < kLapIlp; ++j) {
+                const int e = e0 + j * nt + tid;
+                c[j] = e < re ? mcol[e] : INT_MAX;
+                a[j] = e < re && mval ? mval[e] : 1.0;
+            }
+            int lo = 0, nzl = 0, isd = 0;
+#pragma unroll
+            for (int j = 0; j < kLapIlp; ++j) {
+                isd |= c[j] == r;
+                lo += c[j] < r;
+                nzl += c[j] < r && lap_value(r, c[j], a[j], is, transposed) != 0.0;
+            }
+            has_diag |= __syncthreads_or(isd);
+#pragma unroll
+            for (int j = 1; j <= kLapIlp; ++j) {
+                before += __syncthreads_count(lo >= j);
+                nzb += __syncthreads_count(nzl >= j);
+            }
         }
         const double dv = has_diag ? 0.0 : lap_value(r, r, 0.0, is, transposed);
         const int dshift = (!has_diag && dv != 0.0) ? 1 : 0;
         int64_t pos = orp[r];
-        for (int e0 = rb; e0 < re; e0 += 32) {
-            const int e = e0 + lane;
-            double v = 0.0;
-            int c = 0;
-            if (e < re) {
-                c = mcol[e];
-                v = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed);
+        for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
+            int c[kLapIlp];
+            double v[kLapIlp];
+            unsigned nzm[kLapIlp];
+#pragma unroll
+            for (int j = 0; j < kLapIlp; ++j) {
+                const int e = e0 + j * nt + tid;
+                c[j] = e < re ? mcol[e] : 0;
+                v[j] = e < re && mval ? mval[e] : 1.0;
             }
-            const unsigned nzm = __ballot_sync(0xffffffffu, v != 0.0);
-            const int idx = e - rb;   // entry index within the row
-            const int64_t p = pos + __popc(nzm & lt) + (idx >= before ? dshift : 0);
-            if (v != 0.0 && p < cap) {
-                ocol[p] = c;
-                o32[p] = (float)v;
-                if (o64) o64[p] = v;
+#pragma unroll
+            for (int j = 0; j < kLapIlp; ++j) {
+                const int e = e0 + j * nt + tid;
+                v[j] = e < re ? lap_value(r, c[j], v[j], is, transposed) : 0.0;
+                nzm[j] = __ballot_sync(0xffffffffu, v[j] != 0.0);
+                if (lane == 0) s_warp[j][wid] = __popc(nzm[j]);
             }
-            pos += __popc(nzm);
+            __syncthreads();
+            int run = 0;   // nonzeros of the earlier sub-chunks of this chunk
+#pragma unroll
+            for (int j = 0; j < kLapIlp; ++j) {
+                int off = 0, tot = 0;
+                for (int w = 0; w < nw; ++w) {
+                    const int x = s_warp[j][w];
+                    off += w < wid ? x : 0;
+                    tot += x;
+                }
+                const int e = e0 + j * nt + tid;
+                const int idx = e - rb;   // entry index within the row
+                const int64_t p = pos + run + off + __popc(nzm[j] & lt) + (idx >= before ? dshift : 0);
+                if (v[j] != 0.0 && p < cap) {
+                    ocol[p] = c[j];
+                    o32[p] = (float)v[j];
+                    if (o64) o64[p] = v[j];
+                }
+                run += tot;
+            }
+            pos += run;
+            __syncthreads();   // s_warp is rewritten by the next chunk
         }
-        if (lane == 0 && dshift) {
+        if (tid == 0 && dshift) {
             // position: every nonzero stored entry with column < r precedes it
             const int64_t p = orp[r] + nzb;
             if (p < cap) {
@@ -646,8 +726,9 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
                                                                ins_col, new_rowptr, new_col, new_cap, status,
                                                                long_rows, long_count);
     ::dgnn::note_launch();
-    delta_merge_long_kernel<<<kSMs, 256, 0, st>>>(old_rowptr, old_col, drp, del_col, irp, ins_col, new_rowptr,
-                                                  new_col, new_cap, status, long_rows, long_count);
+    delta_merge_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(
+        old_rowptr, old_col, drp, del_col, irp, ins_col, new_rowptr, new_col, new_cap, status, long_rows,
+        long_count);
     return launch_status("csr_apply_delta");
 }
 
@@ -693,16 +774,23 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     transpose_scatter_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, rowptr, col, val, cursor, stage_col,
                                                                       stage_val, long_rows, long_rows_count);
     ::dgnn::note_launch();
-    transpose_scatter_long_kernel<<<kSMs, 256, 0, st>>>(rowptr, col, val, cursor, stage_col, stage_val, long_rows,
-                                                        long_rows_count);
+    transpose_scatter_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(
+        rowptr, col, val, cursor, stage_col, stage_val, long_rows, long_rows_count);
+    // the hub-row list is free once the scatter has run: it now takes the
+    // columns past kRankMax, the cursor array the mid columns
+    cudaMemsetAsync(long_rows_count, 0, sizeof(int32_t), st);
     ::dgnn::note_launch();
     seg_sort_small_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, t_rowptr, stage_col, stage_val, t_col,
+                                                                   val ? t_val : nullptr, cursor, long_count,
+                                                                   long_rows, long_rows_count);
+    ::dgnn::note_launch();
+    seg_sort_mid_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
                                                                    val ? t_val : nullptr, cursor, long_count);
     ::dgnn::note_launch();
     const int sort_smem = 2 * kBitonicMax * (int)sizeof(int32_t);
     cudaFuncSetAttribute(seg_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem);
     seg_sort_large_kernel<<<kSMs, 1024, sort_smem, st>>>(t_rowptr, stage_col, stage_val, t_col,
-                                                         val ? t_val : nullptr, cursor, long_count);
+                                                         val ? t_val : nullptr, long_rows, long_rows_count);
     return launch_status("csr_transpose");
 }
 
@@ -736,16 +824,17 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
                                         long_count);
     ::dgnn::note_launch();
-    lap_count_long_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
-                                                long_count);
+    lap_count_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(m_rowptr, m_col, m_val, is, transposed,
+                                                                     out_rowptr, long_rows, long_count);
     int rc = exclusive_scan_i32(out_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
     if (rc) return rc;
     ::dgnn::note_launch();
     lap_write_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
                                         out_val32, out_val64, out_cap);
     ::dgnn::note_launch();
-    lap_write_long_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
-                                                out_val32, out_val64, out_cap, long_rows, long_count);
+    lap_write_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(
+        m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col, out_val32, out_val64, out_cap, long_rows,
+        long_count);
     return launch_status("laplacian");
 }
 

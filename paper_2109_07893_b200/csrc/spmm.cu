@@ -95,7 +95,24 @@ __global__ void __launch_bounds__(256) hub_rows_kernel(int32_t n, const int32_t*
             const int row = list[k];
             const int eb = rp[row], ee = rp[row + 1];
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int e = eb + slot; e < ee; e += EPS)
+            int e = eb + slot;
+            // 8 of the slot's edges in flight at once (a hub of ~8000 edges was a
+            // 250-step chain of dependent col -> x loads); same summation order
+            for (; e + 7 * EPS < ee; e += 8 * EPS) {
+                int c[8];
+                float v[8];
+                float4 xv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    c[j] = __ldg(col + e + j * EPS);
+                    v[j] = __ldg(val + e + j * EPS);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) xv[j] = ldg4(frame_row<const float>(x, c[j]) + 4 * gl);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) fma4(acc, v[j], xv[j]);
+            }
+            for (; e < ee; e += EPS)
                 fma4(acc, __ldg(val + e), ldg4(frame_row<const float>(x, __ldg(col + e)) + 4 * gl));
             part[slot][gl] = acc;
             __syncthreads();

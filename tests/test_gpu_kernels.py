@@ -459,8 +459,9 @@ def test_spmm_f32_large(f):
 
 @pytest.mark.gpu
 def test_laplacian_and_transpose_heavy_tailed_bit_exact(oracle):
-    """Hub rows (> 64 entries: warp-per-row count / write / scatter, with and
-    without a stored diagonal, entries on both sides of it, zero products
+    """Hub rows (> 16 entries: CTA-per-row count / write / scatter, with and
+    without a stored diagonal, entries on both sides of it, one chunk or
+    many, the last row among them, zero products
     elided) and hub columns (bitonic shared-memory sort, and one past its
     16384-entry capacity: the rank fallback) against the oracle, bit-exact."""
     rng = np.random.default_rng(11)
@@ -469,6 +470,9 @@ def test_laplacian_and_transpose_heavy_tailed_bit_exact(oracle):
     for h in (5, 77, 12345):                       # hub rows
         parts_r.append(np.full(3000, h))
         parts_c.append(rng.permutation(n)[:3000])
+    for h, d in ((n - 1, 300), (600, 40)):         # a ragged second chunk; a single chunk
+        parts_r.append(np.full(d, h))
+        parts_c.append(rng.permutation(n)[:d])
     parts_r.append(np.array([77]))                  # row 77 stores its diagonal
     parts_c.append(np.array([77]))
     parts_r.append(rng.permutation(n)[:17000])      # a column past the bitonic capacity
@@ -493,7 +497,7 @@ def test_laplacian_and_transpose_heavy_tailed_bit_exact(oracle):
 
 @pytest.mark.gpu
 def test_apply_hub_rows_round_trip_and_corruption():
-    """Rows longer than 64 entries go through the warp-per-row merge: round
+    """Rows longer than 16 entries go through the CTA-per-row merge: round
     trips through diff / apply on hub rows, and the corrupt-delta checks
     (delete absent, insert present) still fire on them."""
     rng = np.random.default_rng(5)
