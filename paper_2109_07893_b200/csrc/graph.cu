@@ -259,6 +259,7 @@ __global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ col, in
 // to warp-per-row kernels through a device list, so one thread never walks
 // thousands of entries while the rest of the grid idles.
 constexpr int kLongRow = 16;
+constexpr int kCtaRow = 512;   // Laplacian rows past this: a CTA each (below: a warp each)
 
 __global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ rp,
                                          const int32_t* __restrict__ col, const double* __restrict__ val,
@@ -294,7 +295,6 @@ __global__ void __launch_bounds__(kLongThreads) transpose_scatter_long_kernel(
 
 constexpr int kSmallSeg = 32;
 constexpr int kRankMax = 1024;       // mid segments: rank sort of a shared-memory copy
-constexpr int kBitonicMax = 16384;   // long segments sorted in shared memory up to this length
 
 // Short segments: one thread sorts its column in registers/local memory.
 __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp,
@@ -351,64 +351,78 @@ __global__ void __launch_bounds__(kLongThreads) seg_sort_mid_kernel(
     }
 }
 
-// Long segments: one block per segment.  Up to kBitonicMax entries: a
-// bitonic sort of (row, source index) pairs in shared memory (padded to a
-// power of two with INT_MAX keys), O(d log^2 d).  Longer ones: rank = #smaller
-// keys (keys are distinct rows), O(d^2) -- a fallback for extreme hubs.
-__global__ void __launch_bounds__(1024) seg_sort_large_kernel(const int32_t* __restrict__ trp,
-                                                              const int32_t* __restrict__ src_col,
-                                                              const double* __restrict__ src_val,
-                                                              int32_t* __restrict__ dst_col,
-                                                              double* __restrict__ dst_val,
-                                                              const int32_t* __restrict__ long_list,
-                                                              const int32_t* __restrict__ long_count) {
-    extern __shared__ int32_t ssort[];   // [kBitonicMax] keys | [kBitonicMax] source index
-    int32_t* skey = ssort;
-    int32_t* sidx = ssort + kBitonicMax;
+// Long segments (d > kRankMax: the few largest hub columns), spread over
+// the whole grid instead of one CTA's bitonic network (~120 us for an
+// 8000-entry column): (1) every kRankMax-entry chunk is rank-sorted in place
+// in the staging arrays by its own CTA; (2) each entry's final position is
+// its index in its chunk plus, for every other chunk, the number of smaller
+// keys there (a binary search of that sorted chunk).  Keys are distinct rows,
+// so the result is the sorted segment.
+__global__ void __launch_bounds__(kLongThreads) seg_chunk_sort_kernel(
+        const int32_t* __restrict__ trp, int32_t* __restrict__ stage_col, double* __restrict__ stage_val,
+        const int32_t* __restrict__ long_list, const int32_t* __restrict__ long_count) {
+    __shared__ int32_t skey[kRankMax];
     const int cnt = *long_count;
-    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+    constexpr int kPer = kRankMax / kLongThreads;
+    const int G = gridDim.x;
+    int g0 = 0;   // chunks of the earlier segments: chunks are dealt round-robin over the whole list
+    for (int li = 0; li < cnt; ++li) {
         const int c = long_list[li];
-        const int b = trp[c], e = trp[c + 1], d = e - b;
-        if (d <= kBitonicMax) {
-            int p2 = 1;
-            while (p2 < d) p2 <<= 1;
-            for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-                skey[i] = i < d ? src_col[b + i] : INT_MAX;
-                sidx[i] = b + i;
+        const int b = trp[c], d = trp[c + 1] - b;
+        const int nch = (d + kRankMax - 1) / kRankMax;
+        const int first = (int)(((int64_t)blockIdx.x - g0) % G + G) % G;
+        g0 = (g0 + nch) % G;
+        for (int ch = first; ch < nch; ch += G) {
+            const int cb = b + ch * kRankMax, cd = min(kRankMax, d - ch * kRankMax);
+            int key[kPer];
+            double v[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const int i = j * kLongThreads + threadIdx.x;
+                key[j] = i < cd ? stage_col[cb + i] : 0;
+                v[j] = (i < cd && stage_val) ? stage_val[cb + i] : 0.0;
+                if (i < cd) skey[i] = key[j];
             }
             __syncthreads();
-            for (int k = 2; k <= p2; k <<= 1) {
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-                        const int ij = i ^ j;
-                        if (ij > i) {
-                            const bool up = (i & k) == 0;
-                            const int a0 = skey[i], a1 = skey[ij];
-                            if ((a0 > a1) == up) {
-                                skey[i] = a1;
-                                skey[ij] = a0;
-                                const int t = sidx[i];
-                                sidx[i] = sidx[ij];
-                                sidx[ij] = t;
-                            }
-                        }
-                    }
-                    __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const int i = j * kLongThreads + threadIdx.x;
+                if (i < cd) {
+                    int rank = 0;
+                    for (int q = 0; q < cd; ++q) rank += skey[q] < key[j];
+                    stage_col[cb + rank] = key[j];
+                    if (stage_val) stage_val[cb + rank] = v[j];
                 }
             }
-            for (int i = threadIdx.x; i < d; i += blockDim.x) {
-                dst_col[b + i] = skey[i];
-                if (dst_val) dst_val[b + i] = src_val[sidx[i]];
-            }
             __syncthreads();
-        } else {
-            for (int i = threadIdx.x; i < d; i += blockDim.x) {
-                const int k = src_col[b + i];
-                int rank = 0;
-                for (int j = 0; j < d; ++j) rank += src_col[b + j] < k;
-                dst_col[b + rank] = k;
-                if (dst_val) dst_val[b + rank] = src_val[b + i];
+        }
+    }
+}
+
+__global__ void seg_chunk_merge_kernel(const int32_t* __restrict__ trp, const int32_t* __restrict__ stage_col,
+                                       const double* __restrict__ stage_val, int32_t* __restrict__ dst_col,
+                                       double* __restrict__ dst_val, const int32_t* __restrict__ long_list,
+                                       const int32_t* __restrict__ long_count) {
+    const int cnt = *long_count;
+    const int T = gridDim.x * blockDim.x;
+    int t0 = 0;   // entries of the earlier segments (dealt round-robin over all threads)
+    for (int li = 0; li < cnt; ++li) {
+        const int c = long_list[li];
+        const int b = trp[c], d = trp[c + 1] - b;
+        const int nch = (d + kRankMax - 1) / kRankMax;
+        const int first = (int)(((int64_t)(blockIdx.x * blockDim.x + threadIdx.x) - t0) % T + T) % T;
+        t0 = (int)(((int64_t)t0 + d) % T);
+        for (int i = first; i < d; i += T) {
+            const int key = stage_col[b + i];
+            const int own = i / kRankMax;
+            int pos = i - own * kRankMax;
+            for (int k = 0; k < nch; ++k) {
+                if (k == own) continue;
+                const int kb = k * kRankMax;
+                pos += lower_bound_i32(stage_col + b + kb, min(kRankMax, d - kb), key);
             }
+            dst_col[b + pos] = key;
+            if (dst_val) dst_val[b + pos] = stage_val[b + i];
         }
     }
 }
@@ -440,7 +454,12 @@ __global__ void lap_count_kernel(int32_t n, const int32_t* __restrict__ mrp, con
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r > n) return;
     if (r == n) { cnt[n] = 0; return; }
-    if (mrp[r + 1] - mrp[r] > kLongRow) {
+    const int deg = mrp[r + 1] - mrp[r];
+    if (deg > kCtaRow) {
+        long_rows[n - 1 - atomicAdd(long_count + 1, 1)] = (int32_t)r;
+        return;
+    }
+    if (deg > kLongRow) {
         long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
         return;
     }
@@ -486,21 +505,109 @@ __global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, con
     if (!diag_done) emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
 }
 
-// CTA-per-row versions for the long rows (hub rows of heavy-tailed graphs;
-// a warp per row made the largest hub a serial tail of the whole call).
+// Warp-per-row versions for the long rows up to kCtaRow entries.  Entries
+// of a row are sorted by column; the identity term of a row without a stored
+// diagonal is inserted before its first column > r.  Output order and values
+// are the thread kernels' exactly.
+__global__ void lap_count_warp_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+                                      const double* __restrict__ mval, const double* __restrict__ is,
+                                      int transposed, int32_t* __restrict__ cnt,
+                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
+    const int lane = threadIdx.x & 31;
+    const int nl = *long_count;
+    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+        const int r = long_rows[li];
+        int k = 0;
+        bool diag = false;
+        for (int e0 = mrp[r]; e0 < mrp[r + 1]; e0 += 32) {
+            const int e = e0 + lane;
+            bool nz = false, isd = false;
+            if (e < mrp[r + 1]) {
+                const int c = mcol[e];
+                isd = c == r;
+                nz = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
+            }
+            k += __popc(__ballot_sync(0xffffffffu, nz));
+            diag |= __any_sync(0xffffffffu, isd);
+        }
+        if (lane == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
+    }
+}
+
+__global__ void lap_write_warp_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+                                      const double* __restrict__ mval, const double* __restrict__ is,
+                                      int transposed, const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
+                                      float* __restrict__ o32, double* __restrict__ o64, int64_t cap,
+                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int nl = *long_count;
+    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
+        const int r = long_rows[li];
+        const int rb = mrp[r], re = mrp[r + 1];
+        // insertion of the identity term: before the first column > r when no
+        // column == r is stored (the thread kernel's diag_done logic)
+        bool has_diag = false;
+        int before = 0, nzb = 0;   // stored entries with column < r, and how many of them are nonzero
+        for (int e0 = rb; e0 < re; e0 += 32) {
+            const int e = e0 + lane;
+            const int c = e < re ? mcol[e] : INT_MAX;
+            has_diag |= __any_sync(0xffffffffu, c == r);
+            before += __popc(__ballot_sync(0xffffffffu, c < r));
+            const bool nzl = c < r && lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
+            nzb += __popc(__ballot_sync(0xffffffffu, nzl));
+        }
+        const double dv = has_diag ? 0.0 : lap_value(r, r, 0.0, is, transposed);
+        const int dshift = (!has_diag && dv != 0.0) ? 1 : 0;
+        int64_t pos = orp[r];
+        for (int e0 = rb; e0 < re; e0 += 32) {
+            const int e = e0 + lane;
+            double v = 0.0;
+            int c = 0;
+            if (e < re) {
+                c = mcol[e];
+                v = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed);
+            }
+            const unsigned nzm = __ballot_sync(0xffffffffu, v != 0.0);
+            const int idx = e - rb;   // entry index within the row
+            const int64_t p = pos + __popc(nzm & lt) + (idx >= before ? dshift : 0);
+            if (v != 0.0 && p < cap) {
+                ocol[p] = c;
+                o32[p] = (float)v;
+                if (o64) o64[p] = v;
+            }
+            pos += __popc(nzm);
+        }
+        if (lane == 0 && dshift) {
+            // position: every nonzero stored entry with column < r precedes it
+            const int64_t p = orp[r] + nzb;
+            if (p < cap) {
+                ocol[p] = r;
+                o32[p] = (float)dv;
+                if (o64) o64[p] = dv;
+            }
+        }
+    }
+}
+
+
+// CTA-per-row versions for the rows past kCtaRow entries (the largest hubs
+// of heavy-tailed graphs; a warp per row made the largest hub a serial tail
+// of the whole call).  Their list is filled from the top of the long-row
+// array down (long_rows[n - 1 - i], counter long_count[1]).
 // Entries of a row are sorted by column; the identity term of a row without
 // a stored diagonal is inserted before its first column > r.  Output order
 // and values are the thread kernels' exactly.
 constexpr int kLapIlp = 4;   // entries per thread per chunk of a hub row (loads in flight)
 
 __global__ void __launch_bounds__(kLongThreads) lap_count_long_kernel(
-        const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+        int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
         const double* __restrict__ is, int transposed, int32_t* __restrict__ cnt,
         const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int nl = *long_count;
+    const int nl = long_count[1];
     const int nt = blockDim.x;
     for (int li = blockIdx.x; li < nl; li += gridDim.x) {
-        const int r = long_rows[li];
+        const int r = long_rows[n - 1 - li];
         const int rb = mrp[r], re = mrp[r + 1];
         int k = 0, diag = 0;
         for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
@@ -527,16 +634,16 @@ __global__ void __launch_bounds__(kLongThreads) lap_count_long_kernel(
 }
 
 __global__ void __launch_bounds__(kLongThreads) lap_write_long_kernel(
-        const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+        int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
         const double* __restrict__ is, int transposed, const int32_t* __restrict__ orp,
         int32_t* __restrict__ ocol, float* __restrict__ o32, double* __restrict__ o64, int64_t cap,
         const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
     __shared__ int s_warp[kLapIlp][kLongThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5, nt = blockDim.x;
     const unsigned lt = (1u << lane) - 1u;
-    const int nl = *long_count;
+    const int nl = long_count[1];
     for (int li = blockIdx.x; li < nl; li += gridDim.x) {
-        const int r = long_rows[li];
+        const int r = long_rows[n - 1 - li];
         const int rb = mrp[r], re = mrp[r + 1];
         // insertion of the identity term: before the first column > r when no
         // column == r is stored (the thread kernel's diag_done logic).  Columns
@@ -787,10 +894,12 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     seg_sort_mid_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
                                                                    val ? t_val : nullptr, cursor, long_count);
     ::dgnn::note_launch();
-    const int sort_smem = 2 * kBitonicMax * (int)sizeof(int32_t);
-    cudaFuncSetAttribute(seg_sort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem);
-    seg_sort_large_kernel<<<kSMs, 1024, sort_smem, st>>>(t_rowptr, stage_col, stage_val, t_col,
-                                                         val ? t_val : nullptr, long_rows, long_rows_count);
+    seg_chunk_sort_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col,
+                                                                     val ? stage_val : nullptr, long_rows,
+                                                                     long_rows_count);
+    ::dgnn::note_launch();
+    seg_chunk_merge_kernel<<<kSMs * kLongCTAs, 256, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
+                                                             val ? t_val : nullptr, long_rows, long_rows_count);
     return launch_status("csr_transpose");
 }
 
@@ -817,14 +926,17 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     size_t sws_bytes = ws_bytes - (size_t)round64(n) * sizeof(double) -
                        (size_t)round64((int64_t)n + 1) * sizeof(int32_t) - 64 * sizeof(int32_t);
     const unsigned g = (unsigned)cdiv((int64_t)n + 1, 128);
-    cudaMemsetAsync(long_count, 0, sizeof(int32_t), st);
+    cudaMemsetAsync(long_count, 0, 2 * sizeof(int32_t), st);
     ::dgnn::note_launch();
     inv_sqrt_deg_kernel<<<g, 128, 0, st>>>(n, a_rowptr, is);
     ::dgnn::note_launch();
     lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
                                         long_count);
     ::dgnn::note_launch();
-    lap_count_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(m_rowptr, m_col, m_val, is, transposed,
+    lap_count_warp_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
+                                                long_count);
+    ::dgnn::note_launch();
+    lap_count_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed,
                                                                      out_rowptr, long_rows, long_count);
     int rc = exclusive_scan_i32(out_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
     if (rc) return rc;
@@ -832,8 +944,11 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     lap_write_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
                                         out_val32, out_val64, out_cap);
     ::dgnn::note_launch();
+    lap_write_warp_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
+                                                out_val32, out_val64, out_cap, long_rows, long_count);
+    ::dgnn::note_launch();
     lap_write_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(
-        m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col, out_val32, out_val64, out_cap, long_rows,
+        n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col, out_val32, out_val64, out_cap, long_rows,
         long_count);
     return launch_status("laplacian");
 }

@@ -370,6 +370,8 @@ def test_gcn_forward_tensor_cores(fp, hp, skip, agg):
     n = 5000 + 37
     deg = rng.integers(0, 4, size=n)
     deg[1234] = 3000
+    deg[777] = 100                  # a hub row just past kHubRow (64)
+    deg[2000:2140] = 60             # a tile of rows just below it
     rows = np.repeat(np.arange(n), deg)
     cols = rng.integers(0, n, size=rows.size).astype(np.int32)
     val = rng.uniform(-1, 1, size=rows.size).astype(np.float32)
@@ -444,6 +446,8 @@ def test_spmm_f32_large(f):
     n = 148 * 128 * 5 + 13          # several tiles per persistent CTA
     deg = rng.integers(0, 5, size=n)
     deg[4321] = 2500
+    deg[999] = 65
+    deg[3000:3200] = 64
     rows = np.repeat(np.arange(n), deg)
     cols = rng.integers(0, n, size=rows.size).astype(np.int32)
     val = rng.uniform(-1, 1, size=rows.size).astype(np.float32)
@@ -462,8 +466,8 @@ def test_laplacian_and_transpose_heavy_tailed_bit_exact(oracle):
     """Hub rows (> 16 entries: CTA-per-row count / write / scatter, with and
     without a stored diagonal, entries on both sides of it, one chunk or
     many, the last row among them, zero products
-    elided) and hub columns (bitonic shared-memory sort, and one past its
-    16384-entry capacity: the rank fallback) against the oracle, bit-exact."""
+    elided) and hub columns (past 1024 entries: chunk rank sorts merged by
+    binary-search ranks, 5 and 17 chunks) against the oracle, bit-exact."""
     rng = np.random.default_rng(11)
     n = 20000
     parts_r, parts_c = [rng.integers(0, n, 30000)], [rng.integers(0, n, 30000)]
@@ -475,9 +479,9 @@ def test_laplacian_and_transpose_heavy_tailed_bit_exact(oracle):
         parts_c.append(rng.permutation(n)[:d])
     parts_r.append(np.array([77]))                  # row 77 stores its diagonal
     parts_c.append(np.array([77]))
-    parts_r.append(rng.permutation(n)[:17000])      # a column past the bitonic capacity
+    parts_r.append(rng.permutation(n)[:17000])      # a 17-chunk column
     parts_c.append(np.full(17000, 9))
-    parts_r.append(rng.permutation(n)[:5000])       # a bitonic column
+    parts_r.append(rng.permutation(n)[:5000])       # a 5-chunk column
     parts_c.append(np.full(5000, 4242))
     rows, cols = np.concatenate(parts_r), np.concatenate(parts_c)
     vals = rng.standard_normal(rows.shape[0])
