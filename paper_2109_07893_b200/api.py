@@ -320,7 +320,28 @@ def _check(cfg, data, workers, nblk, scheduler):
 
 
 def _by_time(labels):
-    return labels.by_time if labels is not None else {}
+    if labels is None:
+        return {}
+    return labels if isinstance(labels, dict) else labels.by_time
+
+
+def _labels_key(*labelsets):
+    """Content fingerprint of label sets (the engine caches device labels
+    under it): per frame the pair count, coordinate and label sums and a
+    label-weighted coordinate sum -- a few ms at 3M pairs, and unlike an
+    object id it cannot be reused by a different (or mutated) label set."""
+    key = []
+    for ls in labelsets:
+        bt = _by_time(ls)
+        ent = []
+        for t in sorted(bt):
+            p, lab = bt[t]
+            p = np.asarray(p, dtype=np.int64).reshape(-1, 2)
+            lab = np.asarray(lab, dtype=np.int64)
+            ent.append((int(t), p.shape[0], int(p.sum()), int(lab.sum()),
+                        int(np.dot(p[:, 0] + 3 * p[:, 1], lab)) if p.shape[0] else 0))
+        key.append(tuple(ent))
+    return tuple(key)
 
 
 def _count(labels):
@@ -343,7 +364,7 @@ def distributed_epoch(cfg, data, labels, params: dict, workers: int, nblk: int,
     transfer = transfer if transfer is not None else TransferLedger()
     act = act_ledger if act_ledger is not None else ActivationLedger()
     eng = get_engine(cfg, data, workers, nblk)
-    eng.set_labels(_by_time(labels), None, key=(id(labels), None))
+    eng.set_labels(_by_time(labels), None, key=_labels_key(labels, None))
     eng.params.load(params)
     before = sum(r.mat.bytes_h2d for r in eng.ranks), sum(r.mat.bytes_full_equiv for r in eng.ranks)
     loss_dev, grads = eng.epoch(comm, transfer, act, _count(labels), reduction)
@@ -385,7 +406,7 @@ def train_distributed(cfg, data, train_labels, test_labels, epochs: int, seed: i
         return trace, params, comm, transfer, act
     eng = get_engine(cfg, data, workers, nblk)
     eng.set_labels(_by_time(train_labels), _by_time(test_labels),
-                   key=(id(train_labels), id(test_labels)))
+                   key=_labels_key(train_labels, test_labels))
     eng.params.load(params)
     eng.params.step = 0
     eng.params.m.zero_()
@@ -394,7 +415,11 @@ def train_distributed(cfg, data, train_labels, test_labels, epochs: int, seed: i
     for epoch in range(1, epochs + 1):
         before = sum(r.mat.bytes_h2d for r in eng.ranks), sum(r.mat.bytes_full_equiv for r in eng.ranks)
         loss_dev, grads = eng.epoch(comm, transfer, act, count, "mean")
-        loss = eng.finish(loss_dev, grads) if count else 0.0
+        if count:
+            loss = eng.finish(loss_dev, grads)
+        else:
+            loss = 0.0
+            eng.check()
         transfer.h2d_bytes += sum(r.mat.bytes_h2d for r in eng.ranks) - before[0]
         transfer.full_equiv_bytes += sum(r.mat.bytes_full_equiv for r in eng.ranks) - before[1]
         eng.params.adam(lr)

@@ -18,8 +18,10 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-constexpr int kSMs = 148;  // B200
-// CTAs of the persistent (one CTA per SM) kernels: kSMs minus the SMs kept
+constexpr int kMaxSMs = 192;  // static bound for device-side arrays; launches use num_sms()
+// multiprocessors of the current device (queried once per device; 148 on B200)
+int num_sms();
+// CTAs of the persistent (one CTA per SM) kernels: num_sms() minus the SMs kept
 // free for concurrent communication kernels (dgnn_set_sm_reserve)
 int persistent_ctas();
 

@@ -132,10 +132,10 @@ __global__ void tn_reduce_kernel(int M, int N, int nchunks, const float* __restr
     else colsum[n] += s;
 }
 
-constexpr int kMaxChunks = 2 * kSMs;
+constexpr int kMaxChunks = 2 * kMaxSMs;
 
 static int chunks_for(int64_t rows, int tiles) {
-    int64_t c = cdiv(2 * kSMs, tiles);             // ~2 CTAs per SM in total
+    int64_t c = cdiv(2 * num_sms(), tiles);             // ~2 CTAs per SM in total
     const int64_t by_rows = cdiv(rows, 4 * TN_BR);  // at least 64 rows per chunk
     if (c > by_rows) c = by_rows;
     if (c < 1) c = 1;

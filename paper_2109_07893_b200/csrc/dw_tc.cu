@@ -50,7 +50,7 @@ constexpr int DW_SMEM_MAX = 232448;
 constexpr int DW_PROBE = DGNN_DW_PROBE;
 #if DGNN_DW_PROBE & 16
 // probe 16: per-CTA cycles each role spends blocked on its barriers
-__device__ unsigned long long dw_prof[kSMs * 8];
+__device__ unsigned long long dw_prof[kMaxSMs * 8];
 #endif
 __device__ __forceinline__ void dw_wait(uint64_t* bar, uint32_t parity, long long& acc) {
     if (DW_PROBE & 16) {
@@ -416,7 +416,7 @@ int lstm_dw_tc_t(int64_t rows, int64_t np, int kx, const float* x, int64_t ldx, 
     // always one CTA per SM: the CTA row ranges (and so the fp32 period
     // sums) must not depend on dgnn_set_sm_reserve, or results would differ
     // between single- and multi-GPU runs
-    const int grid = kSMs;
+    const int grid = num_sms();
     const size_t need = (size_t)grid * S.M * S.N * sizeof(float) + (size_t)grid * S.M * sizeof(double);
     if (ws_bytes < need) {
         set_error("lstm_weight_grad_tc: workspace too small");
@@ -446,7 +446,7 @@ extern "C" {
 
 size_t dgnn_lstm_weight_grad_tc_workspace(int32_t kx, int32_t hp) {
     const DwShape S = dw_shape(hp, kx);
-    return (size_t)kSMs * S.M * S.N * sizeof(float) + (size_t)kSMs * S.M * sizeof(double) + 256;
+    return (size_t)num_sms() * S.M * S.N * sizeof(float) + (size_t)num_sms() * S.M * sizeof(double) + 256;
 }
 
 int dgnn_lstm_weight_grad_tc(int64_t rows, int64_t np, int32_t kx, int32_t hp, const float* x, int64_t ldx,

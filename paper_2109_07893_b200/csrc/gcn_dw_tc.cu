@@ -274,7 +274,7 @@ __global__ void gdw_reduce_kernel(int nct, int ma, int n, int fp, int hp, const 
 size_t gcn_dw_tc_workspace(int fp, int hp) {
     if (hp > 128 || fp > 128) return 0;
     const GdwShape S = gdw_shape(hp <= 64 ? 64 : 128, fp);
-    return (size_t)kSMs * S.N * S.MA * sizeof(float) + 256;
+    return (size_t)num_sms() * S.N * S.MA * sizeof(float) + 256;
 }
 
 // -1 when the shape has no instance (the caller then uses the SIMT path)
@@ -287,7 +287,7 @@ int gcn_dw_tc(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int fp, int 
     const int ma = hp <= 64 ? 64 : 128;
     const GdwShape S = gdw_shape(ma, fp);
     if (S.stages < 3) return -1;
-    const size_t need = (size_t)kSMs * S.N * S.MA * sizeof(float);
+    const size_t need = (size_t)num_sms() * S.N * S.MA * sizeof(float);
     if (ws_bytes < need) {
         set_error("gcn_weight_grad (tcgen05): workspace too small");
         return DGNN_EWORKSPACE;
@@ -297,7 +297,7 @@ int gcn_dw_tc(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int fp, int 
     const size_t smem = (size_t)S.stages * S.stage + 1024 + 256;
     // always one CTA per SM: the CTA row ranges (and so the fp32 period sums)
     // must not depend on dgnn_set_sm_reserve
-    const int grid = kSMs;
+    const int grid = num_sms();
     const int off = skip ? fp : 0;
     if (ma == 64) {
         cudaFuncSetAttribute(gcn_dw_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

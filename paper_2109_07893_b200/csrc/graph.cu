@@ -17,7 +17,20 @@ static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static std::atomic<int> g_sm_reserve{0};
-int persistent_ctas() { return kSMs - g_sm_reserve.load(std::memory_order_relaxed); }
+
+int num_sms() {
+    static std::atomic<int> cached[64];   // per device ordinal; 0 = not yet queried
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    int v = cached[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        if (v > kMaxSMs) v = kMaxSMs;
+        cached[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+int persistent_ctas() { return num_sms() - g_sm_reserve.load(std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
@@ -777,7 +790,7 @@ long long dgnn_launch_count(void) { return dgnn::launch_count(); }
 
 void dgnn_set_sm_reserve(int sms) {
     if (sms < 0) sms = 0;
-    if (sms > dgnn::kSMs / 2) sms = dgnn::kSMs / 2;
+    if (sms > dgnn::num_sms() / 2) sms = dgnn::num_sms() / 2;
     dgnn::g_sm_reserve.store(sms, std::memory_order_relaxed);
 }
 
@@ -833,7 +846,7 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
                                                                ins_col, new_rowptr, new_col, new_cap, status,
                                                                long_rows, long_count);
     ::dgnn::note_launch();
-    delta_merge_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(
+    delta_merge_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(
         old_rowptr, old_col, drp, del_col, irp, ins_col, new_rowptr, new_col, new_cap, status, long_rows,
         long_count);
     return launch_status("csr_apply_delta");
@@ -881,7 +894,7 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     transpose_scatter_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, rowptr, col, val, cursor, stage_col,
                                                                       stage_val, long_rows, long_rows_count);
     ::dgnn::note_launch();
-    transpose_scatter_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(
+    transpose_scatter_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(
         rowptr, col, val, cursor, stage_col, stage_val, long_rows, long_rows_count);
     // the hub-row list is free once the scatter has run: it now takes the
     // columns past kRankMax, the cursor array the mid columns
@@ -891,14 +904,14 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
                                                                    val ? t_val : nullptr, cursor, long_count,
                                                                    long_rows, long_rows_count);
     ::dgnn::note_launch();
-    seg_sort_mid_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
+    seg_sort_mid_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
                                                                    val ? t_val : nullptr, cursor, long_count);
     ::dgnn::note_launch();
-    seg_chunk_sort_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col,
+    seg_chunk_sort_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col,
                                                                      val ? stage_val : nullptr, long_rows,
                                                                      long_rows_count);
     ::dgnn::note_launch();
-    seg_chunk_merge_kernel<<<kSMs * kLongCTAs, 256, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
+    seg_chunk_merge_kernel<<<num_sms() * kLongCTAs, 256, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
                                                              val ? t_val : nullptr, long_rows, long_rows_count);
     return launch_status("csr_transpose");
 }
@@ -933,10 +946,10 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
                                         long_count);
     ::dgnn::note_launch();
-    lap_count_warp_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
+    lap_count_warp_kernel<<<num_sms(), 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
                                                 long_count);
     ::dgnn::note_launch();
-    lap_count_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed,
+    lap_count_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed,
                                                                      out_rowptr, long_rows, long_count);
     int rc = exclusive_scan_i32(out_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
     if (rc) return rc;
@@ -944,10 +957,10 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     lap_write_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
                                         out_val32, out_val64, out_cap);
     ::dgnn::note_launch();
-    lap_write_warp_kernel<<<kSMs, 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
+    lap_write_warp_kernel<<<num_sms(), 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
                                                 out_val32, out_val64, out_cap, long_rows, long_count);
     ::dgnn::note_launch();
-    lap_write_long_kernel<<<kSMs * kLongCTAs, kLongThreads, 0, st>>>(
+    lap_write_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(
         n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col, out_val32, out_val64, out_cap, long_rows,
         long_count);
     return launch_status("laplacian");

@@ -207,7 +207,7 @@ int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const dou
     constexpr int G = EP / 4 >= 32 ? 32 : EP / 4;
     constexpr int RW = 32 / G;
     int64_t blocks = cdiv(cdiv(n, RW), 8);
-    blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+    blocks = blocks < 1 ? 1 : (blocks > 16 * num_sms() ? 16 * num_sms() : blocks);
     ::dgnn::note_launch();
     head_scatter_kernel<EP><<<(unsigned)blocks, 256, (size_t)2 * EP * C * sizeof(float), st>>>(n, ptr, slot, dl,
                                                                                                 hw, C, dz);
@@ -224,7 +224,7 @@ int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const dou
 // accumulators of its 8 dims (u and v side).  Pairs are assigned statically
 // (fixed grid), groups / warps / CTAs are combined in fixed order and the
 // per-CTA partials are reduced by head_lg_reduce_kernel: deterministic.
-constexpr int kHeadCtas = kSMs;
+static int head_ctas() { return num_sms(); }
 
 template <int EP>
 __global__ void __launch_bounds__(256) head_loss_grad_kernel(int64_t npairs, const int32_t* __restrict__ u,
@@ -353,7 +353,7 @@ int head_loss_grad_t(int64_t npairs, const int32_t* u, const int32_t* v, const i
                      const float* hw, const float* hb, double scale, double* loss_pp, double* dlogits, double* ghw,
                      double* ghb, double* part, cudaStream_t st) {
     int64_t blocks = cdiv(npairs, 256 / (EP / 8));
-    blocks = blocks > kHeadCtas ? kHeadCtas : (blocks < 1 ? 1 : blocks);
+    blocks = blocks > head_ctas() ? head_ctas() : (blocks < 1 ? 1 : blocks);
     note_launch();
     head_loss_grad_kernel<EP><<<(unsigned)blocks, 256, 0, st>>>(npairs, u, v, y, z, 2, hw, hb, scale, loss_pp,
                                                                  dlogits, part);
@@ -376,7 +376,7 @@ int dgnn_head_loss(int64_t npairs, const int32_t* u, const int32_t* v, const int
     DGNN_CHECK_ARG(n_partials >= npairs, "head_loss: per-pair loss buffer too small");
     if (npairs == 0) return DGNN_OK;
     int64_t blocks = cdiv(npairs, 8);
-    blocks = blocks > 32 * kSMs ? 32 * kSMs : blocks;
+    blocks = blocks > 32 * num_sms() ? 32 * num_sms() : blocks;
     ::dgnn::note_launch();
     head_loss_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(npairs, u, v, y, z, ep, c, hw, hb, scale,
                                                                       loss_pp, dlogits);
@@ -388,7 +388,7 @@ int dgnn_head_predict(int64_t npairs, const int32_t* u, const int32_t* v, const 
     DGNN_CHECK_ARG(c >= 2 && c <= kMaxClasses, "head_predict: classes outside [2, 8]");
     if (npairs == 0) return DGNN_OK;
     int64_t blocks = cdiv(npairs, 8);
-    blocks = blocks > 32 * kSMs ? 32 * kSMs : blocks;
+    blocks = blocks > 32 * num_sms() ? 32 * num_sms() : blocks;
     ::dgnn::note_launch();
     head_predict_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
         npairs, u, v, y, z, ep, c, hw, hb, reinterpret_cast<unsigned long long*>(correct));
@@ -396,7 +396,7 @@ int dgnn_head_predict(int64_t npairs, const int32_t* u, const int32_t* v, const 
 }
 
 size_t dgnn_head_grad_workspace(int32_t ep, int32_t c) {
-    return (size_t)(4 * kSMs) * (2 * ep + 1) * c * sizeof(double) + 256;
+    return (size_t)(4 * num_sms()) * (2 * ep + 1) * c * sizeof(double) + 256;
 }
 
 int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_frame z, int32_t ep, int32_t c,
@@ -409,7 +409,7 @@ int dgnn_head_grad(int64_t npairs, const int32_t* u, const int32_t* v, dgnn_fram
     if (npairs == 0) return DGNN_OK;
     cudaStream_t st = as_stream(stream);
     int64_t nch = cdiv(npairs, 256);
-    nch = nch > 4 * kSMs ? 4 * kSMs : nch;
+    nch = nch > 4 * num_sms() ? 4 * num_sms() : nch;
     const int64_t per = cdiv(npairs, nch);
     nch = cdiv(npairs, per);
     double* part = reinterpret_cast<double*>(ws);

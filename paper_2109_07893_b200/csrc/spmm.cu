@@ -150,7 +150,7 @@ template <int F, int H, int MODE>
 int hub_rows_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val, dgnn_frame x, const float* w,
                dgnn_frame s_out, dgnn_frame r_out, cudaStream_t st) {
     int64_t blocks = cdiv(n, 256);
-    blocks = blocks > 4 * kSMs ? 4 * kSMs : (blocks < 1 ? 1 : blocks);
+    blocks = blocks > 4 * num_sms() ? 4 * num_sms() : (blocks < 1 ? 1 : blocks);
     ::dgnn::note_launch();
     hub_rows_kernel<F, H, MODE><<<(unsigned)blocks, 256, 0, st>>>(n, rp, col, val, x, w, s_out, r_out);
     return launch_status("hub_rows");
@@ -332,7 +332,7 @@ int spmm_f32_t(int32_t n, const int32_t* rp, const int32_t* col, const float* va
                dgnn_frame out, cudaStream_t st) {
     constexpr int RW = 32 / (F / 4);
     int64_t blocks = cdiv(cdiv(n, RW), 8);
-    blocks = blocks < 1 ? 1 : (blocks > 32 * kSMs ? 32 * kSMs : blocks);
+    blocks = blocks < 1 ? 1 : (blocks > 32 * num_sms() ? 32 * num_sms() : blocks);
     ::dgnn::note_launch();
     spmm_f32_kernel<F><<<(unsigned)blocks, 256, 0, st>>>(n, rp, col, val, x, out);
     const int rc = launch_status("spmm_f32");
@@ -346,7 +346,7 @@ int gcn_fwd_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val
     if constexpr (FP == 4 && !AGG) {
         constexpr int LPR = HP / 4 >= 32 ? 32 : HP / 4, RPW = 32 / LPR;
         int64_t blocks = cdiv(cdiv(n, RPW), 8);
-        blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+        blocks = blocks < 1 ? 1 : (blocks > 16 * num_sms() ? 16 * num_sms() : blocks);
         ::dgnn::note_launch();
         gcn_fwd_narrow_kernel<HP, SKIP><<<(unsigned)blocks, 256, 0, st>>>(n, x, w, s_out, r_out);
         return launch_status("gcn_forward (narrow)");
@@ -356,7 +356,7 @@ int gcn_fwd_t(int32_t n, const int32_t* rp, const int32_t* col, const float* val
     auto k = gcn_fwd_kernel<FP, HP, SKIP, AGG>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t blocks = cdiv(cdiv(n, RW), 8);
-    blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+    blocks = blocks < 1 ? 1 : (blocks > 16 * num_sms() ? 16 * num_sms() : blocks);
     ::dgnn::note_launch();
     k<<<(unsigned)blocks, 256, smem, st>>>(n, rp, col, val, x, w, s_out, r_out);
     return launch_status("gcn_forward");
@@ -369,7 +369,7 @@ int gcn_bwd_t(int32_t n, dgnn_frame dr, dgnn_frame r, const float* w, dgnn_frame
     auto k = gcn_bwd_rows_kernel<FP, HP, SKIP>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t blocks = cdiv(cdiv(n, RW), 8);
-    blocks = blocks < 1 ? 1 : (blocks > 16 * kSMs ? 16 * kSMs : blocks);
+    blocks = blocks < 1 ? 1 : (blocks > 16 * num_sms() ? 16 * num_sms() : blocks);
     ::dgnn::note_launch();
     k<<<(unsigned)blocks, 256, smem, st>>>(n, dr, r, w, ds);
     return launch_status("gcn_backward_rows");

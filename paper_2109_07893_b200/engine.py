@@ -132,6 +132,11 @@ class Rank:
         wmax = max(Ly.ho for Ly in layers)
         self.dZ_own = _zeros(P * C * NP * wmax, device=dev)
         self.dY_vm = self.dZ_own if same else recv(B * NP * wmax)
+        # peer pushes: the owner pushes layer l-1's seeds as soon as every
+        # rank's ds of one step has arrived, while the receiver may still read
+        # lower steps of layer l's seeds; the two layers' seeds therefore
+        # alternate between two receive buffers (layer parity)
+        self.dY_alt = recv(B * NP * wmax) if (peer is not None and not same) else self.dY_vm
         self.dR_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
         self.dR_vm = self.dR_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
         self.dS = _zeros(N * max(Ly.fp for Ly in layers), device=dev)
@@ -183,6 +188,10 @@ class Rank:
     def vm(self, buf, W, i):
         NP = self.eng.plan.NP
         return buf[i * NP * W:(i + 1) * NP * W]
+
+    def dy_buf(self, l):
+        """Vertex-major receive buffer of layer l's output gradients."""
+        return self.dY_alt if l % 2 else self.dY_vm
 
     def plain(self, buf, W, c=0) -> _lib.Frame:
         N = self.eng.plan.N
@@ -681,7 +690,7 @@ class Rank:
         for step, i in enumerate(reversed(range(B))):
             if before_step is not None:
                 before_step(i)
-            dy = self.vm(self.dY_vm, ho, i)
+            dy = self.vm(self.dy_buf(l), ho, i)
             gates = self.vm(self.G_vm[l], 4 * ho, i)
             c_prev = self.vm(self.C_vm[l], ho, i - 1) if i > 0 else self.act[l][1]
             c_new = self.vm(self.C_vm[l], ho, i)
@@ -741,7 +750,7 @@ class Rank:
         first = {}
         for t in ts:
             lo = max(0, t - w + 1)
-            dzt = self.vm(self.dY_vm, Ly.ho, t - ts[0])
+            dzt = self.vm(self.dy_buf(l), Ly.ho, t - ts[0])
             for k in range(lo, t + 1):
                 coef = float(m[t, k])
                 if k >= ts[0]:
@@ -871,13 +880,18 @@ class Engine:
             wmax = max(Ly.ho for Ly in lay.layers)
             need = sum(Pn * Cn * NPn * Ly.ho + 64 for Ly in lay.layers)
             need += sum(Bn * NPn * Ly.fp + Pn * Cn * NPn * Ly.fp + 128 for Ly in lay.layers[1:])
-            need += Bn * NPn * wmax + 64
+            need += 2 * (Bn * NPn * wmax + 64)
             try:
                 self.peer = PeerExchange(torch.device(device) if device is not None else
                                          torch.device("cuda", torch.cuda.current_device()), need)
             except Exception as exc:     # no symmetric memory on this node: NCCL transport
                 import warnings
                 warnings.warn(f"peer exchange unavailable ({exc}); using NCCL all-to-alls")
+                self.peer = None
+            if self.peer is not None and self._ch(3, len(lay.layers) - 1, Bn - 1) > self.peer.max_channel:
+                import warnings
+                warnings.warn(f"peer exchange needs {self._ch(3, len(lay.layers) - 1, Bn - 1)} signal channels, "
+                              f"the pad holds {self.peer.max_channel}; using NCCL all-to-alls")
                 self.peer = None
         # one rank per GPU: per-step exchanges overlapping the split GCN / LSTM
         # (measured, N = 2: 247 vs 260 ms per epoch; N = 4: 304 vs 264 -- at
@@ -904,7 +918,9 @@ class Engine:
 
     # ------------------------------------------------------------------ setup
     def set_labels(self, train_by_time, test_by_time=None, key=None):
-        key = key if key is not None else (id(train_by_time), id(test_by_time))
+        if key is None:
+            from .api import _labels_key
+            key = _labels_key(train_by_time or {}, test_by_time or {})
         if self.prepared_labels == key:
             return
         for r in self.ranks:
@@ -1042,7 +1058,7 @@ class Engine:
             r._head_step(c, r.ts[c])
             for k in range(P):
                 q = (me + k) % P
-                peer.push(r.own_slab_rows(r.dZ_own, top.ho, c, q), r.vm(r.dY_vm, top.ho, j), q,
+                peer.push(r.own_slab_rows(r.dZ_own, top.ho, c, q), r.vm(r.dy_buf(len(layers) - 1), top.ho, j), q,
                           self._ch(DY, len(layers) - 1, j))
         self.bytes_moved += F32 * C * plan.NP * top.ho * (P - 1)
         for l in reversed(range(len(layers))):
@@ -1072,7 +1088,7 @@ class Engine:
                     r.gcn_transpose_aggregate_step(l, c)
                     for k in range(P):
                         q = (me + k) % P
-                        peer.push(r.own_slab_rows(r.dZ_own, Ly.fp, c, q), r.vm(r.dY_vm, Ly.fp, j), q,
+                        peer.push(r.own_slab_rows(r.dZ_own, Ly.fp, c, q), r.vm(r.dy_buf(l - 1), Ly.fp, j), q,
                                   self._ch(DY, l - 1, j))
                 self.bytes_moved += F32 * C * plan.NP * Ly.fp * (P - 1)
         peer.drain()
@@ -1239,10 +1255,20 @@ class Engine:
         return loss_dev, grads
 
     def finish(self, loss_dev, grads):
-        loss = float(loss_dev.item()) * (self.scale if self.scale else 1.0)
+        try:
+            loss = float(loss_dev.item()) * (self.scale if self.scale else 1.0)
+        except RuntimeError as exc:
+            if self.peer is not None:
+                # a peer signal that never arrived traps its wait kernel (peer.TIMEOUT_MS)
+                raise ProtocolError(f"peer exchange failed: a block push was not received ({exc})") from exc
+            raise
+        self.check()
+        return loss
+
+    def check(self):
+        """CorruptDeltaError if any rank's graph rebuild saw an inconsistent delta."""
         for r in self.ranks:
             r.mat.check()
-        return loss
 
     def evaluate(self):
         """Straight-line forward with the current parameters (`models.py:275-323`)
@@ -1258,6 +1284,7 @@ class Engine:
             for r in self.ranks:
                 r.predict(b)
         correct = self.fabric.allreduce([sum_ranks([r.correct for r in self.ranks])])
+        self.check()
         total = sum(d["n"] for r in self.ranks for d in r.lab.get("test", {}).values())
         if self.fabric.distributed:
             t = torch.tensor([total], dtype=torch.int64, device=self.device)
@@ -1283,6 +1310,7 @@ class Engine:
                     for q in range(plan.P):
                         rows.append(r.own_slab_rows(r.Y_own[-1], Ly.ho, c, q).view(plan.NP, Ly.ho)[:, :E])
                     frames[t] = torch.cat(rows).double().cpu().numpy()
+        self.check()
         return frames
 
 

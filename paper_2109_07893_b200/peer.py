@@ -14,7 +14,14 @@ so a block's offset in the local buffer is its offset on every peer.
 
 from __future__ import annotations
 
+import os
+
 import torch
+
+# a signal that does not arrive within this time traps the waiting kernel (a
+# lost push or a rank that left the schedule); the engine reports it as
+# ProtocolError instead of hanging (engine.Engine.finish)
+TIMEOUT_MS = int(os.environ.get("DGNN_PEER_TIMEOUT_MS", "120000"))
 
 
 class PeerExchange:
@@ -67,7 +74,7 @@ class PeerExchange:
     def wait(self, src_rank: int, channel: int) -> None:
         """The current stream waits for `src_rank`'s push on `channel`."""
         if src_rank != self.rank:
-            self.hdl.wait_signal(src_rank, channel)
+            self.hdl.wait_signal(src_rank, channel, timeout_ms=TIMEOUT_MS)
 
     def drain(self) -> None:
         """The current stream waits for every push issued so far (before a
@@ -77,4 +84,4 @@ class PeerExchange:
     def barrier(self) -> None:
         """Stream-ordered barrier of all ranks (channel 0): nobody pushes into
         a buffer a peer may still be reading from the previous pass."""
-        self.hdl.barrier(channel=0)
+        self.hdl.barrier(channel=0, timeout_ms=TIMEOUT_MS)
