@@ -79,14 +79,18 @@ VALUE_ENTRY_BYTES = 8
 @dataclass
 class TransferLedger:
     """Reference counters for the Laplacian stream (`delta.py:57-100`);
-    `h2d_bytes` / `full_equiv_bytes` are what this package actually copied
-    over PCIe and what the same encoding would cost without deltas."""
+    `h2d_bytes` is what this package actually copied over PCIe,
+    `full_equiv_bytes` what the reference schedule (every snapshot of every
+    pass streamed) would cost with full snapshots in the same encoding, and
+    `full_built_bytes` the full-snapshot bytes of the passes that were
+    actually streamed and rebuilt (like for like)."""
     index_entries_sent: int = 0
     value_entries_sent: int = 0
     snapshots_full: int = 0
     snapshots_delta: int = 0
     h2d_bytes: int = 0
     full_equiv_bytes: int = 0
+    full_built_bytes: int = 0
 
     def charge_full(self, snapshot) -> None:
         self.index_entries_sent += snapshot.nnz
@@ -100,7 +104,7 @@ class TransferLedger:
 
     def merge(self, other: "TransferLedger") -> None:
         for k in ("index_entries_sent", "value_entries_sent", "snapshots_full", "snapshots_delta",
-                  "h2d_bytes", "full_equiv_bytes"):
+                  "h2d_bytes", "full_equiv_bytes", "full_built_bytes"):
             setattr(self, k, getattr(self, k) + getattr(other, k))
 
     def delta_fraction(self) -> float:
@@ -344,6 +348,18 @@ def _labels_key(*labelsets):
     return tuple(key)
 
 
+def _bytes(eng):
+    return tuple(sum(getattr(r.mat, k) for r in eng.ranks)
+                 for k in ("bytes_h2d", "bytes_full_equiv", "bytes_full_built"))
+
+
+def _charge_bytes(transfer, eng, before):
+    now = _bytes(eng)
+    transfer.h2d_bytes += now[0] - before[0]
+    transfer.full_equiv_bytes += now[1] - before[1]
+    transfer.full_built_bytes += now[2] - before[2]
+
+
 def _count(labels):
     return sum(np.asarray(p).shape[0] for p, _ in _by_time(labels).values())
 
@@ -366,11 +382,10 @@ def distributed_epoch(cfg, data, labels, params: dict, workers: int, nblk: int,
     eng = get_engine(cfg, data, workers, nblk)
     eng.set_labels(_by_time(labels), None, key=_labels_key(labels, None))
     eng.params.load(params)
-    before = sum(r.mat.bytes_h2d for r in eng.ranks), sum(r.mat.bytes_full_equiv for r in eng.ranks)
+    before = _bytes(eng)
     loss_dev, grads = eng.epoch(comm, transfer, act, _count(labels), reduction)
     loss = eng.finish(loss_dev, grads)
-    transfer.h2d_bytes += sum(r.mat.bytes_h2d for r in eng.ranks) - before[0]
-    transfer.full_equiv_bytes += sum(r.mat.bytes_full_equiv for r in eng.ranks) - before[1]
+    _charge_bytes(transfer, eng, before)
     g = eng.layout.unflatten(grads.cpu().numpy())
     if not _count(labels):
         loss = 0.0
@@ -413,15 +428,14 @@ def train_distributed(cfg, data, train_labels, test_labels, epochs: int, seed: i
     eng.params.v.zero_()
     count = _count(train_labels)
     for epoch in range(1, epochs + 1):
-        before = sum(r.mat.bytes_h2d for r in eng.ranks), sum(r.mat.bytes_full_equiv for r in eng.ranks)
+        before = _bytes(eng)
         loss_dev, grads = eng.epoch(comm, transfer, act, count, "mean")
         if count:
             loss = eng.finish(loss_dev, grads)
         else:
             loss = 0.0
             eng.check()
-        transfer.h2d_bytes += sum(r.mat.bytes_h2d for r in eng.ranks) - before[0]
-        transfer.full_equiv_bytes += sum(r.mat.bytes_full_equiv for r in eng.ranks) - before[1]
+        _charge_bytes(transfer, eng, before)
         eng.params.adam(lr)
         acc = eng.evaluate()
         trace.append({"epoch": epoch, "loss": loss, "test_accuracy": acc})

@@ -60,6 +60,12 @@ SPLIT_GCN = os.environ.get("DGNN_SPLIT_GCN", "1")
 # into symmetric (NVLink peer) memory, per block, overlapping compute;
 # "nccl" = NCCL all-to-alls (bulk, or per step at P = 2)
 EXCHANGE = os.environ.get("DGNN_EXCHANGE", "peer")
+# keep every owned snapshot rebuilt in an epoch's forward sweep for the
+# checkpoint rerun and evaluation ("auto": when the slot sets fit 12% of HBM)
+KEEP_GRAPHS = os.environ.get("DGNN_KEEP_GRAPHS", "auto")
+# rebuild a chunk head from the 1-step delta on top of the previous rank's
+# last snapshot (handed over NVLink between GPUs) instead of shipping it full
+HEAD_CHAIN = os.environ.get("DGNN_HEAD_CHAIN", "1")
 
 
 class Plan:
@@ -106,13 +112,22 @@ class Rank:
         plan, layers = eng.plan, eng.layout.layers
         P, C, B, N, NP = plan.P, plan.chunk, plan.bsize, plan.N, plan.NP
         dev = self.dev
-        self.mat = Materializer(eng.enc, dev, slots=C, resident=eng.resident, sets=2)
-        self.prefetched = {}     # block -> (slots, ready event) rebuilt ahead of its pass
+        # graph slot sets: with keep_graphs one set per block (+ one for the
+        # next epoch's block 0): every owned snapshot rebuilt in the forward
+        # sweep stays resident for the checkpoint rerun and the evaluation
+        # passes; otherwise two sets, the next pass's chunk rebuilt ahead
+        self.keep_graphs = eng.keep_graphs
+        self.mat = Materializer(eng.enc, dev, slots=C, resident=eng.resident,
+                                sets=plan.nblk + 1 if self.keep_graphs else 2, graph_stream=eng.shared_graph_stream)
+        self.prefetched = {}     # block -> (slots, ready event) rebuilt ahead of its pass (two-set mode)
         self.set_turn = 0
+        self.built = {}          # block -> (slots, ready event, epoch tag) (keep_graphs mode)
         self.skip = eng.skip
         L = len(layers)
         # snapshot-major (owner layout) and vertex-major buffers
-        self.R_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
+        # the split GCN (cd-gcn, P > 1) keeps r / dr vertex-major only: no owner-layout copies
+        split_mode = eng.split
+        self.R_own = [_zeros(0 if split_mode else P * C * NP * Ly.rw, device=dev) for Ly in layers]
         # receive buffers of the peer (copy-engine) exchange live in one
         # symmetric allocation, same offsets on every rank
         peer = eng.peer
@@ -137,7 +152,7 @@ class Rank:
         # lower steps of layer l's seeds; the two layers' seeds therefore
         # alternate between two receive buffers (layer parity)
         self.dY_alt = recv(B * NP * wmax) if (peer is not None and not same) else self.dY_vm
-        self.dR_own = [_zeros(P * C * NP * Ly.rw, device=dev) for Ly in layers]
+        self.dR_own = [_zeros(0 if split_mode else P * C * NP * Ly.rw, device=dev) for Ly in layers]
         self.dR_vm = self.dR_own if same else [_zeros(B * NP * Ly.rw, device=dev) for Ly in layers]
         self.dS = _zeros(N * max(Ly.fp for Ly in layers), device=dev)
         if self.skip:
@@ -266,30 +281,47 @@ class Rank:
             self.loss_t.zero_()
         self.correct.zero_()
 
-    def begin_block(self, b, keep, ledger=None, count_bytes=True, next_b=None):
+    def begin_block(self, b, keep, ledger=None, count_bytes=True, next_b=None, fresh=False):
         """`dist.py:301-318`: stream the owned chunk through the codec and pick
         the carried state (forward sweep) or pi_{b-1} (checkpoint rerun).
-        `next_b`: the block of the following pass, whose graph is rebuilt on
-        the graph stream (into the other slot set) while this block computes."""
+        `fresh`: the epoch's forward sweep, which streams and rebuilds the
+        chunk (keep_graphs mode: the rerun and evaluation passes reuse it).
+        Two-set mode: `next_b` is the block of the following pass, rebuilt on
+        the graph stream (into the other slot set) while this block computes;
+        keep_graphs mode: see `prefetch`."""
         self.b, self.keep = b, keep
         self.ts = self.eng.plan.steps_of(self.q, b)
         # everything enqueued so far (the previous block) is done with the
         # slot set that block used two passes ago
         released = torch.cuda.Event()
         released.record(torch.cuda.current_stream(self.dev))
-        if b in self.prefetched:
+        self.released = released
+        if self.keep_graphs:
+            ent = self.built.get(b)
+            if ent is None or (fresh and ent[2] != self.eng.epoch_id):
+                ent = self._build(b, self.eng.epoch_id, released, chained=not keep, count_bytes=count_bytes)
+            self.slots, self.ready_ev = ent[0], ent[1]
+            self.mat.account(self.ts, ledger, count_bytes)
+        elif b in self.prefetched:
             self.slots, self.ready_ev = self.prefetched.pop(b)
             self.mat.account(self.ts, ledger, count_bytes)
         else:
             self.set_turn ^= 1
             self.slots = self.mat.materialize(self.ts, ledger=ledger, count_bytes=count_bytes,
-                                              set_idx=self.set_turn, after=released)
+                                              set_idx=self.set_turn, after=released,
+                                              head_prev=None if keep else self._neighbor_head(self.ts[0]))
             self.ready_ev = self.mat.ready
-        if next_b is not None and len(self.eng.plan.steps_of(self.q, next_b)):
+            if not keep:
+                self._after_build(self.ts)
+        if not self.keep_graphs and next_b is not None and len(self.eng.plan.steps_of(self.q, next_b)):
             self.set_turn ^= 1
             nts = self.eng.plan.steps_of(self.q, next_b)
-            slots = self.mat.materialize(nts, ledger=None, count_bytes=False, set_idx=self.set_turn,
-                                         after=released)
+            ascending = next_b > b or (next_b == b and not keep)
+            slots = self.mat.materialize(nts, ledger=None, count_bytes=count_bytes, set_idx=self.set_turn,
+                                         after=released, consume=False,
+                                         head_prev=self._neighbor_head(nts[0]) if ascending and next_b != b else None)
+            if ascending and next_b != b:
+                self._after_build(nts)
             self.prefetched[next_b] = (slots, self.mat.ready)
         self.graph_waited = False
         if self.skip:
@@ -297,6 +329,63 @@ class Rank:
                 self.act = self.pi[b - 1] if b > 0 else self.zero_state
             else:
                 self.act = self.state
+
+    def prefetch(self, b, next_epoch=False, count_bytes=True):
+        """keep_graphs mode: rebuild block b's chunk ahead of its pass, for
+        this epoch's forward sweep (or, `next_epoch`, the next one's), while
+        the current block computes.  Called for every rank after every rank's
+        `begin_block`, so the chunks of one block are rebuilt in rank order
+        and each head can be rebuilt from its predecessor's last snapshot."""
+        if not self.keep_graphs or b >= self.eng.plan.nblk:
+            return
+        tag = self.eng.epoch_id + (1 if next_epoch else 0)
+        ent = self.built.get(b)
+        if ent is not None and ent[2] == tag:
+            return
+        self._build(b, tag, self.released, chained=True, count_bytes=count_bytes)
+
+    def _build(self, b, tag, after, chained, count_bytes):
+        plan = self.eng.plan
+        ts = plan.steps_of(self.q, b)
+        # block 0 alternates between two sets across epochs: the next epoch's
+        # block 0 is rebuilt while this epoch's last rerun still reads it
+        set_idx = plan.nblk if (b == 0 and tag % 2) else b
+        slots = self.mat.materialize(ts, ledger=None, count_bytes=count_bytes, set_idx=set_idx, after=after,
+                                     head_prev=self._neighbor_head(ts[0]) if chained else None, consume=False)
+        if chained:
+            self._after_build(ts)
+        ent = (slots, self.mat.ready, tag)
+        self.built[b] = ent
+        return ent
+
+    def _neighbor_head(self, t0):
+        """head_prev for a chunk whose head t0 > 0 follows a snapshot owned
+        by another rank: that rank's raw CSR of A_{t0-1} (emulated ranks:
+        read in place on the shared graph stream; one rank per GPU: received
+        over NVLink, `HeadChain`), or None (the head travels in full)."""
+        eng, plan = self.eng, self.eng.plan
+        if t0 == 0 or not eng.head_chain_on:
+            return None
+        src = plan.owner_of(t0 - 1)
+        if src == self.q:
+            return None          # own previous snapshot: the materialiser's raw_t chain
+        if not eng.fabric.distributed:
+            nb = eng.rank_of[src]
+            return nb.mat.raw() if nb.mat.raw_t == t0 - 1 else None
+        return eng.head_chain.recv_spec(src, int(eng.enc.nnz[t0 - 1]))
+
+    def _after_build(self, ts):
+        """One rank per GPU: hand the chunk's last raw snapshot to the rank
+        whose chunk starts right after it (NVLink, on the graph stream)."""
+        eng, plan = self.eng, self.eng.plan
+        t1 = ts[-1]
+        if eng.head_chain is None or t1 + 1 >= plan.T:
+            return
+        dst = plan.owner_of(t1 + 1)
+        if dst == self.q:
+            return
+        rp, col = self.mat.raw()
+        eng.head_chain.send(rp, col, int(eng.enc.nnz[t1]), dst, self.mat.graph_stream)
 
     def _wait_graph(self):
         if not self.graph_waited:
@@ -563,10 +652,16 @@ class Rank:
             for j, k in enumerate(range(lo, t + 1)):
                 call("dgnn_axpy_frame", cnt, float(m[t, k]), ptr(src(k)), ptr(out), int(j == 0), st)
         if not self.keep:
-            # the rerun of block b+1 reads these again (reference keeps them all, dist.py:359-361)
+            # the rerun of block b+1 reads these again (the reference keeps
+            # them for the whole epoch, dist.py:359-361)
             keepn = min(w, len(ts))
             for t in ts[-keepn:]:
                 self.trail[l][t] = self.vm(self.R_vm[l], Ly.rw, t - ts[0]).clone()
+        else:
+            # frames produced by block b-1 were last read by this rerun (block
+            # b-1's own rerun recomputes them): free them (HBM plan, c5)
+            for k in [k for k in self.trail[l] if ts[0] - len(ts) <= k < ts[0]]:
+                del self.trail[l][k]
 
     def store_pi(self, b):
         if self.skip and b < self.eng.plan.nblk - 1:
@@ -901,6 +996,23 @@ class Engine:
         self.bytes_moved = 0      # bytes that crossed the fabric (all ranks of this process)
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
+        self.epoch_id = 0
+        self.keep_graphs = self._plan_keep_graphs(dev)
+        # emulated ranks share one graph stream: a chunk head is rebuilt from
+        # the previous rank's last raw snapshot in place, in stream order
+        self.shared_graph_stream = (torch.cuda.Stream(device=dev, priority=-1)
+                                    if (not self.fabric.distributed and workers > 1) else None)
+        self.head_chain_on = HEAD_CHAIN != "0"
+        self.head_chain = None
+        if self.fabric.distributed and workers > 1 and self.keep_graphs and self.head_chain_on:
+            try:
+                from .peer import HeadChain
+                self.head_chain = HeadChain(dev, N, self.enc.cap_a)
+            except Exception as exc:     # no symmetric memory: chunk heads travel in full
+                import warnings
+                warnings.warn(f"NVLink head chain unavailable ({exc}); chunk heads are sent in full")
+        if self.fabric.distributed and workers > 1 and self.head_chain is None:
+            self.head_chain_on = False
         self.params = DeviceParams(self.layout, dev)
         if self.fabric.distributed:
             import torch.distributed as dist
@@ -912,9 +1024,21 @@ class Engine:
         else:
             ids = list(range(workers))
         self.ranks = [Rank(self, q, dev) for q in ids]
+        self.rank_of = {r.q: r for r in self.ranks}
         self.feats_host = feats_host
         self.prepared_labels = None
         self.scale = 1.0
+
+    def _plan_keep_graphs(self, dev):
+        """Keep every owned snapshot of an epoch resident (SURVEY §7 hard
+        part 3, fix 3) when its slot sets fit the HBM budget."""
+        if KEEP_GRAPHS in ("0", "1"):
+            return KEEP_GRAPHS == "1"
+        plan, enc = self.plan, self.enc
+        slot = 2 * 4 * (plan.N + 1) + 2 * enc.cap_hat * (4 + 4)
+        need = (plan.nblk + 1) * plan.chunk * slot
+        total = torch.cuda.get_device_properties(dev).total_memory
+        return need <= 0.12 * total
 
     # ------------------------------------------------------------------ setup
     def set_labels(self, train_by_time, test_by_time=None, key=None):
@@ -1182,9 +1306,12 @@ class Engine:
         for r in self.ranks:
             r.reset_state()
         self.params.zero_grad()
+        self.epoch_id += 1
         for b in range(plan.nblk):
             for r in self.ranks:
-                r.begin_block(b, keep=False, ledger=transfer, next_b=b + 1 if b + 1 < plan.nblk else b)
+                r.begin_block(b, keep=False, ledger=transfer, next_b=b + 1 if b + 1 < plan.nblk else b, fresh=True)
+            for r in self.ranks:
+                r.prefetch(b + 1)
             self._layers_forward(b, "forward", comm)
             for r in self.ranks:
                 if self.cfg.classes != 2:
@@ -1199,6 +1326,9 @@ class Engine:
                 # the last rerun prefetches block 0 again: the next pass (the
                 # next epoch's forward sweep, or an evaluation) starts there
                 r.begin_block(b, keep=True, ledger=transfer, next_b=b - 1 if b > 0 else 0)
+            if b == 0:
+                for r in self.ranks:
+                    r.prefetch(0, next_epoch=True)
             self._layers_forward(b, "rerun", comm)
             if self.split_pipe or self.peer is not None:
                 if self.peer is not None:
@@ -1208,6 +1338,7 @@ class Engine:
                 if act is not None:
                     act.free_activations(plan.bsize * 2 * L)
                     act.free_checkpoint(1.0)
+                self._release_checkpoint(b)
                 continue
             pipe_gcn, pipe_lstm = self._pipelining()
             works = []
@@ -1244,6 +1375,7 @@ class Engine:
             if act is not None:
                 act.free_activations(plan.bsize * 2 * L)
                 act.free_checkpoint(1.0)
+            self._release_checkpoint(b)
         grads = self.fabric.allreduce([self.params.gather_grads()])
         self.params.g.copy_(grads)
         if comm is not None:
@@ -1253,6 +1385,13 @@ class Engine:
                 call("dgnn_sum_f64", plan.T, ptr(r.loss_t), ptr(r.loss_acc), 0, _lib.stream_handle())
         loss_dev = self.fabric.allreduce([sum_ranks([r.loss_acc for r in self.ranks])])
         return loss_dev, grads
+
+    def _release_checkpoint(self, b):
+        """pi_{b-1} was last read by block b's rerun and backward: free it
+        (the reference keeps every pi_b until the epoch ends, dist.py:368, 381;
+        at c5 the checkpoints of every block would not fit beside the caches)."""
+        for r in self.ranks:
+            r.pi.pop(b - 1, None)
 
     def finish(self, loss_dev, grads):
         try:

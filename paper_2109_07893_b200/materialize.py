@@ -202,7 +202,7 @@ class Materializer:
     """Device-side rebuild of the snapshots a rank owns, chunk by chunk."""
 
     def __init__(self, enc: SnapshotEncoding, device, slots: int, resident: bool = False,
-                 with_f64: bool = False, sets: int = 1):
+                 with_f64: bool = False, sets: int = 1, graph_stream=None):
         self.enc = enc
         self.device = torch.device(device)
         n = enc.n
@@ -214,7 +214,8 @@ class Materializer:
         # high priority: the rebuild kernels take SMs as soon as they free up, so
         # a graph-bound pass (large value-carrying graphs) is not starved by
         # the compute stream's persistent kernels
-        self.graph_stream = torch.cuda.Stream(device=self.device, priority=-1)
+        self.graph_stream = graph_stream if graph_stream is not None else \
+            torch.cuda.Stream(device=self.device, priority=-1)
         # encoded input on device: everything (resident) or a chunk-sized staging area
         if resident:
             self.full_dev = enc.full.to(self.device)
@@ -253,16 +254,39 @@ class Materializer:
                     torch.empty(cap_h, **f64) if with_f64 else None))
         self.slots = self.sets[0]
         self.ready_sets = [torch.cuda.Event() for _ in range(sets)]
-        self.bytes_h2d = 0
-        self.bytes_full_equiv = 0
+        self.bytes_h2d = 0            # bytes this materialiser copied host -> device
+        self.bytes_full_equiv = 0     # full-snapshot bytes of every pass consumed (reference schedule)
+        self.bytes_full_built = 0     # full-snapshot bytes of every chunk actually built (like for like)
+        self.builds = []              # (ts, bytes copied, head rebuilt from a delta) per counted build
         self.ready = torch.cuda.Event()
+        self.raw_t = -1               # timestep whose raw CSR sits in a_rowptr[cur] / a_col[cur]
+        self.cur = 0
+        # when a list: (start event, end event, bytes) of every chunk's H2D copies (PCIe timing)
+        self.copy_log = None
 
-    def materialize(self, ts, ledger=None, count_bytes: bool = True, set_idx: int = 0, after=None):
+    def materialize(self, ts, ledger=None, count_bytes: bool = True, set_idx: int = 0, after=None,
+                    head_prev=None, consume: bool = True):
         """Rebuild Ahat_t for the contiguous run `ts` into slots 0..len(ts)-1
         of slot set `set_idx`.  Returns the slots; the set's ready event (and
         `self.ready`) is recorded on the graph stream.  `after`: an event
         marking the end of the set's previous consumers (default: everything
-        already enqueued on the current stream)."""
+        already enqueued on the current stream).
+
+        Chunk head (graph difference across chunks, SURVEY §7 hard part 3):
+        the reference ships the first snapshot of every chunk in full
+        (`delta.py:161-163`).  Here the head A_{t0} is rebuilt from the
+        1-step delta of t0 whenever A_{t0-1} is on the device at this point
+        of the graph stream: this materialiser's own last snapshot (chunks
+        built in time order, e.g. consecutive blocks at P = 1), or
+        `head_prev` = (rowptr, col) of A_{t0-1} from the rank that owns t0-1
+        (a neighbouring rank's raw CSR, same device or received over NVLink;
+        `head_prev[2]`, if given, is an event or callable the graph stream
+        waits on first; `head_prev[3]`, if given, is called once the head
+        has been rebuilt).  Only t = 0 then travels in full.
+
+        `count_bytes` charges the real H2D bytes of this build; `consume`
+        also charges the pass that consumes it (`account`) -- the engine
+        builds ahead of the consuming pass and charges that pass itself."""
         enc = self.enc
         self.slots = self.sets[set_idx]
         self.ready = self.ready_sets[set_idx]
@@ -272,25 +296,46 @@ class Materializer:
         n = enc.n
         gs = self.graph_stream
         gsh = gs.cuda_stream
-        # inputs: H2D on the copy stream (pinned -> HBM) unless resident
+        t0 = ts[0]
+        own_prev = t0 > 0 and self.raw_t == t0 - 1
+        use_delta_head = t0 > 0 and (own_prev or head_prev is not None)
+        # H2D ranges of this build: deltas of t0+1..t1 (and of t0 itself when
+        # the head is rebuilt from A_{t0-1}), the full head otherwise
+        fo, fc = plan.full_range
+        do, dc = plan.delta_range
+        if use_delta_head:
+            fc = 0
+            do = int(enc.delta_off[t0])
+            dc = int(enc.delta_off[ts[-1] + 1] - enc.delta_off[t0])
+        vo, vc = plan.val_range
         if self.resident:
-            fbase, dbase, vbase = plan.full_range[0], plan.delta_range[0], plan.val_range[0]
+            fbase, dbase, vbase = fo, do, vo
         else:
             fbase = dbase = vbase = 0
             cs = self.copy_stream
             cs.wait_stream(gs)                 # staging is free once the previous chunk's rebuild ran
             with torch.cuda.stream(cs):
-                fo, fc = plan.full_range
-                self.full_dev[:fc].copy_(enc.full[fo:fo + fc], non_blocking=True)
-                do, dc = plan.delta_range
+                if self.copy_log is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(cs)
+                if fc:
+                    self.full_dev[:fc].copy_(enc.full[fo:fo + fc], non_blocking=True)
                 if dc:
                     self.delta_dev[:dc].copy_(enc.delta[do:do + dc], non_blocking=True)
                 if not enc.unit:
-                    vo, vc = plan.val_range
                     self.vals_dev[:vc].copy_(enc.vals[vo:vo + vc], non_blocking=True)
+                if self.copy_log is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(cs)
+                    self.copy_log.append((e0, e1, 4 * (fc + dc) + (0 if enc.unit else 8 * vc)))
             gs.wait_stream(cs)
-        self.account(ts, ledger, count_bytes)
-        cur = 0
+        built_bytes = 4 * (fc + dc) + (0 if enc.unit else 8 * vc)
+        if count_bytes:
+            self.bytes_h2d += built_bytes
+            self.bytes_full_built += enc.full_bytes(ts)
+            self.builds.append((list(ts), built_bytes, bool(use_delta_head)))
+        if consume:
+            self.account(ts, ledger, count_bytes)
         voff = vbase
         # slots are overwritten: wait for their consumers on the compute stream
         if after is not None:
@@ -298,23 +343,37 @@ class Materializer:
         else:
             gs.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(gs):
+            cur = self.cur
+            dpos = dbase
+            if use_delta_head and not own_prev:
+                prev_rp, prev_col = head_prev[0], head_prev[1]
+                if len(head_prev) > 2 and head_prev[2] is not None:
+                    w = head_prev[2]
+                    w() if callable(w) else gs.wait_event(w)
+            elif use_delta_head:
+                prev_rp, prev_col = self.a_rowptr[cur], self.a_col[cur]
             for i, t in enumerate(ts):
                 m = int(enc.nnz[t])
-                if i == 0:
+                if i == 0 and not use_delta_head:
                     rows = self.full_dev[fbase:fbase + m]
-                    a_col = self.full_dev[fbase + m:fbase + 2 * m]
                     call("dgnn_rowptr_from_sorted_rows", n, m, ptr(rows), ptr(self.a_rowptr[cur]), gsh)
                     a_rowptr = self.a_rowptr[cur]
-                    dpos = dbase
+                    # the raw CSR lives in a_rowptr / a_col (the staging area is reused)
+                    a_col = self.a_col[cur]
+                    a_col[:m].copy_(self.full_dev[fbase + m:fbase + 2 * m])
                 else:
+                    if i > 0:
+                        prev_rp, prev_col = a_rowptr, a_col
                     nd, ni = int(enc.n_del[t]), int(enc.n_ins[t])
                     d = self.delta_dev[dpos:dpos + 2 * (nd + ni)]
                     dpos += 2 * (nd + ni)
                     nxt = 1 - cur
-                    call("dgnn_csr_apply_delta", n, ptr(a_rowptr), ptr(a_col), nd, ptr(d[:nd]),
+                    call("dgnn_csr_apply_delta", n, ptr(prev_rp), ptr(prev_col), nd, ptr(d[:nd]),
                          ptr(d[nd:2 * nd]), ni, ptr(d[2 * nd:2 * nd + ni]), ptr(d[2 * nd + ni:]),
                          ptr(self.a_rowptr[nxt]), ptr(self.a_col[nxt]), enc.cap_a, ptr(self.ws_apply),
                          self.ws_apply.numel(), ptr(self.status), gsh)
+                    if i == 0 and not own_prev and len(head_prev) > 3 and head_prev[3] is not None:
+                        head_prev[3]()
                     cur = nxt
                     a_rowptr, a_col = self.a_rowptr[cur], self.a_col[cur]
                 a_val = None
@@ -332,15 +391,24 @@ class Materializer:
                      ptr(self.at_val), 1, ptr(s.t_rowptr), ptr(s.t_col), ptr(s.t_val), ptr(s.t_val64),
                      enc.cap_hat, ptr(self.ws_lap), self.ws_lap.numel(), gsh)
                 s.a_rowptr, s.a_t_rowptr, s.t = a_rowptr, self.at_rowptr, t
+            self.cur = cur
+            self.raw_t = ts[-1]
             self.ready.record(gs)
         return self.slots[:len(ts)]
 
+    def raw(self):
+        """(rowptr, col) of the last rebuilt raw snapshot A_{raw_t} (valid at
+        the current end of the graph stream, until the next rebuild)."""
+        return self.a_rowptr[self.cur], self.a_col[self.cur]
+
     def account(self, ts, ledger=None, count_bytes: bool = True):
-        """Charge one streaming pass of `ts` (reference-equivalent ledger
-        counters, real H2D bytes).  Called when a pass consumes a chunk; a
-        chunk rebuilt ahead of its pass is charged by that pass."""
+        """Charge one streaming pass of `ts` as the reference schedule sees it
+        (`stream_block` at every pass, `dist.py:301-312`): the reference
+        ledger counters, and `bytes_full_equiv` = the bytes of this pass's
+        snapshots sent in full.  The real H2D bytes are charged when a chunk
+        is built (`materialize`); a pass that reuses kept snapshots (the
+        checkpoint rerun) copies nothing."""
         if count_bytes:
-            self.bytes_h2d += self.enc.chunk_bytes(ts)
             self.bytes_full_equiv += self.enc.full_bytes(ts)
         if ledger is not None:
             self.enc.charge(ledger, ts)

@@ -85,3 +85,62 @@ class PeerExchange:
         """Stream-ordered barrier of all ranks (channel 0): nobody pushes into
         a buffer a peer may still be reading from the previous pass."""
         self.hdl.barrier(channel=0, timeout_ms=TIMEOUT_MS)
+
+
+class HeadChain:
+    """NVLink hand-off of chunk-boundary snapshots between the graph streams
+    of neighbouring ranks (SURVEY §7 hard part 3, fix 2).
+
+    In a block the ranks own consecutive chunks of timesteps, so the head
+    A_{t0} of rank q's chunk directly follows the last snapshot A_{t0-1} of
+    rank q-1's chunk (rank P-1 -> rank 0 across blocks).  Instead of
+    shipping the head in full over PCIe, rank q-1 pushes its raw CSR of
+    A_{t0-1} (rowptr + col, int32) into rank q's receive buffer with the copy
+    engine and signals; rank q's graph stream waits for it, applies the
+    1-step delta of t0 on top and acknowledges, which frees the buffer for
+    the next hand-off.  Channels: DATA (q-1 -> q), ACK (q -> q-1).  A
+    missing signal traps after TIMEOUT_MS (ProtocolError at the engine)."""
+
+    DATA, ACK = 1, 2
+
+    def __init__(self, device, n: int, cap_a: int):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        group = dist.group.WORLD.group_name
+        symm.enable_symm_mem_for_group(group)
+        self.n = int(n)
+        self.buf = symm.empty(self.n + 1 + int(cap_a), dtype=torch.int32, device=device)
+        self.hdl = symm.rendezvous(self.buf, group)
+        self.sent = {}             # destination -> hand-offs so far
+        self.bytes_pushed = 0
+
+    def send(self, rowptr: torch.Tensor, col: torch.Tensor, nnz: int, dst: int, stream) -> None:
+        """On `stream`: wait until `dst` released the previous hand-off, copy
+        A's raw CSR into its receive buffer, signal."""
+        n = self.n
+        with torch.cuda.stream(stream):
+            if self.sent.get(dst, 0):
+                self.hdl.wait_signal(dst, self.ACK, timeout_ms=TIMEOUT_MS)
+            peer = self.hdl.get_buffer(dst, (n + 1 + nnz,), torch.int32, 0)
+            peer[:n + 1].copy_(rowptr[:n + 1], non_blocking=True)
+            if nnz:
+                peer[n + 1:n + 1 + nnz].copy_(col[:nnz], non_blocking=True)
+            self.hdl.put_signal(dst, self.DATA)
+        self.sent[dst] = self.sent.get(dst, 0) + 1
+        self.bytes_pushed += 4 * (n + 1 + nnz)
+
+    def recv_spec(self, src: int, nnz: int):
+        """head_prev for Materializer.materialize: the local receive buffer,
+        a wait for `src`'s DATA signal and the ACK once the head is rebuilt
+        (both enqueued on the graph stream current at the call)."""
+        n = self.n
+
+        def wait():
+            self.hdl.wait_signal(src, self.DATA, timeout_ms=TIMEOUT_MS)
+
+        def done():
+            self.hdl.put_signal(src, self.ACK)
+
+        return self.buf[:n + 1], self.buf[n + 1:n + 1 + max(nnz, 1)], wait, done

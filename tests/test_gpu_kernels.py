@@ -525,3 +525,51 @@ def test_apply_hub_rows_round_trip_and_corruption():
                            np.concatenate([a.vals, [1.0]]))
     with pytest.raises(pk.CorruptDeltaError):
         pk.apply(a, bad)
+
+
+@pytest.mark.gpu
+def test_materializer_chunk_heads_rebuilt_from_deltas():
+    """SURVEY §7 hard part 3, fixes 2/3: a chunk whose head follows the
+    materialiser's own last snapshot, or a neighbour's (read in place on a
+    shared graph stream), is rebuilt from the 1-step delta -- bit-exact, and
+    only t = 0 crosses PCIe in full."""
+    from paper_2109_07893_b200.materialize import Materializer, SnapshotEncoding
+    from paper_2109_07893_b200.synth import churn_keys
+    n, T = 30_000, 8
+    keys = churn_keys(n, T, 60_000, 0.1, seed=21)
+    g = pk.DynamicGraph(n, [pk.SparseMatrix.from_canonical(n, k // n, k % n) for k in keys])
+    enc = SnapshotEncoding(g)
+
+    def check(slots, ts):
+        for s, t in zip(slots, ts):
+            rp = s.rowptr.cpu().numpy().astype(np.int64)
+            m = int(rp[-1])
+            got = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp)) * n + s.col[:m].cpu().numpy()
+            assert np.array_equal(got, np.union1d(keys[t], np.arange(n, dtype=np.int64) * (n + 1))), t
+
+    # own chain: consecutive chunks, one materialiser
+    mat = Materializer(enc, "cuda", slots=2, sets=2)
+    for i, ts in enumerate(([0, 1], [2, 3], [4, 5], [6, 7])):
+        slots = mat.materialize(ts, set_idx=i % 2)
+        mat.wait()
+        check(slots, ts)
+    assert mat.bytes_h2d == 4 * (int(enc.full_off[1]) + int(enc.delta_off[T] - enc.delta_off[1]))
+    assert [b[2] for b in mat.builds] == [False, True, True, True]
+    # neighbour chain: two materialisers on one graph stream (emulated ranks)
+    gs = torch.cuda.Stream()
+    a = Materializer(enc, "cuda", slots=2, graph_stream=gs)
+    b = Materializer(enc, "cuda", slots=2, graph_stream=gs)
+    sa = a.materialize([0, 1])
+    sb = b.materialize([2, 3], head_prev=a.raw())
+    b.wait()
+    check(sa, [0, 1])
+    check(sb, [2, 3])
+    assert b.builds[0][2] and b.bytes_h2d == 4 * int(enc.delta_off[4] - enc.delta_off[2])
+    # not following anything: the head travels in full
+    c = Materializer(enc, "cuda", slots=2)
+    sc = c.materialize([5, 6])
+    c.wait()
+    check(sc, [5, 6])
+    assert not c.builds[0][2]
+    for m in (mat, a, b, c):
+        m.check()
