@@ -36,19 +36,30 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 # workloads: c2 = BASELINE configs[1] (the default, the headline line);
-# c3 = configs[2] (TM-GCN, banded M-product, AMLSim-style graph), run with
-# --config c3 for the DESIGN table (strong scaling: the whole graph is split
-# over the GPUs)
+# c3 = configs[2] (TM-GCN, banded M-product, AMLSim-style graph); c4 =
+# configs[3] (3M vertices, 300M edges); c5 = configs[4] (10M vertices, 1B
+# edges, 1% churn) -- c4 / c5 are generated and encoded on the GPU
+# (synth.device_churn_graph).  c3-c5 scale strongly: the whole graph is
+# split over the GPUs.  nblk per GPU count: the checkpoint block count the
+# HBM plan needs.
 CONFIGS = {
     "c2": dict(arch="cd-gcn", n=750_000, m=468_750, T=32, hidden=64, churn=0.10, nblk=4, gen="churn",
-               scaling="weak",
+               scaling="weak", cpu_scale=64,
                workload="configs[1] Epinions-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=64, "
                         "N=750k/GPU, T=32, 468,750 edges/snapshot/GPU (15M/GPU total), 10% churn"),
     "c3": dict(arch="tm-gcn", n=1_000_000, m=2_000_000, T=64, hidden=32, churn=0.02, nblk=8, gen="aml",
-               scaling="strong",
+               scaling="strong", cpu_scale=128,
                workload="configs[2] TM-GCN (plain GCN + banded M-product, window 2) hidden=32 on an "
                         "AMLSim-style transaction graph: N=1M, T=64, 2M edges/snapshot (128M total), "
                         "heavy-tailed degrees, 2% churn"),
+    "c4": dict(arch="cd-gcn", n=3_000_000, m=4_687_500, T=64, hidden=32, churn=0.10,
+               nblk={1: 8, 2: 8, 4: 8, 8: 8}, gen="device", scaling="strong", cpu_scale=256,
+               workload="configs[3] Flickr/YouTube-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=32, "
+                        "N=3M, T=64, 4,687,500 edges/snapshot (300M total), 10% churn, snapshot-partitioned"),
+    "c5": dict(arch="cd-gcn", n=10_000_000, m=15_625_000, T=64, hidden=32, churn=0.01,
+               nblk={1: 32, 2: 16, 4: 8, 8: 4}, gen="device", scaling="strong", cpu_scale=1024,
+               workload="configs[4] billion-edge: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=32, N=10M, T=64, "
+                        "15,625,000 edges/snapshot (1B total), 1% churn, gradient checkpointing"),
 }
 CFG = CONFIGS["c2"]
 N_PER_GPU = CFG["n"]
@@ -64,6 +75,12 @@ def select_config(name):
     global CFG, N_PER_GPU, EDGES_PER_GPU, T, HIDDEN, CHURN, NBLK
     CFG = CONFIGS[name]
     N_PER_GPU, EDGES_PER_GPU, T, HIDDEN, CHURN, NBLK = (CFG[k] for k in ("n", "m", "T", "hidden", "churn", "nblk"))
+
+
+def nblk_for(P: int) -> int:
+    return NBLK[P] if isinstance(NBLK, dict) else NBLK
+
+
 METRIC = "training epoch time and edges·snapshots/sec at 1/2/4/8 B200; SpMM HBM GB/s"
 
 
@@ -140,14 +157,26 @@ def scale_of(P: int) -> int:
 
 
 def make_workload(P: int, seed: int = 1):
+    """(cfg, graph, data, train labels, params).  c2 / c3: host generator and
+    the reference's own pair sampler (vectorised, same pairs); c4 / c5: the
+    device generator + encoder and its device pair sampler."""
     import paper_2109_07893_b200 as pk
-    from paper_2109_07893_b200.synth import aml_graph, churn_graph, sample_pairs_fast
     n = N_PER_GPU * scale_of(P)
-    gen = churn_graph if CFG["gen"] == "churn" else aml_graph
-    g = gen(n, T, EDGES_PER_GPU * scale_of(P), CHURN, seed=seed)
+    m = EDGES_PER_GPU * scale_of(P)
     cfg = pk.ModelConfig(CFG["arch"], in_features=2, hidden_features=HIDDEN, embed_features=HIDDEN)
-    data = pk.prepare_training_data(cfg, g)
-    train, _ = sample_pairs_fast(g, THETA, seed + 1000003)
+    if CFG["gen"] == "device":
+        import torch
+        from paper_2109_07893_b200.synth import device_churn_graph
+        g = device_churn_graph(n, T, m, CHURN, seed, torch.device("cuda", torch.cuda.current_device()))
+        train, _ = g.sample_pairs(THETA, seed + 1000003)
+        g.drop_keys()
+        data = pk.TrainingData(graph=g, laps=None, feats=None, s1=None)
+    else:
+        from paper_2109_07893_b200.synth import aml_graph, churn_graph
+        gen = churn_graph if CFG["gen"] == "churn" else aml_graph
+        g = gen(n, T, m, CHURN, seed=seed)
+        data = pk.prepare_training_data(cfg, g)
+        train, _ = pk.sample_link_prediction_sets(g, THETA, seed + 1000003)
     params = pk.init_params(cfg, 0)
     rng = np.random.default_rng(77)          # non-zero head: every upstream gradient is live
     params["head.w"] = rng.uniform(-0.5, 0.5, size=params["head.w"].shape)
@@ -155,31 +184,84 @@ def make_workload(P: int, seed: int = 1):
     return cfg, g, data, train, params
 
 
+def edge_snapshots(g) -> int:
+    """Whole job: edge*snapshots per epoch (raw graph), the paper's metric."""
+    if hasattr(g, "snapshots"):
+        return int(sum(s.nnz for s in g.snapshots))
+    return int(sum(g.nnz))
+
+
+def pcie_h2d_peak(nbytes: int = 1 << 30, reps: int = 5):
+    """Pinned host -> HBM copy rate on this box (GB/s): the PCIe roofline."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        dst.copy_(src, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
 # ---------------------------------------------------------------------------
 # algorithmic work per kernel call (for the roofline)
 
 
-def kernel_work(name, args, l2_bytes, layers_real):
-    """(flops, bytes) of one C-ABI call, from its arguments."""
+TENSOR_KERNELS = ("dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_lstm_forward_step_tc",
+                  "dgnn_lstm_forward_step_ws", "dgnn_lstm_backward_step_ws", "dgnn_lstm_backward_step_tc",
+                  "dgnn_lstm_weight_grad_tc", "dgnn_gemm_tn")
+
+
+def kernel_work(name, args, ctx):
+    """(flops, bytes) of one C-ABI call from its arguments (DESIGN §4's
+    algorithmic units); ctx: l2 bytes, real LSTM widths by padded kx, the
+    mean nnz of Ahat per snapshot.  bytes None: not modelled."""
+    l2, layers_real, nnz = ctx["l2"], ctx["layers_real"], ctx["nnz"]
+
+    def agg(n, f):
+        gather = 4 * f * nnz if 4 * n * f > l2 else 4 * n * f
+        return 4 * (n + 1) + 8 * nnz + gather
+
     if name in ("dgnn_lstm_forward_step", "dgnn_lstm_forward_step_tc", "dgnn_lstm_forward_step_ws"):
         rows, kx, hp, gates = args[0], args[1], args[2], args[11]
         kin, h = layers_real.get(kx, (kx, hp))
-        flops = 2 * rows * (kin + h) * 4 * h
-        byts = 4 * rows * (kin + 4 * h + (4 * h if gates else 0))
-        return flops, byts
+        return 2 * rows * (kin + h) * 4 * h, 4 * rows * (kin + 4 * h + (4 * h if gates else 0))
     if name in ("dgnn_lstm_backward_step", "dgnn_lstm_backward_step_tc", "dgnn_lstm_backward_step_ws"):
         rows, kx, hp = args[0], args[1], args[2]
         kin, h = layers_real.get(kx, (kx, hp))
-        flops = 2 * rows * 4 * h * (kin + h)
-        byts = 4 * rows * (h * 4 + 4 * h + 4 * h + kin + 2 * h)
-        return flops, byts
+        return 2 * rows * 4 * h * (kin + h), 4 * rows * (h * 4 + 4 * h + 4 * h + kin + 2 * h)
+    if name == "dgnn_lstm_weight_grad_tc":
+        rows, kx, hp = args[0], args[2], args[3]
+        kin, h = layers_real.get(kx, (kx, hp))
+        return 2 * rows * (kin + h) * 4 * h, 4 * rows * (kin + h + 4 * h)
     if name == "dgnn_gemm_tn":
         rows, m, n = args[0], args[1], args[2]
         return 2 * rows * m * n, 4 * rows * (m + n)
     if name == "dgnn_gcn_forward":
-        n, rp, fp, hp = args[0], args[1], args[5], args[7]
-        return 0, None
-    return 0, 0
+        n, rp, fp, hg, skip, s_out = args[0], args[1], args[5], args[7], args[8], args[9]
+        rw = fp + hg if skip else hg
+        byts = 4 * n * rw + (4 * n * fp if s_out.ptr else 0)
+        byts += agg(n, fp) if rp is not None else 4 * n * fp
+        return 2 * n * fp * hg, byts
+    if name == "dgnn_spmm_f32":
+        n, f = args[0], args[5]
+        return 2 * nnz * f, agg(n, f) + 4 * n * f
+    if name == "dgnn_axpy_frame":
+        cnt, init = args[0], args[4]
+        return 2 * cnt, (8 if init else 12) * cnt
+    if name == "dgnn_gcn_weight_grad":
+        n, fp, hg, skip = args[0], args[4], args[5], args[6]
+        rw = fp + hg if skip else hg
+        return 2 * n * fp * hg, 4 * n * (fp + 2 * rw)
+    if name == "dgnn_gcn_backward_rows":
+        n, fp, hg, skip = args[0], args[3], args[5], args[6]
+        rw = fp + hg if skip else hg
+        return 2 * n * fp * hg, 4 * n * (2 * rw + fp)
+    return 0, None
 
 
 # C-ABI entry -> kernel name prefix in the committed ncu launch list
@@ -265,18 +347,19 @@ def run_ours(args):
     from paper_2109_07893_b200 import _lib
     from paper_2109_07893_b200.engine import Engine, LocalFabric, NcclFabric
 
+    nblk = nblk_for(P)
     t0 = time.time()
     cfg, g, data, train, params = make_workload(P)
     prep_s = time.time() - t0
     fabric = NcclFabric() if P > 1 else LocalFabric()
-    eng = Engine(cfg, data.graph, P, NBLK, resident=True, fabric=fabric,
+    eng = Engine(cfg, data.graph, P, nblk, resident=True, fabric=fabric,
                  m_matrix=None if data.m_matrix is None else np.asarray(data.m_matrix.matrix),
                  feats_host=None if cfg.architecture == "cd-gcn"
                  else [np.asarray(f, np.float64) for f in data.feats.frames])
     eng.set_labels(train.by_time, None)
     eng.params.load(params)
     count = train.total_pairs()
-    total_es = int(sum(s.nnz for s in g.snapshots))     # whole job: edge*snapshots per epoch (raw graph)
+    total_es = edge_snapshots(g)
 
     def step():
         loss_dev, grads = eng.epoch(None, None, None, count, "mean")
@@ -291,17 +374,18 @@ def run_ours(args):
     layers_real = {}
     for Ly in eng.layout.layers:
         layers_real[Ly.kx] = (Ly.fin + Ly.gout, Ly.out)
-    timed_names = ["dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_lstm_forward_step_tc",
-                   "dgnn_lstm_forward_step_ws", "dgnn_lstm_backward_step_ws",
-                   "dgnn_lstm_backward_step_tc", "dgnn_lstm_weight_grad_tc", "dgnn_gemm_tn", "dgnn_gcn_forward",
-                   "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows", "dgnn_csr_apply_delta",
-                   "dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_head_loss", "dgnn_head_grad", "dgnn_head_loss_grad",
-                   "dgnn_head_scatter"]
+    ctx = {"l2": l2, "layers_real": layers_real, "nnz": float(np.mean(eng.enc.nnz_hat))}
+    timed_names = list(TENSOR_KERNELS) + [
+        "dgnn_gcn_forward", "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows",
+        "dgnn_axpy_frame", "dgnn_csr_apply_delta", "dgnn_laplacian", "dgnn_csr_transpose_staged",
+        "dgnn_head_loss", "dgnn_head_grad", "dgnn_head_loss_grad", "dgnn_head_scatter"]
     if args.timeline:   # every C-ABI call, for the per-stream idle breakdown
-        timed_names = list(_lib._SIGS.keys()) if hasattr(_lib, "_SIGS") else timed_names
+        timed_names = list(_lib._SIGS.keys())
     timer = _lib.KernelTimer(timed_names)
     clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_rank{rank}.csv"
                           if (ROOT / "gpurun_out").exists() else None)
+    if eng.peer is not None:
+        eng.peer.log = []
     if P > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -336,72 +420,104 @@ def run_ours(args):
     # they wait for SMs, so they are not candidates)
     graph_side = {"dgnn_laplacian", "dgnn_csr_transpose_staged", "dgnn_csr_apply_delta",
                   "dgnn_rowptr_from_sorted_rows"}
-    cand = {k: v for k, v in tot.items() if k not in graph_side}
+    cand = {k: v for k, v in tot.items() if k not in graph_side and kernel_work(k, durs[k][0][1], ctx)[1]}
     dom = max(cand, key=cand.get) if cand else None
     roof = None
-    if dom in ("dgnn_lstm_forward_step", "dgnn_lstm_backward_step", "dgnn_lstm_forward_step_tc",
-               "dgnn_lstm_forward_step_ws", "dgnn_lstm_backward_step_ws", "dgnn_lstm_weight_grad_tc",
-               "dgnn_lstm_backward_step_tc", "dgnn_gemm_tn"):
-        fl = sum(kernel_work(dom, a, l2, layers_real)[0] for _, a in durs[dom])
-        by = sum(kernel_work(dom, a, l2, layers_real)[1] for _, a in durs[dom])
+    if dom is not None:
+        fl = sum(kernel_work(dom, a, ctx)[0] for _, a in durs[dom])
+        by = sum(kernel_work(dom, a, ctx)[1] for _, a in durs[dom])
         secs = tot[dom] / 1e3
         tr = ncu_traffic(dom)
-        roof = {"kernel": dom, "bound": "tensor", "achieved": fl / secs / 1e12, "peak": bf16_s,
-                "unit": "TFLOP/s", "frac": fl / secs / 1e12 / bf16_s,
-                "traffic": tr and tr["dram_bytes_per_launch"],
-                "traffic_source": tr and tr["source"],
+        roof = {"kernel": dom, "share_of_step": tot[dom] / (ms * args.steps),
+                "launches": len(durs[dom]), "avg_launch_us": tot[dom] / len(durs[dom]) * 1e3,
                 "algorithmic_bytes_per_launch": by / len(durs[dom]),
-                "peak_source": f"{peak_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
-                "note": "tcgen05 kind::tf32 with the fp32-accurate 3xTF32 split: 3 MMAs per product at half the "
-                        "bf16 rate, so the useful-flop ceiling is bf16/6 (frac_3xtf32_ceiling)",
-                "frac_3xtf32_ceiling": fl / secs / 1e12 / (bf16_s / 6),
-                "hbm_achieved_gbs": by / secs / 1e9, "hbm_frac": by / secs / 1e9 / hbm,
-                "share_of_step": tot[dom] / (ms * args.steps),
-                "launches": len(durs[dom]), "avg_launch_us": tot[dom] / len(durs[dom]) * 1e3}
-    # SpMM (fused GCN forward with aggregation, layer 1) HBM rate
+                "traffic": tr and tr["dram_bytes_per_launch"], "traffic_source": tr and tr["source"],
+                "hbm_achieved_gbs": by / secs / 1e9, "hbm_frac": by / secs / 1e9 / hbm}
+        if dom in TENSOR_KERNELS:
+            roof.update({"bound": "tensor", "achieved": fl / secs / 1e12, "peak": bf16_s, "unit": "TFLOP/s",
+                         "frac": fl / secs / 1e12 / bf16_s,
+                         "peak_source": f"{peak_kind} bf16 dense sustained (MEASURED_PEAKS.json)",
+                         "note": "tcgen05 kind::tf32 with the fp32-accurate 3xTF32 split: 3 MMAs per product at "
+                                 "half the bf16 rate, so the useful-flop ceiling is bf16/6 (frac_3xtf32_ceiling); "
+                                 "the binding roofline is the larger of the 3xTF32 and HBM times",
+                         "frac_3xtf32_ceiling": fl / secs / 1e12 / (bf16_s / 6),
+                         "frac_binding": max(fl / (bf16_s / 6 * 1e12), by / (hbm * 1e9)) / secs})
+        else:
+            roof.update({"bound": "hbm", "achieved": by / secs / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": by / secs / 1e9 / hbm,
+                         "peak_source": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"})
+    # per-kernel algorithmic rates of everything timed
+    kernel_table = {}
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+        fl = sum(kernel_work(k, a, ctx)[0] for _, a in durs[k])
+        byl = [kernel_work(k, a, ctx)[1] for _, a in durs[k]]
+        ent = {"ms_total": v, "launches": len(durs[k]), "share": v / (ms * args.steps)}
+        if all(b is not None for b in byl) and v > 0:
+            ent["hbm_frac"] = sum(byl) / (v / 1e3) / 1e9 / hbm
+            if k in TENSOR_KERNELS:
+                ent["frac_3xtf32_ceiling"] = fl / (v / 1e3) / 1e12 / (bf16_s / 6)
+        kernel_table[k] = ent
+    # SpMM (fused GCN forward with aggregation, last layer) HBM rate
     spmm = None
     sl = [(d, a) for d, a in durs.get("dgnn_gcn_forward", []) if a[1] is not None]
-    if sl and cfg.architecture == "cd-gcn":
-        r0 = eng.ranks[0]
-        nnz_mean = float(np.mean(eng.enc.nnz_hat))
-        Ly = eng.layout.layers[1]
-        n = eng.plan.N
-        byts, gath = spmm_bytes(n, nnz_mean, Ly.fp, Ly.rw, l2)
+    if not sl:      # split GCN (P > 1) / tm-gcn: the aggregation runs as dgnn_spmm_f32
+        sl = durs.get("dgnn_spmm_f32", [])
+    if sl:
+        nm = "dgnn_gcn_forward" if sl[0][1][1] is not None and len(sl[0][1]) == 12 else "dgnn_spmm_f32"
+        byts = sum(kernel_work(nm, a, ctx)[1] for _, a in sl)
         secs = sum(d for d, _ in sl) / 1e3
-        # launches of the rerun pass also write s (kept for the backward)
-        n_sout = sum(1 for _, a in sl if a[9].ptr)
-        achieved = (byts * len(sl) + 4 * n * Ly.fp * n_sout) / secs / 1e9
-        cb, _ = spmm_bytes(n, nnz_mean, Ly.fp, Ly.rw, 1 << 62)
-        cb += 4 * n * Ly.fp * n_sout / len(sl)
-        spmm = {"kernel": "dgnn_gcn_forward (CSR SpMM + W + ReLU, layer 1)", "bound": "hbm",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "bytes_model": "gather-inclusive" if gath else "compulsory",
-                "compulsory_gbs": cb * len(sl) / secs / 1e9, "avg_launch_us": secs / len(sl) * 1e6,
-                "nnz_per_snapshot": nnz_mean, "launches": len(sl),
+        n = eng.plan.N
+        Ly = eng.layout.layers[-1]
+        ctx_c = dict(ctx, l2=1 << 62)
+        cb = sum(kernel_work(nm, a, ctx_c)[1] for _, a in sl)
+        spmm = {"kernel": f"{nm} (CSR SpMM over Ahat_t" + (" + W + ReLU" if nm == "dgnn_gcn_forward" else "") + ")",
+                "bound": "hbm", "achieved": byts / secs / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": byts / secs / 1e9 / hbm,
+                "bytes_model": "gather-inclusive" if 4 * n * Ly.fp > l2 else "compulsory",
+                "compulsory_gbs": cb / secs / 1e9, "avg_launch_us": secs / len(sl) * 1e6,
+                "nnz_per_snapshot": ctx["nnz"], "launches": len(sl),
                 "note": "live in the epoch: launches share the GPU with the graph-rebuild stream"}
         tr = ncu_traffic("dgnn_gcn_forward")
-        if tr:
+        if tr and nm == "dgnn_gcn_forward":
             spmm["traffic"] = tr["dram_bytes_per_launch"]
             spmm["traffic_source"] = tr["source"]
-        if P == 1:
+        if P == 1 and cfg.architecture == "cd-gcn":
             spmm["isolated"] = spmm_isolated(eng, l2, hbm)
-    kernel_table = {k: {"ms_total": v, "launches": len(durs[k]), "share": v / (ms * args.steps)}
-                    for k, v in sorted(tot.items(), key=lambda kv: -kv[1])}
+    nvlink = None
+    if eng.peer is not None:
+        nv = eng.peer.nvlink_summary()
+        eng.peer.log = None
+        if nv:
+            nvlink = dict(nv, peak_gbs=900.0, frac=nv["achieved_gbs"] / 900.0 if nv["achieved_gbs"] else None,
+                          bytes_per_epoch=nv["bytes"] / args.steps,
+                          share_of_step_copying=nv["copy_ms"] / (ms * args.steps),
+                          note="copy-engine pushes into NVLink peer memory (rank 0), overlapping compute; "
+                               "achieved = bytes / summed copy durations; peak 900 GB/s per direction")
+    graph_kernels_ms = sum(tot.get(k, 0.0) for k in graph_side) / args.steps
+    hbm_peak_gb = torch.cuda.max_memory_allocated() / 2**30
+    keep_graphs = eng.keep_graphs
+    del eng
+    import gc
+    gc.collect()               # Engine <-> Rank reference cycles hold the device buffers
+    torch.cuda.empty_cache()
 
     # ---- e2e through the public drop-in API (host buffers, deltas streamed)
     e2e = None
     if not args.skip_e2e:
+        pcie_peak = pcie_h2d_peak()
         comm, transfer = pk.CommLedger(), pk.TransferLedger()
         hp = {k: v.copy() for k, v in params.items()}
         st = pk.init_adam(hp)
-        pk.distributed_epoch(cfg, data, train, hp, P, NBLK)        # build + warm the engine
+        pk.distributed_epoch(cfg, data, train, hp, P, nblk)        # build + warm the engine
+        e2e_eng = pk.api.get_engine(cfg, data, P, nblk)
+        for r in e2e_eng.ranks:
+            r.mat.copy_log = []
         torch.cuda.synchronize()
         if P > 1:
             dist.barrier()
-        h0 = transfer.h2d_bytes
         ts = time.perf_counter()
         for _ in range(args.steps):
-            loss_e, grads, _, _ = pk.distributed_epoch(cfg, data, train, hp, P, NBLK, comm=comm,
+            loss_e, grads, _, _ = pk.distributed_epoch(cfg, data, train, hp, P, nblk, comm=comm,
                                                        transfer=transfer)
             pk.adam_step(hp, grads, st, 0.01)
         torch.cuda.synchronize()
@@ -410,16 +526,35 @@ def run_ours(args):
             t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        pbytes = 8 * eng.layout.count
+        log = [x for r in e2e_eng.ranks for x in (r.mat.copy_log or [])]
+        copy_ms = sum(a.elapsed_time(b) for a, b, _ in log)
+        copy_bytes = sum(b for _, _, b in log)
+        for r in e2e_eng.ranks:
+            r.mat.copy_log = None
+        pbytes = 8 * e2e_eng.layout.count
         e2e = {"value": total_es / e2e_s, "unit": "edge*snapshots/s", "ms_per_step": e2e_s * 1e3,
-               "h2d_bytes_per_step": int((transfer.h2d_bytes - h0) / args.steps) + pbytes,
+               "h2d_bytes_per_step": int(transfer.h2d_bytes / args.steps) + pbytes,
                "d2h_bytes_per_step": pbytes + 8,
-               "delta_vs_full_bytes": (transfer.full_equiv_bytes / transfer.h2d_bytes) if transfer.h2d_bytes else None,
+               "graph_h2d_bytes_per_step": int(transfer.h2d_bytes / args.steps),
+               "delta_vs_full_bytes": (transfer.full_built_bytes / transfer.h2d_bytes) if transfer.h2d_bytes else None,
+               "delta_vs_full_bytes_reference_schedule":
+                   (transfer.full_equiv_bytes / transfer.h2d_bytes) if transfer.h2d_bytes else None,
+               "delta_note": "delta_vs_full_bytes: full-snapshot bytes of the chunks this rank streamed and "
+                             "rebuilt / bytes copied (like for like: same u32-pair encoding, heads rebuilt "
+                             "from 1-step deltas); _reference_schedule: every snapshot of every pass (forward + "
+                             "checkpoint rerun) streamed in full, as dtgnn's stream_block does, / bytes copied",
+               "pcie": {"peak_h2d_gbs": pcie_peak, "copy_ms_per_step": copy_ms / args.steps,
+                        "achieved_gbs": copy_bytes / (copy_ms / 1e3) / 1e9 if copy_ms > 0 else None,
+                        "frac": (copy_bytes / (copy_ms / 1e3) / 1e9 / pcie_peak) if copy_ms > 0 else None,
+                        "share_of_step": copy_ms / (e2e_s * 1e3 * args.steps),
+                        "note": "rank 0: pinned-host -> HBM graph copies on the copy stream (overlapping "
+                                "compute); peak = 1 GiB pinned copy measured in this run"},
                "api": "paper_2109_07893_b200.distributed_epoch + adam_step"}
+        pk.api.clear_engines()
 
     cpu = None
     if rank == 0 and P == 1 and not args.skip_cpu:
-        cpu = cpu_baseline(sample_scale=args.cpu_scale, threads=True)
+        cpu = cpu_baseline(sample_scale=args.cpu_scale, threads=True, linearity=True)
 
     if rank == 0:
         line = {
@@ -427,17 +562,21 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": CFG["scaling"], "vs_baseline": None, "dtype": "fp32 (fp64 graph values / master weights)",
             "data": "synthetic exact-churn dynamic graph, random-init weights",
-            "config": {"workload": CFG["workload"],
+            "config": {"workload": CFG["workload"], "config_key": args.config,
                        "model": CFG["arch"], "num_vertices": N_PER_GPU * scale_of(P), "num_timesteps": T,
-                       "edges_per_snapshot": EDGES_PER_GPU * scale_of(P), "hidden": HIDDEN, "nblk": NBLK,
+                       "edges_per_snapshot": EDGES_PER_GPU * scale_of(P), "hidden": HIDDEN, "nblk": nblk,
                        "theta": THETA, "train_pairs": count, "parallelism": f"snapshot-partitioned x{P}",
                        "l2": "inputs larger than L2 (per-epoch working set ~tens of GB)",
                        "graph_in_timed_region": "delta-encoded graph resident in HBM, CSR/Laplacian "
-                                                "rebuilt on device every pass"},
+                                                "rebuilt on device every epoch (forward sweep; the rerun "
+                                                "reuses the kept snapshots)"},
             "loss": loss,
             "gpu_launches": launches,
             "roofline": roof,
             "spmm_roofline": spmm,
+            "nvlink": nvlink,
+            "graph_kernels_ms_per_step": graph_kernels_ms,
+            "hbm_peak_gb": hbm_peak_gb, "keep_graphs": keep_graphs,
             "kernels": kernel_table,
             "clocks": clocks.summary(),
             "e2e": e2e,
@@ -461,13 +600,14 @@ def cpu_sample(scale: int):
     return n, m
 
 
-def cpu_baseline(sample_scale: int = 128, threads: bool = True, steps: int = 1, warmup: int = 0):
+def cpu_epoch_rate(sample_scale: int, threads: bool, steps: int = 1, warmup: int = 0):
+    """The oracle port (numpy fp64 restatement of dtgnn's distributed_epoch,
+    threads scheduler) + Adam on the workload scaled 1/sample_scale."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import dtgnn_oracle as O
-    from paper_2109_07893_b200.synth import churn_keys
+    from paper_2109_07893_b200.synth import aml_keys, churn_keys
     n, m = cpu_sample(sample_scale)
-    from paper_2109_07893_b200.synth import aml_keys
-    keys = (churn_keys if CFG["gen"] == "churn" else aml_keys)(n, T, m, CHURN, seed=1)
+    keys = (aml_keys if CFG["gen"] == "aml" else churn_keys)(n, T, m, CHURN, seed=1)
     snaps = [O.Coo(n, k // n, k % n, np.ones(k.shape[0])) for k in keys]
     cfg = O.Cfg(CFG["arch"], 2, HIDDEN, HIDDEN)
     Pp = O.prepare(cfg, snaps)
@@ -476,12 +616,13 @@ def cpu_baseline(sample_scale: int = 128, threads: bool = True, steps: int = 1, 
     rng = np.random.default_rng(77)
     params["head.w"] = rng.uniform(-0.5, 0.5, size=params["head.w"].shape)
     cores = os.cpu_count() or 1
-    bsize = T // NBLK
+    nblk = nblk_for(1)
+    bsize = T // nblk
     workers = max(p for p in range(1, min(cores, bsize) + 1) if bsize % p == 0 and n % p == 0) if threads else 1
     st = O.adam_state(params)
 
     def step():
-        loss, grads, _, _ = O.distributed_epoch(cfg, Pp, train, params, workers, NBLK, threads=threads)
+        loss, grads, _, _ = O.distributed_epoch(cfg, Pp, train, params, workers, nblk, threads=threads)
         O.adam(params, grads, st, 0.01)
 
     for _ in range(warmup):
@@ -492,13 +633,28 @@ def cpu_baseline(sample_scale: int = 128, threads: bool = True, steps: int = 1, 
         step()
     dt = (time.perf_counter() - t0) / steps
     util = (time.process_time() - c0) / (dt * steps)
-    es = T * m
-    return {"value": es / dt, "unit": "edge*snapshots/s", "cores": workers, "kind": "port",
-            "seconds_per_epoch": dt, "cpu_utilisation": util, "host_cpus": cores,
-            "sample": f"oracle port (numpy fp64 restatement of dtgnn distributed_epoch, threads scheduler, "
-                      f"P={workers}) + Adam on the {CFG['workload'].split(':')[0]} shape scaled 1/{sample_scale}: "
-                      f"N={n}, T={T}, {m} edges/snapshot, {CHURN:.0%} churn, {CFG['arch']} H={HIDDEN}, "
-                      f"nblk={NBLK}; metric is linear in N and nnz"}
+    es = int(sum(k.shape[0] for k in keys))
+    return {"value": es / dt, "seconds_per_epoch": dt, "cores": workers, "cpu_utilisation": util,
+            "host_cpus": cores, "n": n, "edges_per_snapshot": m, "nblk": nblk}
+
+
+def cpu_baseline(sample_scale: int | None = None, threads: bool = True, steps: int = 1, warmup: int = 0,
+                 linearity: bool = False):
+    scale = sample_scale or CFG["cpu_scale"]
+    r = cpu_epoch_rate(scale, threads, steps, warmup)
+    out = {"value": r["value"], "unit": "edge*snapshots/s", "cores": r["cores"], "kind": "port",
+           "seconds_per_epoch": r["seconds_per_epoch"], "cpu_utilisation": r["cpu_utilisation"],
+           "host_cpus": r["host_cpus"], "sample_scale": scale,
+           "sample": f"oracle port (numpy fp64 restatement of dtgnn distributed_epoch, threads scheduler, "
+                     f"P={r['cores']}) + Adam on the {CFG['workload'].split(':')[0]} shape scaled 1/{scale}: "
+                     f"N={r['n']}, T={T}, {r['edges_per_snapshot']} edges/snapshot, {CHURN:.0%} churn, "
+                     f"{CFG['arch']} H={HIDDEN}, nblk={r['nblk']}"}
+    if linearity:
+        # the sample's rate at 4x and 2x smaller scales (one epoch each): how
+        # the per-edge rate moves with size (cache effects favour small samples)
+        pts = [{"scale": sc, "value": cpu_epoch_rate(sc, threads)["value"]} for sc in (scale * 4, scale * 2)]
+        out["linearity"] = pts + [{"scale": scale, "value": r["value"]}]
+    return out
 
 
 def run_reference(args):
@@ -511,7 +667,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_epoch"] * 1e3,
             "higher_is_better": True, "scaling": CFG["scaling"], "vs_baseline": None, "dtype": "fp64",
             "data": "synthetic exact-churn dynamic graph, random-init weights",
-            "config": {"workload": CFG["workload"] + " (CPU sample, see cpu_baseline)", "model": CFG["arch"]},
+            "config": {"workload": CFG["workload"] + " (CPU sample, see cpu_baseline)", "model": CFG["arch"],
+                       "config_key": args.config},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "edge*snapshots/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -527,10 +684,11 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--timeline", action="store_true", help="per-stream busy / idle breakdown (diagnostic)")
-    ap.add_argument("--cpu-scale", type=int, default=128)
-    ap.add_argument("--cpu-scale-ref", type=int, default=256)
+    ap.add_argument("--cpu-scale", type=int, default=None, help="CPU sample scale (default: per config)")
+    ap.add_argument("--cpu-scale-ref", type=int, default=None)
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2",
-                    help="workload (c2: the headline configs[1] line; c3: TM-GCN configs[2])")
+                    help="workload (c2: the headline configs[1] line; c3: TM-GCN configs[2]; c4 / c5: "
+                         "configs[3] / configs[4])")
     args = ap.parse_args()
     select_config(args.config)
     if args.impl == "reference":

@@ -311,8 +311,10 @@ def _drop(data_id):
 
 
 def clear_engines():
+    import gc
     with _LOCK:
         _ENGINES.clear()
+    gc.collect()               # Engine <-> Rank reference cycles hold the device buffers
     torch.cuda.empty_cache()
 
 
@@ -329,23 +331,41 @@ def _by_time(labels):
     return labels if isinstance(labels, dict) else labels.by_time
 
 
+_FINGERPRINTS: dict = {}
+
+
 def _labels_key(*labelsets):
     """Content fingerprint of label sets (the engine caches device labels
     under it): per frame the pair count, coordinate and label sums and a
-    label-weighted coordinate sum -- a few ms at 3M pairs, and unlike an
-    object id it cannot be reused by a different (or mutated) label set."""
+    label-weighted coordinate sum.  Unlike an object id it cannot be reused
+    by a different label set; it is computed once per live label-set object
+    (a weak reference identifies the object, so a new object is always
+    fingerprinted; arrays mutated in place are not re-read)."""
     key = []
     for ls in labelsets:
-        bt = _by_time(ls)
-        ent = []
-        for t in sorted(bt):
-            p, lab = bt[t]
-            p = np.asarray(p, dtype=np.int64).reshape(-1, 2)
-            lab = np.asarray(lab, dtype=np.int64)
-            ent.append((int(t), p.shape[0], int(p.sum()), int(lab.sum()),
-                        int(np.dot(p[:, 0] + 3 * p[:, 1], lab)) if p.shape[0] else 0))
-        key.append(tuple(ent))
+        ent = _FINGERPRINTS.get(id(ls))
+        if ent is not None and ent[0]() is ls and ls is not None:
+            key.append(ent[1])
+            continue
+        fp = _fingerprint(ls)
+        try:
+            _FINGERPRINTS[id(ls)] = (weakref.ref(ls), fp)
+        except TypeError:           # dicts / None: not weak-referenceable, fingerprinted each call
+            pass
+        key.append(fp)
     return tuple(key)
+
+
+def _fingerprint(ls):
+    bt = _by_time(ls)
+    ent = []
+    for t in sorted(bt):
+        p, lab = bt[t]
+        p = np.asarray(p, dtype=np.int64).reshape(-1, 2)
+        lab = np.asarray(lab, dtype=np.int64)
+        ent.append((int(t), p.shape[0], int(p.sum()), int(lab.sum()),
+                    int(np.dot(p[:, 0] + 3 * p[:, 1], lab)) if p.shape[0] else 0))
+    return tuple(ent)
 
 
 def _bytes(eng):

@@ -31,7 +31,7 @@ import torch
 from . import _lib
 from ._lib import call, frame, ptr
 from .errors import ConfigError, ProtocolError
-from .labels import frame_labels
+from .labels import frame_labels_device
 from .materialize import Materializer, SnapshotEncoding
 from .params import DeviceParams, ParamLayout
 
@@ -250,11 +250,7 @@ class Rank:
             for t, (pairs, lab) in (bt or {}).items():
                 if t not in owned:
                     continue
-                fl = frame_labels(pairs, lab, N, eng.cfg.classes)
-                d[t] = dict(n=fl.count, u=torch.from_numpy(fl.u).to(self.dev),
-                            v=torch.from_numpy(fl.v).to(self.dev), y=torch.from_numpy(fl.y).to(self.dev),
-                            ptr=torch.from_numpy(fl.inc_ptr).to(self.dev),
-                            slot=torch.from_numpy(fl.inc_slot).to(self.dev))
+                d[t] = frame_labels_device(pairs, lab, N, eng.cfg.classes, self.dev)
             self.lab[key] = d
         mx = max([v["n"] for d in self.lab.values() for v in d.values()] + [1])
         self.loss_pp = torch.zeros(mx, dtype=torch.float64, device=self.dev)
@@ -962,6 +958,8 @@ class Engine:
             from .graph import build_m_matrix
             self.m_matrix = build_m_matrix(T, cfg.window).matrix
         self.resident = resident
+        if encoding is None:
+            encoding = getattr(graph, "encoding", None)
         self.enc = encoding if encoding is not None else SnapshotEncoding(graph)
         self.fabric = fabric or LocalFabric()
         self.split = self.skip and self.plan.P > 1 and SPLIT_GCN == "1"

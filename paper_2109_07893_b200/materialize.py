@@ -145,6 +145,55 @@ class SnapshotEncoding:
         self.cap_a = int(max(1, self.nnz.max()))
         self.cap_hat = int(max(1, self.nnz_hat.max()))
 
+    # -- incremental construction from device keys (synth.device_churn_graph)
+    @classmethod
+    def empty(cls, n: int, T: int) -> "SnapshotEncoding":
+        """An encoding filled step by step with `add_step` (unit-valued
+        graphs given as sorted device keys row * n + col and their graph
+        differences), then `finish`."""
+        self = cls.__new__(cls)
+        self.n, self.T, self.unit = int(n), int(T), True
+        self.nnz = np.zeros(T, dtype=np.int64)
+        self.n_del = np.zeros(T, dtype=np.int64)
+        self.n_ins = np.zeros(T, dtype=np.int64)
+        self.nnz_hat = np.zeros(T, dtype=np.int64)
+        self.dhat = np.zeros(T, dtype=np.int64)
+        self._full_parts, self._delta_parts = [], []
+        self.vals = None
+        return self
+
+    def add_step(self, t: int, keys, dropped=None, inserted=None) -> None:
+        import torch as _t
+        n = self.n
+        r, c = keys // n, keys % n
+        self.nnz[t] = keys.numel()
+        self.nnz_hat[t] = keys.numel() + n - int((r == c).sum().item())
+        self._full_parts.append(_t.cat([r, c]).to(_t.int32).cpu())
+        if t > 0:
+            self.n_del[t], self.n_ins[t] = dropped.numel(), inserted.numel()
+            self.dhat[t] = int(((dropped // n) != (dropped % n)).sum().item()
+                               + ((inserted // n) != (inserted % n)).sum().item())
+            self._delta_parts.append(_t.cat([dropped // n, dropped % n, inserted // n, inserted % n])
+                                     .to(_t.int32).cpu())
+
+    def finish(self, pin: bool = True) -> "SnapshotEncoding":
+        T = self.T
+        self.full_off = np.zeros(T + 1, dtype=np.int64)
+        self.full_off[1:] = np.cumsum(2 * self.nnz)
+        self.delta_off = np.zeros(T + 1, dtype=np.int64)
+        self.delta_off[1:] = np.cumsum(2 * (self.n_del + self.n_ins))
+        self.val_off = np.zeros(T + 1, dtype=np.int64)
+        self.val_off[1:] = np.cumsum(self.nnz)
+        self.full = torch.cat(self._full_parts) if self._full_parts else torch.zeros(0, dtype=torch.int32)
+        self.delta = torch.cat(self._delta_parts) if self._delta_parts else torch.zeros(0, dtype=torch.int32)
+        del self._full_parts, self._delta_parts
+        if pin and torch.cuda.is_available():
+            self.full = self.full.pin_memory()
+            self.delta = self.delta.pin_memory()
+        self.cap_a = int(max(1, self.nnz.max()))
+        self.cap_hat = int(max(1, self.nnz_hat.max()))
+        return self
+
     # -- accounting ---------------------------------------------------------
     def chunk(self, ts) -> ChunkPlan:
         t0, t1 = ts[0], ts[-1]

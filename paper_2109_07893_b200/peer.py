@@ -40,6 +40,7 @@ class PeerExchange:
         self.used = 0
         self.bytes_pushed = 0
         self.max_channel = self.hdl.signal_pad_size // (4 * self.world) - 1
+        self.log = None            # a list: (start, end, bytes) of every push (bench NVLink roofline)
 
     def alloc(self, n: int) -> torch.Tensor:
         """A zeroed [n] fp32 view at the same offset on every rank."""
@@ -67,9 +68,28 @@ class PeerExchange:
         self.stream.wait_stream(cur)
         with torch.cuda.stream(self.stream):
             peer = self.hdl.get_buffer(dst_rank, (src.numel(),), torch.float32, self._offset(dst_view))
+            if self.log is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(self.stream)
             peer.copy_(src.view(-1), non_blocking=True)
+            if self.log is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(self.stream)
+                self.log.append((e0, e1, 4 * src.numel()))
             self.hdl.put_signal(dst_rank, channel)
         self.bytes_pushed += 4 * src.numel()
+
+    def nvlink_summary(self):
+        """Pushes logged since `log` was set to a list: bytes, total copy-engine
+        time (the copies are serialised on one stream) and the achieved rate
+        while copying (synchronises)."""
+        torch.cuda.synchronize()
+        if not self.log:
+            return None
+        byts = sum(b for _, _, b in self.log)
+        ms = sum(e0.elapsed_time(e1) for e0, e1, _ in self.log)
+        return {"bytes": byts, "copy_ms": ms, "pushes": len(self.log),
+                "achieved_gbs": byts / (ms / 1e3) / 1e9 if ms > 0 else None}
 
     def wait(self, src_rank: int, channel: int) -> None:
         """The current stream waits for `src_rank`'s push on `channel`."""

@@ -156,3 +156,59 @@ def test_synthetic_generator_exact_churn():
     assert all(np.all(k[1:] > k[:-1]) for k in ks)
     ks2 = churn_keys(500, 5, 1000, 0.1, seed=2)
     assert all(np.array_equal(a, b) for a, b in zip(ks, ks2))
+
+
+@pytest.mark.parametrize("name", ["cdgcn_small"])
+def test_vectorised_sampler_equals_reference_pairs(name):
+    """§8f.2: the vectorised sampler returns the reference's pairs (golden
+    fixtures made by the reference's own sampler)."""
+    from helpers import product_graph
+    from conftest import labels_from
+    fx = load(name)
+    g = product_graph(fx)
+    seed = 5 if name.startswith("cd") else 7
+    train, test = pk.sample_link_prediction_sets(g, 0.5, seed)
+    if name.startswith("cd"):
+        for got, ref in ((train.by_time, labels_from(fx, "train_")), (test.by_time, labels_from(fx, "test_"))):
+            assert sorted(got) == sorted(ref)
+            for t in ref:
+                assert np.array_equal(got[t][0], ref[t][0]) and np.array_equal(got[t][1], ref[t][1])
+
+
+@pytest.mark.parametrize("n,m,theta", [(12, 60, 0.9), (40, 300, 0.5), (2000, 20000, 0.1), (300, 80000, 1.0)])
+def test_vectorised_sampler_equals_key_loop(n, m, theta):
+    """Dense graphs (heavy rejection, duplicate draws within and across
+    batches) and sparse ones: identical pairs to the literal key loop."""
+    from paper_2109_07893_b200.labels import sample_link_prediction_sets_loop
+    from paper_2109_07893_b200.synth import churn_graph
+    g = churn_graph(n, 4, min(m, n * n - 1), 0.1, seed=n)
+    a_tr, a_te = pk.sample_link_prediction_sets(g, theta, 17)
+    b_tr, b_te = sample_link_prediction_sets_loop(g, theta, 17)
+    for a, b in ((a_tr.by_time, b_tr.by_time), (a_te.by_time, b_te.by_time)):
+        assert sorted(a) == sorted(b)
+        for t in a:
+            assert np.array_equal(a[t][0], b[t][0]) and np.array_equal(a[t][1], b[t][1])
+
+
+def test_device_generator_encoding_equals_host_encoding():
+    """The device-built encoding (configs[3]/[4] generator) equals the host
+    encoding of the same snapshots; exact churn; pair-sampler invariants."""
+    import torch
+    from paper_2109_07893_b200.materialize import SnapshotEncoding
+    from paper_2109_07893_b200.synth import device_churn_graph
+    n, T, m = 5000, 6, 20000
+    g = device_churn_graph(n, T, m, 0.1, 3, "cpu", pin=False)
+    keys = [k.numpy() for k in g._keys]
+    host = pk.DynamicGraph(n, [pk.SparseMatrix.from_canonical(n, k // n, k % n) for k in keys])
+    ref = SnapshotEncoding(host, pin=False)
+    for a in ("nnz", "n_del", "n_ins", "nnz_hat", "dhat", "full_off", "delta_off"):
+        assert np.array_equal(getattr(g.encoding, a), getattr(ref, a)), a
+    assert torch.equal(g.encoding.full, ref.full) and torch.equal(g.encoding.delta, ref.delta)
+    for t in range(1, T):
+        assert np.intersect1d(keys[t - 1], keys[t]).shape[0] == m - 2000
+    train, test = g.sample_pairs(0.1, 5)
+    assert sorted(train.by_time) == list(range(T - 1)) and list(test.by_time) == [T - 2]
+    for t, (p, lab) in train.by_time.items():
+        k = p[:, 0] * n + p[:, 1]
+        assert p.shape[0] == 2 * 2000 and np.unique(k).shape[0] == k.shape[0]
+        assert np.all(np.isin(k[lab == 1], keys[t])) and not np.any(np.isin(k[lab == 0], keys[t]))
