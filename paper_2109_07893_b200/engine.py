@@ -116,9 +116,9 @@ class Rank:
         # next epoch's block 0): every owned snapshot rebuilt in the forward
         # sweep stays resident for the checkpoint rerun and the evaluation
         # passes; otherwise two sets, the next pass's chunk rebuilt ahead
-        self.keep_graphs = eng.keep_graphs
-        self.mat = Materializer(eng.enc, dev, slots=C, resident=eng.resident,
-                                sets=plan.nblk + 1 if self.keep_graphs else 2, graph_stream=eng.shared_graph_stream)
+        self.keep_graphs = False          # Engine.enable_keep_graphs after the buffers are placed
+        self.mat = Materializer(eng.enc, dev, slots=C, resident=eng.resident, sets=2,
+                                graph_stream=eng.shared_graph_stream)
         self.prefetched = {}     # block -> (slots, ready event) rebuilt ahead of its pass (two-set mode)
         self.set_turn = 0
         self.built = {}          # block -> (slots, ready event, epoch tag) (keep_graphs mode)
@@ -325,6 +325,10 @@ class Rank:
                 self.act = self.pi[b - 1] if b > 0 else self.zero_state
             else:
                 self.act = self.state
+
+    def enable_keep_graphs(self):
+        self.mat.add_sets(self.eng.plan.nblk + 1 - len(self.mat.sets))
+        self.keep_graphs = True
 
     def prefetch(self, b, next_epoch=False, count_bytes=True):
         """keep_graphs mode: rebuild block b's chunk ahead of its pass, for
@@ -995,22 +999,13 @@ class Engine:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.epoch_id = 0
-        self.keep_graphs = self._plan_keep_graphs(dev)
+        self.keep_graphs = KEEP_GRAPHS == "1"    # final decision after the rank buffers are placed
         # emulated ranks share one graph stream: a chunk head is rebuilt from
         # the previous rank's last raw snapshot in place, in stream order
         self.shared_graph_stream = (torch.cuda.Stream(device=dev, priority=-1)
                                     if (not self.fabric.distributed and workers > 1) else None)
         self.head_chain_on = HEAD_CHAIN != "0"
         self.head_chain = None
-        if self.fabric.distributed and workers > 1 and self.keep_graphs and self.head_chain_on:
-            try:
-                from .peer import HeadChain
-                self.head_chain = HeadChain(dev, N, self.enc.cap_a)
-            except Exception as exc:     # no symmetric memory: chunk heads travel in full
-                import warnings
-                warnings.warn(f"NVLink head chain unavailable ({exc}); chunk heads are sent in full")
-        if self.fabric.distributed and workers > 1 and self.head_chain is None:
-            self.head_chain_on = False
         self.params = DeviceParams(self.layout, dev)
         if self.fabric.distributed:
             import torch.distributed as dist
@@ -1023,20 +1018,34 @@ class Engine:
             ids = list(range(workers))
         self.ranks = [Rank(self, q, dev) for q in ids]
         self.rank_of = {r.q: r for r in self.ranks}
+        self.keep_graphs = self._plan_keep_graphs(dev)
+        if self.keep_graphs:
+            for r in self.ranks:
+                r.enable_keep_graphs()
+        if self.fabric.distributed and workers > 1 and self.keep_graphs and self.head_chain_on:
+            try:
+                from .peer import HeadChain
+                self.head_chain = HeadChain(dev, N, self.enc.cap_a)
+            except Exception as exc:     # no symmetric memory: chunk heads travel in full
+                import warnings
+                warnings.warn(f"NVLink head chain unavailable ({exc}); chunk heads are sent in full")
+        if self.fabric.distributed and workers > 1 and self.head_chain is None:
+            self.head_chain_on = False
         self.feats_host = feats_host
         self.prepared_labels = None
         self.scale = 1.0
 
     def _plan_keep_graphs(self, dev):
         """Keep every owned snapshot of an epoch resident (SURVEY §7 hard
-        part 3, fix 3) when its slot sets fit the HBM budget."""
+        part 3, fix 3) when the extra slot sets fit beside the rank buffers
+        already placed, leaving 20% of HBM for labels, workspaces and the
+        allocator."""
         if KEEP_GRAPHS in ("0", "1"):
             return KEEP_GRAPHS == "1"
-        plan, enc = self.plan, self.enc
-        slot = 2 * 4 * (plan.N + 1) + 2 * enc.cap_hat * (4 + 4)
-        need = (plan.nblk + 1) * plan.chunk * slot
-        total = torch.cuda.get_device_properties(dev).total_memory
-        return need <= 0.12 * total
+        plan = self.plan
+        need = len(self.ranks) * (plan.nblk + 1 - 2) * plan.chunk * Materializer.slot_bytes(self.enc)
+        free, total = torch.cuda.mem_get_info(dev)
+        return need <= free - 0.2 * total
 
     # ------------------------------------------------------------------ setup
     def set_labels(self, train_by_time, test_by_time=None, key=None):

@@ -292,17 +292,10 @@ class Materializer:
         # `sets` independent slot sets: with two, the next block's graph is
         # rebuilt on the graph stream while the current block computes
         self.sets = []
-        for _ in range(sets):
-            self.sets.append([])
-            self.slots = self.sets[-1]
-            for _ in range(slots):
-                self.slots.append(LapSlot(
-                    torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
-                    torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
-                    torch.empty(cap_h, **f64) if with_f64 else None,
-                    torch.empty(cap_h, **f64) if with_f64 else None))
+        self.ready_sets = []
+        self.nslots, self.with_f64 = slots, with_f64
+        self.add_sets(sets)
         self.slots = self.sets[0]
-        self.ready_sets = [torch.cuda.Event() for _ in range(sets)]
         self.bytes_h2d = 0            # bytes this materialiser copied host -> device
         self.bytes_full_equiv = 0     # full-snapshot bytes of every pass consumed (reference schedule)
         self.bytes_full_built = 0     # full-snapshot bytes of every chunk actually built (like for like)
@@ -444,6 +437,24 @@ class Materializer:
             self.raw_t = ts[-1]
             self.ready.record(gs)
         return self.slots[:len(ts)]
+
+    def add_sets(self, k: int) -> None:
+        """k more slot sets of `slots` slots each."""
+        n, cap_h = self.enc.n, self.enc.cap_hat
+        i32 = dict(dtype=torch.int32, device=self.device)
+        f32 = dict(dtype=torch.float32, device=self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        for _ in range(k):
+            self.sets.append([LapSlot(
+                torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
+                torch.empty(n + 1, **i32), torch.empty(cap_h, **i32), torch.empty(cap_h, **f32),
+                torch.empty(cap_h, **f64) if self.with_f64 else None,
+                torch.empty(cap_h, **f64) if self.with_f64 else None) for _ in range(self.nslots)])
+            self.ready_sets.append(torch.cuda.Event())
+
+    @staticmethod
+    def slot_bytes(enc, with_f64: bool = False) -> int:
+        return 2 * 4 * (enc.n + 1) + 2 * enc.cap_hat * (4 + 4 + (8 if with_f64 else 0))
 
     def raw(self):
         """(rowptr, col) of the last rebuilt raw snapshot A_{raw_t} (valid at
