@@ -697,6 +697,65 @@ def model_forward(cfg: Cfg, P: Prepared, params) -> list:
     return frames
 
 
+def _rows_of(a: Coo, rows: np.ndarray):
+    """Entries of canonical `a` whose row is in sorted `rows` (canonical order)."""
+    lo = np.searchsorted(a.rows, rows, side="left")
+    cnt = np.searchsorted(a.rows, rows, side="right") - lo
+    if cnt.sum() == 0:
+        return np.zeros(0, np.int64)
+    start = np.repeat(lo - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt)
+    return (start + np.arange(cnt.sum())).astype(np.int64)
+
+
+def model_forward_rows(cfg: Cfg, laps_at, feats_at, T: int, params, rows, m=None, window: int = 2):
+    """`model_forward` (models.py:275-323) restricted to output rows `rows`
+    (test infrastructure for the large-config parity protocol, SURVEY §8c:
+    rows of the SpMM and per-vertex LSTM / M-product timelines are
+    independent, `test_models.py:267-285`).  Layer l needs its inputs only at
+    the union over t of the Laplacian neighbourhoods of the rows it outputs,
+    so the forward runs on that dependency cone -- identical arithmetic per
+    row (spmm in canonical entry order, `core.py:142-152`).  `laps_at(t)` /
+    `feats_at(t)` return the full Laplacian / input frame of step t.
+    Returns {t: frame rows} for the requested rows (sorted)."""
+    rows = np.unique(np.asarray(rows, np.int64))
+    dims = cfg.dims()
+    L = len(dims)
+    need = [None] * L
+    need[L - 1] = rows
+    for l in range(L - 1, 0, -1):
+        acc = [need[l]]
+        for t in range(T):
+            a = laps_at(t)
+            acc.append(a.cols[_rows_of(a, need[l])])
+        need[l - 1] = np.unique(np.concatenate(acc))
+    skip = cfg.architecture == "cd-gcn"
+    prev_rows, frames = None, None
+    for l, (fin, g, o) in enumerate(dims):
+        R = need[l]
+        w = params[f"gcn{l}.w"]
+        out = []
+        if skip:
+            h, c = np.zeros((R.size, o)), np.zeros((R.size, o))
+            wx, wh, b = params[f"lstm{l}.wx"], params[f"lstm{l}.wh"], params[f"lstm{l}.b"]
+        for t in range(T):
+            a = laps_at(t)
+            idx = _rows_of(a, R)
+            x = feats_at(t) if l == 0 else frames[t]
+            cols = a.cols[idx] if l == 0 else np.searchsorted(prev_rows, a.cols[idx])
+            s = np.zeros((R.size, x.shape[1]))
+            np.add.at(s, np.searchsorted(R, a.rows[idx]), a.vals[idx][:, None] * x[cols])
+            if skip:
+                r = np.maximum(np.concatenate([s, s @ w], 1), 0.0)
+                ys, (h, c), _ = lstm_fwd(wx, wh, b, (h, c), [t], {t: r})
+                out.append(ys[t])
+            else:
+                out.append(np.maximum(s @ w, 0.0))
+        if not skip:
+            out = m_transform_frames(out, m, window)
+        prev_rows, frames = R, out
+    return {t: frames[t] for t in range(T)}
+
+
 def accuracy(z_frames, test_by_time, params):
     """training.py:189-197 (first-index argmax)."""
     ok = tot = 0

@@ -20,6 +20,6 @@ from .params import ModelConfig, init_params, parameter_count  # noqa: F401
 from .api import (ActivationLedger, AdamState, BlockPlan, CommLedger, SnapshotPartition, TrainingData,  # noqa: F401
                   TransferLedger, backward_checkpoint, backward_full, distributed_epoch,
                   adam_step, init_adam, plan_snapshot_partition, prepare_training_data,
-                  train_distributed, train_epochs)
+                  model_forward_frames, train_distributed, train_epochs)
 from .ops import (SnapshotDelta, apply, diff, lstm_block_backward, lstm_block_forward,  # noqa: F401
                   naive_cost, normalize_laplacian, spmm, spmm_transpose, stream_block)

@@ -469,12 +469,13 @@ def train_epochs(cfg, data, train_labels, test_labels, epochs: int, seed: int, n
     return trace, params
 
 
-def model_forward_frames(cfg, data, params: dict, nblk: int = 1) -> list:
-    """Embedding frames of the straight-line forward (`models.py:275-323`)."""
-    eng = get_engine(cfg, data, 1, nblk)
+def model_forward_frames(cfg, data, params: dict, nblk: int = 1, rows=None, workers: int = 1) -> list:
+    """Embedding frames of the straight-line forward (`models.py:275-323`);
+    `rows`: only those vertex rows of every frame."""
+    eng = get_engine(cfg, data, workers, nblk)
     eng.set_labels({}, None, key=("forward",)) if eng.prepared_labels is None else None
     eng.params.load(params)
-    return eng.forward_frames()
+    return eng.forward_frames(rows)
 
 
 # ---------------------------------------------------------------------------

@@ -77,10 +77,14 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 // LSTM gate activations, shared by every LSTM kernel (SIMT, tensor-core,
-// warp-specialised) so their results stay bitwise equal.  MUFU ex2/rcp:
-// a few ulp relative for sigmoid, <= ~1e-7 absolute for tanh -- the same
-// order as the tensor-core accumulation rounding, far inside the 1e-4
-// parity budget -- at a quarter of the instructions of expf + IEEE divide.
+// warp-specialised) so their results stay bitwise equal.  sigmoid: MUFU
+// ex2/rcp, a few ulp relative.  tanh: for |x| < 0.6 an odd minimax
+// polynomial x + x^3 Q(x^2) (<= 0.6 ulp relative in fp32, fitted on
+// [0, 0.6]) -- the 2 sigmoid(2x) - 1 form loses all relative accuracy near
+// 0 (~2.4e-7 absolute), which after a few dozen recurrent steps showed up as
+// ~1.6e-6 absolute error in near-zero embeddings at configs[1]; for
+// |x| >= 0.6, 1 - 2 / (1 + e^{2|x|}) with the sign restored (MUFU, ~3e-7
+// relative).
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -92,7 +96,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 __device__ __forceinline__ float act_sigmoid(float x) { return rcp_approx(1.0f + ex2_approx(-1.4426950408889634f * x)); }
-__device__ __forceinline__ float act_tanh(float x) { return fmaf(2.0f, act_sigmoid(2.0f * x), -1.0f); }
+__device__ __forceinline__ float act_tanh(float x) {
+    const float ax = fabsf(x);
+    const float u = x * x;
+    float q = fmaf(-0.005984960589557886f, u, 0.020868148654699326f);
+    q = fmaf(q, u, -0.053803566843271255f);
+    q = fmaf(q, u, 0.13332132995128632f);
+    q = fmaf(q, u, -0.3333330452442169f);
+    const float small = fmaf(x * u, q, x);
+    const float big = fmaf(-2.0f, rcp_approx(1.0f + ex2_approx(2.885390081777927f * ax)), 1.0f);
+    return ax < 0.6f ? small : copysignf(big, x);
+}
 
 // device-wide exclusive scan (in place), implemented in graph.cu
 size_t scan_workspace_bytes(int64_t n);

@@ -1437,12 +1437,15 @@ class Engine:
             total = int(self.fabric.allreduce([t]).item())
         return (int(correct.item()) / total) if total else None
 
-    def forward_frames(self):
-        """All T output frames (host fp64) of the straight-line forward."""
+    def forward_frames(self, rows=None):
+        """All T output frames (host fp64) of the straight-line forward, or
+        only the vertex rows `rows` (sorted, unique) of each frame.  One rank
+        per GPU: the frames of this rank's owned steps (None elsewhere)."""
         plan = self.plan
         Ly = self.layout.layers[-1]
         E = self.cfg.embed_features
         frames = [None] * plan.T
+        idx = None if rows is None else torch.as_tensor(np.unique(np.asarray(rows, np.int64)), device=self.device)
         for r in self.ranks:
             r.reset_state()
         for b in range(plan.nblk):
@@ -1452,10 +1455,10 @@ class Engine:
             self._layers_forward(b, "eval", None)
             for r in self.ranks:
                 for c, t in enumerate(r.ts):
-                    rows = []
-                    for q in range(plan.P):
-                        rows.append(r.own_slab_rows(r.Y_own[-1], Ly.ho, c, q).view(plan.NP, Ly.ho)[:, :E])
-                    frames[t] = torch.cat(rows).double().cpu().numpy()
+                    slabs = [r.own_slab_rows(r.Y_own[-1], Ly.ho, c, q).view(plan.NP, Ly.ho)[:, :E]
+                             for q in range(plan.P)]
+                    full = torch.cat(slabs)
+                    frames[t] = (full if idx is None else full[idx]).double().cpu().numpy()
         self.check()
         return frames
 

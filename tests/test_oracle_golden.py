@@ -237,3 +237,22 @@ def test_c1_pins(oracle):
     assert loss == pytest.approx(float(fx["loss"]), rel=1e-12)
     for k in grads:
         np.testing.assert_allclose(grads[k], fx[f"g_{k}"], rtol=1e-8, atol=1e-12, err_msg=k)
+
+
+@pytest.mark.parametrize("arch", ["cd-gcn", "tm-gcn"])
+def test_cone_forward_equals_full_forward(oracle, arch):
+    """The dependency-cone forward used by the large-config parity tests is
+    bit-identical to the full forward on the sampled rows."""
+    from paper_2109_07893_b200.synth import aml_keys, churn_keys
+    n = 400
+    keys = (churn_keys if arch == "cd-gcn" else aml_keys)(n, 6, 900, 0.1, seed=3)
+    snaps = [oracle.Coo(n, k // n, k % n, np.ones(k.shape[0])) for k in keys]
+    cfg = oracle.Cfg(arch, 2, 8, 8)
+    P = oracle.prepare(cfg, snaps)
+    params = oracle.init_params(cfg, 1)
+    full = oracle.model_forward(cfg, P, params)
+    rows = np.array([3, 50, 51, 399, 200])
+    part = oracle.model_forward_rows(cfg, lambda t: P.laps[t], lambda t: P.feats[t], P.T, params, rows, P.m,
+                                     P.window)
+    for t in range(P.T):
+        assert np.array_equal(full[t][np.unique(rows)], part[t])
