@@ -110,6 +110,19 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr,
 int dgnn_degree_features(int32_t n, const int32_t* rowptr, const int32_t* t_rowptr,
                          double* x, int64_t ld, void* stream);
 
+/* M-smoothing of the snapshot sequence, window 2 (TM-GCN preprocessing on
+ * the device; replaces `m_transform_graph` -> `sparse_weighted_sum`,
+ * dtdg.py:239-252, core.py:173-192): out = wa A + wb B as a canonical CSR
+ * with fp64 values, fl(fl(wa a) + fl(wb b)) where both hold the entry (the
+ * reference's ascending-k np.add.at order), bit-identical.  val_a / val_b
+ * may be NULL (unit values).  out_cap >= nnz_a + nnz_b. */
+size_t dgnn_csr_weighted_merge_workspace(int32_t n, int64_t nnz_b);
+int dgnn_csr_weighted_merge(int32_t n, const int32_t* rp_a, const int32_t* col_a, const double* val_a,
+                            int64_t nnz_a, double wa, const int32_t* rp_b, const int32_t* col_b,
+                            const double* val_b, int64_t nnz_b, double wb, int32_t* out_rowptr,
+                            int32_t* out_col, double* out_val, int64_t out_cap, void* ws, size_t ws_bytes,
+                            void* stream);
+
 /* ---------------- sparse products (K3/K4) ------------------------------ */
 
 /* Reference `spmm` (core.py:142-152) in fp64, sequential per row in

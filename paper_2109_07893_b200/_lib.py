@@ -41,6 +41,9 @@ _SIGS = {
     "dgnn_laplacian_workspace": (c_size_t, [c_int32]),
     "dgnn_laplacian": (c_int, [c_int32, P, P, P, P, c_int, P, P, P, P, c_int64, P, c_size_t, P]),
     "dgnn_degree_features": (c_int, [c_int32, P, P, P, c_int64, P]),
+    "dgnn_csr_weighted_merge_workspace": (c_size_t, [c_int32, c_int64]),
+    "dgnn_csr_weighted_merge": (c_int, [c_int32, P, P, P, c_int64, c_double, P, P, P, c_int64, c_double, P, P, P,
+                                        c_int64, P, c_size_t, P]),
     "dgnn_spmm_f64": (c_int, [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, P]),
     "dgnn_spmm_f32": (c_int, [c_int32, P, P, P, Frame, c_int32, Frame, P]),
     "dgnn_gcn_forward": (c_int, [c_int32, P, P, P, Frame, c_int32, P, c_int32, c_int, Frame, Frame, P]),

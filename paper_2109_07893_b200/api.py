@@ -30,7 +30,7 @@ import torch
 
 from .engine import Engine, LocalFabric, NcclFabric, Plan
 from .errors import ConfigError, InputError, ProtocolError
-from .graph import (DynamicGraph, FeatureSequence, MMatrix, build_m_matrix, degree_features,
+from .graph import (DynamicGraph, FeatureSequence, MMatrix, SmoothedGraph, build_m_matrix, degree_features,
                     m_transform_features, m_transform_graph)
 from .params import ModelConfig, as_config, init_params, parameter_count
 
@@ -252,7 +252,9 @@ def prepare_training_data(cfg, graph) -> TrainingData:
     m = None
     if cfg.architecture == "tm-gcn":
         m = build_m_matrix(graph.num_timesteps, cfg.window)
-        smoothed = m_transform_graph(graph, m)
+        # smoothed on the device by the engine (graph.SmoothedGraph); the
+        # host smoothing runs only if something reads .snapshots
+        smoothed = SmoothedGraph(graph, m)
         feats = m_transform_features(degree_features(graph), m)
     elif cfg.architecture == "cd-gcn":
         smoothed, feats = graph, degree_features(graph)

@@ -217,3 +217,55 @@ def m_transform_graph(g, m: MMatrix) -> DynamicGraph:
         v = np.concatenate([float(w) * np.asarray(s.vals) for w, s in terms])
         out.append(SparseMatrix.from_entries(g.num_vertices, r, c, v))
     return DynamicGraph(g.num_vertices, out)
+
+
+class SmoothedGraph:
+    """The M-smoothed graph of tm-gcn (`training.py:234-237`: data.graph =
+    m_transform_graph(raw, M)), smoothed on the device by the engine.
+
+    The engine streams the *raw* snapshots' graph differences (structure
+    only) and rebuilds A~_t = M[t,t-1] A_{t-1} + M[t,t] A_t per step with the
+    bit-exact weighted merge (`dgnn_csr_weighted_merge`).  Host code that
+    reads `snapshots` gets the reference's host smoothing, computed on first
+    access.  Device smoothing applies to unit-valued raw graphs with window
+    <= 2; otherwise the engine streams the host-smoothed snapshots with
+    values (the reference's own path)."""
+
+    def __init__(self, raw, m: MMatrix):
+        if raw.num_timesteps != m.size:
+            raise InputError(f"graph has {raw.num_timesteps} snapshots, M expects {m.size}")
+        self.raw, self.m = raw, m
+        self.num_vertices = raw.num_vertices
+        self._host = None
+        self._encoding = None
+
+    @property
+    def num_timesteps(self) -> int:
+        return self.raw.num_timesteps
+
+    @property
+    def device_smoothing(self) -> bool:
+        return (self.m.window <= 2 and bool(np.all(self.m.matrix >= 0.0))
+                and all(bool(np.all(np.asarray(s.vals) == 1.0)) for s in self.raw.snapshots))
+
+    @property
+    def snapshots(self) -> list:
+        if self._host is None:
+            self._host = m_transform_graph(self.raw, self.m).snapshots
+        return self._host
+
+    def total_nnz(self) -> int:
+        return sum(s.nnz for s in self.snapshots)
+
+    @property
+    def encoding(self):
+        """The encoding the engine streams: raw graph differences with the
+        smoothing plan attached, or (no device smoothing) the smoothed
+        snapshots with values."""
+        if self._encoding is None:
+            from .materialize import SnapshotEncoding
+            if self.device_smoothing:
+                self._encoding = SnapshotEncoding(self.raw, smooth=(self.m.matrix, self.m.window))
+            else:
+                self._encoding = SnapshotEncoding(DynamicGraph(self.num_vertices, self.snapshots))
+        return self._encoding

@@ -65,7 +65,10 @@ class ChunkPlan:
 class SnapshotEncoding:
     """Pinned host encoding of a dynamic graph (see module docstring)."""
 
-    def __init__(self, graph, pin: bool = True):
+    def __init__(self, graph, pin: bool = True, smooth=None):
+        """`smooth` = (M matrix, window <= 2): `graph` is the raw, unit-valued
+        graph of a tm-gcn run whose M-smoothed snapshots are rebuilt on the
+        device; the ledger counts are those of the smoothed Laplacians."""
         n = int(graph.num_vertices)
         T = int(graph.num_timesteps)
         if n >= 2 ** 31 - 1:
@@ -127,7 +130,13 @@ class SnapshotEncoding:
         # reference-equivalent ledger counts for the Laplacians (delta.py:75-84)
         self.nnz_hat = np.zeros(T, dtype=np.int64)
         self.dhat = np.zeros(T, dtype=np.int64)
-        if self.unit:
+        self.smooth = None
+        if smooth is not None:
+            if not self.unit or smooth[1] > 2:
+                raise InputError("device smoothing needs a unit-valued raw graph and window <= 2")
+            self.smooth = (np.asarray(smooth[0], np.float64), int(smooth[1]))
+            self._smoothed_counts(keys)
+        elif self.unit:
             # Ahat = A + I structurally and nothing can cancel: the diagonal is
             # always present, so diagonal entries of the A-delta do not change Ahat
             for t in range(T):
@@ -144,6 +153,29 @@ class SnapshotEncoding:
                                 + np.setdiff1d(hat[t], hat[t - 1], assume_unique=True).shape[0])
         self.cap_a = int(max(1, self.nnz.max()))
         self.cap_hat = int(max(1, self.nnz_hat.max()))
+
+    def _smoothed_counts(self, keys) -> None:
+        """nnz of A~_t (union of the window's structures: positive weights,
+        unit values -- nothing cancels), and the ledger counts of its
+        Laplacian L_t = A~_t + I: nnz_hat = |L_t|, dhat = |L_{t-1} xor L_t|.
+        Sorted-key set algebra in torch (on the GPU when there is one)."""
+        n, T = self.n, self.T
+        dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+        diag = torch.arange(n, dtype=torch.int64, device=dev) * (n + 1)
+        w = self.smooth[1]
+        self.nnz_sm = np.zeros(T, dtype=np.int64)
+        prev_k, prev_l = None, None
+        for t in range(T):
+            k = torch.from_numpy(np.ascontiguousarray(keys[t])).to(dev)
+            sm = torch.unique(torch.cat([prev_k, k])) if (prev_k is not None and w == 2) else k
+            lap = torch.unique(torch.cat([sm, diag]))
+            self.nnz_sm[t] = sm.numel()
+            self.nnz_hat[t] = lap.numel()
+            if prev_l is not None:
+                pos = torch.searchsorted(prev_l, lap).clamp_(max=prev_l.numel() - 1)
+                common = int((prev_l[pos] == lap).sum().item())
+                self.dhat[t] = prev_l.numel() + lap.numel() - 2 * common
+            prev_k, prev_l = k, lap
 
     # -- incremental construction from device keys (synth.device_churn_graph)
     @classmethod
@@ -275,13 +307,26 @@ class Materializer:
             self.delta_dev = torch.empty(int(enc.delta_off[-1]) + 1, **i32)
             self.vals_dev = None if enc.unit else torch.empty(int(enc.val_off[-1]) + 1, **f64)
         cap_a, cap_h = enc.cap_a, enc.cap_hat
+        # M-smoothing on the device (tm-gcn, window <= 2, unit raw graph): the
+        # rebuilt raw A_{t-1}, A_t are merged into A~_t, which then goes
+        # through the transpose and the Laplacian like a value-carrying graph
+        self.smooth = getattr(enc, "smooth", None)
+        cap_g = 2 * cap_a if self.smooth is not None else cap_a      # the graph the Laplacian reads
+        valued = (not enc.unit) or self.smooth is not None
         self.a_rowptr = [torch.empty(n + 1, **i32) for _ in range(2)]
         self.a_col = [torch.empty(cap_a, **i32) for _ in range(2)]
         self.at_rowptr = torch.empty(n + 1, **i32)
-        self.at_col = torch.empty(cap_a, **i32)
-        self.stage_col = torch.empty(cap_a, **i32)
-        self.at_val = None if enc.unit else torch.empty(cap_a, **f64)
-        self.stage_val = None if enc.unit else torch.empty(cap_a, **f64)
+        self.at_col = torch.empty(cap_g, **i32)
+        self.stage_col = torch.empty(cap_g, **i32)
+        self.at_val = torch.empty(cap_g, **f64) if valued else None
+        self.stage_val = torch.empty(cap_g, **f64) if valued else None
+        if self.smooth is not None:
+            self.sm_rowptr = torch.empty(n + 1, **i32)
+            self.sm_col = torch.empty(cap_g, **i32)
+            self.sm_val = torch.empty(cap_g, **f64)
+            self.zero_rowptr = torch.zeros(n + 1, **i32)
+            self.ws_merge = torch.empty(query("dgnn_csr_weighted_merge_workspace", n, cap_a), dtype=torch.uint8,
+                                        device=self.device)
         self.ws_apply = torch.empty(query("dgnn_csr_apply_delta_workspace", n), dtype=torch.uint8,
                                     device=self.device)
         self.ws_tr = torch.empty(query("dgnn_csr_transpose_workspace", n), dtype=torch.uint8,
@@ -323,8 +368,10 @@ class Materializer:
         `head_prev` = (rowptr, col) of A_{t0-1} from the rank that owns t0-1
         (a neighbouring rank's raw CSR, same device or received over NVLink;
         `head_prev[2]`, if given, is an event or callable the graph stream
-        waits on first; `head_prev[3]`, if given, is called once the head
-        has been rebuilt).  Only t = 0 then travels in full.
+        waits on first; `head_prev[3]`, if given, is called once A_{t0-1}
+        has been read).  Only t = 0 then travels in full.  With device
+        smoothing a head that follows nothing ships A_{t0-1} in full (the
+        smoothed A~_{t0} needs it) and A_{t0} as its delta.
 
         `count_bytes` charges the real H2D bytes of this build; `consume`
         also charges the pass that consumes it (`account`) -- the engine
@@ -339,16 +386,26 @@ class Materializer:
         gs = self.graph_stream
         gsh = gs.cuda_stream
         t0 = ts[0]
-        own_prev = t0 > 0 and self.raw_t == t0 - 1
-        use_delta_head = t0 > 0 and (own_prev or head_prev is not None)
+        sm = self.smooth
+        if t0 > 0 and self.raw_t == t0 - 1:
+            head = "own"
+        elif t0 > 0 and head_prev is not None:
+            head = "neighbor"
+        elif t0 > 0 and sm is not None:
+            head = "full_prev"
+        else:
+            head = "full"
         # H2D ranges of this build: deltas of t0+1..t1 (and of t0 itself when
-        # the head is rebuilt from A_{t0-1}), the full head otherwise
+        # the head is rebuilt from A_{t0-1}), the full head (or A_{t0-1}) otherwise
         fo, fc = plan.full_range
         do, dc = plan.delta_range
-        if use_delta_head:
-            fc = 0
+        if head != "full":
             do = int(enc.delta_off[t0])
             dc = int(enc.delta_off[ts[-1] + 1] - enc.delta_off[t0])
+            if head == "full_prev":
+                fo, fc = int(enc.full_off[t0 - 1]), int(2 * enc.nnz[t0 - 1])
+            else:
+                fc = 0
         vo, vc = plan.val_range
         if self.resident:
             fbase, dbase, vbase = fo, do, vo
@@ -375,7 +432,7 @@ class Materializer:
         if count_bytes:
             self.bytes_h2d += built_bytes
             self.bytes_full_built += enc.full_bytes(ts)
-            self.builds.append((list(ts), built_bytes, bool(use_delta_head)))
+            self.builds.append((list(ts), built_bytes, head != "full"))
         if consume:
             self.account(ts, ledger, count_bytes)
         voff = vbase
@@ -387,16 +444,25 @@ class Materializer:
         with torch.cuda.stream(gs):
             cur = self.cur
             dpos = dbase
-            if use_delta_head and not own_prev:
+            release = None
+            prev_rp = prev_col = None
+            if head == "neighbor":
                 prev_rp, prev_col = head_prev[0], head_prev[1]
                 if len(head_prev) > 2 and head_prev[2] is not None:
                     w = head_prev[2]
                     w() if callable(w) else gs.wait_event(w)
-            elif use_delta_head:
+                release = head_prev[3] if len(head_prev) > 3 else None
+            elif head == "own":
+                prev_rp, prev_col = self.a_rowptr[cur], self.a_col[cur]
+            elif head == "full_prev":
+                mp = int(enc.nnz[t0 - 1])
+                call("dgnn_rowptr_from_sorted_rows", n, mp, ptr(self.full_dev[fbase:fbase + mp]),
+                     ptr(self.a_rowptr[cur]), gsh)
+                self.a_col[cur][:mp].copy_(self.full_dev[fbase + mp:fbase + 2 * mp])
                 prev_rp, prev_col = self.a_rowptr[cur], self.a_col[cur]
             for i, t in enumerate(ts):
                 m = int(enc.nnz[t])
-                if i == 0 and not use_delta_head:
+                if i == 0 and head == "full":
                     rows = self.full_dev[fbase:fbase + m]
                     call("dgnn_rowptr_from_sorted_rows", n, m, ptr(rows), ptr(self.a_rowptr[cur]), gsh)
                     a_rowptr = self.a_rowptr[cur]
@@ -414,25 +480,39 @@ class Materializer:
                          ptr(d[nd:2 * nd]), ni, ptr(d[2 * nd:2 * nd + ni]), ptr(d[2 * nd + ni:]),
                          ptr(self.a_rowptr[nxt]), ptr(self.a_col[nxt]), enc.cap_a, ptr(self.ws_apply),
                          self.ws_apply.numel(), ptr(self.status), gsh)
-                    if i == 0 and not own_prev and len(head_prev) > 3 and head_prev[3] is not None:
-                        head_prev[3]()
                     cur = nxt
                     a_rowptr, a_col = self.a_rowptr[cur], self.a_col[cur]
-                a_val = None
-                if not enc.unit:
-                    a_val = self.vals_dev[voff:voff + m]
+                if sm is not None:
+                    # A~_t = M[t,t-1] A_{t-1} + M[t,t] A_t (dtdg.py:239-252), window <= 2
+                    mm, w = sm
+                    if t == 0 or w == 1:
+                        pa, ca, na, wa = self.zero_rowptr, self.a_col[1 - cur], 0, 0.0
+                    else:
+                        pa, ca, na, wa = prev_rp, prev_col, int(enc.nnz[t - 1]), float(mm[t, t - 1])
+                    call("dgnn_csr_weighted_merge", n, ptr(pa), ptr(ca), None, na, wa, ptr(a_rowptr), ptr(a_col),
+                         None, m, float(mm[t, t]), ptr(self.sm_rowptr), ptr(self.sm_col), ptr(self.sm_val),
+                         self.sm_col.numel(), ptr(self.ws_merge), self.ws_merge.numel(), gsh)
+                    g_rowptr, g_col, g_val, g_m = self.sm_rowptr, self.sm_col, self.sm_val, int(enc.nnz_sm[t])
+                else:
+                    g_val = None if enc.unit else self.vals_dev[voff:voff + m]
+                    g_rowptr, g_col, g_m = a_rowptr, a_col, m
                 voff += m
-                call("dgnn_csr_transpose_staged", n, m, ptr(a_rowptr), ptr(a_col), ptr(a_val),
+                if i == 0 and release is not None:
+                    release()           # A_{t0-1} (the neighbour's hand-off) has been read
+                    release = None
+                call("dgnn_csr_transpose_staged", n, g_m, ptr(g_rowptr), ptr(g_col), ptr(g_val),
                      ptr(self.at_rowptr), ptr(self.at_col), ptr(self.at_val), ptr(self.stage_col),
                      ptr(self.stage_val), ptr(self.ws_tr), self.ws_tr.numel(), gsh)
                 s = self.slots[i]
-                call("dgnn_laplacian", n, ptr(a_rowptr), ptr(a_rowptr), ptr(a_col), ptr(a_val), 0,
+                call("dgnn_laplacian", n, ptr(g_rowptr), ptr(g_rowptr), ptr(g_col), ptr(g_val), 0,
                      ptr(s.rowptr), ptr(s.col), ptr(s.val), ptr(s.val64), enc.cap_hat,
                      ptr(self.ws_lap), self.ws_lap.numel(), gsh)
-                call("dgnn_laplacian", n, ptr(a_rowptr), ptr(self.at_rowptr), ptr(self.at_col),
+                call("dgnn_laplacian", n, ptr(g_rowptr), ptr(self.at_rowptr), ptr(self.at_col),
                      ptr(self.at_val), 1, ptr(s.t_rowptr), ptr(s.t_col), ptr(s.t_val), ptr(s.t_val64),
                      enc.cap_hat, ptr(self.ws_lap), self.ws_lap.numel(), gsh)
-                s.a_rowptr, s.a_t_rowptr, s.t = a_rowptr, self.at_rowptr, t
+                s.a_rowptr, s.a_t_rowptr, s.t = g_rowptr, self.at_rowptr, t
+            if release is not None:
+                release()
             self.cur = cur
             self.raw_t = ts[-1]
             self.ready.record(gs)

@@ -573,3 +573,51 @@ def test_materializer_chunk_heads_rebuilt_from_deltas():
     assert not c.builds[0][2]
     for m in (mat, a, b, c):
         m.check()
+
+
+@pytest.mark.gpu
+def test_device_smoothing_bit_exact(oracle):
+    """§8f.1: tm-gcn's M-smoothed snapshots rebuilt on the device from the raw
+    graph differences (weighted merge of A_{t-1}, A_t, then transpose and
+    Laplacian) equal the oracle's m_transform_snaps + laplacian bit for bit:
+    heads after the own last snapshot, after nothing (A_{t0-1} shipped in
+    full) and after a neighbour's snapshot; heavy-tailed (hub) rows."""
+    from paper_2109_07893_b200.graph import SmoothedGraph
+    from paper_2109_07893_b200.materialize import Materializer
+    from paper_2109_07893_b200.synth import aml_graph
+    n, T = 20_000, 8
+    g = aml_graph(n, T, 60_000, 0.05, seed=8)
+    m = pk.build_m_matrix(T, 2)
+    enc = SmoothedGraph(g, m).encoding
+    coos = [oracle.Coo(n, np.asarray(s.rows), np.asarray(s.cols), np.asarray(s.vals)) for s in g.snapshots]
+    sm = oracle.m_transform_snaps(coos, m.matrix, 2)
+
+    def check(slots, ts):
+        for s, t in zip(slots, ts):
+            ref = oracle.laplacian(sm[t])
+            rp = s.rowptr.cpu().numpy()
+            mm = int(rp[-1])
+            assert mm == ref.nnz, t
+            assert np.array_equal(np.repeat(np.arange(n), np.diff(rp)), ref.rows)
+            assert np.array_equal(s.col[:mm].cpu().numpy(), ref.cols)
+            assert np.array_equal(s.val64[:mm].cpu().numpy(), ref.vals), t
+            order = np.lexsort((ref.rows, ref.cols))
+            assert np.array_equal(s.t_col[:mm].cpu().numpy(), ref.rows[order])
+            assert np.array_equal(s.t_val64[:mm].cpu().numpy(), ref.vals[order])
+
+    mat = Materializer(enc, "cuda", slots=3, with_f64=True, sets=2)
+    for i, ts in enumerate(([0, 1, 2], [3, 4, 5], [6, 7])):      # own-chain heads
+        check(mat.materialize(ts, set_idx=i % 2), ts)
+    other = Materializer(enc, "cuda", slots=3, with_f64=True)
+    check(other.materialize([4, 5, 6]), [4, 5, 6])                # head after nothing: A_3 in full
+    gs = torch.cuda.Stream()
+    a = Materializer(enc, "cuda", slots=3, with_f64=True, graph_stream=gs)
+    b = Materializer(enc, "cuda", slots=3, with_f64=True, graph_stream=gs)
+    sa = a.materialize([1, 2, 3])
+    sb = b.materialize([4, 5, 6], head_prev=a.raw())               # neighbour's A_3
+    b.wait()
+    check(sb, [4, 5, 6])
+    check(sa, [1, 2, 3])
+    assert [x[2] for x in mat.builds] == [False, True, True] and other.builds[0][2]
+    for x in (mat, other, a, b):
+        x.check()

@@ -212,3 +212,22 @@ def test_device_generator_encoding_equals_host_encoding():
         k = p[:, 0] * n + p[:, 1]
         assert p.shape[0] == 2 * 2000 and np.unique(k).shape[0] == k.shape[0]
         assert np.all(np.isin(k[lab == 1], keys[t])) and not np.any(np.isin(k[lab == 0], keys[t]))
+
+
+def test_smoothed_encoding_counts_equal_host_smoothing():
+    """§8f.1: the raw-graph encoding with device smoothing charges exactly the
+    reference ledger counts of the smoothed Laplacians (`delta.py:75-84` over
+    `m_transform_graph` snapshots), AMLSim-style graph with hubs."""
+    from paper_2109_07893_b200.graph import SmoothedGraph
+    from paper_2109_07893_b200.materialize import SnapshotEncoding
+    from paper_2109_07893_b200.synth import aml_graph
+    g = aml_graph(3000, 7, 9000, 0.05, seed=4)
+    m = pk.build_m_matrix(7, 2)
+    sg = SmoothedGraph(g, m)
+    assert sg.device_smoothing
+    dev = sg.encoding
+    host = SnapshotEncoding(pk.DynamicGraph(g.num_vertices, pk.m_transform_graph(g, m).snapshots), pin=False)
+    assert np.array_equal(dev.nnz_hat, host.nnz_hat)
+    assert np.array_equal(dev.dhat, host.dhat)
+    assert np.array_equal(dev.nnz_sm, host.nnz)
+    assert dev.unit and not host.unit
