@@ -178,3 +178,85 @@ def test_c2_emulated_four_ranks_equal_one_rank(c2):
     assert comm.redistribution_units == 6 * 2 * T * n * 3 // 4
     # the whole job streamed every snapshot after t = 0 as a 1-step delta
     assert tr.full_built_bytes / tr.h2d_bytes > 4.0
+
+
+@pytest.fixture(scope="module")
+def c3(oracle):
+    """configs[2]: TM-GCN (window 2) hidden 32 on the AMLSim-style graph,
+    N = 1M, T = 64, 2M edges per snapshot, heavy-tailed degrees, 2% churn,
+    nblk 8 -- the bench workload (smoothed on the device)."""
+    from paper_2109_07893_b200.synth import aml_graph
+    g = aml_graph(1_000_000, 64, 2_000_000, 0.02, seed=1)
+    cfg = pk.ModelConfig("tm-gcn", hidden_features=32, embed_features=32)
+    data = pk.prepare_training_data(cfg, g)
+    params = _head(pk.init_params(cfg, 0))
+    coos = [oracle.Coo(g.num_vertices, np.asarray(s.rows), np.asarray(s.cols), np.asarray(s.vals))
+            for s in g.snapshots]
+    m = data.m_matrix.matrix
+    yield dict(g=g, cfg=cfg, data=data, params=params, coos=coos, m=m, laps={})
+    pk.api.clear_engines()
+
+
+def _slap(oracle, case, t):
+    """Oracle Laplacian of the M-smoothed snapshot t (dtdg.py:239-252, 178-191)."""
+    if t not in case["laps"]:
+        m = case["m"]
+        terms = [(m[t, k], case["coos"][k]) for k in range(max(0, t - 1), t + 1)]
+        case["laps"][t] = oracle.laplacian(oracle.weighted_sum(terms))
+    return case["laps"][t]
+
+
+def test_c3_smoothed_snapshots_rebuilt_bit_exact(oracle, c3):
+    """configs[2] smoothed snapshots rebuilt on the device (raw graph
+    differences -> weighted merge -> transpose -> Laplacian) against the
+    oracle's host smoothing + Laplacian, bit for bit, hub rows included."""
+    from paper_2109_07893_b200.materialize import Materializer
+    enc = c3["data"].graph.encoding
+    n = c3["g"].num_vertices
+    mat = Materializer(enc, "cuda", slots=8, resident=False, with_f64=True)
+    for ts in (list(range(0, 8)), list(range(8, 16)), list(range(56, 64))):
+        slots = mat.materialize(ts)
+        mat.wait()
+        torch.cuda.synchronize()
+        for s, t in zip(slots, ts):
+            if t in (0, 1, 8, 56, 63):
+                ref = _slap(oracle, c3, t)
+                _check_slot(s, ref, n)
+                assert np.array_equal(s.val64[:ref.nnz].cpu().numpy(), ref.vals)
+    mat.check()
+
+
+def test_c3_forward_sampled_vertices_vs_oracle(oracle, c3):
+    """The full configs[2] tm-gcn forward (T = 64, nblk = 8, 1M vertices,
+    device smoothing) against the oracle's forward on the dependency cone of
+    256 sampled vertices (GCN rows + per-vertex M-product timelines)."""
+    g, cfg, params = c3["g"], c3["cfg"], c3["params"]
+    n, T = g.num_vertices, g.num_timesteps
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(n, 256, replace=False))
+    got = pk.model_forward_frames(cfg, c3["data"], params, nblk=8, rows=rows)
+    feats = oracle.m_transform_frames(oracle.degree_feats(c3["coos"]), c3["m"], 2)
+    want = oracle.model_forward_rows(oracle.Cfg("tm-gcn", 2, 32, 32), lambda t: _slap(oracle, c3, t),
+                                     lambda t: feats[t], T, params, rows, c3["m"], 2)
+    need = 0.0
+    for t in range(T):
+        ok, worst, nbad = guarded_close(got[t], want[t], RTOL, 1e-6)
+        assert ok, (t, worst, nbad)
+        ex = np.maximum(0.0, np.abs(got[t] - want[t]) - RTOL * np.maximum(np.abs(got[t]), np.abs(want[t])))
+        need = max(need, float(ex.max() / max(np.abs(want[t]).max(), 1e-300)))
+    print(f"c3 forward: needed atol fraction {need:.2e}")
+
+
+def test_c3_emulated_four_ranks_equal_one_rank(c3):
+    """A full configs[2] training epoch (device smoothing, value-carrying
+    smoothed Laplacians rebuilt every epoch, M-product trailing frames):
+    emulated P = 4 against P = 1."""
+    cfg, data, params = c3["cfg"], c3["data"], c3["params"]
+    train, _ = pk.sample_link_prediction_sets(c3["g"], 0.1, 1 + 1000003)
+    l1, g1 = pk.backward_checkpoint(cfg, data, train, params, 8)
+    pk.api.clear_engines()
+    l4, g4, comm, tr = pk.distributed_epoch(cfg, data, train, params, 4, 8)
+    pk.api.clear_engines()
+    assert l4 == pytest.approx(l1, rel=1e-6)
+    assert_grads_close(g4, g1, RTOL, ENGINE_ATOL)
+    assert tr.full_built_bytes / tr.h2d_bytes > 3.0
