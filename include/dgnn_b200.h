@@ -344,6 +344,22 @@ int dgnn_params_to_device(int64_t n, const double* p, const int64_t* pos0, const
 int dgnn_grads_gather(int64_t n, const double* gpad, const int64_t* pos0, double* g,
                       void* stream);
 
+/* out[pos[i]] = p[i] (fp64 padded image of the master parameters) */
+int dgnn_scatter_f64(int64_t n, const double* p, const int64_t* pos, double* out, void* stream);
+
+/* EGCN-O weight evolution (egcn_evolve, models.py:247-268; evolve chain,
+ * training.py:466-509), elementwise over cnt (padded F x H) weights, fp64,
+ * `steps` timesteps of a block.  Forward: from w_in, writes the final weight
+ * to w_out, every step's weight as fp32 to images[s * cnt ...] and (if
+ * non-NULL) the per-step cache [w_prev | i | f | o | g | tanh c] to
+ * cache[s * 6 cnt ...].  Backward: seeds[s * cnt ...] = dL/dW_s (NULL: none),
+ * dw_carry in = gradient w.r.t. the block's final weight, out = w.r.t. its
+ * input weight; dgates / dbias (4 cnt each) += the block's gate gradients. */
+int dgnn_evolve_forward(int64_t cnt, int32_t steps, const double* gates, const double* bias, const double* w_in,
+                        double* w_out, float* images, double* cache, void* stream);
+int dgnn_evolve_backward(int64_t cnt, int32_t steps, const double* gates, const double* cache,
+                         const double* seeds, double* dw_carry, double* dgates, double* dbias, void* stream);
+
 /* Elementwise helpers for frame plumbing. */
 int dgnn_fill_f32(int64_t n, float value, float* x, void* stream);
 int dgnn_cast_f64_to_f32_frame(int32_t n, int32_t f, const double* x, int64_t ldx,

@@ -295,7 +295,13 @@ def init_params(cfg: Cfg, seed: int) -> dict:
     p = {}
     for l, (fin, g, o) in enumerate(cfg.dims()):
         if cfg.architecture == "egcn-o":
-            raise OracleConfigError("egcn-o is outside the hot path")
+            # models.py:157-163: w0, then the four gate matrices; forget bias 1
+            p[f"evolve{l}.w0"] = glorot(fin, g)
+            p[f"evolve{l}.gates"] = np.stack([glorot(fin, g) for _ in range(4)])
+            bias = np.zeros((4, fin, g))
+            bias[1] = 1.0
+            p[f"evolve{l}.bias"] = bias
+            continue
         p[f"gcn{l}.w"] = glorot(fin, g)
         if cfg.architecture == "cd-gcn":
             k = fin + g
@@ -544,7 +550,10 @@ def prepare(cfg: Cfg, snaps) -> Prepared:
     elif cfg.architecture == "cd-gcn":
         g, feats = list(snaps), degree_feats(snaps)
     else:
-        raise OracleConfigError("egcn-o is outside the hot path")
+        # training.py:238-240: edge life (dtdg.py:194-208), degrees of the smoothed graph
+        life = cfg.edge_life
+        g = [weighted_sum([(1.0, snaps[k]) for k in range(max(0, t - life + 1), t + 1)]) for t in range(T)]
+        feats = degree_feats(g)
     laps = [laplacian(s) for s in g]
     s1 = [spmm(a, x) for a, x in zip(laps, feats)]
     return Prepared(g, laps, feats, s1, m, cfg.window)
@@ -563,9 +572,55 @@ def from_reference_data(data, window: int) -> Prepared:
 # sequential block engine (training.py:516-865)
 
 
-def _state0(cfg, n):
-    return [(np.zeros((n, o)), np.zeros((n, o))) if cfg.architecture == "cd-gcn" else None
-            for (_, _, o) in cfg.dims()]
+def _state0(cfg, n, params=None, grads=False):
+    """training.py:516-539: LSTM state, or the evolving weight (w0; zero for
+    its gradient carry) for egcn-o."""
+    out = []
+    for l, (_, _, o) in enumerate(cfg.dims()):
+        if cfg.architecture == "cd-gcn":
+            out.append((np.zeros((n, o)), np.zeros((n, o))))
+        elif cfg.architecture == "egcn-o":
+            w0 = params[f"evolve{l}.w0"]
+            out.append(np.zeros_like(w0) if grads else w0)
+        else:
+            out.append(None)
+    return out
+
+
+def evolve_fwd(gates, bias, w_in, ts):
+    """training.py:466-484 (egcn_evolve, models.py:247-268): elementwise
+    matrix-LSTM chain; returns ({t: W_t}, W_last, cache)."""
+    w, w_by_t, cache = w_in, {}, []
+    for t in ts:
+        z = gates * w + bias
+        i, f, o = sig(z[0]), sig(z[1]), sig(z[2])
+        g = np.tanh(z[3])
+        c = f * w + i * g
+        tc = np.tanh(c)
+        w_new = o * tc
+        cache.append((w, i, f, o, g, tc))
+        w_by_t[t] = w_new
+        w = w_new
+    return w_by_t, w, cache
+
+
+def evolve_bwd(gates, ts, cache, seeds, dw_out):
+    """training.py:487-509 -> (dgates, dbias, dw_in)."""
+    dgates, dbias = np.zeros_like(gates), np.zeros_like(gates)
+    carry = dw_out.copy()
+    for t, (wp, i, f, o, g, tc) in zip(reversed(ts), reversed(cache)):
+        dwn = carry + seeds[t] if t in seeds else carry
+        do = dwn * tc
+        dc = dwn * o * (1.0 - tc * tc)
+        df, di, dg = dc * wp, dc * g, dc * i
+        dwp = dc * f
+        dzs = (di * i * (1.0 - i), df * f * (1.0 - f), do * o * (1.0 - o), dg * (1.0 - g * g))
+        for k, dz in enumerate(dzs):
+            dgates[k] += dz * wp
+            dbias[k] += dz
+            dwp = dwp + dz * gates[k]
+        carry = dwp
+    return dgates, dbias, carry
 
 
 def block_forward(cfg, P: Prepared, params, ts, state_in, trailing, keep):
@@ -573,6 +628,18 @@ def block_forward(cfg, P: Prepared, params, ts, state_in, trailing, keep):
     skip = cfg.architecture == "cd-gcn"
     cur, st_out, tr_out, caches = None, [], [], ([] if keep else None)
     for l, (fin, g, o) in enumerate(cfg.dims()):
+        if cfg.architecture == "egcn-o":
+            w_by_t, w_last, ev = evolve_fwd(params[f"evolve{l}.gates"], params[f"evolve{l}.bias"], state_in[l], ts)
+            st_out.append(w_last)
+            tr_out.append({})
+            gout, gc = {}, {}
+            for t in ts:
+                s = P.s1[t] if l == 0 else spmm(P.laps[t], cur[t])
+                gout[t], gc[t] = gcn_fwd(s, w_by_t[t], False)
+            if keep:
+                caches.append({"gcn": gc, "evolve": ev, "w_by_t": w_by_t})
+            cur = gout
+            continue
         w = params[f"gcn{l}.w"]
         gout, gc = {}, {}
         for t in ts:
@@ -606,6 +673,16 @@ def block_backward(cfg, P: Prepared, params, ts, caches, dz, dstate, dtr_in):
     dcur = dz
     for l in reversed(range(cfg.layers)):
         lc = caches[l]
+        if cfg.architecture == "egcn-o":
+            seeds, prev = {}, {}
+            for t in ts:
+                seeds[t], ds = gcn_bwd(lc["gcn"][t], dcur[t], lc["w_by_t"][t], False)
+                if l > 0:
+                    prev[t] = spmm_t(P.laps[t], ds)
+            dg, dbias, dst_in[l] = evolve_bwd(params[f"evolve{l}.gates"], ts, lc["evolve"], seeds, dstate[l])
+            dp[f"evolve{l}.gates"], dp[f"evolve{l}.bias"] = dg, dbias
+            dcur = prev
+            continue
         if skip:
             dy, dst, (dwx, dwh, db) = lstm_bwd(params[f"lstm{l}.wx"], params[f"lstm{l}.wh"],
                                                ts, lc["lstm"], dcur, dstate[l])
@@ -637,7 +714,7 @@ def backward_checkpoint(cfg: Cfg, P: Prepared, by_time, params, nblk: int, mean=
         raise OracleConfigError("nblk must divide T")
     bs = T // nblk
     blocks = [list(range(b * bs, (b + 1) * bs)) for b in range(nblk)]
-    state = _state0(cfg, P.N)
+    state = _state0(cfg, P.N, params)
     trail = [dict() for _ in range(cfg.layers)]
     pis, tot, cnt = {}, 0.0, 0
     for b, ts in enumerate(blocks):
@@ -652,9 +729,9 @@ def backward_checkpoint(cfg: Cfg, P: Prepared, by_time, params, nblk: int, mean=
     scale = (1.0 / cnt) if (mean and cnt) else 1.0
     loss = tot * scale
     grads = {k: np.zeros_like(v) for k, v in params.items()}
-    dstate = _state0(cfg, P.N)
+    dstate = _state0(cfg, P.N, params, grads=True)
     dtr = [dict() for _ in range(cfg.layers)]
-    init = _state0(cfg, P.N)
+    init = _state0(cfg, P.N, params)
     for b in reversed(range(nblk)):
         ts = blocks[b]
         zf, _, _, caches = block_forward(cfg, P, params, ts, pis[b - 1] if b else init, trail, True)
@@ -671,6 +748,9 @@ def backward_checkpoint(cfg: Cfg, P: Prepared, by_time, params, nblk: int, mean=
         for l in range(cfg.layers):
             for t, g in dtr_out[l].items():
                 dtr[l][t] = dtr[l][t] + g if t in dtr[l] else g
+    if cfg.architecture == "egcn-o":      # training.py:750-754: the initial weights' gradient
+        for l in range(cfg.layers):
+            grads[f"evolve{l}.w0"] += dstate[l]
     return loss, grads
 
 
@@ -680,6 +760,11 @@ def model_forward(cfg: Cfg, P: Prepared, params) -> list:
     T, n = P.T, P.N
     skip = cfg.architecture == "cd-gcn"
     for l, (fin, g, o) in enumerate(cfg.dims()):
+        if cfg.architecture == "egcn-o":       # models.py:315-321
+            w_by_t, _, _ = evolve_fwd(params[f"evolve{l}.gates"], params[f"evolve{l}.bias"],
+                                      params[f"evolve{l}.w0"], list(range(T)))
+            frames = [np.maximum(spmm(P.laps[t], frames[t]) @ w_by_t[t], 0.0) for t in range(T)]
+            continue
         w = params[f"gcn{l}.w"]
         if skip:
             h, c = np.zeros((n, o)), np.zeros((n, o))

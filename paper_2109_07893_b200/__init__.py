@@ -21,5 +21,6 @@ from .api import (ActivationLedger, AdamState, BlockPlan, CommLedger, SnapshotPa
                   TransferLedger, backward_checkpoint, backward_full, distributed_epoch,
                   adam_step, init_adam, plan_snapshot_partition, prepare_training_data,
                   model_forward_frames, train_distributed, train_epochs)
+from .wire import read_delta_stream, train_report, write_delta_stream  # noqa: F401
 from .ops import (SnapshotDelta, apply, diff, lstm_block_backward, lstm_block_forward,  # noqa: F401
                   naive_cost, normalize_laplacian, spmm, spmm_transpose, stream_block)

@@ -42,6 +42,9 @@ _SIGS = {
     "dgnn_laplacian": (c_int, [c_int32, P, P, P, P, c_int, P, P, P, P, c_int64, P, c_size_t, P]),
     "dgnn_degree_features": (c_int, [c_int32, P, P, P, c_int64, P]),
     "dgnn_csr_weighted_merge_workspace": (c_size_t, [c_int32, c_int64]),
+    "dgnn_scatter_f64": (c_int, [c_int64, P, P, P, P]),
+    "dgnn_evolve_forward": (c_int, [c_int64, c_int32, P, P, P, P, P, P, P]),
+    "dgnn_evolve_backward": (c_int, [c_int64, c_int32, P, P, P, P, P, P, P]),
     "dgnn_csr_weighted_merge": (c_int, [c_int32, P, P, P, c_int64, c_double, P, P, P, c_int64, c_double, P, P, P,
                                         c_int64, P, c_size_t, P]),
     "dgnn_spmm_f64": (c_int, [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, P]),

@@ -30,8 +30,8 @@ import torch
 
 from .engine import Engine, LocalFabric, NcclFabric, Plan
 from .errors import ConfigError, InputError, ProtocolError
-from .graph import (DynamicGraph, FeatureSequence, MMatrix, SmoothedGraph, build_m_matrix, degree_features,
-                    m_transform_features, m_transform_graph)
+from .graph import (DynamicGraph, FeatureSequence, LazyDegreeFeatures, MMatrix, SmoothedGraph, build_m_matrix,
+                    degree_features, edge_life_matrix, m_transform_features, m_transform_graph)
 from .params import ModelConfig, as_config, init_params, parameter_count
 
 SCHEDULERS = ("round-robin", "threads")
@@ -259,7 +259,11 @@ def prepare_training_data(cfg, graph) -> TrainingData:
     elif cfg.architecture == "cd-gcn":
         smoothed, feats = graph, degree_features(graph)
     else:
-        raise ConfigError("egcn-o is outside this package's hot path (SURVEY §8f)")
+        # egcn-o (training.py:238-240): edge life (dtdg.py:194-208) applied on
+        # the device like the tm-gcn smoothing; the degree features of the
+        # smoothed graph are computed on the device too (host copy on demand)
+        smoothed = SmoothedGraph(graph, edge_life_matrix(graph.num_timesteps, cfg.edge_life))
+        feats = LazyDegreeFeatures(smoothed)
     if feats.width != cfg.in_features:
         raise ConfigError(f"configured in_features={cfg.in_features} but input frames have width {feats.width}")
     return TrainingData(graph=smoothed, laps=None, feats=feats, s1=None, m_matrix=m)

@@ -123,6 +123,7 @@ class Rank:
         self.set_turn = 0
         self.built = {}          # block -> (slots, ready event, epoch tag) (keep_graphs mode)
         self.skip = eng.skip
+        self.evolve = eng.evolve
         L = len(layers)
         # snapshot-major (owner layout) and vertex-major buffers
         # the split GCN (cd-gcn, P > 1) keeps r / dr vertex-major only: no owner-layout copies
@@ -132,9 +133,11 @@ class Rank:
         # symmetric allocation, same offsets on every rank
         peer = eng.peer
         recv = (lambda n: peer.alloc(n)) if peer is not None else (lambda n: _zeros(n, device=dev))
-        self.Y_own = [recv(P * C * NP * Ly.ho) for Ly in layers]
+        # egcn-o has no temporal feature operator: a layer's output is its GCN
+        # output, snapshot-major throughout (no exchange)
+        self.Y_own = self.R_own if eng.evolve else [recv(P * C * NP * Ly.ho) for Ly in layers]
         self.S_own = [None] + [_zeros(C * N * Ly.fp, device=dev) for Ly in layers[1:]]
-        same = P == 1
+        same = P == 1 or eng.evolve
         self.split = eng.split
         if self.split:
             # S_own is in the owner layout [P][C][NP][fp] (all-to-all ready)
@@ -160,7 +163,8 @@ class Rank:
             self.C_vm = [_zeros(B * NP * Ly.ho, device=dev) for Ly in layers]
             self.cbuf = [_zeros(2 * NP * Ly.ho, device=dev) for Ly in layers]
             self.state = [(_zeros(NP * Ly.ho, device=dev), _zeros(NP * Ly.ho, device=dev)) for Ly in layers]
-            self.zero_state = [(_zeros(NP * Ly.ho, device=dev), _zeros(NP * Ly.ho, device=dev)) for Ly in layers]
+            zs = [_zeros(NP * Ly.ho, device=dev) for Ly in layers]      # read only
+            self.zero_state = [(z, z) for z in zs]
             self.dstate = [(_zeros(NP * Ly.ho, device=dev), _zeros(NP * Ly.ho, device=dev)) for Ly in layers]
             self.dcarry = [(_zeros(2 * NP * Ly.ho, device=dev), _zeros(2 * NP * Ly.ho, device=dev))
                            for Ly in layers]
@@ -170,6 +174,18 @@ class Rank:
             self.trail = [dict() for _ in layers]
             self.dtrail = [dict() for _ in layers]
             self.Z_vm = self.Y_vm    # M-product output, vertex-major
+        if self.evolve:
+            # weight evolution (fp64, padded F x H per layer): carried state,
+            # rerun scratch, gradient carry, the block's per-step fp32 weight
+            # images, per-step cache and per-step weight-gradient seeds
+            f64 = torch.float64
+            cnts = [Ly.fp * Ly.hg for Ly in layers]
+            self.wstate = [_zeros(c, f64, dev) for c in cnts]
+            self.wtmp = [_zeros(c, f64, dev) for c in cnts]
+            self.dwcarry = [_zeros(c, f64, dev) for c in cnts]
+            self.wimg = [_zeros(B * c, device=dev) for c in cnts]
+            self.wcache = [_zeros(B * 6 * c, f64, dev) for c in cnts]
+            self.wseed = [_zeros(B * c, f64, dev) for c in cnts]
         self.pi = {}
         # first-layer products s1[t] = Ahat_t X_t for owned steps, [N, fp0] fp32
         self.s1 = {}
@@ -261,6 +277,10 @@ class Rank:
 
     # ---------------------------------------------------------------- phases
     def reset_state(self):
+        if self.evolve:
+            for l, w in enumerate(self.wstate):
+                w.copy_(self.eng.params.w64_block(f"evolve{l}.w0").reshape(-1))
+                self.dwcarry[l].zero_()
         if self.skip:
             for h, c in self.state:
                 h.zero_()
@@ -325,6 +345,14 @@ class Rank:
                 self.act = self.pi[b - 1] if b > 0 else self.zero_state
             else:
                 self.act = self.state
+        if self.evolve:
+            # the weight entering the block: pi_{b-1} / w0 in the rerun, the
+            # carried state in the forward sweep (training.py:516-523)
+            if keep:
+                self.w_in = self.pi[b - 1] if b > 0 else [self.eng.params.w64_block(f"evolve{l}.w0").reshape(-1)
+                                                          for l in range(len(self.wstate))]
+            else:
+                self.w_in = self.wstate
 
     def enable_keep_graphs(self):
         self.mat.add_sets(self.eng.plan.nblk + 1 - len(self.mat.sets))
@@ -436,11 +464,64 @@ class Rank:
                     works += dist.batch_isend_irecv(ops)
         return works
 
+    def _gcn_w(self, l, t):
+        """Device pointer of the GCN weight used at step t: the evolved W_t
+        (egcn-o) or the layer's parameter."""
+        if self.evolve:
+            Ly = self.eng.layout.layers[l]
+            i = t - self.b * self.eng.plan.bsize
+            return self.wimg[l].data_ptr() + F32 * i * Ly.fp * Ly.hg
+        return ptr(self.eng.params.w(f"gcn{l}.w"))
+
+    def evolve_forward(self, b, l):
+        """egcn-o: the weight chain over all of block b's steps (every rank
+        runs it; `dist.py:322-330`), its per-step fp32 images, and in the
+        rerun the cache for the backward."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        cnt = Ly.fp * Ly.hg
+        out = self.wtmp[l] if self.keep else self.wstate[l]
+        call("dgnn_evolve_forward", cnt, eng.plan.bsize, ptr(eng.params.w64_block(f"evolve{l}.gates")),
+             ptr(eng.params.w64_block(f"evolve{l}.bias")), ptr(self.w_in[l]), ptr(out), ptr(self.wimg[l]),
+             ptr(self.wcache[l]) if self.keep else None, _lib.stream_handle())
+
+    def evolve_backward(self, b, l):
+        """egcn-o backward of layer l for block b (`dist.py:422-447`): per
+        owned step the plain-GCN backward with the evolved W_t (weight
+        gradient as the chain's seed dW_t, ds and Ahat^T ds for layer l-1),
+        then the chain backward over the block (gates / bias gradients, the
+        carry into block b-1; other ranks' steps contribute no seed here --
+        their share arrives through the gradient all-reduce)."""
+        eng = self.eng
+        plan = eng.plan
+        Ly = eng.layout.layers[l]
+        st = _lib.stream_handle()
+        N, rw, fp, hg = plan.N, Ly.rw, Ly.fp, Ly.hg
+        cnt = fp * hg
+        n_own = plan.P * plan.chunk * plan.NP * rw
+        self.dR_own[l][:n_own].copy_(self.dZ_own[:n_own])      # dL/dy of this layer (owner layout)
+        self.wseed[l].zero_()
+        for c, t in enumerate(self.ts):
+            i = t - b * plan.bsize
+            dr = self.own(self.dR_own[l], rw, c)
+            r = self.own(self.R_own[l], rw, c)
+            s = self.plain(self.s1[t], fp) if l == 0 else self.plain(self.S_own[l], fp, c)
+            call("dgnn_gcn_weight_grad", N, s, dr, r, fp, hg, 0, self.wseed[l].data_ptr() + 8 * i * cnt,
+                 ptr(self.ws_tn), self.ws_tn.numel(), st)
+            if l > 0:
+                ds = self.plain(self.dS, fp)
+                call("dgnn_gcn_backward_rows", N, dr, r, fp, self._gcn_w(l, t), hg, 0, ds, st)
+                sl = self.slots[c]
+                call("dgnn_spmm_f32", N, ptr(sl.t_rowptr), ptr(sl.t_col), ptr(sl.t_val), ds, fp,
+                     self.own(self.dZ_own, fp, c), st)
+        call("dgnn_evolve_backward", cnt, plan.bsize, ptr(eng.params.w64_block(f"evolve{l}.gates")),
+             ptr(self.wcache[l]), ptr(self.wseed[l]), ptr(self.dwcarry[l]),
+             ptr(eng.params.gw(f"evolve{l}.gates")), ptr(eng.params.gw(f"evolve{l}.bias")), st)
+
     def gcn_forward(self, b, l):
         eng = self.eng
         Ly = eng.layout.layers[l]
         st = _lib.stream_handle()
-        w = eng.params.w(f"gcn{l}.w")
         for c, t in enumerate(self.ts):
             if l == 0:
                 x = self.plain(self.s1[t], Ly.fp)
@@ -451,7 +532,7 @@ class Rank:
                 s = self.slots[c]
                 rp, col, val = ptr(s.rowptr), ptr(s.col), ptr(s.val)
             s_out = self.plain(self.S_own[l], Ly.fp, c) if (self.keep and l > 0) else _lib.Frame(None, 0, 0, 0)
-            call("dgnn_gcn_forward", eng.plan.N, rp, col, val, x, Ly.fp, ptr(w), Ly.hg, int(self.skip),
+            call("dgnn_gcn_forward", eng.plan.N, rp, col, val, x, Ly.fp, self._gcn_w(l, t), Ly.hg, int(self.skip),
                  s_out, self.own(self.R_own[l], Ly.rw, c), st)
 
     # ----------------------------------------------- split GCN (P > 1, cd-gcn)
@@ -666,6 +747,8 @@ class Rank:
     def store_pi(self, b):
         if self.skip and b < self.eng.plan.nblk - 1:
             self.pi[b] = [(h.clone(), c.clone()) for h, c in self.state]
+        if self.evolve and b < self.eng.plan.nblk - 1:
+            self.pi[b] = [w.clone() for w in self.wstate]
 
     def block_loss(self, b):
         eng = self.eng
@@ -950,15 +1033,16 @@ class Engine:
         self.tensor_cores = bool(tensor_cores)
         # persistent warp-specialised tcgen05 step kernels (else one CTA per tile)
         self.warp_specialized = WARP_SPECIALIZED
-        if cfg.architecture not in ("cd-gcn", "tm-gcn"):
-            raise ConfigError(f"architecture {cfg.architecture!r} is outside this package's hot path")
+        if cfg.architecture not in ("cd-gcn", "tm-gcn", "egcn-o"):
+            raise ConfigError(f"unknown architecture {cfg.architecture!r}")
         self.cfg = cfg
         self.skip = cfg.architecture == "cd-gcn"
+        self.evolve = cfg.architecture == "egcn-o"
         N, T = graph.num_vertices, graph.num_timesteps
         self.plan = Plan(T, workers, nblk, N)
         self.layout = ParamLayout(cfg)
         self.m_matrix = None if m_matrix is None else np.asarray(m_matrix, dtype=np.float64)
-        if not self.skip and self.m_matrix is None:
+        if cfg.architecture == "tm-gcn" and self.m_matrix is None:
             from .graph import build_m_matrix
             self.m_matrix = build_m_matrix(T, cfg.window).matrix
         self.resident = resident
@@ -1076,7 +1160,7 @@ class Engine:
 
     def _pipelining(self):
         """(GCN-side, LSTM-side) exchange pipelining for this run."""
-        if self.split:
+        if self.split or self.evolve:
             return False, False
         if not (self.fabric.distributed and self.plan.P > 1) or PIPELINED_EXCHANGE == "0":
             return False, False
@@ -1269,6 +1353,13 @@ class Engine:
         if self.peer is not None:
             self.peer.barrier()
         for l, Ly in enumerate(layers):
+            if self.evolve:
+                # egcn-o: weight chain + GCN per owned snapshot; no feature
+                # RNN, hence no redistribution (dist.py:530-541)
+                for r in self.ranks:
+                    r.evolve_forward(b, l)
+                    r.gcn_forward(b, l)
+                continue
             if self.peer is not None:
                 self._peer_layer_forward(b, l, phase, comm)
                 continue
@@ -1347,6 +1438,17 @@ class Engine:
                     act.free_checkpoint(1.0)
                 self._release_checkpoint(b)
                 continue
+            if self.evolve:
+                for r in self.ranks:
+                    r.loss_grads(b)
+                for l in reversed(range(L)):
+                    for r in self.ranks:
+                        r.evolve_backward(b, l)
+                if act is not None:
+                    act.free_activations(plan.bsize * 2 * L)
+                    act.free_checkpoint(1.0)
+                self._release_checkpoint(b)
+                continue
             pipe_gcn, pipe_lstm = self._pipelining()
             works = []
             for r in self.ranks:
@@ -1383,6 +1485,10 @@ class Engine:
                 act.free_activations(plan.bsize * 2 * L)
                 act.free_checkpoint(1.0)
             self._release_checkpoint(b)
+        if self.evolve:     # the initial weights' gradient (training.py:750-754, dist.py:453-457)
+            for r in self.ranks:
+                for l, d in enumerate(r.dwcarry):
+                    self.params.gw(f"evolve{l}.w0").view(-1).add_(d)
         grads = self.fabric.allreduce([self.params.gather_grads()])
         self.params.g.copy_(grads)
         if comm is not None:

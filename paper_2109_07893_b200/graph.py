@@ -269,3 +269,43 @@ class SmoothedGraph:
             else:
                 self._encoding = SnapshotEncoding(DynamicGraph(self.num_vertices, self.snapshots))
         return self._encoding
+
+
+def edge_life_matrix(num_timesteps: int, life: int) -> MMatrix:
+    """`apply_edge_life` (dtdg.py:194-208) as a weighting: snapshot t becomes
+    sum_{k = max(0, t-life+1)}^{t} 1.0 * A_k (ascending k), i.e. the M-product
+    with a banded matrix of ones -- smoothed by the same device merge."""
+    if life < 1:
+        raise InputError(f"edge life must be >= 1, got {life}")
+    m = np.zeros((num_timesteps, num_timesteps))
+    for t in range(num_timesteps):
+        m[t, max(0, t - life + 1):t + 1] = 1.0
+    return MMatrix(num_timesteps, life, m)
+
+
+class LazyDegreeFeatures:
+    """Degree features of a smoothed graph (`degree_features`,
+    dtdg.py:255-266), built on the host only if read: the engine computes
+    them on the device from the rebuilt snapshots."""
+
+    def __init__(self, graph):
+        self.graph = graph
+        self._fs = None
+
+    @property
+    def width(self) -> int:
+        return 2
+
+    @property
+    def num_timesteps(self) -> int:
+        return self.graph.num_timesteps
+
+    @property
+    def num_vertices(self) -> int:
+        return self.graph.num_vertices
+
+    @property
+    def frames(self) -> list:
+        if self._fs is None:
+            self._fs = degree_features(self.graph)
+        return self._fs.frames

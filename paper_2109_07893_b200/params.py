@@ -93,11 +93,17 @@ def _glorot(rng, fan_in, fan_out):
 def init_params(cfg, seed: int) -> dict:
     """Seeded parameters in the reference's key and draw order."""
     cfg = as_config(cfg)
-    if cfg.architecture == "egcn-o":
-        raise ConfigError("egcn-o is outside this package's hot path (SURVEY §8f)")
     rng = np.random.default_rng(seed)
     params = {}
     for layer, d in enumerate(cfg.layer_dims()):
+        if cfg.architecture == "egcn-o":
+            # models.py:157-163: initial weight, four gate matrices, forget bias 1
+            params[f"evolve{layer}.w0"] = _glorot(rng, d.fin, d.gcn_out)
+            params[f"evolve{layer}.gates"] = np.stack([_glorot(rng, d.fin, d.gcn_out) for _ in range(4)])
+            bias = np.zeros((4, d.fin, d.gcn_out))
+            bias[1] = 1.0
+            params[f"evolve{layer}.bias"] = bias
+            continue
         params[f"gcn{layer}.w"] = _glorot(rng, d.fin, d.gcn_out)
         if cfg.architecture == "cd-gcn":
             f_in, hid = d.fin + d.gcn_out, d.out
@@ -177,7 +183,14 @@ class ParamLayout:
             self.blocks[name] = (size, rows, cols)
             size += (rows * cols + self.ALIGN - 1) // self.ALIGN * self.ALIGN
 
+        self.evolve = cfg.architecture == "egcn-o"
         for l, L in enumerate(self.layers):
+            if self.evolve:
+                # the evolving GCN weight: initial matrix, stacked gates / biases
+                alloc(f"evolve{l}.w0", L.fp, L.hg)
+                alloc(f"evolve{l}.gates", 4 * L.fp, L.hg)
+                alloc(f"evolve{l}.bias", 4 * L.fp, L.hg)
+                continue
             alloc(f"gcn{l}.w", L.fp, L.hg)
             if L.skip:
                 alloc(f"lstm{l}.wcat", L.kx + L.ho, 4 * L.ho)
@@ -201,7 +214,15 @@ class ParamLayout:
         self.count = int(self.pos0.shape[0])
 
     def _positions(self, key, shape):
-        L_idx = None
+        if key.startswith("evolve"):
+            l = int(key[6:key.index(".")])
+            off, _, cols = self.blocks[key]
+            fp = self.layers[l].fp
+            if key.endswith(".w0"):
+                k, j = np.meshgrid(np.arange(shape[0]), np.arange(shape[1]), indexing="ij")
+                return (off + k * cols + j).ravel(), np.full(k.size, -1)
+            g, k, j = np.meshgrid(np.arange(4), np.arange(shape[1]), np.arange(shape[2]), indexing="ij")
+            return (off + (g * fp + k) * cols + j).ravel(), np.full(k.size, -1)
         if key.startswith("gcn"):
             l = int(key[3:key.index(".")])
             L = self.layers[l]
@@ -269,6 +290,11 @@ class ParamLayout:
 def init_params_shapes(cfg: ModelConfig) -> dict:
     shapes = {}
     for layer, d in enumerate(cfg.layer_dims()):
+        if cfg.architecture == "egcn-o":
+            shapes[f"evolve{layer}.w0"] = np.empty((d.fin, d.gcn_out))
+            shapes[f"evolve{layer}.gates"] = np.empty((4, d.fin, d.gcn_out))
+            shapes[f"evolve{layer}.bias"] = np.empty((4, d.fin, d.gcn_out))
+            continue
         shapes[f"gcn{layer}.w"] = np.empty((d.fin, d.gcn_out))
         if cfg.architecture == "cd-gcn":
             shapes[f"lstm{layer}.wx"] = np.empty((d.fin + d.gcn_out, 4 * d.out))
@@ -292,6 +318,8 @@ class DeviceParams:
         self.v = torch.zeros_like(self.p64)
         self.g = torch.zeros_like(self.p64)          # flat gradient (all-reduce / Adam input)
         self.w32 = torch.zeros(layout.size, dtype=torch.float32, device=dev)
+        # egcn-o: the weight-evolution chain runs in fp64 (an fp64 padded image)
+        self.w64 = torch.zeros(layout.size, dtype=torch.float64, device=dev) if layout.evolve else None
         self.gpad = torch.zeros(layout.size, dtype=torch.float64, device=dev)
         self.pos0 = torch.from_numpy(layout.pos0).to(dev)
         self.pos1 = torch.from_numpy(layout.pos1).to(dev)
@@ -318,6 +346,8 @@ class DeviceParams:
         sh = _lib.stream_handle(stream)
         call("dgnn_params_to_device", self.layout.count, ptr(self.p64), ptr(self.pos0), ptr(self.pos1),
              ptr(self.w32), sh)
+        if self.w64 is not None:
+            call("dgnn_scatter_f64", self.layout.count, ptr(self.p64), ptr(self.pos0), ptr(self.w64), sh)
         for l, L in enumerate(self.layout.layers):
             if L.skip:
                 K = L.kx + L.ho
@@ -328,6 +358,9 @@ class DeviceParams:
 
     def w(self, name: str) -> torch.Tensor:
         return self.layout.block(self.w32, name)
+
+    def w64_block(self, name: str) -> torch.Tensor:
+        return self.layout.block(self.w64, name)
 
     def gw(self, name: str) -> torch.Tensor:
         return self.layout.block(self.gpad, name)

@@ -10,7 +10,7 @@ reuses the kept snapshots, the head chain and the label cache) with one rank
 per GPU and compares loss, gradients and the communication ledger.  Cases:
 hidden = embed = 64 (the bench widths) and hidden 32 / embed 64 (layer 1's
 input narrower than its output: the seed buffers of the two layers differ
-in width), cd-gcn; tm-gcn at hidden 32.  Transport: DGNN_EXCHANGE=peer
+in width), cd-gcn; tm-gcn and egcn-o at hidden 32.  Transport: DGNN_EXCHANGE=peer
 (default) or nccl.  Results: gpurun_out/nccl_check_P_<transport>.json.
 """
 
@@ -30,7 +30,8 @@ sys.path.insert(0, str(ROOT))
 import paper_2109_07893_b200 as pk  # noqa: E402
 from paper_2109_07893_b200.synth import churn_graph  # noqa: E402
 
-CASES = {"cd64": ("cd-gcn", 64, 64), "cd32x64": ("cd-gcn", 32, 64), "tm32": ("tm-gcn", 32, 32)}
+CASES = {"cd64": ("cd-gcn", 64, 64), "cd32x64": ("cd-gcn", 32, 64), "tm32": ("tm-gcn", 32, 32),
+         "eg32": ("egcn-o", 32, 32)}
 
 
 def problem(arch, hidden, embed):

@@ -262,6 +262,12 @@ def delta_bytes():
     (HERE / "delta_record.bin").write_bytes(buf.getvalue())
 
 
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "egcn":
+    # the EGCN-O fixture alone (added in round 2; the others are unchanged)
+    model_fixture("egcn_small", "egcn-o", n=16, t_count=8, m=24, churn=0.25, hidden=8,
+                  seed_graph=8, theta=0.5, label_seed=9, param_seed=4)
+    sys.exit(0)
+
 if __name__ == "__main__":
     codec_fixture()
     spmm_fixture()
@@ -270,6 +276,8 @@ if __name__ == "__main__":
                   seed_graph=4, theta=0.5, label_seed=5, param_seed=3)
     model_fixture("tmgcn_small", "tm-gcn", n=16, t_count=8, m=24, churn=0.25, hidden=8,
                   seed_graph=6, theta=0.5, label_seed=7, param_seed=2)
+    model_fixture("egcn_small", "egcn-o", n=16, t_count=8, m=24, churn=0.25, hidden=8,
+                  seed_graph=8, theta=0.5, label_seed=9, param_seed=4)
     cli_report()
     delta_bytes()
     c1_pins()

@@ -29,7 +29,7 @@ def _fresh_engines():
     pk.api.clear_engines()
 
 
-@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small", "egcn_small"])
 @pytest.mark.parametrize("nblk", [1, 2, 4])
 def test_backward_checkpoint_vs_reference(name, nblk):
     fx, cfg, data, train, _, params = product_case(name)
@@ -38,7 +38,7 @@ def test_backward_checkpoint_vs_reference(name, nblk):
     assert_grads_close(grads, params_from(fx, f"ckpt{nblk}_g_"), RTOL, ENGINE_ATOL)
 
 
-@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small", "egcn_small"])
 def test_backward_full_vs_reference(name):
     fx, cfg, data, train, _, params = product_case(name)
     loss, grads = pk.backward_full(cfg, data, train, params)
@@ -46,7 +46,7 @@ def test_backward_full_vs_reference(name):
     assert_grads_close(grads, params_from(fx, "full_g_"), RTOL, ENGINE_ATOL)
 
 
-@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small", "egcn_small"])
 @pytest.mark.parametrize("workers,nblk", [(2, 2), (4, 1), (2, 1)])
 def test_distributed_epoch_vs_reference(name, workers, nblk):
     fx, cfg, data, train, _, params = product_case(name)
@@ -78,10 +78,10 @@ def test_multi_rank_matches_single_rank():
     assert_grads_close(g4, g1, RTOL, ENGINE_ATOL)
 
 
-@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small", "egcn_small"])
 def test_train_distributed_vs_reference(name):
     fx, cfg, data, train, test, _ = product_case(name)
-    seed = 3 if name.startswith("cd") else 2
+    seed = {"cdgcn_small": 3, "tmgcn_small": 2, "egcn_small": 4}[name]
     trace, params, comm, tr, act = pk.train_distributed(cfg, data, train, test, epochs=3, seed=seed,
                                                         workers=2, nblk=2)
     ref = jload(fx["train_trace"])
@@ -217,3 +217,44 @@ def test_graph_residency_modes_match_reference(keep, workers, nblk, monkeypatch)
             assert tr.full_equiv_bytes == 2 * tr.full_built_bytes
         if keep == "1" or workers == 1:    # every head after t = 0 rebuilt from a delta
             assert tr.h2d_bytes < tr.full_built_bytes
+
+
+def test_train_report_matches_reference_cli_golden():
+    """§8f.3: the dtgnn.report/1 document of the reference CLI's frozen
+    golden run, produced by this package on the GPU (timing excluded)."""
+    from paper_2109_07893_b200 import wire
+    fx = load("cli_report")
+    ref = jload(fx["report"])
+    g = product_graph(fx)
+    rep, _ = wire.train_report(g, dict(ref["config"]))
+    assert rep["schema"] == ref["schema"] == "dtgnn.report/1"
+    assert set(rep) == set(ref) | {"timing"}
+    assert rep["config"] == ref["config"]
+    assert rep["comm"] == ref["comm"] and rep["transfer"] == ref["transfer"]
+    assert rep["activation_peak"] == ref["activation_peak"]
+    for a, b in zip(rep["epochs"], ref["epochs"]):
+        assert a["epoch"] == b["epoch"] and a["loss"] == pytest.approx(b["loss"], rel=RTOL)
+
+
+def test_egcn_midsize_vs_oracle(oracle):
+    """§8f.4 EGCN-O at N = 20k, T = 8, hidden 32: P = 1 and emulated P = 4
+    against the oracle's checkpointed backward (pinned to the reference by
+    tests/test_oracle_golden.py::test_egcn_oracle_pinned)."""
+    from paper_2109_07893_b200.synth import churn_graph
+    g = churn_graph(20_000, 8, 30_000, 0.10, seed=6)
+    cfg = pk.ModelConfig("egcn-o", hidden_features=32, embed_features=32)
+    data = pk.prepare_training_data(cfg, g)
+    train, _ = pk.sample_link_prediction_sets(g, 0.1, 10)
+    params = pk.init_params(cfg, 5)
+    rng = np.random.default_rng(2)
+    params["head.w"] = rng.uniform(-0.5, 0.5, size=params["head.w"].shape)
+    l1, g1 = pk.backward_checkpoint(cfg, data, train, params, 2)
+    l4, g4, comm, tr = pk.distributed_epoch(cfg, data, train, params, 4, 2)
+    ocfg = oracle.Cfg("egcn-o", 2, 32, 32)
+    P = oracle.prepare(ocfg, [oracle.Coo(s.dim, s.rows, s.cols, s.vals) for s in g.snapshots])
+    lo, go = oracle.backward_checkpoint(ocfg, P, train.by_time, params, 2)
+    assert l1 == pytest.approx(lo, rel=RTOL)
+    assert l4 == pytest.approx(lo, rel=RTOL)
+    assert_grads_close(g1, go, RTOL, ENGINE_ATOL)
+    assert_grads_close(g4, go, RTOL, ENGINE_ATOL)
+    assert comm.redistribution_units == 0 and comm.alltoall_events() == []

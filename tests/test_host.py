@@ -231,3 +231,38 @@ def test_smoothed_encoding_counts_equal_host_smoothing():
     assert np.array_equal(dev.dhat, host.dhat)
     assert np.array_equal(dev.nnz_sm, host.nnz)
     assert dev.unit and not host.unit
+
+
+def test_delta_stream_wire_format():
+    """§8f.3: the reference's record layout -- golden bytes
+    (`test_delta.py:200-215`), round trip, truncation, and a record file
+    loaded straight into the engine's encoding."""
+    import io
+    from pathlib import Path
+    from helpers import product_graph
+    from paper_2109_07893_b200 import wire
+    from paper_2109_07893_b200.materialize import SnapshotEncoding
+    a = pk.SparseMatrix.from_entries(2, [0], [1], [1.0])
+    b = pk.SparseMatrix.from_entries(2, [1], [1], [2.5])
+    buf = io.BytesIO()
+    wire.write_delta_stream([a, b], buf)
+    assert buf.getvalue() == (Path(__file__).parent / "golden" / "delta_record.bin").read_bytes()
+    for prefix in ("g_", "gw_"):
+        g = product_graph(load("codec"), prefix)
+        buf = io.BytesIO()
+        wire.write_delta_stream(g.snapshots, buf)
+        raw = buf.getvalue()
+        buf.seek(0)
+        back = wire.graph_from_delta_stream(g.snapshots[0], buf)
+        assert all(x == y for x, y in zip(back.snapshots, g.snapshots))
+        enc = wire.encoding_from_delta_stream(g.snapshots[0], io.BytesIO(raw), pin=False)
+        ref = SnapshotEncoding(g, pin=False)
+        assert enc.unit == ref.unit and torch_equal(enc.delta, ref.delta) and torch_equal(enc.full, ref.full)
+        assert np.array_equal(enc.nnz_hat, ref.nnz_hat) and np.array_equal(enc.dhat, ref.dhat)
+        with pytest.raises(pk.CorruptDeltaError):
+            wire.read_delta_stream(io.BytesIO(raw[:-3]), g.num_vertices)
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))

@@ -256,3 +256,28 @@ def test_cone_forward_equals_full_forward(oracle, arch):
                                      P.window)
     for t in range(P.T):
         assert np.array_equal(full[t][np.unique(rows)], part[t])
+
+
+def test_egcn_oracle_pinned(oracle):
+    """§8f.4 EGCN-O: the oracle's restatement (edge life, weight-evolution
+    chain forward / backward, initial-weight gradient) against the
+    reference's own outputs: init params, full backward, checkpointed
+    backward at nblk 1 / 2 / 4, forward frames."""
+    fx, cfg, P = _case(oracle, "egcn_small")
+    init = oracle.init_params(cfg, 4)
+    ref_init = params_from(fx, "init_")
+    assert sorted(init) == sorted(ref_init)
+    for k in ref_init:
+        assert np.array_equal(init[k], ref_init[k]), k
+    params = params_from(fx, "p_")
+    train = labels_from(fx, "train_")
+    for nblk, tag in ((1, "full"), (1, "ckpt1"), (2, "ckpt2"), (4, "ckpt4")):
+        loss, grads = oracle.backward_checkpoint(cfg, P, train, params, nblk)
+        assert loss == pytest.approx(float(fx[f"{tag}_loss"]), rel=1e-12)
+        ref = params_from(fx, f"{tag}_g_")
+        assert sorted(grads) == sorted(ref)
+        for k in ref:
+            np.testing.assert_allclose(grads[k], ref[k], rtol=1e-9, atol=1e-12, err_msg=(tag, k))
+    z = oracle.model_forward(cfg, P, params)
+    for t, f in enumerate(z):
+        np.testing.assert_allclose(f, fx[f"z{t}"], rtol=1e-11, atol=1e-13)
