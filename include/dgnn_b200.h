@@ -223,6 +223,12 @@ int dgnn_lstm_forward_step_tc(int64_t rows, int32_t kx, int32_t hp, const float*
  * epilogue warps, 4-stage smem ring, double-buffered TMEM accumulator; one
  * CTA per SM).  Same contracts and operand images as the _tc entries;
  * hp in {16, 32, 64}. */
+/* K5 on CTA pairs (tcgen05.mma.cta_group::2, 2-CTA clusters): same contract
+ * and bitwise the same results as dgnn_lstm_forward_step_ws; each CTA stages
+ * its 128 rows and half of the weight chunk (hp 32 or 64). */
+int dgnn_lstm_forward_step_pair(int64_t rows, int32_t kx, int32_t hp, const float* x, int64_t ldx,
+                                const float* h_prev, const float* c_prev, const float* wimg, const float* bias,
+                                float* h_out, float* c_out, float* gates, void* stream);
 int dgnn_lstm_forward_step_ws(int64_t rows, int32_t kx, int32_t hp, const float* x, int64_t ldx,
                               const float* h_prev, const float* c_prev, const float* wimg,
                               const float* bias, float* h_out, float* c_out, float* gates,

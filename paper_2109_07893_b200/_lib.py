@@ -69,6 +69,7 @@ _SIGS = {
     "dgnn_tc_gemm_test": (c_int, [c_int32, c_int32, c_int32, P, c_int64, P, P, c_int64, P]),
     "dgnn_lstm_forward_step_tc": (c_int, [c_int64, c_int32, c_int32, P, c_int64, P, P, P, P, P, P, P, P]),
     "dgnn_lstm_forward_step_ws": (c_int, [c_int64, c_int32, c_int32, P, c_int64, P, P, P, P, P, P, P, P]),
+    "dgnn_lstm_forward_step_pair": (c_int, [c_int64, c_int32, c_int32, P, c_int64, P, P, P, P, P, P, P, P]),
     "dgnn_lstm_backward_step_ws": (c_int, [c_int64, c_int32, c_int32, P, P, P, P, P, P, P, P, c_int64, P, P,
                                            P]),
     "dgnn_lstm_backward_step": (c_int, [c_int64, c_int32, c_int32, P, P, P, P, P, P, P, P, P, c_int64,

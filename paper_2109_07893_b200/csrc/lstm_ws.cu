@@ -52,7 +52,12 @@ struct WsRoles {
 // forward: heavy cell epilogue -- 16 epilogue warps (each a quarter of the
 // units of its TMEM lane quarter) when every warp still gets >= 8 units
 template <int HP>
-using FwdRoles = WsRoles<4, (HP >= 32 ? 16 : 8)>;
+using FwdRoles = WsRoles<8, (HP >= 32 ? 16 : 8), (HP >= 64 ? 3 : 4)>;
+// forward activation landing ring (fp32 chunks, cp.async), decoupled from
+// the operand stages so loads run RAW_RING - 1 chunks ahead (6 at hidden 64:
+// the operand stages are 48 KB and the c_prev tile takes 32 KB)
+template <int HP>
+constexpr int raw_ring() { return HP >= 64 ? 6 : 8; }
 // backward: 8 dz-producer warps fed from shared memory by one loader warp
 // (the extra warp), 3-stage A/B ring to leave room for the raw input ring
 using BwdRoles = WsRoles<8, 4, 3, 1>;
@@ -64,6 +69,7 @@ __host__ __device__ constexpr int ws_tmem_cols(int n2) {
 struct WsBars {
     uint64_t full_a[wsk::MAX_STAGES], full_b[wsk::MAX_STAGES], empty[wsk::MAX_STAGES], accfull[2], accempty[2];
     uint64_t raw_full[wsk::MAX_STAGES], raw_empty[wsk::MAX_STAGES];   // backward input ring
+    uint64_t cp_full, cp_empty;                                         // forward c_prev tile
     uint32_t tmem;
 };
 
@@ -198,30 +204,30 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
     const int K = kx + HP;
     const int nch = (K + wsk::KC - 1) / wsk::KC;
     const uint32_t b_bytes = 2 * N * 64;
+    const uint32_t cpbuf = sm.base + R::STAGES * sm.stage + 1024 + raw_ring<HP>() * wsk::A_TILE;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->cp_full, 1);
+        mbar_init(&bars->cp_empty, R::NEPI);
+        fence_mbar_init();
+    }
+    __syncthreads();
 
     if (warp < R::NPROD) {
-        // cp.async the raw fp32 chunk straight into the (swizzled) hi tile,
-        // LA chunks ahead, then split it in place: deep memory-level
-        // parallelism without holding the data in registers.
-        constexpr int LA = R::STAGES - 1;
+        // Activations land (cp.async, fp32, SW64) in a raw ring RAW_RING
+        // chunks deep, decoupled from the (few, 48 KB) operand stages: the
+        // loads run up to RAW_RING - 1 chunks (56 KB) ahead, which covers
+        // HBM latency at the MMA pace; the split writes the hi / lo operand
+        // tiles once the stage is free.  Each producer thread loads, splits
+        // and reloads only its own items, so a raw slot needs no barrier.
+        constexpr int RS = raw_ring<HP>();
         const int ptid = threadIdx.x;
         const int my_tiles = blockIdx.x < ntiles ? (int)cdiv(ntiles - blockIdx.x, gridDim.x) : 0;
         const uint32_t G = (uint32_t)my_tiles * nch;
+        const uint32_t raw0 = sm.base + R::STAGES * sm.stage + 1024;
         auto issue = [&](uint32_t g) {
             const int tile = blockIdx.x + (int)(g / nch) * gridDim.x;
             const int ch = (int)(g % nch);
-            const int s = g % R::STAGES;
-            const uint32_t j = g / R::STAGES;
-            if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
-            if (ptid == 0) {
-                if (wsk::PROBE & 4) {
-                    mbar_arrive(&bars->full_b[s]);
-                } else {
-                    mbar_arrive_expect_tx(&bars->full_b[s], b_bytes);
-                    bulk_g2s(sm.b(s), reinterpret_cast<const char*>(img) + (size_t)ch * b_bytes, b_bytes,
-                             &bars->full_b[s]);
-                }
-            }
+            const uint32_t slot = raw0 + (g % RS) * wsk::A_TILE;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const int idx = ptid + R::NPT * i;
@@ -230,36 +236,60 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
                 const int k = ch * wsk::KC + 4 * q;
                 const bool ok = gr < rows && k < K && !(wsk::PROBE & 2);
                 const float* src = !ok ? x : (k < kx ? x + gr * ldx + k : hprev + gr * HP + (k - kx));
-                cp_async16(sm.a_hi(s) + sw64(r, q), src, ok ? 16u : 0u);
+                cp_async16(slot + sw64(r, q), src, ok ? 16u : 0u);
             }
         };
-        for (uint32_t g = 0; g < (uint32_t)LA; ++g) {
+        for (uint32_t g = 0; g < (uint32_t)(RS - 1); ++g) {
             if (g < G) issue(g);
             cp_async_commit();
         }
-        // Split chunk g before waiting for the stage chunk g + LA reuses:
-        // that wait is on the MMAs of chunk g - 1, and holding the split of
-        // an already-landed chunk behind it would serialise MMA and producer.
         for (uint32_t g = 0; g < G; ++g) {
-            cp_async_wait<LA - 1>();
             const int s = g % R::STAGES;
+            const uint32_t j = g / R::STAGES;
+            if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
+            if (ptid == 0) {
+                if (wsk::PROBE & 4) {
+                    mbar_arrive(&bars->full_b[s]);
+                } else {
+                    const int ch = (int)(g % nch);
+                    mbar_arrive_expect_tx(&bars->full_b[s], b_bytes);
+                    bulk_g2s(sm.b(s), reinterpret_cast<const char*>(img) + (size_t)ch * b_bytes, b_bytes,
+                             &bars->full_b[s]);
+                }
+            }
+            cp_async_wait<RS - 2>();
+            const uint32_t slot = raw0 + (g % RS) * wsk::A_TILE;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const int idx = ptid + R::NPT * i;
                 const uint32_t off = sw64(idx >> 2, idx & 3);
                 float4 hi, lo;
-                split4(lds128(sm.a_hi(s) + off), hi, lo);
+                split4(lds128(slot + off), hi, lo);
                 sts128(sm.a_hi(s) + off, hi);
                 sts128(sm.a_lo(s) + off, lo);
             }
             fence_async_smem();
             __syncwarp();
             if ((ptid & 31) == 0) mbar_arrive(&bars->full_a[s]);
-            if (g + LA < G) issue(g + LA);
+            if (g + RS - 1 < G) issue(g + RS - 1);
             cp_async_commit();
         }
     } else if (warp == R::MMA_WARP) {
-        if (lane == 0) ws_mma_loop<R>(sm, bars, N, ntiles, nch);
+        if (lane == 0) {
+            ws_mma_loop<R>(sm, bars, N, ntiles, nch);
+        } else if (lane == 1) {
+            // c_prev is tile-blocked: a tile's rows are one contiguous block.
+            // Bulk-copy it into shared memory as soon as the epilogue has read
+            // the previous one, so the tile's cell update never waits on HBM.
+            uint32_t it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                if (it >= 1) mbar_wait(&bars->cp_empty, (it - 1) & 1);
+                const int64_t t0 = (int64_t)tile * wsk::BM;
+                const uint32_t bytes = (uint32_t)((rows - t0 < wsk::BM ? rows - t0 : wsk::BM) * HP * 4);
+                mbar_arrive_expect_tx(&bars->cp_full, bytes);
+                bulk_g2s(cpbuf, cprev + t0 * HP, bytes, &bars->cp_full);
+            }
+        }
         __syncwarp();
     } else {
         const int e = warp - R::MMA_WARP - 1;
@@ -270,17 +300,21 @@ __global__ void __launch_bounds__(FwdRoles<HP>::THREADS, 1) lstm_fwd_ws_kernel(
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const uint32_t a = it & 1, u = it >> 1;
             const int64_t row = (int64_t)tile * wsk::BM + 32 * q + lane;
+            const int64_t t0 = (int64_t)tile * wsk::BM;
             const bool valid = row < rows;
             float cp[UPW];
+            mbar_wait(&bars->cp_full, it & 1);
 #pragma unroll
             for (int i = 0; i < UPW / 4; ++i) {
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (valid) v = __ldg(reinterpret_cast<const float4*>(cprev + tb_off(row, part * UPW + 4 * i, HP, rows)));
+                if (valid) v = lds128(cpbuf + 4 * (uint32_t)(tb_off(row, part * UPW + 4 * i, HP, rows) - t0 * HP));
                 cp[4 * i] = v.x;
                 cp[4 * i + 1] = v.y;
                 cp[4 * i + 2] = v.z;
                 cp[4 * i + 3] = v.w;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->cp_empty);
             mbar_wait(&bars->accfull[a], u & 1);
             fence_after();
             const uint32_t tq = bars->tmem + lane_off + a * N;
@@ -504,7 +538,8 @@ int lstm_fwd_ws_t(int64_t rows, int kx, const float* x, int64_t ldx, const float
                   const float* img, const float* b, float* h, float* c, float* gates, cudaStream_t st) {
     constexpr int N = 4 * HP;
     auto k = lstm_fwd_ws_kernel<HP>;
-    const size_t smem = ws_smem_bytes<FwdRoles<HP>>(N);
+    const size_t smem = ws_smem_bytes<FwdRoles<HP>>(N) + 1024 + (size_t)raw_ring<HP>() * wsk::A_TILE +
+                        (size_t)wsk::BM * HP * 4;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int ntiles = (int)cdiv(rows, wsk::BM);
     const int grid = ntiles < persistent_ctas() ? ntiles : persistent_ctas();

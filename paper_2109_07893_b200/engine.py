@@ -66,6 +66,9 @@ KEEP_GRAPHS = os.environ.get("DGNN_KEEP_GRAPHS", "auto")
 # rebuild a chunk head from the 1-step delta on top of the previous rank's
 # last snapshot (handed over NVLink between GPUs) instead of shipping it full
 HEAD_CHAIN = os.environ.get("DGNN_HEAD_CHAIN", "1")
+# skip the forward-sweep pass of the last checkpoint block (its rerun is the
+# same computation and nothing reads its outputs); "0" runs it as the reference does
+SKIP_LAST_FORWARD = os.environ.get("DGNN_SKIP_LAST_FORWARD", "1") == "1"
 
 
 class Plan:
@@ -1391,6 +1394,15 @@ class Engine:
                 src = (lambda r: r.Y_vm[l]) if self.skip else (lambda r: r.Z_vm[l])
                 self._xchg(src, lambda r: r.Y_own[l], Ly.ho, comm, phase, b, l)
 
+    def _record_forward_pass(self, b, phase, comm):
+        """The CommLedger events of one forward pass of block b (two
+        redistributions per layer with a feature RNN), without the work."""
+        if comm is None or self.evolve:
+            return
+        for l in range(len(self.layout.layers)):
+            self._record_xchg(comm, phase, b, l)
+            self._record_xchg(comm, phase, b, l)
+
     def epoch(self, comm=None, transfer=None, act=None, count_total=None, reduction="mean"):
         """Forward sweep + checkpointed reverse sweep; returns (loss, flat fp64 grads)."""
         plan = self.plan
@@ -1410,7 +1422,15 @@ class Engine:
                 r.begin_block(b, keep=False, ledger=transfer, next_b=b + 1 if b + 1 < plan.nblk else b, fresh=True)
             for r in self.ranks:
                 r.prefetch(b + 1)
-            self._layers_forward(b, "forward", comm)
+            if b == plan.nblk - 1 and self.cfg.classes == 2 and SKIP_LAST_FORWARD:
+                # the last block's forward-sweep pass produces nothing that is
+                # read later: no checkpoint follows it and the loss comes from
+                # the reverse sweep's fused head, whose rerun of this block is
+                # the identical (deterministic) computation.  The ledger still
+                # records the reference's schedule (dist.py:548-551).
+                self._record_forward_pass(b, "forward", comm)
+            else:
+                self._layers_forward(b, "forward", comm)
             for r in self.ranks:
                 if self.cfg.classes != 2:
                     r.block_loss(b)

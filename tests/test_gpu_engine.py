@@ -258,3 +258,24 @@ def test_egcn_midsize_vs_oracle(oracle):
     assert_grads_close(g1, go, RTOL, ENGINE_ATOL)
     assert_grads_close(g4, go, RTOL, ENGINE_ATOL)
     assert comm.redistribution_units == 0 and comm.alltoall_events() == []
+
+
+@pytest.mark.parametrize("arch", ["cd-gcn", "tm-gcn", "egcn-o"])
+def test_first_layer_products_bit_exact(oracle, arch):
+    """H5 (`models.py:326-332`, `training.py:212`): the device's s1[t] =
+    Ahat_t X_t -- degree features (of the raw graph, M-smoothed for tm-gcn,
+    of the edge-life graph for egcn-o) and the fp64 SpMM in canonical order
+    -- equals the oracle's fp64 s1 rounded once to fp32, for every t."""
+    from paper_2109_07893_b200.synth import aml_graph
+    g = aml_graph(5000, 6, 20_000, 0.1, seed=3)
+    cfg = pk.ModelConfig(arch, hidden_features=16, embed_features=16)
+    data = pk.prepare_training_data(cfg, g)
+    eng = pk.api.get_engine(cfg, data, 1, 2)
+    eng.set_labels({}, None)
+    ocfg = oracle.Cfg(arch, 2, 16, 16)
+    P = oracle.prepare(ocfg, [oracle.Coo(s.dim, s.rows, s.cols, s.vals) for s in g.snapshots])
+    r = eng.ranks[0]
+    for t in range(g.num_timesteps):
+        got = r.s1[t].view(g.num_vertices, -1).cpu().numpy()
+        assert np.array_equal(got[:, :2], P.s1[t].astype(np.float32)), t
+        assert not got[:, 2:].any()

@@ -621,3 +621,40 @@ def test_device_smoothing_bit_exact(oracle):
     assert [x[2] for x in mat.builds] == [False, True, True] and other.builds[0][2]
     for x in (mat, other, a, b):
         x.check()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("hp,kx", [(64, 128), (64, 68), (32, 64), (32, 36)])
+@pytest.mark.parametrize("rows", [1, 200, 256 * 74 * 2 + 77, 300_001])
+def test_pair_lstm_forward_matches_single_cta_bitwise(hp, kx, rows):
+    """K5 on CTA pairs (cta_group::2, M = 256, each CTA half of the weight
+    chunk) against the one-CTA warp-specialised kernel: h, c and the gate
+    cache bitwise equal, with and without the cache, ragged pair tiles
+    (a lone 128-row half, rows < 128) and more pair tiles than pairs."""
+    from paper_2109_07893_b200 import _lib
+    from paper_2109_07893_b200._lib import call, ptr, query
+    g = torch.Generator(device="cuda").manual_seed(rows + hp + kx)
+    dev = torch.device("cuda")
+    K, N4 = kx + hp, 4 * hp
+    x = torch.randn(rows, kx, device=dev, generator=g)
+    h = torch.randn(rows, hp, device=dev, generator=g) * 0.5
+    c = torch.randn(rows, hp, device=dev, generator=g) * 0.5
+    wt = (torch.randn(N4, K, device=dev, generator=g) * 0.1).contiguous()
+    img = torch.zeros(query("dgnn_tc_weight_image_bytes", N4, K) // 4, device=dev)
+    st = _lib.stream_handle()
+    call("dgnn_tc_weight_image", N4, K, ptr(wt), K, ptr(img), st)
+    b = torch.randn(N4, device=dev, generator=g) * 0.1
+    outs = {}
+    for fn in ("dgnn_lstm_forward_step_ws", "dgnn_lstm_forward_step_pair"):
+        for keep in (False, True):
+            ho, co = torch.full((rows, hp), 7.0, device=dev), torch.full((rows, hp), 7.0, device=dev)
+            gg = torch.full((rows, N4), 7.0, device=dev)
+            call(fn, rows, kx, hp, ptr(x), kx, ptr(h), ptr(c), ptr(img), ptr(b), ptr(ho), ptr(co),
+                 ptr(gg) if keep else None, st)
+            torch.cuda.synchronize()
+            outs[fn, keep] = (ho, co, gg if keep else None)
+    for keep in (False, True):
+        a, p = outs["dgnn_lstm_forward_step_ws", keep], outs["dgnn_lstm_forward_step_pair", keep]
+        assert torch.equal(a[0], p[0]) and torch.equal(a[1], p[1])
+        if keep:
+            assert torch.equal(a[2], p[2])
