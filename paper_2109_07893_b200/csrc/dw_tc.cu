@@ -11,12 +11,10 @@
 // in lstm_tc.cu.  One persistent CTA per SM owns a contiguous row range.
 //
 // Warp-specialised (same scheme as lstm_ws.cu):
-//   warps 0..7  loaders: cp.async the raw fp32 rows of a stage straight into
-//               the swizzled hi tiles as soon as its slot is free, completion
-//               tracked by landed[s] (cp.async.mbarrier.arrive);
-//   warps 8..15 converters: split each landed stage in place (hi, lo), fold
-//               dz into fp64 column sums (db), arrive full[s] -- never
-//               blocked behind the slot-reuse wait;
+//   warps 0..15 producers: load their items of a stage DW_PD stages ahead
+//               into registers, split (hi, lo) straight into the swizzled
+//               tiles once the slot is free, fold dz into fp64 column sums
+//               (db), arrive full[s];
 //   warp 16     MMA issuer: 2 x mt x 3 MMAs per 16-row stage;
 //   warps 17..20 epilogue: promotion of each finished accumulation period.
 //
@@ -38,7 +36,8 @@ constexpr int DW_ROWS = 16;      // reduction rows per stage = two 8-row K steps
 #endif
 constexpr int DW_PERIOD = DGNN_DW_PERIOD;   // rows per TMEM accumulation period
 constexpr int DW_MAX_STAGES = 4;
-constexpr int DW_NLOAD = 8, DW_NCONV = 8, DW_NPROD = DW_NLOAD + DW_NCONV, DW_MMA_WARP = DW_NPROD, DW_NEPI = 4;
+constexpr int DW_NPROD = 16, DW_MMA_WARP = DW_NPROD, DW_NEPI = 4;
+constexpr int DW_PD = 2;         // stages of operand loads each producer keeps in flight (registers)
 constexpr int DW_THREADS = 32 * (DW_NPROD + 1 + DW_NEPI);
 constexpr int DW_SMEM_MAX = 232448;
 // Bottleneck probe (scripts/dw_probe.cu, -DDGNN_DW_PROBE=mask): 1 skip MMAs,
@@ -89,7 +88,7 @@ __host__ __device__ inline DwShape dw_shape(int hp, int kx) {
 inline size_t dw_smem_bytes(const DwShape& s) { return (size_t)s.stages * s.stage + 1024 + 256; }
 
 struct DwBars {
-    uint64_t landed[DW_MAX_STAGES], full[DW_MAX_STAGES], empty[DW_MAX_STAGES], accfull[2], accempty[2];
+    uint64_t full[DW_MAX_STAGES], empty[DW_MAX_STAGES], accfull[2], accempty[2];
     uint32_t tmem;
 };
 
@@ -113,11 +112,9 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
                                                                    float* __restrict__ slots,
                                                                    double* __restrict__ dbs) {
     constexpr int M = 4 * HP;
-    constexpr int NLT = 32 * DW_NLOAD, NCT = 32 * DW_NCONV;   // loader / converter threads
-    constexpr int LA_ITEMS = DW_ROWS * (M / 4) / NLT;    // A float4 items per loader thread per stage
-    constexpr int LB_ITEMS = (DW_ROWS * 64 + NLT - 1) / NLT;   // B items (N <= 256)
-    constexpr int CA_ITEMS = DW_ROWS * (M / 4) / NCT;    // per converter thread
-    constexpr int CB_ITEMS = (DW_ROWS * 64 + NCT - 1) / NCT;
+    constexpr int NPT = 32 * DW_NPROD;                          // producer threads
+    constexpr int A_ITEMS = DW_ROWS * (M / 4) / NPT;            // A float4 items per producer per stage
+    constexpr int B_ITEMS = (DW_ROWS * 64 + NPT - 1) / NPT;     // B items (N <= 256)
     const DwShape S = dw_shape(HP, kx);
     const int K = kx + HP;
     const int BVEC = DW_ROWS * S.N / 4;
@@ -131,8 +128,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
     if (warp == DW_MMA_WARP) tmem_alloc(&bars->tmem, S.tmem_cols);
     if (threadIdx.x == 0) {
         for (int i = 0; i < S.stages; ++i) {
-            mbar_init(&bars->landed[i], 32 * DW_NLOAD);
-            mbar_init(&bars->full[i], DW_NCONV);
+            mbar_init(&bars->full[i], DW_NPROD);
             mbar_init(&bars->empty[i], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -153,127 +149,139 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
     const int period_st = DW_PERIOD / DW_ROWS;
     const int nper = (nst + period_st - 1) / period_st;
     float* slot = slots + (size_t)blockIdx.x * M * S.N;   // [N][M]
-    double dbacc[4] = {0.0, 0.0, 0.0, 0.0};
+    double dbacc[4 * (DW_ROWS * (4 * HP / 4) / (32 * DW_NPROD))] = {};
     long long wacc0 = 0, wacc1 = 0;
     const long long t_start = clock64();
 
-    if (warp < DW_NLOAD) {
-        const int lt = threadIdx.x;
-        int arow[LA_ITEMS], brow[LB_ITEMS], bcol[LB_ITEMS], acol[LA_ITEMS];
-        uint32_t aoff[LA_ITEMS], boff[LB_ITEMS];
+    if (warp < DW_NPROD) {
+        // Producers: global -> registers (DW_PD stages in flight) -> tf32
+        // split -> the SW128_32B hi / lo tiles, and the fp64 column sums of
+        // dz (db).  Shared memory sees only the split stores: the operand
+        // reads of the 3xTF32 MMAs already take most of its bandwidth, and a
+        // raw landing copy plus its re-read measured as the kernel's
+        // bottleneck (scripts/dw_probe2.sh: -27% without the split pass).
+        const int pt = threadIdx.x;
+        int acol[A_ITEMS], brow[B_ITEMS], bcol[B_ITEMS];
+        uint32_t aoff[A_ITEMS], boff[B_ITEMS];
+        const int arow = pt % DW_ROWS;      // every A item of a thread is the same stage row
 #pragma unroll
-        for (int i = 0; i < LA_ITEMS; ++i) {
-            // consecutive lanes take consecutive rows of one 4-column group:
+        for (int i = 0; i < A_ITEMS; ++i) {
+            // consecutive threads take consecutive rows of one 4-column group:
             // 16 rows x 16 B contiguous in the tile-blocked dz
-            const int idx = lt + 32 * DW_NLOAD * i;
-            arow[i] = idx % DW_ROWS;
+            const int idx = pt + NPT * i;
             acol[i] = 4 * (idx / DW_ROWS);
-            aoff[i] = mn_off(arow[i], acol[i], S.atoms_a);
+            aoff[i] = mn_off(arow, acol[i], S.atoms_a);
         }
 #pragma unroll
-        for (int i = 0; i < LB_ITEMS; ++i) {
-            const int idx = lt + 32 * DW_NLOAD * i;
+        for (int i = 0; i < B_ITEMS; ++i) {
+            const int idx = pt + NPT * i;
             brow[i] = idx < BVEC ? idx / (S.N / 4) : -1;
             bcol[i] = idx < BVEC ? 4 * (idx % (S.N / 4)) : 0;
             boff[i] = idx < BVEC ? mn_off(brow[i], bcol[i], S.atoms_b) : 0u;
         }
-        // dz is tile-blocked per step (common.cuh tb_off, rows r = t np + v).
-        // Every A item of this thread is the same stage row (lt % 16), so the
-        // row part of the address is formed once per stage from an
-        // incrementally tracked (t, v); items add their column block.
-        int64_t ct = r_begin / np, cv = r_begin - ct * np + (lt % DW_ROWS);
+        // dz is tile-blocked per step (common.cuh tb_off, rows r = t np + v):
+        // the (t, v) of this thread's stage row is tracked incrementally
+        int64_t ct = r_begin / np, cv = r_begin - ct * np + arow;
         while (cv >= np) {
             cv -= np;
             ++ct;
         }
-        for (int g = 0; g < nst; ++g) {
-            const int s = g % S.stages;
-            const int j = g / S.stages;
-            if (j >= 1) dw_wait(&bars->empty[s], (j - 1) & 1, wacc0);
+        // the CTA walks a contiguous row range: every 8 stages, pull the rows
+        // 128..255 ahead into L2 with bulk prefetches (x, y / h0 and the
+        // tile-blocked dz blocks holding them), so the register loads of a
+        // stage (DW_PD stages ahead) hit L2
+        const int64_t dz_end = rows * M;
+        auto prefetch_rows = [&](int64_t ra) {
+            const int64_t rb = min(r_end, ra + 128);
+            if (ra >= rb || (DW_PROBE & 2)) return;
+            bulk_prefetch_l2(x + ra * ldx, (uint32_t)((rb - ra) * ldx * 4));
+            const int64_t ya = ra < np ? ra : ra, yb = rb;
+            if (ya < np) bulk_prefetch_l2(h0 + ya * HP, (uint32_t)((min(yb, np) - ya) * HP * 4));
+            if (yb > np) bulk_prefetch_l2(y + (max(ya, np) - np) * HP, (uint32_t)((yb - max(ya, np)) * HP * 4));
+            const int64_t ta = ra / np, tb = (rb - 1) / np;
+            const int64_t da = (ta * np + ((ra - ta * np) & ~(int64_t)127)) * M;
+            const int64_t db_ = min(dz_end, (tb * np + (((rb - 1) - tb * np) & ~(int64_t)127) + 128) * M);
+            bulk_prefetch_l2(dz + da, (uint32_t)((db_ - da) * 4));
+        };
+        if (pt == 0) prefetch_rows(r_begin);
+        auto load = [&](int g, float4 (&va)[A_ITEMS], float4 (&vb)[B_ITEMS]) {
             const int64_t r0 = r_begin + (int64_t)g * DW_ROWS;
-            const uint32_t a_hi = sb + s * S.stage, b_hi = a_hi + 2 * S.a_half;
-            {
-                const int64_t v0 = cv & ~(int64_t)127;
-                const int64_t tr = min((int64_t)128, np - v0);
-                const float* rowp = dz + (ct * np + v0) * M + (cv - v0) * 4;   // tb_off(cv, 0, M, np)
-                const bool ok = r0 + arow[0] < r_end && !(DW_PROBE & 2);
+            if (pt == 0 && (g & 7) == 0) prefetch_rows(r0 + 128);
+            const int64_t v0 = cv & ~(int64_t)127;
+            const int64_t tr = min((int64_t)128, np - v0);
+            const float* rowp = dz + (ct * np + v0) * M + (cv - v0) * 4;   // tb_off(cv, 0, M, np)
+            const bool aok = r0 + arow < r_end && !(DW_PROBE & 2);
 #pragma unroll
-                for (int i = 0; i < LA_ITEMS; ++i)
-                    cp_async16(a_hi + aoff[i], ok ? rowp + (int64_t)acol[i] * tr : dz, ok ? 16u : 0u);
-                cv += DW_ROWS;
-                while (cv >= np) {
-                    cv -= np;
-                    ++ct;
-                }
+            for (int i = 0; i < A_ITEMS; ++i)
+                va[i] = aok ? ldg_stream4(rowp + (int64_t)acol[i] * tr) : make_float4(0.f, 0.f, 0.f, 0.f);
+            cv += DW_ROWS;
+            while (cv >= np) {
+                cv -= np;
+                ++ct;
             }
 #pragma unroll
-            for (int i = 0; i < LB_ITEMS; ++i) {
+            for (int i = 0; i < B_ITEMS; ++i) {
+                vb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (brow[i] >= 0) {
                     const int64_t gr = r0 + brow[i];
                     const int c = bcol[i];
-                    const float* src = x;
-                    const bool ok = gr < r_end && c < K && !(DW_PROBE & 2);
-                    if (ok) {
-                        if (c < kx) src = x + gr * ldx + c;
-                        else if (gr >= np) src = y + (gr - np) * HP + (c - kx);
-                        else src = h0 + gr * HP + (c - kx);
+                    if (gr < r_end && c < K && !(DW_PROBE & 2)) {
+                        const float* src = c < kx ? x + gr * ldx + c
+                                                  : (gr >= np ? y + (gr - np) * HP + (c - kx) : h0 + gr * HP + (c - kx));
+                        vb[i] = ldg_stream4(src);
                     }
-                    cp_async16(b_hi + boff[i], src, ok ? 16u : 0u);
                 }
             }
-            cp_async_mbar_arrive(&bars->landed[s]);
-        }
-        cp_async_wait<0>();
-    } else if (warp < DW_NPROD) {
-        const int ct = threadIdx.x - 32 * DW_NLOAD;
-        const int acol = 4 * (ct % (M / 4));   // 32 * DW_NCONV is a multiple of M / 4
-        uint32_t aoff[CA_ITEMS], boff[CB_ITEMS];
+        };
+        float4 ra[DW_PD][A_ITEMS], rb[DW_PD][B_ITEMS];
 #pragma unroll
-        for (int i = 0; i < CA_ITEMS; ++i) aoff[i] = mn_off((ct + 32 * DW_NCONV * i) / (M / 4), acol, S.atoms_a);
+        for (int d = 0; d < DW_PD; ++d)
+            if (d < nst) load(d, ra[d], rb[d]);
+        for (int g0 = 0; g0 < nst; g0 += DW_PD) {
 #pragma unroll
-        for (int i = 0; i < CB_ITEMS; ++i) {
-            const int idx = ct + 32 * DW_NCONV * i;
-            boff[i] = idx < BVEC ? mn_off(idx / (S.N / 4), 4 * (idx % (S.N / 4)), S.atoms_b) : 0xFFFFFFFFu;
-        }
-        for (int g = 0; g < nst; ++g) {
-            const int s = g % S.stages;
-            dw_wait(&bars->landed[s], (g / S.stages) & 1, wacc0);
-            const uint32_t a_hi = sb + s * S.stage, a_lo = a_hi + S.a_half;
-            const uint32_t b_hi = a_lo + S.a_half, b_lo = b_hi + S.b_half;
-            // all shared loads first (the asm accessors keep program order),
-            // then split + stores: one smem latency per stage, not per item
-            float4 va[CA_ITEMS], vb[CB_ITEMS];
+            for (int d = 0; d < DW_PD; ++d) {
+                const int g = g0 + d;
+                if (g >= nst) break;
+                const int s = g % S.stages;
+                const int j = g / S.stages;
+                if (j >= 1) dw_wait(&bars->empty[s], (j - 1) & 1, wacc0);
+                const uint32_t a_hi = sb + s * S.stage, a_lo = a_hi + S.a_half;
+                const uint32_t b_hi = a_lo + S.a_half, b_lo = b_hi + S.b_half;
 #pragma unroll
-            for (int i = 0; i < CA_ITEMS; ++i) va[i] = lds128(a_hi + aoff[i]);
-#pragma unroll
-            for (int i = 0; i < CB_ITEMS; ++i)
-                if (boff[i] != 0xFFFFFFFFu) vb[i] = lds128(b_hi + boff[i]);
-#pragma unroll
-            for (int i = 0; i < CA_ITEMS * !(DW_PROBE & 8); ++i) {
-                float4 hi, lo;
-                split4(va[i], hi, lo);
-                sts128(a_hi + aoff[i], hi);
-                sts128(a_lo + aoff[i], lo);
-            }
-#pragma unroll
-            for (int i = 0; i < CB_ITEMS * !(DW_PROBE & 8); ++i) {
-                if (boff[i] != 0xFFFFFFFFu) {
+                for (int i = 0; i < A_ITEMS; ++i) {
                     float4 hi, lo;
-                    split4(vb[i], hi, lo);
-                    sts128(b_hi + boff[i], hi);
-                    sts128(b_lo + boff[i], lo);
+                    if (DW_PROBE & 8) {
+                        hi = ra[d][i];
+                        lo = hi;
+                    } else {
+                        split4(ra[d][i], hi, lo);
+                    }
+                    sts128(a_hi + aoff[i], hi);
+                    sts128(a_lo + aoff[i], lo);
+                    dbacc[4 * i + 0] += ra[d][i].x;
+                    dbacc[4 * i + 1] += ra[d][i].y;
+                    dbacc[4 * i + 2] += ra[d][i].z;
+                    dbacc[4 * i + 3] += ra[d][i].w;
                 }
-            }
 #pragma unroll
-            for (int i = 0; i < CA_ITEMS; ++i) {
-                dbacc[0] += va[i].x;
-                dbacc[1] += va[i].y;
-                dbacc[2] += va[i].z;
-                dbacc[3] += va[i].w;
+                for (int i = 0; i < B_ITEMS; ++i) {
+                    if (brow[i] >= 0) {
+                        float4 hi, lo;
+                        if (DW_PROBE & 8) {
+                            hi = rb[d][i];
+                            lo = hi;
+                        } else {
+                            split4(rb[d][i], hi, lo);
+                        }
+                        sts128(b_hi + boff[i], hi);
+                        sts128(b_lo + boff[i], lo);
+                    }
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->full[s]);
+                if (g + DW_PD < nst) load(g + DW_PD, ra[d], rb[d]);
             }
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->full[s]);
         }
     } else if (warp == DW_MMA_WARP) {
         if (lane == 0) {
@@ -355,8 +363,8 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
         }
     }
 #if DGNN_DW_PROBE & 16
-    if (lane == 0 && (warp == 0 || warp == DW_NLOAD || warp == DW_MMA_WARP || warp == DW_MMA_WARP + 1)) {
-        const int k = warp == 0 ? 0 : (warp == DW_NLOAD ? 1 : (warp == DW_MMA_WARP ? 2 : 4));
+    if (lane == 0 && (warp == 0 || warp == 8 || warp == DW_MMA_WARP || warp == DW_MMA_WARP + 1)) {
+        const int k = warp == 0 ? 0 : (warp == 8 ? 1 : (warp == DW_MMA_WARP ? 2 : 4));
         dw_prof[blockIdx.x * 8 + k] = wacc0;
         if (warp == DW_MMA_WARP) dw_prof[blockIdx.x * 8 + 3] = wacc1;
         if (warp == 0) dw_prof[blockIdx.x * 8 + 5] = clock64() - t_start;
@@ -366,16 +374,25 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
     __syncthreads();
     // db partial: producer threads sharing a column group combine in fixed
     // order (the stage ring is free now)
+    // dbred[item][thread][4]: producer thread pt, item i holds column group
+    // (pt + NPT i) / 16 of the 16 stage rows pt % 16
     double* dbred = reinterpret_cast<double*>(base);
-    if (warp >= DW_NLOAD && warp < DW_NPROD) {
+    if (warp < DW_NPROD) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) dbred[(threadIdx.x - 32 * DW_NLOAD) * 4 + t] = dbacc[t];
+        for (int i = 0; i < A_ITEMS; ++i)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dbred[((size_t)i * NPT + threadIdx.x) * 4 + t] = dbacc[4 * i + t];
     }
     __syncthreads();
     if (threadIdx.x < M / 4) {
+        // column group cg = idx / 16 with idx = pt + NPT i: the 16 producer
+        // slots of that group, summed in fixed (row) order
         double s4[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int t = threadIdx.x; t < NCT; t += M / 4)
-            for (int jj = 0; jj < 4; ++jj) s4[jj] += dbred[t * 4 + jj];
+        for (int r = 0; r < DW_ROWS; ++r) {
+            const int idx = 16 * threadIdx.x + r;
+            const int i = idx / NPT, pt = idx % NPT;
+            for (int jj = 0; jj < 4; ++jj) s4[jj] += dbred[((size_t)i * NPT + pt) * 4 + jj];
+        }
         for (int jj = 0; jj < 4; ++jj) dbs[(size_t)blockIdx.x * M + 4 * threadIdx.x + jj] = s4[jj];
     }
     fence_before();
