@@ -256,6 +256,8 @@ def kernel_work(name, args, ctx):
     if name == "dgnn_spmm_f32":
         n, f = args[0], args[5]
         return 2 * nnz * f, agg(n, f) + 4 * n * f
+    if name == "dgnn_frames_combine":
+        return 0, None      # bytes depend on the table: not modelled per call
     if name == "dgnn_axpy_frame":
         cnt, init = args[0], args[4]
         return 2 * cnt, (8 if init else 12) * cnt
@@ -383,7 +385,7 @@ def run_ours(args):
     ctx = {"l2": l2, "layers_real": layers_real, "nnz": float(np.mean(eng.enc.nnz_hat))}
     timed_names = list(TENSOR_KERNELS) + [
         "dgnn_gcn_forward", "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows",
-        "dgnn_axpy_frame", "dgnn_csr_apply_delta", "dgnn_laplacian", "dgnn_csr_transpose_staged",
+        "dgnn_axpy_frame", "dgnn_frames_combine", "dgnn_csr_apply_delta", "dgnn_laplacian", "dgnn_csr_transpose_staged",
         "dgnn_head_loss", "dgnn_head_grad", "dgnn_head_loss_grad", "dgnn_head_scatter"]
     if args.timeline:   # every C-ABI call, for the per-stream idle breakdown
         timed_names = list(_lib._SIGS.keys())

@@ -284,6 +284,15 @@ int dgnn_gemm_tn(int64_t rows, int32_t m, int32_t n, const float* a, int64_t lda
                  const float* b, int64_t ldb, double* out, int64_t ldo, double* colsum,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* Banded frame combinations in one launch (the M-product forward / adjoint,
+ * training.py:430-460): for i < nout, out_i = [out_i +] sum_j tcoef[j] *
+ * tsrc[j] over j in [tptr[i], tptr[i+1]) in order (each product rounded,
+ * then added: dgnn_axpy_frame's arithmetic).  outs / tsrc hold device
+ * addresses of fp32 frames of `count` floats (a multiple of 4); accum[i] = 1
+ * adds onto the existing out_i.  Outputs are produced in order, so an
+ * output may read frames written by earlier outputs of the same call. */
+int dgnn_frames_combine(int64_t count, int32_t nout, const int64_t* outs, const int32_t* accum, const int32_t* tptr,
+                        const int64_t* tsrc, const float* tcoef, void* stream);
 /* K7 -- banded M-product term (training.py:430-441): z = coef * y (init=1)
  * or z += coef * y (init=0), over rows x width contiguous fp32. */
 int dgnn_axpy_frame(int64_t count, float coef, const float* y, float* z, int init, void* stream);

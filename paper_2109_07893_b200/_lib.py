@@ -78,6 +78,7 @@ _SIGS = {
     "dgnn_gemm_tn": (c_int, [c_int64, c_int32, c_int32, P, c_int64, P, c_int64, P, c_int64, P, P,
                              c_size_t, P]),
     "dgnn_axpy_frame": (c_int, [c_int64, c_float, P, P, c_int, P]),
+    "dgnn_frames_combine": (c_int, [c_int64, c_int32, P, P, P, P, P, P]),
     "dgnn_head_loss": (c_int, [c_int64, P, P, P, Frame, c_int32, c_int32, P, P, c_double, P, c_int32,
                                P, P]),
     "dgnn_head_grad_workspace": (c_size_t, [c_int32, c_int32]),

@@ -41,7 +41,7 @@ __device__ __forceinline__ T* frame_row(const dgnn_frame& f, int64_t i) {
 // waits) and computed afterwards by hub_rows_kernel (spmm.cu): a CTA per hub
 // row, edges split over lane groups, partials reduced in a fixed tree --
 // deterministic, and the same for the tcgen05 and SIMT instances.
-constexpr int kHubRow = 64;   // c3 (heavy-tailed): 256 left ~6000 rows of 65..256 entries as per-tile serial tails
+constexpr int kHubRow = 16;   // c3 (heavy-tailed): 64 left most 128-row tiles holding a 17..64-entry row as a serial tail (median tile max degree 21)
 
 // ---- tile-blocked layout of the LSTM step caches -----------------------
 // The per-step cell state c, the gate cache (overwritten in place by dz) and

@@ -188,8 +188,35 @@ __global__ void axpy_kernel(int64_t n, float coef, const float* __restrict__ y, 
                             int init) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float t = coef * y[i];
-    z[i] = init ? t : z[i] + t;
+    const float t = __fmul_rn(coef, y[i]);
+    z[i] = init ? t : __fadd_rn(z[i], t);
+}
+
+// Banded frame combinations in one pass (the M-product, training.py:430-460):
+// out_i = [out_i +] sum_j c_ij * src_ij, terms in table order, each product
+// rounded then added (the axpy sequence above, bitwise).  One thread per
+// float4 of a frame runs every output in order, so a source frame shared by
+// consecutive outputs is re-read from L1/L2, and an output may be a source
+// of a LATER output (the table is built that way).
+__global__ void frames_combine_kernel(int64_t n4, int nout, const int64_t* __restrict__ outs,
+                                      const int32_t* __restrict__ accum, const int32_t* __restrict__ tptr,
+                                      const int64_t* __restrict__ tsrc, const float* __restrict__ tcoef) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+        for (int i = 0; i < nout; ++i) {
+            float4* out = reinterpret_cast<float4*>(outs[i]) + e;
+            float4 acc = accum[i] ? *out : make_float4(0.f, 0.f, 0.f, 0.f);
+            bool first = !accum[i];
+            for (int j = tptr[i]; j < tptr[i + 1]; ++j) {
+                const float4 v = reinterpret_cast<const float4*>(tsrc[j])[e];
+                const float c = tcoef[j];
+                const float4 t = make_float4(__fmul_rn(c, v.x), __fmul_rn(c, v.y), __fmul_rn(c, v.z), __fmul_rn(c, v.w));
+                acc = first ? t : make_float4(__fadd_rn(acc.x, t.x), __fadd_rn(acc.y, t.y), __fadd_rn(acc.z, t.z),
+                                              __fadd_rn(acc.w, t.w));
+                first = false;
+            }
+            *out = acc;
+        }
+    }
 }
 
 // row-major <-> tile-blocked (common.cuh tb_off), one float per thread
@@ -262,6 +289,18 @@ int dgnn_sum_f64(int64_t n, const double* x, double* out, int accumulate, void* 
     ::dgnn::note_launch();
     sum_f64_kernel<<<1, 1024, 0, as_stream(stream)>>>(n, x, out, accumulate);
     return launch_status("sum_f64");
+}
+
+int dgnn_frames_combine(int64_t count, int32_t nout, const int64_t* outs, const int32_t* accum, const int32_t* tptr,
+                        const int64_t* tsrc, const float* tcoef, void* stream) {
+    DGNN_CHECK_ARG(count % 4 == 0 && nout >= 0, "frames_combine: count must be a multiple of 4");
+    if (count == 0 || nout == 0) return DGNN_OK;
+    const int64_t n4 = count / 4;
+    int64_t blocks = cdiv(n4, 256);
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    ::dgnn::note_launch();
+    frames_combine_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(n4, nout, outs, accum, tptr, tsrc, tcoef);
+    return launch_status("frames_combine");
 }
 
 int dgnn_axpy_frame(int64_t count, float coef, const float* y, float* z, int init, void* stream) {

@@ -128,45 +128,65 @@ __global__ void head_grad_reduce_kernel(int nchunks, int ep, int C, const double
 }
 
 // dz[x][k] = sum_{slot s of x} sum_c dl[s/2][c] hw[side(s)*ep + k][c]; group of ep/4 lanes per vertex.
-template <int EP>
+template <int EP, int CC>   // CC: classes (compile time), 0: runtime C <= kMaxClasses
 __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int32_t* __restrict__ ptr,
                                                            const int32_t* __restrict__ slot,
                                                            const double* __restrict__ dl,
-                                                           const float* __restrict__ hw, int C, dgnn_frame dz) {
-    constexpr int G = EP / 4 >= 32 ? 32 : EP / 4;  // lanes per vertex
-    constexpr int V = EP / (4 * G);                // float4 per lane
-    constexpr int RW = 32 / G;
-    extern __shared__ float hws[];                 // [2*EP][C]
+                                                           const float* __restrict__ hw, int C_rt, dgnn_frame dz) {
+    // dz[x] = sum over x's incident pair endpoints (p, side) of dl[p] . W_side^T
+    //       = S_0[x] . W_u^T + S_1[x] . W_v^T,  S_side[x][c] = sum dl[p][c]:
+    // 8 lanes per vertex (4 vertices per warp in flight) sum the 2C fp64
+    // dlogits over the incidence list, 8 slots at a time, in a fixed
+    // butterfly, then form the E outputs -- a hub vertex (heavy-tailed
+    // graphs: tens of thousands of incident pairs) costs 1/8 of a serial
+    // walk and no vector work per pair.
+    constexpr int CM = CC ? CC : kMaxClasses;
+    constexpr int GL = 8;                           // lanes per vertex
+    constexpr int PER = (EP + GL - 1) / GL;         // outputs per lane
+    const int C = CC ? CC : C_rt;
+    extern __shared__ float hws[];                  // [2*EP][C]
     for (int i = threadIdx.x; i < 2 * EP * C; i += blockDim.x) hws[i] = hw[i];
     __syncthreads();
-    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t x = warp * RW + sub; x < n; x += nwarps * RW) {
-        double acc[V][4];
+    const int lane = threadIdx.x & 31, gl = lane & (GL - 1);
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GL;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / GL;
+    const int64_t iters = (n + ngrp - 1) / ngrp;    // uniform trip count: the shuffles need whole warps
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t x = grp + it * ngrp;
+        const bool ok = x < n;
+        double sacc[2 * CM];
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
-        for (int e = ptr[x]; e < ptr[x + 1]; ++e) {
-            const int s = slot[e];
-            const int p = s >> 1, side = s & 1;
-            for (int c = 0; c < C; ++c) {
-                const double d = dl[(int64_t)p * C + c];
+        for (int i = 0; i < 2 * CM; ++i) sacc[i] = 0.0;
+        if (ok) {
+            const int e1 = ptr[x + 1];
+            for (int e = ptr[x] + gl; e < e1; e += GL) {
+                const int sl = slot[e];
+                const int p = sl >> 1, side = sl & 1;
 #pragma unroll
-                for (int i = 0; i < V; ++i) {
-                    const int k = 4 * (gl + G * i);
-                    const float* hr = hws + (side * EP + k) * C + c;
-                    acc[i][0] += d * (double)hr[0];
-                    acc[i][1] += d * (double)hr[C];
-                    acc[i][2] += d * (double)hr[2 * C];
-                    acc[i][3] += d * (double)hr[3 * C];
-                }
+                for (int c = 0; c < CM; ++c)
+                    if (c < C) sacc[side * CM + c] += dl[(int64_t)p * C + c];
             }
         }
-        float* out = frame_row<float>(dz, x);
 #pragma unroll
-        for (int i = 0; i < V; ++i)
-            *reinterpret_cast<float4*>(out + 4 * (gl + G * i)) =
-                make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
+        for (int i = 0; i < 2 * CM; ++i)
+#pragma unroll
+            for (int o = GL / 2; o > 0; o >>= 1) sacc[i] += __shfl_xor_sync(0xffffffffu, sacc[i], o);
+        if (!ok) continue;
+        float* out = frame_row<float>(dz, x);
+        float v[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int k = gl * PER + j;
+            double a = 0.0;
+            if (k < EP)
+                for (int c = 0; c < C; ++c)
+                    a += sacc[c] * (double)hws[k * C + c] + sacc[CM + c] * (double)hws[(EP + k) * C + c];
+            v[j] = (float)a;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; j += 4)
+            if (gl * PER + j < EP)
+                *reinterpret_cast<float4*>(out + gl * PER + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     }
 }
 
@@ -204,13 +224,19 @@ __global__ void grads_gather_kernel(int64_t n, const double* __restrict__ gp, co
 template <int EP>
 int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const double* dl, const float* hw, int C,
                    dgnn_frame dz, cudaStream_t st) {
-    constexpr int G = EP / 4 >= 32 ? 32 : EP / 4;
-    constexpr int RW = 32 / G;
-    int64_t blocks = cdiv(cdiv(n, RW), 8);
+    if (C > kMaxClasses) {
+        set_error("head_scatter: %d classes exceed %d", C, kMaxClasses);
+        return DGNN_EUNSUPPORTED;
+    }
+    int64_t blocks = cdiv(n, 32);
     blocks = blocks < 1 ? 1 : (blocks > 16 * num_sms() ? 16 * num_sms() : blocks);
     ::dgnn::note_launch();
-    head_scatter_kernel<EP><<<(unsigned)blocks, 256, (size_t)2 * EP * C * sizeof(float), st>>>(n, ptr, slot, dl,
-                                                                                                hw, C, dz);
+    if (C == 2)
+        head_scatter_kernel<EP, 2><<<(unsigned)blocks, 256, (size_t)2 * EP * C * sizeof(float), st>>>(n, ptr, slot,
+                                                                                                   dl, hw, C, dz);
+    else
+        head_scatter_kernel<EP, 0><<<(unsigned)blocks, 256, (size_t)2 * EP * C * sizeof(float), st>>>(n, ptr, slot,
+                                                                                                   dl, hw, C, dz);
     return launch_status("head_scatter");
 }
 

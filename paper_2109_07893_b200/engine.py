@@ -174,9 +174,18 @@ class Rank:
         else:
             # M-product: trailing operator-input frames (training.py:598-603) and
             # owed gradients for frames of earlier blocks (training.py:644-647)
-            self.trail = [dict() for _ in layers]
-            self.dtrail = [dict() for _ in layers]
             self.Z_vm = self.Y_vm    # M-product output, vertex-major
+            if not eng.evolve:
+                # static trailing-frame buffers (their addresses go into the
+                # cached M-product tables): the last min(w, B) operator inputs
+                # of every block, and the w - 1 owed-gradient frames
+                w = eng.cfg.window
+                self.keepn = min(w, B)
+                self.trail_buf = [_zeros(plan.nblk * self.keepn * NP * Ly.ho if plan.nblk > 1 else 0, device=dev)
+                                  for Ly in layers]
+                self.dtrail_buf = [_zeros((w - 1) * NP * Ly.ho if plan.nblk > 1 else 0, device=dev)
+                                   for Ly in layers]
+                self.mp_tables = {}
         if self.evolve:
             # weight evolution (fp64, padded F x H per layer): carried state,
             # rerun scratch, gradient carry, the block's per-step fp32 weight
@@ -291,9 +300,6 @@ class Rank:
             for dh, dc in self.dstate:
                 dh.zero_()
                 dc.zero_()
-        else:
-            self.trail = [dict() for _ in self.eng.layout.layers]
-            self.dtrail = [dict() for _ in self.eng.layout.layers]
         self.pi = {}
         self.loss_acc.zero_()
         if hasattr(self, "loss_t"):
@@ -714,38 +720,62 @@ class Rank:
         ops = [dist.P2POp(dist.irecv, self.own_slab_rows(own_buf, W, c, src), src) for src in range(P) if src != me]
         return dist.batch_isend_irecv(ops) if ops else []
 
+    def _mp_table(self, key, outs, terms):
+        """Device table of one dgnn_frames_combine call (built once: every
+        frame address involved is static)."""
+        tab = self.mp_tables.get(key)
+        if tab is None:
+            tptr = np.zeros(len(outs) + 1, np.int32)
+            src, coef = [], []
+            for i, ts_ in enumerate(terms):
+                tptr[i + 1] = tptr[i] + len(ts_)
+                for a, c in ts_:
+                    src.append(a)
+                    coef.append(c)
+            dev = self.dev
+            tab = (len(outs), torch.tensor([o for o, _ in outs], dtype=torch.int64, device=dev),
+                   torch.tensor([a for _, a in outs], dtype=torch.int32, device=dev),
+                   torch.from_numpy(tptr).to(dev), torch.tensor(src + [0], dtype=torch.int64, device=dev),
+                   torch.tensor(coef + [0.0], dtype=torch.float32, device=dev))
+            self.mp_tables[key] = tab
+        return tab
+
+    def _frame(self, buf, i, cnt):
+        return buf.data_ptr() + F32 * i * cnt
+
     def _mprod_forward(self, b, l):
-        """`training.py:430-441` over the vertex chunk; trailing frames from
-        earlier blocks are kept as device copies (`training.py:598-603`)."""
+        """`training.py:430-441` over the vertex chunk, one launch per block
+        and layer (dgnn_frames_combine): Z_t = sum_k M[t,k] R_k over the
+        window, operator inputs of earlier blocks from the static trailing
+        buffer; in the forward sweep the block's last min(w, B) inputs are
+        stored there too (`training.py:598-603`)."""
         eng = self.eng
         Ly = eng.layout.layers[l]
-        NP = eng.plan.NP
-        ts = eng.plan.block_steps(b)
+        plan = eng.plan
+        NP, B = plan.NP, plan.bsize
+        ts = plan.block_steps(b)
         m, w = eng.m_matrix, eng.cfg.window
-        st = _lib.stream_handle()
         cnt = NP * Ly.ho
-
-        def src(k):
-            if k >= ts[0]:
-                return self.vm(self.R_vm[l], Ly.rw, k - ts[0])
-            return self.trail[l][k]
-
-        for i, t in enumerate(ts):
-            out = self.vm(self.Z_vm[l], Ly.ho, i)
-            lo = max(0, t - w + 1)
-            for j, k in enumerate(range(lo, t + 1)):
-                call("dgnn_axpy_frame", cnt, float(m[t, k]), ptr(src(k)), ptr(out), int(j == 0), st)
-        if not self.keep:
-            # the rerun of block b+1 reads these again (the reference keeps
-            # them for the whole epoch, dist.py:359-361)
-            keepn = min(w, len(ts))
-            for t in ts[-keepn:]:
-                self.trail[l][t] = self.vm(self.R_vm[l], Ly.rw, t - ts[0]).clone()
-        else:
-            # frames produced by block b-1 were last read by this rerun (block
-            # b-1's own rerun recomputes them): free them (HBM plan, c5)
-            for k in [k for k in self.trail[l] if ts[0] - len(ts) <= k < ts[0]]:
-                del self.trail[l][k]
+        kn = self.keepn
+        store = (not self.keep) and b < plan.nblk - 1
+        key = ("f", b, l, store)
+        tab = self.mp_tables.get(key)
+        if tab is None:
+            def src(k):
+                if k >= ts[0]:
+                    return self._frame(self.R_vm[l], k - ts[0], NP * Ly.rw)
+                return self._frame(self.trail_buf[l], (b - 1) * kn + k - (ts[0] - kn), cnt)
+            outs, terms = [], []
+            for i, t in enumerate(ts):
+                outs.append((self._frame(self.Z_vm[l], i, cnt), 0))
+                terms.append([(src(k), float(m[t, k])) for k in range(max(0, t - w + 1), t + 1)])
+            if store:
+                for j, t in enumerate(ts[-kn:]):
+                    outs.append((self._frame(self.trail_buf[l], b * kn + j, cnt), 0))
+                    terms.append([(src(t), 1.0)])
+            tab = self._mp_table(key, outs, terms)
+        nout, o, a, tp, sr, co = tab
+        call("dgnn_frames_combine", cnt, nout, ptr(o), ptr(a), ptr(tp), ptr(sr), ptr(co), _lib.stream_handle())
 
     def store_pi(self, b):
         if self.skip and b < self.eng.plan.nblk - 1:
@@ -919,37 +949,38 @@ class Rank:
         return works
 
     def _mprod_backward(self, b, l):
-        """`training.py:444-460` + owed trailing gradients (`dist.py:396-407`)."""
+        """`training.py:444-460` + owed trailing gradients (`dist.py:396-407`)
+        in one launch: dR_k = sum_t M[t,k] dZ_t over the block's t (ascending)
+        plus the gradient owed by block b+1 for its window; then the owed
+        gradients of block b-1's last w-1 frames (static buffer, read above
+        before being rewritten here: outputs run in order)."""
         eng = self.eng
         Ly = eng.layout.layers[l]
-        NP = eng.plan.NP
-        ts = eng.plan.block_steps(b)
+        plan = eng.plan
+        NP = plan.NP
+        ts = plan.block_steps(b)
         m, w = eng.m_matrix, eng.cfg.window
-        st = _lib.stream_handle()
         cnt = NP * Ly.ho
-        out = self.dR_vm[l]
-        first = {}
-        for t in ts:
-            lo = max(0, t - w + 1)
-            dzt = self.vm(self.dy_buf(l), Ly.ho, t - ts[0])
-            for k in range(lo, t + 1):
-                coef = float(m[t, k])
-                if k >= ts[0]:
-                    dst = self.vm(out, Ly.rw, k - ts[0])
-                    init = k not in first
-                    first[k] = True
-                else:
-                    if k not in self.dtrail[l]:
-                        self.dtrail[l][k] = torch.zeros(cnt, dtype=torch.float32, device=self.dev)
-                    dst = self.dtrail[l][k]
-                    init = 0
-                call("dgnn_axpy_frame", cnt, coef, ptr(dzt), ptr(dst), int(init), st)
-        for k in ts:
-            if k not in first:
-                self.vm(out, Ly.rw, k - ts[0]).zero_()
-            if k in self.dtrail[l]:
-                g = self.dtrail[l].pop(k)
-                call("dgnn_axpy_frame", cnt, 1.0, ptr(g), ptr(self.vm(out, Ly.rw, k - ts[0])), 0, st)
+        key = ("b", b, l)
+        tab = self.mp_tables.get(key)
+        if tab is None:
+            dy = self.dy_buf(l)
+            outs, terms = [], []
+            nxt0 = ts[-1] + 1                       # first step of block b+1
+            for k in ts:
+                tt = [(self._frame(dy, t - ts[0], cnt), float(m[t, k])) for t in ts if max(0, t - w + 1) <= k <= t]
+                if b < plan.nblk - 1 and k >= nxt0 - (w - 1):
+                    tt.append((self._frame(self.dtrail_buf[l], k - (nxt0 - (w - 1)), cnt), 1.0))
+                outs.append((self._frame(self.dR_vm[l], k - ts[0], NP * Ly.rw), 0))
+                terms.append(tt)
+            if b > 0:
+                for k in range(max(0, ts[0] - (w - 1)), ts[0]):
+                    outs.append((self._frame(self.dtrail_buf[l], k - (ts[0] - (w - 1)), cnt), 0))
+                    terms.append([(self._frame(dy, t - ts[0], cnt), float(m[t, k])) for t in ts
+                                  if max(0, t - w + 1) <= k <= t])
+            tab = self._mp_table(key, outs, terms)
+        nout, o, a, tp, sr, co = tab
+        call("dgnn_frames_combine", cnt, nout, ptr(o), ptr(a), ptr(tp), ptr(sr), ptr(co), _lib.stream_handle())
 
     def gcn_backward(self, b, l, pipelined=False):
         """K4 for every owned step; when pipelined, each step's input gradient
@@ -1045,6 +1076,9 @@ class Engine:
         self.plan = Plan(T, workers, nblk, N)
         self.layout = ParamLayout(cfg)
         self.m_matrix = None if m_matrix is None else np.asarray(m_matrix, dtype=np.float64)
+        if cfg.architecture == "tm-gcn" and cfg.window - 1 > self.plan.bsize:
+            raise ConfigError(f"window {cfg.window} reaches past the previous checkpoint block "
+                              f"(block size {self.plan.bsize}): use fewer blocks")
         if cfg.architecture == "tm-gcn" and self.m_matrix is None:
             from .graph import build_m_matrix
             self.m_matrix = build_m_matrix(T, cfg.window).matrix
