@@ -29,8 +29,11 @@ int persistent_ctas();
 template <typename T>
 __device__ __forceinline__ T* frame_row(const dgnn_frame& f, int64_t i) {
     if (f.rows_per_slab <= 0) return reinterpret_cast<T*>(f.ptr) + i * f.ld;
-    const int64_t s = i / f.rows_per_slab;
-    const int64_t r = i - s * f.rows_per_slab;
+    // row indices are vertex ids (< 2^31): a 32-bit division, several times
+    // cheaper than the 64-bit one on the gather path of the owner layout
+    const uint32_t rps = (uint32_t)f.rows_per_slab;
+    const int64_t s = (uint32_t)i / rps;
+    const int64_t r = (uint32_t)i - (uint32_t)s * rps;
     return reinterpret_cast<T*>(f.ptr) + s * f.slab_stride + r * f.ld;
 }
 

@@ -1,6 +1,7 @@
 """Summarise the ncu captures of scripts/profile.sh into profiles/<tag>_*.md.
 
     python scripts/ncu_summary.py r01
+    python scripts/ncu_summary.py r02 c2     # launches_c2.csv, full_c2_*.ncu-rep (scripts/profile_r02.sh)
 
 Reads gpurun_out/launches.csv (per-launch gpu__time_duration + DRAM bytes of
 one whole timed epoch, serialised and cold-cache under ncu) and the
@@ -27,8 +28,8 @@ def short(name: str) -> str:
     return n
 
 
-def launches(tag: str) -> str:
-    rows = list(csv.reader(open(OUT / "launches.csv")))
+def launches(tag: str, src: str = "launches.csv") -> str:
+    rows = list(csv.reader(open(OUT / src)))
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hdr]
     iK, iM, iV, iU = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
@@ -62,7 +63,7 @@ def launches(tag: str) -> str:
     (ROOT / "profiles" / f"{tag}_traffic.json").write_text(json.dumps(
         {name: {"launches": n, "avg_us": t / n / 1e3, "dram_bytes_per_launch": b / n}
          for name, (n, t, b) in agg.items()}, indent=1, sort_keys=True) + "\n")
-    lines = [f"# {tag}: launch list of one timed epoch (bench.py --steps 1 --warmup 1)", "",
+    lines = [f"# {tag}: launch list of one timed epoch (scripts/profile_r02.sh / profile.sh)", "",
              "`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
              "--clock-control none` over exactly the launches of the timed epoch. ncu serialises "
              "launches and starts each cold, so absolute times exceed the bench's; the *share* "
@@ -130,11 +131,13 @@ def kernel_page(tag: str, rep: Path) -> str:
 
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    cfg = sys.argv[2] if len(sys.argv) > 2 else None
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
-    (prof / f"{tag}_launches.md").write_text(launches(tag))
-    for rep in sorted(OUT.glob("full_*.ncu-rep")):
-        k = rep.stem[len("full_"):]
+    pre = f"full_{cfg}_" if cfg else "full_"
+    (prof / f"{tag}_launches.md").write_text(launches(tag, f"launches_{cfg}.csv" if cfg else "launches.csv"))
+    for rep in sorted(OUT.glob(pre + "*.ncu-rep")):
+        k = rep.stem[len(pre):]
         (prof / f"{tag}_{k}.md").write_text(kernel_page(tag, rep))
     print("\n".join(str(p) for p in sorted(prof.glob(f"{tag}_*"))))
 
