@@ -434,6 +434,9 @@ def run_ours(args):
         eng.peer.log = []       # NVLink copy timing: the instrumented region
     ms_instr, _, _, e0i = timed_region(True)
     timeline = timer.gaps(e0i) if args.timeline else None
+    if timeline is not None and (ROOT / "gpurun_out").exists():
+        (ROOT / "gpurun_out" / f"timeline_{args.config}_n{P}_rank{rank}.json").write_text(
+            json.dumps({"ms_per_step_instrumented": ms_instr, "streams": timeline}, indent=1))
     loss = float(loss_dev.item()) * eng.scale
     durs = timer.durations()
 

@@ -262,6 +262,14 @@ int dgnn_lstm_weight_grad_tc(int64_t rows, int64_t np, int32_t kx, int32_t hp, c
                              int64_t ldx, const float* h_out, const float* h0, const float* dz,
                              double* gwcat, double* gb, void* workspace, size_t workspace_bytes,
                              void* stream);
+/* Same product with the dz operand staged in TMEM (tcgen05 A-from-TMEM MMAs;
+ * shared memory carries xcat only).  Same arguments and workspace
+ * (dgnn_lstm_weight_grad_tc_workspace); results agree to the accumulation
+ * order of the products. */
+int dgnn_lstm_weight_grad_ts(int64_t rows, int64_t np, int32_t kx, int32_t hp, const float* x,
+                             int64_t ldx, const float* h_out, const float* h0, const float* dz,
+                             double* gwcat, double* gb, void* workspace, size_t workspace_bytes,
+                             void* stream);
 
 /* K6 -- one reverse LSTM step (training.py:404-426):
  *   dh = dy + dh_in; do, dc, df, di, dg as the reference; dc_out = dc f

@@ -64,6 +64,8 @@ _SIGS = {
     "dgnn_lstm_weight_grad_tc_workspace": (c_size_t, [c_int32, c_int32]),
     "dgnn_lstm_weight_grad_tc": (c_int, [c_int64, c_int64, c_int32, c_int32, P, c_int64, P, P, P, P, P, P,
                                          c_size_t, P]),
+    "dgnn_lstm_weight_grad_ts": (c_int, [c_int64, c_int64, c_int32, c_int32, P, c_int64, P, P, P, P, P, P,
+                                         c_size_t, P]),
     "dgnn_lstm_backward_step_tc": (c_int, [c_int64, c_int32, c_int32, P, P, P, P, P, P, P, P, c_int64, P, P,
                                            P]),
     "dgnn_tc_gemm_test": (c_int, [c_int32, c_int32, c_int32, P, c_int64, P, P, c_int64, P]),

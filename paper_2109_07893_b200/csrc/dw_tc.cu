@@ -47,6 +47,12 @@ constexpr int DW_SMEM_MAX = 232448;
 #define DGNN_DW_PROBE 0
 #endif
 constexpr int DW_PROBE = DGNN_DW_PROBE;
+// L2 eviction hints on the operand loads (evict-first) and slot reductions
+// (evict-last): measured 3% slower at configs[1] shapes (scripts/dw_hint_ab.sh),
+// so off; -DDGNN_DW_HINTS=1 for the A/B probe
+#ifndef DGNN_DW_HINTS
+#define DGNN_DW_HINTS 0
+#endif
 #if DGNN_DW_PROBE & 16
 // probe 16: per-CTA cycles each role spends blocked on its barriers
 __device__ unsigned long long dw_prof[kMaxSMs * 8];
@@ -161,15 +167,19 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
         // raw landing copy plus its re-read measured as the kernel's
         // bottleneck (scripts/dw_probe2.sh: -27% without the split pass).
         const int pt = threadIdx.x;
+        const uint64_t pol = l2_policy_evict_first();   // operands are read once
         int acol[A_ITEMS], brow[B_ITEMS], bcol[B_ITEMS];
         uint32_t aoff[A_ITEMS], boff[B_ITEMS];
-        const int arow = pt % DW_ROWS;      // every A item of a thread is the same stage row
+        // A items: each group of 8 consecutive threads (one shared-memory
+        // store wavefront of 16-byte stores) covers 4 rows (one swizzle row
+        // group) x 2 column groups (one 32-byte chunk): the 8 stores land in
+        // 8 distinct 16-byte bank slots (no conflicts).  A warp covers all 16
+        // stage rows of 2 column groups: 2 x 256 contiguous bytes of the
+        // tile-blocked dz.  Every A item of a thread is the same stage row.
+        const int arow = 4 * ((pt >> 3) & 3) + (pt & 3);
 #pragma unroll
         for (int i = 0; i < A_ITEMS; ++i) {
-            // consecutive threads take consecutive rows of one 4-column group:
-            // 16 rows x 16 B contiguous in the tile-blocked dz
-            const int idx = pt + NPT * i;
-            acol[i] = 4 * (idx / DW_ROWS);
+            acol[i] = 8 * ((pt >> 5) + (NPT / 32) * i) + 4 * ((pt >> 2) & 1);
             aoff[i] = mn_off(arow, acol[i], S.atoms_a);
         }
 #pragma unroll
@@ -213,7 +223,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
             const bool aok = r0 + arow < r_end && !(DW_PROBE & 2);
 #pragma unroll
             for (int i = 0; i < A_ITEMS; ++i)
-                va[i] = aok ? ldg_stream4(rowp + (int64_t)acol[i] * tr) : make_float4(0.f, 0.f, 0.f, 0.f);
+                va[i] = aok ? (DGNN_DW_HINTS ? ldg_stream4(rowp + (int64_t)acol[i] * tr, pol) : ldg_stream4(rowp + (int64_t)acol[i] * tr)) : make_float4(0.f, 0.f, 0.f, 0.f);
             cv += DW_ROWS;
             while (cv >= np) {
                 cv -= np;
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
                     if (gr < r_end && c < K && !(DW_PROBE & 2)) {
                         const float* src = c < kx ? x + gr * ldx + c
                                                   : (gr >= np ? y + (gr - np) * HP + (c - kx) : h0 + gr * HP + (c - kx));
-                        vb[i] = ldg_stream4(src);
+                        vb[i] = DGNN_DW_HINTS ? ldg_stream4(src, pol) : ldg_stream4(src);
                     }
                 }
             }
@@ -328,6 +338,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
         const int e = warp - DW_MMA_WARP - 1;
         const int q = warp & 3, half = e >> 2;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        const uint64_t keep = l2_policy_evict_last();   // the CTA slot stays in L2
         for (int p = 0; p < nper; ++p) {
             const int a = S.nacc == 2 ? (p & 1) : 0;
             const int u = S.nacc == 2 ? (p >> 1) : p;
@@ -353,7 +364,10 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
                         for (int ci = 0; ci < GR; ++ci)
 #pragma unroll
                             for (int t = 0; t < 8; ++t)
-                                if (c0 + CS * ci < S.N) atomicAdd(slot + (size_t)(c0 + CS * ci + t) * M + j, v[ci][t]);
+                                if (c0 + CS * ci < S.N) {
+                                    if (DGNN_DW_HINTS) red_add(slot + (size_t)(c0 + CS * ci + t) * M + j, v[ci][t], keep);
+                                    else atomicAdd(slot + (size_t)(c0 + CS * ci + t) * M + j, v[ci][t]);
+                                }
                     }
                 }
             }
@@ -385,12 +399,13 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
     }
     __syncthreads();
     if (threadIdx.x < M / 4) {
-        // column group cg = idx / 16 with idx = pt + NPT i: the 16 producer
-        // slots of that group, summed in fixed (row) order
+        // column group cg = threadIdx.x: its 16 producer slots (one per stage
+        // row, the A item mapping above), summed in fixed (row) order
+        const int cg = threadIdx.x, cc = cg >> 1, ch = cg & 1;
+        const int i = cc / (NPT / 32);
         double s4[4] = {0.0, 0.0, 0.0, 0.0};
         for (int r = 0; r < DW_ROWS; ++r) {
-            const int idx = 16 * threadIdx.x + r;
-            const int i = idx / NPT, pt = idx % NPT;
+            const int pt = 32 * (cc % (NPT / 32)) + 8 * (r >> 2) + 4 * ch + (r & 3);
             for (int jj = 0; jj < 4; ++jj) s4[jj] += dbred[((size_t)i * NPT + pt) * 4 + jj];
         }
         for (int jj = 0; jj < 4; ++jj) dbs[(size_t)blockIdx.x * M + 4 * threadIdx.x + jj] = s4[jj];

@@ -69,6 +69,13 @@ HEAD_CHAIN = os.environ.get("DGNN_HEAD_CHAIN", "1")
 # skip the forward-sweep pass of the last checkpoint block (its rerun is the
 # same computation and nothing reads its outputs); "0" runs it as the reference does
 SKIP_LAST_FORWARD = os.environ.get("DGNN_SKIP_LAST_FORWARD", "1") == "1"
+# tm-gcn at P > 1: the M-product runs on each rank's own snapshots with a
+# (w - 1)-frame halo from the neighbouring rank instead of
+# redistributing every frame with all-to-alls; "0" redistributes as the
+# reference does
+TM_HALO = os.environ.get("DGNN_TM_HALO", "1")
+# LSTM block weight gradient: dz staged in shared memory ("tc") or in TMEM ("ts")
+DW_KERNEL = "dgnn_lstm_weight_grad_" + os.environ.get("DGNN_DW_KERNEL", "tc")
 
 
 class Plan:
@@ -140,7 +147,7 @@ class Rank:
         # output, snapshot-major throughout (no exchange)
         self.Y_own = self.R_own if eng.evolve else [recv(P * C * NP * Ly.ho) for Ly in layers]
         self.S_own = [None] + [_zeros(C * N * Ly.fp, device=dev) for Ly in layers[1:]]
-        same = P == 1 or eng.evolve
+        same = P == 1 or eng.evolve or eng.halo
         self.split = eng.split
         if self.split:
             # S_own is in the owner layout [P][C][NP][fp] (all-to-all ready)
@@ -186,6 +193,22 @@ class Rank:
                 self.dtrail_buf = [_zeros((w - 1) * NP * Ly.ho if plan.nblk > 1 else 0, device=dev)
                                    for Ly in layers]
                 self.mp_tables = {}
+                if eng.halo:
+                    # owner-layout halo frames ([P][w - 1][NP][W]): the previous
+                    # rank's last w - 1 operator inputs (forward) or the next
+                    # rank's first w - 1 output gradients (backward); rank 0's
+                    # trailing inputs of every block (from rank P - 1 of the
+                    # block before) and rank P - 1's owed gradients (from
+                    # rank 0 of the block after)
+                    hw = w - 1
+                    self.trail_buf = [_zeros(0, device=dev) for Ly in layers]
+                    self.dtrail_buf = [_zeros(0, device=dev) for Ly in layers]
+                    self.halo_buf = [_zeros(hw * N * Ly.ho, device=dev) for Ly in layers]
+                    self.halo_send = _zeros(hw * N * max(Ly.ho for Ly in layers), device=dev)
+                    self.trail_own = [_zeros(plan.nblk * hw * N * Ly.ho if plan.nblk > 1 else 0, device=dev)
+                                      for Ly in layers]
+                    self.dtrail_own = [_zeros(hw * N * Ly.ho if plan.nblk > 1 else 0, device=dev)
+                                       for Ly in layers]
         if self.evolve:
             # weight evolution (fp64, padded F x H per layer): carried state,
             # rerun scratch, gradient carry, the block's per-step fp32 weight
@@ -661,7 +684,10 @@ class Rank:
         NP, B = eng.plan.NP, eng.plan.bsize
         st = _lib.stream_handle()
         if not self.skip:
-            self._mprod_forward(b, l)
+            if eng.halo:
+                self._mprod_forward_halo(b, l)
+            else:
+                self._mprod_forward(b, l)
             return
         if eng.tensor_cores:
             fn = "dgnn_lstm_forward_step_ws" if (eng.warp_specialized and Ly.ho <= 64) else "dgnn_lstm_forward_step_tc"
@@ -777,6 +803,102 @@ class Rank:
         nout, o, a, tp, sr, co = tab
         call("dgnn_frames_combine", cnt, nout, ptr(o), ptr(a), ptr(tp), ptr(sr), ptr(co), _lib.stream_handle())
 
+    def _oframe(self, buf, c, q, W):
+        """Slab q of owned step c in the owner layout [P][C][NP][W]."""
+        plan = self.eng.plan
+        return buf.data_ptr() + F32 * (q * plan.chunk + c) * plan.NP * W
+
+    def _hframe(self, buf, j, q, W, base=0):
+        """Slab q of halo frame j in a [P][w - 1][NP][W] buffer (at element `base`)."""
+        plan = self.eng.plan
+        return buf.data_ptr() + F32 * (base + (q * (self.eng.cfg.window - 1) + j) * plan.NP * W)
+
+    def _mprod_forward_halo(self, b, l):
+        """`training.py:430-441` on this rank's own snapshots, all vertices:
+        Z_t = sum_k M[t,k] R_k, the operator inputs before the chunk from the
+        halo (previous rank, same block) or rank 0's trailing frames (block
+        b - 1); terms in ascending k as at P = 1 (bit-identical)."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        plan = eng.plan
+        P, B, N = plan.P, plan.bsize, plan.N
+        ts = self.ts
+        t0, bstart = ts[0], b * B
+        m, w = eng.m_matrix, eng.cfg.window
+        hw, W = w - 1, Ly.ho
+        key = ("hf", b, l)
+        tab = self.mp_tables.get(key)
+        if tab is None:
+            def src(k, q):
+                if k >= t0:
+                    return self._oframe(self.R_own[l], k - t0, q, Ly.rw)
+                if k >= bstart:
+                    return self._hframe(self.halo_buf[l], k - (t0 - hw), q, W)
+                return self._hframe(self.trail_own[l], k - (bstart - hw), q, W, base=b * hw * N * W)
+            outs, terms = [], []
+            for c, t in enumerate(ts):
+                for q in range(P):
+                    outs.append((self._oframe(self.Y_own[l], c, q, W), 0))
+                    terms.append([(src(k, q), float(m[t, k])) for k in range(max(0, t - w + 1), t + 1)])
+            tab = self._mp_table(key, outs, terms)
+        nout, o, a, tp, sr, co = tab
+        call("dgnn_frames_combine", plan.NP * W, nout, ptr(o), ptr(a), ptr(tp), ptr(sr), ptr(co),
+             _lib.stream_handle())
+
+    def _mprod_backward_halo(self, b, l):
+        """`training.py:444-460` on this rank's own snapshots: dR_k = sum_t
+        M[t,k] dZ_t over t ascending -- own frames, then the next rank's
+        first w - 1 (halo), then (rank P - 1) the gradient owed by block
+        b + 1 -- as at P = 1.  Rank 0 (b > 0) also writes the gradient its
+        frames owe to block b - 1's last w - 1 frames (sent to rank P - 1)."""
+        eng = self.eng
+        Ly = eng.layout.layers[l]
+        plan = eng.plan
+        P, B = plan.P, plan.bsize
+        ts = self.ts
+        t0, tl, bend = ts[0], ts[-1], (b + 1) * B
+        m, w = eng.m_matrix, eng.cfg.window
+        hw, W = w - 1, Ly.ho
+        dz = self.dy_buf(l)
+        key = ("hb", b, l)
+        tab = self.mp_tables.get(key)
+        if tab is None:
+            outs, terms = [], []
+            for c, k in enumerate(ts):
+                for q in range(P):
+                    tt = []
+                    for t in range(k, min(k + w, plan.T)):
+                        if t <= tl:
+                            tt.append((self._oframe(dz, t - t0, q, W), float(m[t, k])))
+                        elif t < bend:
+                            tt.append((self._hframe(self.halo_buf[l], t - tl - 1, q, W), float(m[t, k])))
+                    if b < plan.nblk - 1 and k >= bend - hw:
+                        tt.append((self._hframe(self.dtrail_own[l], k - (bend - hw), q, W), 1.0))
+                    outs.append((self._oframe(self.dR_own[l], c, q, Ly.rw), 0))
+                    terms.append(tt)
+            if self.q == 0 and b > 0:
+                for k in range(max(0, t0 - hw), t0):
+                    for q in range(P):
+                        outs.append((self._hframe(self.halo_send, k - (t0 - hw), q, W), 0))
+                        terms.append([(self._oframe(dz, t - t0, q, W), float(m[t, k])) for t in ts
+                                      if max(0, t - w + 1) <= k <= t])
+            tab = self._mp_table(key, outs, terms)
+        nout, o, a, tp, sr, co = tab
+        call("dgnn_frames_combine", plan.NP * W, nout, ptr(o), ptr(a), ptr(tp), ptr(sr), ptr(co),
+             _lib.stream_handle())
+
+    def halo_stage(self, buf, W, first):
+        """The first (or last) w - 1 owned frames of `buf` (owner layout),
+        all slabs, copied into the contiguous send buffer [P][w - 1][NP * W]."""
+        plan = self.eng.plan
+        P, C, NP = plan.P, plan.chunk, plan.NP
+        hw = self.eng.cfg.window - 1
+        v = buf[:P * C * NP * W].view(P, C, NP * W)
+        v = v[:, :hw] if first else v[:, C - hw:]
+        out = self.halo_send[:P * hw * NP * W].view(P, hw, NP * W)
+        out.copy_(v)
+        return out.view(-1)
+
     def store_pi(self, b):
         if self.skip and b < self.eng.plan.nblk - 1:
             self.pi[b] = [(h.clone(), c.clone()) for h, c in self.state]
@@ -888,7 +1010,10 @@ class Rank:
         eng = self.eng
         Ly = eng.layout.layers[l]
         if not self.skip:
-            self._mprod_backward(b, l)
+            if eng.halo:
+                self._mprod_backward_halo(b, l)
+            else:
+                self._mprod_backward(b, l)
             return []
         works = []
         NP, B = eng.plan.NP, eng.plan.bsize
@@ -927,7 +1052,7 @@ class Rank:
         g_b = eng.params.gw(f"lstm{l}.b")
         if use_tc and ho >= 32:
             ws = self.ws_dw
-            call("dgnn_lstm_weight_grad_tc", B * NP, NP, Ly.kx, ho, ptr(self.R_vm[l]), Ly.rw, ptr(self.Y_vm[l]),
+            call(DW_KERNEL, B * NP, NP, Ly.kx, ho, ptr(self.R_vm[l]), Ly.rw, ptr(self.Y_vm[l]),
                  ptr(self.act[l][0]), ptr(self.G_vm[l]), ptr(g_wcat), ptr(g_b), ptr(ws), ws.numel(), st)
             return works
         ws = self.ws_tn
@@ -1026,6 +1151,13 @@ class LocalFabric:
             for q, rq in enumerate(ranks):
                 dst(rq)[p * count:(p + 1) * count].copy_(s[q * count:(q + 1) * count])
 
+    def shift(self, ranks, msgs):
+        """Point-to-point messages (src rank, dst rank, send(rank) -> tensor,
+        recv(rank) -> tensor), all ranks on this device."""
+        byq = {r.q: r for r in ranks}
+        for sq, dq, send, recv in msgs:
+            recv(byq[dq]).copy_(send(byq[sq]))
+
     def allreduce(self, tensors):
         total = tensors[0].clone()
         for t in tensors[1:]:
@@ -1048,6 +1180,19 @@ class NcclFabric:
         if P == 1:
             return
         self.dist.all_to_all_single(dst(r)[:P * count], src(r)[:P * count])
+
+    def shift(self, ranks, msgs):
+        (r,) = ranks
+        dist = self.dist
+        ops = []
+        for sq, dq, send, recv in msgs:
+            if sq == r.q:
+                ops.append(dist.P2POp(dist.isend, send(r), dq))
+            if dq == r.q:
+                ops.append(dist.P2POp(dist.irecv, recv(r), sq))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
 
     def allreduce(self, tensors):
         (t,) = tensors
@@ -1088,6 +1233,8 @@ class Engine:
         self.enc = encoding if encoding is not None else SnapshotEncoding(graph)
         self.fabric = fabric or LocalFabric()
         self.split = self.skip and self.plan.P > 1 and SPLIT_GCN == "1"
+        self.halo = (cfg.architecture == "tm-gcn" and self.plan.P > 1 and TM_HALO == "1"
+                     and cfg.window - 1 <= self.plan.chunk)
         # one rank per GPU, split GCN: blocks pushed by the copy engines into
         # peer memory as soon as they are produced (peer.py)
         self.peer = None
@@ -1190,6 +1337,48 @@ class Engine:
             msgs = plan.P * (plan.P - 1)
             comm.record_alltoall(units, msgs, phase, b, l)
 
+    def _halo_forward(self, b, l, phase):
+        """Operator-input halo of layer l: rank p's last w - 1 frames to rank
+        p + 1; in a forward pass (not the checkpoint rerun) rank P - 1's also
+        to rank 0 as block b + 1's trailing frames."""
+        plan = self.plan
+        P, N = plan.P, plan.N
+        Ly = self.layout.layers[l]
+        hw, W = self.cfg.window - 1, Ly.ho
+        n = hw * N * W
+
+        def send(r):
+            return r.halo_stage(r.R_own[l], Ly.rw, first=False)
+        msgs = [(p, p + 1, send, lambda r: r.halo_buf[l]) for p in range(P - 1)]
+        if phase != "rerun" and b < plan.nblk - 1:
+            msgs.append((P - 1, 0, send, lambda r: r.trail_own[l][(b + 1) * n:(b + 2) * n]))
+        self.fabric.shift(self.ranks, msgs)
+        self.bytes_moved += F32 * n * len(msgs)
+
+    def _halo_backward(self, b, l):
+        """Output-gradient halo of layer l: rank p's first w - 1 frames of dZ
+        to rank p - 1."""
+        plan = self.plan
+        Ly = self.layout.layers[l]
+        hw = self.cfg.window - 1
+
+        def send(r):
+            return r.halo_stage(r.dy_buf(l), Ly.ho, first=True)
+        msgs = [(p, p - 1, send, lambda r: r.halo_buf[l]) for p in range(1, plan.P)]
+        self.fabric.shift(self.ranks, msgs)
+        self.bytes_moved += F32 * hw * plan.N * Ly.ho * len(msgs)
+
+    def _halo_owed(self, b, l):
+        """Gradient owed by block b's first frames to block b - 1's last w - 1
+        (written by rank 0's adjoint launch) -> rank P - 1."""
+        plan = self.plan
+        if b == 0 or plan.nblk == 1:
+            return
+        Ly = self.layout.layers[l]
+        n = (self.cfg.window - 1) * plan.N * Ly.ho
+        self.fabric.shift(self.ranks, [(0, plan.P - 1, lambda r: r.halo_send[:n], lambda r: r.dtrail_own[l])])
+        self.bytes_moved += F32 * n
+
     def _record_xchg(self, comm, phase, b, l):
         if comm is not None:
             plan = self.plan
@@ -1197,7 +1386,7 @@ class Engine:
 
     def _pipelining(self):
         """(GCN-side, LSTM-side) exchange pipelining for this run."""
-        if self.split or self.evolve:
+        if self.split or self.evolve or self.halo:
             return False, False
         if not (self.fabric.distributed and self.plan.P > 1) or PIPELINED_EXCHANGE == "0":
             return False, False
@@ -1403,6 +1592,16 @@ class Engine:
             if self.split_pipe:
                 self._split_layer_forward_pipelined(b, l, phase, comm)
                 continue
+            if self.halo:
+                for r in self.ranks:
+                    r.gcn_forward(b, l)
+                self._halo_forward(b, l, phase)
+                for r in self.ranks:
+                    r.rnn_forward(b, l)
+                # the ledger records the reference's two redistributions
+                self._record_xchg(comm, phase, b, l)
+                self._record_xchg(comm, phase, b, l)
+                continue
             if self.split:
                 if l == 0:
                     self._record_xchg(comm, phase, b, l)     # s1 is local: nothing moves
@@ -1509,6 +1708,17 @@ class Engine:
                 works += r.loss_grads(b, pipelined=pipe_gcn)
             for l in reversed(range(L)):
                 Ly = layers[l]
+                if self.halo:
+                    self._halo_backward(b, l)
+                    for r in self.ranks:
+                        r.rnn_backward(b, l)
+                    self._halo_owed(b, l)
+                    self._record_xchg(comm, "backward", b, l)
+                    self._record_xchg(comm, "backward", b, l)
+                    works = []
+                    for r in self.ranks:
+                        works += r.gcn_backward(b, l)
+                    continue
                 if pipe_gcn:
                     self._wait(works)
                     self._record_xchg(comm, "backward", b, l)

@@ -370,9 +370,11 @@ def gcn_backward(dr: np.ndarray, r: np.ndarray, s: np.ndarray, w: np.ndarray, sk
     return (ds.cpu().numpy() if rows_ds else None), gw.view(fp, hp).cpu().numpy()
 
 
-def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np.ndarray, np_rows: int):
-    """Tensor-core block weight gradient (test hook of dgnn_lstm_weight_grad_tc):
-    returns (sum_r xcat[r]^T dz[r]  as (kx+hp) x 4hp, sum_r dz[r]) in fp64."""
+def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np.ndarray, np_rows: int,
+                        variant: str = "tc"):
+    """Tensor-core block weight gradient (test hook of dgnn_lstm_weight_grad_tc,
+    variant "ts": dgnn_lstm_weight_grad_ts): returns (sum_r xcat[r]^T dz[r]
+    as (kx+hp) x 4hp, sum_r dz[r]) in fp64."""
     dev = _dev()
     rows, kx = x.shape
     hp = h0.shape[1]
@@ -383,8 +385,8 @@ def lstm_weight_grad_tc(x: np.ndarray, h_out: np.ndarray, h0: np.ndarray, dz: np
     gw = torch.zeros((kx + hp) * 4 * hp, dtype=torch.float64, device=dev)
     gb = torch.zeros(4 * hp, dtype=torch.float64, device=dev)
     ws = torch.empty(query("dgnn_lstm_weight_grad_tc_workspace", kx, hp), dtype=torch.uint8, device=dev)
-    call("dgnn_lstm_weight_grad_tc", rows, np_rows, kx, hp, ptr(t[0]), kx, ptr(t[1]), ptr(t[2]), ptr(t[3]),
-         ptr(gw), ptr(gb), ptr(ws), ws.numel(), _lib.stream_handle())
+    call(f"dgnn_lstm_weight_grad_{variant}", rows, np_rows, kx, hp, ptr(t[0]), kx, ptr(t[1]), ptr(t[2]),
+         ptr(t[3]), ptr(gw), ptr(gb), ptr(ws), ws.numel(), _lib.stream_handle())
     return gw.view(kx + hp, 4 * hp).cpu().numpy(), gb.cpu().numpy()
 
 

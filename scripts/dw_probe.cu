@@ -25,11 +25,12 @@ int main(int argc, char** argv) {
     const double bytes = (double)rows * (M + kx + hp) * 4;
 #if DGNN_DW_PROBE & 16
     {
-        unsigned long long prof[dgnn::kSMs * 8];
+        unsigned long long prof[dgnn::kMaxSMs * 8];
+        const int nsm = dgnn::num_sms();
         cudaMemcpyFromSymbol(prof, dgnn::dw_prof, sizeof(prof));
         double f[6] = {0, 0, 0, 0, 0, 0};
-        for (int c = 0; c < dgnn::kSMs; ++c)
-            for (int k = 0; k < 6; ++k) f[k] += (double)prof[c * 8 + k] / dgnn::kSMs;
+        for (int c = 0; c < nsm; ++c)
+            for (int k = 0; k < 6; ++k) f[k] += (double)prof[c * 8 + k] / nsm;
         printf("cycles/CTA %.0f: loader wait-empty %.1f%%  converter wait-landed %.1f%%  mma wait-full %.1f%%  "
                "mma wait-accempty %.1f%%  epilogue wait-accfull %.1f%%\n", f[5], 100 * f[0] / f[5], 100 * f[1] / f[5],
                100 * f[2] / f[5], 100 * f[3] / f[5], 100 * f[4] / f[5]);

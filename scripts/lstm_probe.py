@@ -97,6 +97,10 @@ def main():
         byts = 4.0 * B * n * (kx + hp + N4)
         res["dw"] = dict(us=us, floor_tf_us=fl / tf / 1e6, floor_hbm_us=byts / hbm / 1e3, frac_tf=fl / tf / 1e6 / us,
                          frac_hbm=byts / hbm / 1e3 / us)
+        us = timed(lambda: call("dgnn_lstm_weight_grad_ts", B * n, n, kx, hp, ptr(X), kx, ptr(Y), ptr(h), ptr(DZ),
+                                ptr(gw), ptr(gb), ptr(ws), ws.numel(), st), reps=3)
+        res["dw_ts"] = dict(us=us, floor_tf_us=fl / tf / 1e6, floor_hbm_us=byts / hbm / 1e3,
+                            frac_tf=fl / tf / 1e6 / us, frac_hbm=byts / hbm / 1e3 / us)
         out[f"kx{kx}_hp{hp}"] = res
         for k, v in res.items():
             print(f"kx={kx} hp={hp} {k:9s} {v['us']:8.1f} us  3xTF32 floor {v['floor_tf_us']:7.1f} "

@@ -279,3 +279,31 @@ def test_first_layer_products_bit_exact(oracle, arch):
         got = r.s1[t].view(g.num_vertices, -1).cpu().numpy()
         assert np.array_equal(got[:, :2], P.s1[t].astype(np.float32)), t
         assert not got[:, 2:].any()
+
+
+@pytest.mark.parametrize("workers,nblk,window", [(2, 2, 2), (4, 2, 2), (4, 1, 2), (2, 2, 3), (2, 1, 3)])
+def test_tm_halo_matches_redistribution_bitwise(workers, nblk, window, monkeypatch):
+    """tm-gcn at P > 1: the M-product on each rank's own snapshots with a
+    (w - 1)-frame halo (previous rank's operator inputs, next rank's output
+    gradients, cross-block trailing / owed frames) against the reference's
+    snapshot <-> vertex redistribution: identical loss, gradients (bit for
+    bit) and ledgers."""
+    import paper_2109_07893_b200.engine as engine_mod
+    fx = load("tmgcn_small")
+    meta = jload(fx["cfg"])
+    cfg = pk.ModelConfig(architecture="tm-gcn", in_features=2, hidden_features=meta["hidden"],
+                         embed_features=meta["hidden"], window=window)
+    data = pk.prepare_training_data(cfg, product_graph(fx))
+    train = pk.LabelSet(2, labels_from(fx, "train_"))
+    params = params_from(fx, "p_")
+    out = {}
+    for halo in ("1", "0"):
+        monkeypatch.setattr(engine_mod, "TM_HALO", halo)
+        pk.api.clear_engines()
+        out[halo] = pk.distributed_epoch(cfg, data, train, params, workers, nblk)
+    (la, ga, ca, ta), (lb, gb, cb, tb) = out["1"], out["0"]
+    assert la == lb
+    for k in ga:
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ca.as_dict() == cb.as_dict() and ca.events == cb.events
+    assert ta.as_dict() == tb.as_dict()

@@ -302,10 +302,12 @@ def test_lstm_backward_tensor_cores_vs_oracle(oracle, H):
         assert guarded_close(dxs[t], rdxs[t], RTOL, 1e-5)[0]
 
 
+@pytest.mark.parametrize("variant", ["tc", "ts"])
 @pytest.mark.parametrize("hp,kx", [(64, 128), (64, 68), (32, 36), (32, 96)])
-def test_lstm_weight_grad_tc_long_reduction(hp, kx):
+def test_lstm_weight_grad_tc_long_reduction(hp, kx, variant):
     """Block weight gradient over 120k (step, vertex) rows: many CTAs, many
-    TMEM promotion periods; fp64 reference."""
+    TMEM promotion periods; fp64 reference.  Both kernels: dz from shared
+    memory ("tc") and dz from TMEM ("ts")."""
     from paper_2109_07893_b200.ops import lstm_weight_grad_tc
     rng = np.random.default_rng(hp + kx)
     np_rows, steps = 20_000, 6
@@ -314,7 +316,7 @@ def test_lstm_weight_grad_tc_long_reduction(hp, kx):
     h = np.tanh(rng.standard_normal((rows, hp))).astype(np.float32)
     h0 = np.tanh(rng.standard_normal((np_rows, hp))).astype(np.float32)
     dz = (rng.standard_normal((rows, 4 * hp)) * 1e-3).astype(np.float32)
-    gw, gb = lstm_weight_grad_tc(x, h, h0, dz, np_rows)
+    gw, gb = lstm_weight_grad_tc(x, h, h0, dz, np_rows, variant)
     hprev = np.concatenate([h0, h[:-np_rows]]).astype(np.float64)
     xcat = np.concatenate([x.astype(np.float64), hprev], axis=1)
     ref = xcat.T @ dz.astype(np.float64)
