@@ -147,8 +147,10 @@ class KernelTimer:
         out = {}
         last = {}
         for st, name, e0, e1 in self.order:
-            d = out.setdefault(str(st), {"busy_ms": 0.0, "idle_ms": 0.0, "idle_before": {}})
-            d["busy_ms"] += e0.elapsed_time(e1)
+            d = out.setdefault(str(st), {"busy_ms": 0.0, "idle_ms": 0.0, "idle_before": {}, "busy_by_call": {}})
+            dt = e0.elapsed_time(e1)
+            d["busy_ms"] += dt
+            d["busy_by_call"][name] = d["busy_by_call"].get(name, 0.0) + dt
             prev = last.get(st)
             idle = prev.elapsed_time(e0) if prev is not None else t0.elapsed_time(e0)
             if idle > 0:
@@ -157,6 +159,7 @@ class KernelTimer:
             last[st] = e1
         for d in out.values():
             d["idle_before"] = dict(sorted(d["idle_before"].items(), key=lambda kv: -kv[1])[:top])
+            d["busy_by_call"] = dict(sorted(d["busy_by_call"].items(), key=lambda kv: -kv[1])[:2 * top])
         return out
 
     def durations(self):

@@ -357,19 +357,18 @@ class Rank:
             self.set_turn ^= 1
             self.slots = self.mat.materialize(self.ts, ledger=ledger, count_bytes=count_bytes,
                                               set_idx=self.set_turn, after=released,
-                                              head_prev=None if keep else self._neighbor_head(self.ts[0]))
+                                              head_prev=None if keep else self._neighbor_head(self.ts[0]),
+                                              handoff=None if keep else self._handoff(self.ts))
             self.ready_ev = self.mat.ready
-            if not keep:
-                self._after_build(self.ts)
         if not self.keep_graphs and next_b is not None and len(self.eng.plan.steps_of(self.q, next_b)):
             self.set_turn ^= 1
             nts = self.eng.plan.steps_of(self.q, next_b)
             ascending = next_b > b or (next_b == b and not keep)
+            chain = ascending and next_b != b
             slots = self.mat.materialize(nts, ledger=None, count_bytes=count_bytes, set_idx=self.set_turn,
                                          after=released, consume=False,
-                                         head_prev=self._neighbor_head(nts[0]) if ascending and next_b != b else None)
-            if ascending and next_b != b:
-                self._after_build(nts)
+                                         head_prev=self._neighbor_head(nts[0]) if chain else None,
+                                         handoff=self._handoff(nts) if chain else None)
             self.prefetched[next_b] = (slots, self.mat.ready)
         self.graph_waited = False
         if self.skip:
@@ -410,10 +409,10 @@ class Rank:
         # block 0 alternates between two sets across epochs: the next epoch's
         # block 0 is rebuilt while this epoch's last rerun still reads it
         set_idx = plan.nblk if (b == 0 and tag % 2) else b
+        handoff = self._handoff(ts) if chained else None
         slots = self.mat.materialize(ts, ledger=None, count_bytes=count_bytes, set_idx=set_idx, after=after,
-                                     head_prev=self._neighbor_head(ts[0]) if chained else None, consume=False)
-        if chained:
-            self._after_build(ts)
+                                     head_prev=self._neighbor_head(ts[0]) if chained else None, consume=False,
+                                     handoff=handoff)
         ent = (slots, self.mat.ready, tag)
         self.built[b] = ent
         return ent
@@ -434,18 +433,20 @@ class Rank:
             return nb.mat.raw() if nb.mat.raw_t == t0 - 1 else None
         return eng.head_chain.recv_spec(src, int(eng.enc.nnz[t0 - 1]))
 
-    def _after_build(self, ts):
-        """One rank per GPU: hand the chunk's last raw snapshot to the rank
-        whose chunk starts right after it (NVLink, on the graph stream)."""
+    def _handoff(self, ts):
+        """One rank per GPU: the chunk's last raw snapshot goes to the rank
+        whose chunk starts right after it (NVLink, on the graph stream),
+        rebuilt ahead of the chunk's other graph work (Materializer
+        `handoff`); None when nobody waits for it."""
         eng, plan = self.eng, self.eng.plan
         t1 = ts[-1]
         if eng.head_chain is None or t1 + 1 >= plan.T:
-            return
+            return None
         dst = plan.owner_of(t1 + 1)
         if dst == self.q:
-            return
-        rp, col = self.mat.raw()
-        eng.head_chain.send(rp, col, int(eng.enc.nnz[t1]), dst, self.mat.graph_stream)
+            return None
+        gs = self.mat.graph_stream
+        return lambda rp, col, nnz: eng.head_chain.send(rp, col, nnz, dst, gs)
 
     def _wait_graph(self):
         if not self.graph_waited:

@@ -352,7 +352,7 @@ class Materializer:
         self.copy_log = None
 
     def materialize(self, ts, ledger=None, count_bytes: bool = True, set_idx: int = 0, after=None,
-                    head_prev=None, consume: bool = True):
+                    head_prev=None, consume: bool = True, handoff=None):
         """Rebuild Ahat_t for the contiguous run `ts` into slots 0..len(ts)-1
         of slot set `set_idx`.  Returns the slots; the set's ready event (and
         `self.ready`) is recorded on the graph stream.  `after`: an event
@@ -375,7 +375,15 @@ class Materializer:
 
         `count_bytes` charges the real H2D bytes of this build; `consume`
         also charges the pass that consumes it (`account`) -- the engine
-        builds ahead of the consuming pass and charges that pass itself."""
+        builds ahead of the consuming pass and charges that pass itself.
+
+        `handoff(rowptr, col, nnz)`: the chunk's last raw snapshot is wanted
+        by another rank as its head.  It is then rebuilt first, by the raw
+        delta chain alone (`_raw_chain`, private buffers, before waiting for
+        the slots' consumers), and handed over (enqueued on the graph
+        stream) before the chunk's smoothing / transposes / Laplacians:
+        rank q's head no longer waits for rank q-1's whole chunk build,
+        only for its chain of 1-step deltas."""
         enc = self.enc
         self.slots = self.sets[set_idx]
         self.ready = self.ready_sets[set_idx]
@@ -436,6 +444,14 @@ class Materializer:
         if consume:
             self.account(ts, ledger, count_bytes)
         voff = vbase
+        if head == "neighbor" and len(head_prev) > 2 and head_prev[2] is not None:
+            with torch.cuda.stream(gs):
+                w = head_prev[2]
+                w() if callable(w) else gs.wait_event(w)
+        if handoff is not None:
+            with torch.cuda.stream(gs):
+                rp, col = self._raw_chain(ts, head, head_prev, fbase, dbase)
+                handoff(rp, col, int(enc.nnz[ts[-1]]))
         # slots are overwritten: wait for their consumers on the compute stream
         if after is not None:
             gs.wait_event(after)
@@ -448,9 +464,6 @@ class Materializer:
             prev_rp = prev_col = None
             if head == "neighbor":
                 prev_rp, prev_col = head_prev[0], head_prev[1]
-                if len(head_prev) > 2 and head_prev[2] is not None:
-                    w = head_prev[2]
-                    w() if callable(w) else gs.wait_event(w)
                 release = head_prev[3] if len(head_prev) > 3 else None
             elif head == "own":
                 prev_rp, prev_col = self.a_rowptr[cur], self.a_col[cur]
@@ -517,6 +530,47 @@ class Materializer:
             self.raw_t = ts[-1]
             self.ready.record(gs)
         return self.slots[:len(ts)]
+
+    def _raw_chain(self, ts, head, head_prev, fbase, dbase):
+        """Raw CSR of A_{ts[-1]} from the chunk's head source and the 1-step
+        deltas of ts alone, in private ping-pong buffers (graph stream
+        current).  Same kernels and inputs as materialize's chain, hence
+        the same bits."""
+        enc, n = self.enc, self.enc.n
+        gsh = self.graph_stream.cuda_stream
+        if getattr(self, "ch_rowptr", None) is None:
+            i32 = dict(dtype=torch.int32, device=self.device)
+            self.ch_rowptr = [torch.empty(n + 1, **i32) for _ in range(2)]
+            self.ch_col = [torch.empty(enc.cap_a, **i32) for _ in range(2)]
+        t0 = ts[0]
+        cur, dpos, first = 0, dbase, 0
+        if head == "full":
+            m = int(enc.nnz[t0])
+            call("dgnn_rowptr_from_sorted_rows", n, m, ptr(self.full_dev[fbase:fbase + m]), ptr(self.ch_rowptr[0]),
+                 gsh)
+            self.ch_col[0][:m].copy_(self.full_dev[fbase + m:fbase + 2 * m])
+            prev_rp, prev_col, first = self.ch_rowptr[0], self.ch_col[0], 1
+        elif head == "neighbor":
+            prev_rp, prev_col = head_prev[0], head_prev[1]
+        elif head == "own":
+            prev_rp, prev_col = self.a_rowptr[self.cur], self.a_col[self.cur]
+        else:   # full_prev: A_{t0-1} in full
+            mp = int(enc.nnz[t0 - 1])
+            call("dgnn_rowptr_from_sorted_rows", n, mp, ptr(self.full_dev[fbase:fbase + mp]), ptr(self.ch_rowptr[0]),
+                 gsh)
+            self.ch_col[0][:mp].copy_(self.full_dev[fbase + mp:fbase + 2 * mp])
+            prev_rp, prev_col = self.ch_rowptr[0], self.ch_col[0]
+        for t in ts[first:]:
+            nd, ni = int(enc.n_del[t]), int(enc.n_ins[t])
+            d = self.delta_dev[dpos:dpos + 2 * (nd + ni)]
+            dpos += 2 * (nd + ni)
+            nxt = 1 - cur
+            call("dgnn_csr_apply_delta", n, ptr(prev_rp), ptr(prev_col), nd, ptr(d[:nd]), ptr(d[nd:2 * nd]), ni,
+                 ptr(d[2 * nd:2 * nd + ni]), ptr(d[2 * nd + ni:]), ptr(self.ch_rowptr[nxt]), ptr(self.ch_col[nxt]),
+                 enc.cap_a, ptr(self.ws_apply), self.ws_apply.numel(), ptr(self.status), gsh)
+            cur = nxt
+            prev_rp, prev_col = self.ch_rowptr[cur], self.ch_col[cur]
+        return prev_rp, prev_col
 
     def add_sets(self, k: int) -> None:
         """k more slot sets of `slots` slots each."""
