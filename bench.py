@@ -43,7 +43,7 @@ sys.path.insert(0, str(ROOT))
 # split over the GPUs.  nblk per GPU count: the checkpoint block count the
 # HBM plan needs.
 CONFIGS = {
-    "c2": dict(arch="cd-gcn", n=750_000, m=468_750, T=32, hidden=64, churn=0.10, nblk={1: 1, 2: 2, 4: 2, 8: 2},
+    "c2": dict(arch="cd-gcn", n=750_000, m=468_750, T=32, hidden=64, churn=0.10, nblk={1: 1, 2: 1, 4: 1, 8: 1},
                gen="churn",
                scaling="weak", cpu_scale=64,
                workload="configs[1] Epinions-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=64, "
@@ -54,11 +54,11 @@ CONFIGS = {
                         "AMLSim-style transaction graph: N=1M, T=64, 2M edges/snapshot (128M total), "
                         "heavy-tailed degrees, 2% churn"),
     "c4": dict(arch="cd-gcn", n=3_000_000, m=4_687_500, T=64, hidden=32, churn=0.10,
-               nblk={1: 8, 2: 4, 4: 2, 8: 2}, gen="device", scaling="strong", cpu_scale=256,
+               nblk={1: 8, 2: 2, 4: 1, 8: 1}, gen="device", scaling="strong", cpu_scale=256,
                workload="configs[3] Flickr/YouTube-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=32, "
                         "N=3M, T=64, 4,687,500 edges/snapshot (300M total), 10% churn, snapshot-partitioned"),
     "c5": dict(arch="cd-gcn", n=10_000_000, m=15_625_000, T=64, hidden=32, churn=0.01,
-               nblk={1: 16, 2: 16, 4: 8, 8: 4}, gen="device", scaling="strong", cpu_scale=1024,
+               nblk={1: 16, 2: 16, 4: 4, 8: 2}, gen="device", scaling="strong", cpu_scale=1024,
                workload="configs[4] billion-edge: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=32, N=10M, T=64, "
                         "15,625,000 edges/snapshot (1B total), 1% churn, gradient checkpointing"),
 }
