@@ -70,11 +70,13 @@ HIDDEN = CFG["hidden"]
 CHURN = CFG["churn"]
 THETA = 0.10
 NBLK = CFG["nblk"]
+CONFIG_KEY = "c2"
 
 
 def select_config(name):
-    global CFG, N_PER_GPU, EDGES_PER_GPU, T, HIDDEN, CHURN, NBLK
+    global CFG, N_PER_GPU, EDGES_PER_GPU, T, HIDDEN, CHURN, NBLK, CONFIG_KEY
     CFG = CONFIGS[name]
+    CONFIG_KEY = name
     N_PER_GPU, EDGES_PER_GPU, T, HIDDEN, CHURN, NBLK = (CFG[k] for k in ("n", "m", "T", "hidden", "churn", "nblk"))
 
 
@@ -282,8 +284,12 @@ def ncu_traffic(entry):
     """DRAM bytes per launch of the kernel behind a C-ABI entry, from the
     latest committed ncu launch list (profiles/*_traffic.json, written by
     scripts/ncu_summary.py from `dram__bytes_read.sum + dram__bytes_write.sum`)."""
-    files = sorted((ROOT / "profiles").glob("r*_traffic.json"))
+    # the launch list of this config when one is committed (r*_<config>_traffic.json), else configs[1]'s
+    files = sorted((ROOT / "profiles").glob(f"r*_{CONFIG_KEY}_traffic.json")) or \
+        sorted(p for p in (ROOT / "profiles").glob("r*_traffic.json") if p.stem.count("_") == 1)
     pref = NCU_KERNEL.get(entry)
+    if entry == "dgnn_gcn_forward":   # the aggregating instance at this config's width / cell
+        pref = f"gcn_fwd_tc_kernel<{HIDDEN}, {HIDDEN}, {int(CFG['arch'] == 'cd-gcn')}, 1"
     if not files or pref is None:
         return None
     d = json.loads(files[-1].read_text())

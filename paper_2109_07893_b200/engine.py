@@ -76,6 +76,9 @@ SKIP_LAST_FORWARD = os.environ.get("DGNN_SKIP_LAST_FORWARD", "1") == "1"
 TM_HALO = os.environ.get("DGNN_TM_HALO", "1")
 # LSTM block weight gradient: dz staged in shared memory ("tc") or in TMEM ("ts")
 DW_KERNEL = "dgnn_lstm_weight_grad_" + os.environ.get("DGNN_DW_KERNEL", "tc")
+# the block weight gradient runs on a side stream, overlapping the rest of
+# the block's backward (it only feeds the gradient all-reduce); "0" in order
+DW_OVERLAP = os.environ.get("DGNN_DW_OVERLAP", "1") == "1"
 
 
 class Plan:
@@ -222,6 +225,8 @@ class Rank:
             self.wcache = [_zeros(B * 6 * c, f64, dev) for c in cnts]
             self.wseed = [_zeros(B * c, f64, dev) for c in cnts]
         self.pi = {}
+        self.side = None           # side stream of the block weight gradients (DW_OVERLAP)
+        self.side_pending = []
         # first-layer products s1[t] = Ahat_t X_t for owned steps, [N, fp0] fp32
         self.s1 = {}
         # labels for owned frames
@@ -1053,8 +1058,22 @@ class Rank:
         g_b = eng.params.gw(f"lstm{l}.b")
         if use_tc and ho >= 32:
             ws = self.ws_dw
+            dst = st
+            if DW_OVERLAP:
+                # inputs (x, h, dz, h0) stay untouched until the block ends
+                # (Engine._join_side, before pi_{b-1} is released)
+                if self.side is None:
+                    self.side = torch.cuda.Stream(device=self.dev)
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream(self.dev))
+                self.side.wait_event(ev)
+                dst = self.side.cuda_stream
             call(DW_KERNEL, B * NP, NP, Ly.kx, ho, ptr(self.R_vm[l]), Ly.rw, ptr(self.Y_vm[l]),
-                 ptr(self.act[l][0]), ptr(self.G_vm[l]), ptr(g_wcat), ptr(g_b), ptr(ws), ws.numel(), st)
+                 ptr(self.act[l][0]), ptr(self.G_vm[l]), ptr(g_wcat), ptr(g_b), ptr(ws), ws.numel(), dst)
+            if DW_OVERLAP:
+                done = torch.cuda.Event()
+                done.record(self.side)
+                self.side_pending.append(done)
             return works
         ws = self.ws_tn
         K4 = 4 * ho
@@ -1767,8 +1786,13 @@ class Engine:
     def _release_checkpoint(self, b):
         """pi_{b-1} was last read by block b's rerun and backward: free it
         (the reference keeps every pi_b until the epoch ends, dist.py:368, 381;
-        at c5 the checkpoints of every block would not fit beside the caches)."""
+        at c5 the checkpoints of every block would not fit beside the caches).
+        The block's side-stream weight gradients are joined first."""
         for r in self.ranks:
+            cur = torch.cuda.current_stream(r.dev)
+            for e in r.side_pending:
+                cur.wait_event(e)
+            r.side_pending = []
             r.pi.pop(b - 1, None)
 
     def finish(self, loss_dev, grads):
