@@ -37,7 +37,15 @@ constexpr int DW_ROWS = 16;      // reduction rows per stage = two 8-row K steps
 constexpr int DW_PERIOD = DGNN_DW_PERIOD;   // rows per TMEM accumulation period
 constexpr int DW_MAX_STAGES = 4;
 constexpr int DW_NPROD = 16, DW_MMA_WARP = DW_NPROD, DW_NEPI = 4;
-constexpr int DW_PD = 2;         // stages of operand loads each producer keeps in flight (registers)
+#ifndef DGNN_DW_PD
+#define DGNN_DW_PD 2
+#endif
+constexpr int DW_PD = DGNN_DW_PD;   // stages of operand loads each producer keeps in flight (registers)
+// rows ahead of the current stage that the bulk L2 prefetch covers (128-row
+// prefetches every 8 stages; 0 = no prefetch)
+#ifndef DGNN_DW_PF
+#define DGNN_DW_PF 128
+#endif
 constexpr int DW_THREADS = 32 * (DW_NPROD + 1 + DW_NEPI);
 constexpr int DW_SMEM_MAX = 232448;
 // Bottleneck probe (scripts/dw_probe.cu, -DDGNN_DW_PROBE=mask): 1 skip MMAs,
@@ -213,10 +221,11 @@ __global__ void __launch_bounds__(DW_THREADS, 1) lstm_dw_tc_kernel(int64_t rows,
             const int64_t db_ = min(dz_end, (tb * np + (((rb - 1) - tb * np) & ~(int64_t)127) + 128) * M);
             bulk_prefetch_l2(dz + da, (uint32_t)((db_ - da) * 4));
         };
-        if (pt == 0) prefetch_rows(r_begin);
+        if (pt == 0 && DGNN_DW_PF)
+            for (int a = 0; a < DGNN_DW_PF; a += 128) prefetch_rows(r_begin + a);
         auto load = [&](int g, float4 (&va)[A_ITEMS], float4 (&vb)[B_ITEMS]) {
             const int64_t r0 = r_begin + (int64_t)g * DW_ROWS;
-            if (pt == 0 && (g & 7) == 0) prefetch_rows(r0 + 128);
+            if (DGNN_DW_PF && pt == 0 && (g & 7) == 0) prefetch_rows(r0 + DGNN_DW_PF);
             const int64_t v0 = cv & ~(int64_t)127;
             const int64_t tr = min((int64_t)128, np - v0);
             const float* rowp = dz + (ct * np + v0) * M + (cv - v0) * 4;   // tb_off(cv, 0, M, np)

@@ -362,18 +362,22 @@ class Rank:
             self.set_turn ^= 1
             self.slots = self.mat.materialize(self.ts, ledger=ledger, count_bytes=count_bytes,
                                               set_idx=self.set_turn, after=released,
-                                              head_prev=None if keep else self._neighbor_head(self.ts[0]),
-                                              handoff=None if keep else self._handoff(self.ts))
+                                              head_prev=self._chain_head(self.ts[0], keep),
+                                              handoff=self._chain_handoff(self.ts, keep))
             self.ready_ev = self.mat.ready
+        if not self.keep_graphs and next_b == b and not keep:
+            # the rerun of this block follows: it reads this very chunk (the
+            # next build goes into the other set), nothing is rebuilt
+            self.prefetched[b] = (self.slots, self.ready_ev)
+            next_b = None
         if not self.keep_graphs and next_b is not None and len(self.eng.plan.steps_of(self.q, next_b)):
             self.set_turn ^= 1
             nts = self.eng.plan.steps_of(self.q, next_b)
-            ascending = next_b > b or (next_b == b and not keep)
-            chain = ascending and next_b != b
+            ascending = next_b > b
             slots = self.mat.materialize(nts, ledger=None, count_bytes=count_bytes, set_idx=self.set_turn,
                                          after=released, consume=False,
-                                         head_prev=self._neighbor_head(nts[0]) if chain else None,
-                                         handoff=self._handoff(nts) if chain else None)
+                                         head_prev=self._chain_head(nts[0], not ascending),
+                                         handoff=self._chain_handoff(nts, not ascending))
             self.prefetched[next_b] = (slots, self.mat.ready)
         self.graph_waited = False
         if self.skip:
@@ -430,6 +434,8 @@ class Rank:
         eng, plan = self.eng, self.eng.plan
         if t0 == 0 or not eng.head_chain_on:
             return None
+        if eng.fabric.distributed and not eng.chain_cross_block and t0 % plan.bsize == 0:
+            return None
         src = plan.owner_of(t0 - 1)
         if src == self.q:
             return None          # own previous snapshot: the materialiser's raw_t chain
@@ -437,6 +443,19 @@ class Rank:
             nb = eng.rank_of[src]
             return nb.mat.raw() if nb.mat.raw_t == t0 - 1 else None
         return eng.head_chain.recv_spec(src, int(eng.enc.nnz[t0 - 1]))
+
+    def _chain_head(self, t0, keep):
+        """head_prev of a two-set-mode build: one rank per GPU, every build
+        chains within its block (`chain_cross_block` is off); emulated ranks
+        chain in ascending builds only (in place, `_neighbor_head`)."""
+        if self.eng.fabric.distributed or not keep:
+            return self._neighbor_head(t0)
+        return None
+
+    def _chain_handoff(self, ts, keep):
+        if self.eng.fabric.distributed or not keep:
+            return self._handoff(ts)
+        return None
 
     def _handoff(self, ts):
         """One rank per GPU: the chunk's last raw snapshot goes to the rank
@@ -446,6 +465,8 @@ class Rank:
         eng, plan = self.eng, self.eng.plan
         t1 = ts[-1]
         if eng.head_chain is None or t1 + 1 >= plan.T:
+            return None
+        if not eng.chain_cross_block and (t1 + 1) % plan.bsize == 0:
             return None
         dst = plan.owner_of(t1 + 1)
         if dst == self.q:
@@ -1310,7 +1331,13 @@ class Engine:
         if self.keep_graphs:
             for r in self.ranks:
                 r.enable_keep_graphs()
-        if self.fabric.distributed and workers > 1 and self.keep_graphs and self.head_chain_on:
+        # chunk heads across ranks: with keep_graphs every build runs in a
+        # block-ascending chain (forward sweeps, next epoch's block 0), so a
+        # chunk's last snapshot may also feed rank 0 of the next block; in
+        # two-set mode builds also run in the reverse sweep, so heads chain
+        # within a block only (both ends apply the same rule)
+        self.chain_cross_block = self.keep_graphs
+        if self.fabric.distributed and workers > 1 and self.head_chain_on:
             try:
                 from .peer import HeadChain
                 self.head_chain = HeadChain(dev, N, self.enc.cap_a)
