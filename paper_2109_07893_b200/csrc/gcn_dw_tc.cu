@@ -12,15 +12,16 @@
 // straight from their row-major HBM frames (SWIZZLE_128B_BASE32B atoms, as
 // in dw_tc.cu), 3xTF32.
 //
-//   warps 0..7  loaders: cp.async the raw fp32 rows of a 32-row stage (dr and
+//   warps 0..15 loaders (16: 14% faster than 8 at configs[1], scripts/gdw_probe.sh):
+//               cp.async the raw fp32 rows of a 32-row stage (dr and
 //               r of the dq columns into the A hi / mask areas, s into B hi),
 //               completion on landed[s].  Every thread keeps one 4-column
 //               group and steps over rows, so its shared-memory offsets are
 //               fixed and a row address costs one multiply-add;
-//   warps 8..11 converters: dq = dr (.) [r > 0], tf32 split in place (hi, lo);
-//   warp 12     MMA issuer: 4 K steps x 3 MMAs per stage into the TMEM
+//   warps 16..19 converters: dq = dr (.) [r > 0], tf32 split in place (hi, lo);
+//   warp 20     MMA issuer: 4 K steps x 3 MMAs per stage into the TMEM
 //               accumulator of the current 512-row period;
-//   warps 13..16 promotion: each finished period is added (fp32, RED) into the
+//   warps 21..24 promotion: each finished period is added (fp32, RED) into the
 //               CTA's own slot; a second kernel reduces the slots in fp64 in
 //               fixed order -- deterministic, independent of the SM reserve.
 //
@@ -36,7 +37,13 @@ namespace gdw {
 constexpr int ROWS = 32;          // reduction rows per stage (4 MMA K steps of 8)
 constexpr int PERIOD = 512;       // rows per TMEM accumulation period
 constexpr int MAX_STAGES = 6;
-constexpr int NLOAD = 8, NCONV = 4, MMA_WARP = NLOAD + NCONV, NEPI = 4;
+#ifndef DGNN_GDW_NLOAD
+#define DGNN_GDW_NLOAD 16
+#endif
+#ifndef DGNN_GDW_NCONV
+#define DGNN_GDW_NCONV 4
+#endif
+constexpr int NLOAD = DGNN_GDW_NLOAD, NCONV = DGNN_GDW_NCONV, MMA_WARP = NLOAD + NCONV, NEPI = 4;
 constexpr int THREADS = 32 * (NLOAD + NCONV + 1 + NEPI);
 constexpr int SMEM_MAX = 232448;
 }  // namespace gdw

@@ -50,9 +50,17 @@ struct WsRoles {
     static constexpr int NPT = 32 * NP;   // producer threads
 };
 // forward: heavy cell epilogue -- 16 epilogue warps (each a quarter of the
-// units of its TMEM lane quarter) when every warp still gets >= 8 units
+// units of its TMEM lane quarter) at hidden 32; at hidden 64, 8 (half the
+// units each): 17 warps leave more registers per thread, 5-6% faster at
+// configs[1] than 16 (scripts/fwd_roles.sh: 458 vs 481 us at kx 128)
+#ifndef DGNN_FWD_NPROD
+#define DGNN_FWD_NPROD 8
+#endif
+#ifndef DGNN_FWD_NEPI64
+#define DGNN_FWD_NEPI64 8
+#endif
 template <int HP>
-using FwdRoles = WsRoles<8, (HP >= 32 ? 16 : 8), (HP >= 64 ? 3 : 4)>;
+using FwdRoles = WsRoles<DGNN_FWD_NPROD, (HP >= 64 ? DGNN_FWD_NEPI64 : (HP >= 32 ? 16 : 8)), (HP >= 64 ? 3 : 4)>;
 // forward activation landing ring (fp32 chunks, cp.async), decoupled from
 // the operand stages so loads run RAW_RING - 1 chunks ahead (6 at hidden 64:
 // the operand stages are 48 KB and the c_prev tile takes 32 KB)
@@ -60,7 +68,10 @@ template <int HP>
 constexpr int raw_ring() { return HP >= 64 ? 6 : 8; }
 // backward: 8 dz-producer warps fed from shared memory by one loader warp
 // (the extra warp), 3-stage A/B ring to leave room for the raw input ring
-using BwdRoles = WsRoles<8, 4, 3, 1>;
+#ifndef DGNN_BWD_NPROD
+#define DGNN_BWD_NPROD 8
+#endif
+using BwdRoles = WsRoles<DGNN_BWD_NPROD, 4, 3, 1>;
 
 __host__ __device__ constexpr int ws_tmem_cols(int n2) {
     return n2 <= 32 ? 32 : (n2 <= 64 ? 64 : (n2 <= 128 ? 128 : (n2 <= 256 ? 256 : 512)));
