@@ -52,7 +52,10 @@ namespace gtc {
 #endif
 constexpr int PROBE = DGNN_GTB_PROBE;
 constexpr int BM = 128;
-constexpr int NGATHER = 20, IDX_WARP = 20, MMA_WARP = 21, EPI0 = 22, NEPI = 4;
+#ifndef DGNN_GTC_NGATHER
+#define DGNN_GTC_NGATHER 20
+#endif
+constexpr int NGATHER = DGNN_GTC_NGATHER, IDX_WARP = NGATHER, MMA_WARP = NGATHER + 1, EPI0 = NGATHER + 2, NEPI = 4;
 constexpr int THREADS = 32 * (EPI0 + NEPI);
 constexpr int ASTAGES = 2, ISTAGES = 3;
 constexpr int ECAP = 1024;   // edges per tile staged in shared memory (else read from global)
