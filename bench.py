@@ -392,7 +392,7 @@ def run_ours(args):
     timed_names = list(TENSOR_KERNELS) + [
         "dgnn_gcn_forward", "dgnn_spmm_f32", "dgnn_gcn_weight_grad", "dgnn_gcn_backward_rows",
         "dgnn_axpy_frame", "dgnn_frames_combine", "dgnn_csr_apply_delta", "dgnn_laplacian", "dgnn_csr_transpose_staged",
-        "dgnn_head_loss", "dgnn_head_grad", "dgnn_head_loss_grad", "dgnn_head_scatter"]
+        "dgnn_head_loss", "dgnn_head_grad", "dgnn_head_loss_grad", "dgnn_head_scatter", "dgnn_head_scatter_active"]
     if args.timeline:   # every C-ABI call, for the per-stream idle breakdown
         timed_names = list(_lib._SIGS.keys())
     timer = _lib.KernelTimer(timed_names)

@@ -342,6 +342,13 @@ int dgnn_head_loss_grad(int64_t npairs, const int32_t* u, const int32_t* v, cons
 int dgnn_head_scatter(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot,
                       const double* dlogits, const float* hw, int32_t ep, int32_t c,
                       dgnn_frame dz, void* stream);
+/* Same seeds with the list of vertices that have incident pairs
+ * (`active`, ascending, n_active of them): rows without pairs are
+ * zero-filled by a flat pass and only the active rows are gathered
+ * (bit-identical to dgnn_head_scatter). */
+int dgnn_head_scatter_active(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot, int32_t n_active,
+                             const int32_t* active, const double* dlogits, const float* hw, int32_t ep, int32_t c,
+                             dgnn_frame dz, void* stream);
 
 /* Test accuracy (training.py:189-197): *correct += #pairs whose first-index
  * argmax of the logits equals the label (int64 counter, integer atomics). */

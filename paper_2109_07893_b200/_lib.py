@@ -88,6 +88,7 @@ _SIGS = {
     "dgnn_head_loss_grad": (c_int, [c_int64, P, P, P, Frame, c_int32, c_int32, P, P, c_double, P, c_int32, P, P, P,
                                     P, c_size_t, P]),
     "dgnn_head_scatter": (c_int, [c_int32, P, P, P, P, c_int32, c_int32, Frame, P]),
+    "dgnn_head_scatter_active": (c_int, [c_int32, P, P, c_int32, P, P, P, c_int32, c_int32, Frame, P]),
     "dgnn_head_predict": (c_int, [c_int64, P, P, P, Frame, c_int32, c_int32, P, P, P, P]),
     "dgnn_sum_f64": (c_int, [c_int64, P, P, c_int, P]),
     "dgnn_adam": (c_int, [c_int64, P, P, P, P, c_double, c_double, c_double, c_double, c_double,

@@ -128,32 +128,54 @@ __global__ void head_grad_reduce_kernel(int nchunks, int ep, int C, const double
 }
 
 // dz[x][k] = sum_{slot s of x} sum_c dl[s/2][c] hw[side(s)*ep + k][c]; group of ep/4 lanes per vertex.
-template <int EP, int CC>   // CC: classes (compile time), 0: runtime C <= kMaxClasses
+// lanes per vertex: GL over every vertex, GLA over an active-vertex list
+// (scripts/head_probe.sh)
+#ifndef DGNN_HS_GL
+#define DGNN_HS_GL 8
+#endif
+#ifndef DGNN_HS_GLA
+#define DGNN_HS_GLA 4
+#endif
+template <int EP, int CC, int GL>   // CC: classes (compile time), 0: runtime C <= kMaxClasses
 __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int32_t* __restrict__ ptr,
                                                            const int32_t* __restrict__ slot,
                                                            const double* __restrict__ dl,
-                                                           const float* __restrict__ hw, int C_rt, dgnn_frame dz) {
+                                                           const float* __restrict__ hw, int C_rt, dgnn_frame dz,
+                                                           int32_t nact, const int32_t* __restrict__ act) {
     // dz[x] = sum over x's incident pair endpoints (p, side) of dl[p] . W_side^T
     //       = S_0[x] . W_u^T + S_1[x] . W_v^T,  S_side[x][c] = sum dl[p][c]:
     // 8 lanes per vertex (4 vertices per warp in flight) sum the 2C fp64
     // dlogits over the incidence list, 8 slots at a time, in a fixed
     // butterfly, then form the E outputs -- a hub vertex (heavy-tailed
-    // graphs: tens of thousands of incident pairs) costs 1/8 of a serial
+    // graphs: tens of thousands of incident pairs) costs 1/GL of a serial
     // walk and no vector work per pair.
+    // With `act` (the vertices that have incident pairs, ascending), rows
+    // without any are zero-filled by a flat float4 pass and the lane
+    // groups visit only the active vertices (same arithmetic per row).
     constexpr int CM = CC ? CC : kMaxClasses;
-    constexpr int GL = 8;                           // lanes per vertex
     constexpr int PER = (EP + GL - 1) / GL;         // outputs per lane
     const int C = CC ? CC : C_rt;
     extern __shared__ float hws[];                  // [2*EP][C]
     for (int i = threadIdx.x; i < 2 * EP * C; i += blockDim.x) hws[i] = hw[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, gl = lane & (GL - 1);
+    if (act) {
+        constexpr int Q = EP / 4;
+        const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t i = tid; i < (int64_t)n * Q; i += nth) {
+            const int32_t x = (int32_t)(i / Q);
+            if (ptr[x + 1] == ptr[x])
+                *reinterpret_cast<float4*>(frame_row<float>(dz, x) + 4 * (int)(i % Q)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    const int64_t nv = act ? nact : n;
     const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GL;
     const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / GL;
-    const int64_t iters = (n + ngrp - 1) / ngrp;    // uniform trip count: the shuffles need whole warps
+    const int64_t iters = (nv + ngrp - 1) / ngrp;   // uniform trip count: the shuffles need whole warps
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t x = grp + it * ngrp;
-        const bool ok = x < n;
+        const int64_t xi = grp + it * ngrp;
+        const bool ok = xi < nv;
+        const int64_t x = ok && act ? act[xi] : xi;
         double sacc[2 * CM];
 #pragma unroll
         for (int i = 0; i < 2 * CM; ++i) sacc[i] = 0.0;
@@ -223,20 +245,28 @@ __global__ void grads_gather_kernel(int64_t n, const double* __restrict__ gp, co
 
 template <int EP>
 int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const double* dl, const float* hw, int C,
-                   dgnn_frame dz, cudaStream_t st) {
+                   dgnn_frame dz, cudaStream_t st, int32_t nact = 0, const int32_t* act = nullptr) {
     if (C > kMaxClasses) {
         set_error("head_scatter: %d classes exceed %d", C, kMaxClasses);
         return DGNN_EUNSUPPORTED;
     }
     int64_t blocks = cdiv(n, 32);
-    blocks = blocks < 1 ? 1 : (blocks > 16 * num_sms() ? 16 * num_sms() : blocks);
+#ifndef DGNN_HS_BLK
+#define DGNN_HS_BLK 16
+#endif
+    blocks = blocks < 1 ? 1 : (blocks > DGNN_HS_BLK * num_sms() ? DGNN_HS_BLK * num_sms() : blocks);
     ::dgnn::note_launch();
-    if (C == 2)
-        head_scatter_kernel<EP, 2><<<(unsigned)blocks, 256, (size_t)2 * EP * C * sizeof(float), st>>>(n, ptr, slot,
-                                                                                                   dl, hw, C, dz);
-    else
-        head_scatter_kernel<EP, 0><<<(unsigned)blocks, 256, (size_t)2 * EP * C * sizeof(float), st>>>(n, ptr, slot,
-                                                                                                   dl, hw, C, dz);
+    const size_t sm = (size_t)2 * EP * C * sizeof(float);
+    if (act) {
+        if (C == 2)
+            head_scatter_kernel<EP, 2, DGNN_HS_GLA><<<(unsigned)blocks, 256, sm, st>>>(n, ptr, slot, dl, hw, C, dz, nact, act);
+        else
+            head_scatter_kernel<EP, 0, DGNN_HS_GLA><<<(unsigned)blocks, 256, sm, st>>>(n, ptr, slot, dl, hw, C, dz, nact, act);
+    } else if (C == 2) {
+        head_scatter_kernel<EP, 2, DGNN_HS_GL><<<(unsigned)blocks, 256, sm, st>>>(n, ptr, slot, dl, hw, C, dz, 0, nullptr);
+    } else {
+        head_scatter_kernel<EP, 0, DGNN_HS_GL><<<(unsigned)blocks, 256, sm, st>>>(n, ptr, slot, dl, hw, C, dz, 0, nullptr);
+    }
     return launch_status("head_scatter");
 }
 
@@ -467,6 +497,24 @@ int dgnn_head_loss_grad(int64_t npairs, const int32_t* u, const int32_t* v, cons
         case 128: return head_loss_grad_t<128>(npairs, u, v, y, z, hw, hb, scale, loss_pp, dlogits, ghw, ghb, part, st);
     }
     set_error("head_loss_grad: unsupported width %d", ep);
+    return DGNN_EUNSUPPORTED;
+}
+
+int dgnn_head_scatter_active(int32_t n, const int32_t* inc_ptr, const int32_t* inc_slot, int32_t n_active,
+                             const int32_t* active, const double* dlogits, const float* hw, int32_t ep, int32_t c,
+                             dgnn_frame dz, void* stream) {
+    DGNN_CHECK_ARG(c >= 1 && c <= kMaxClasses, "head_scatter: classes outside [1, 8]");
+    DGNN_CHECK_ARG(n_active >= 0 && (active || n_active == 0), "head_scatter: bad active list");
+    if (n == 0) return DGNN_OK;
+    cudaStream_t st = as_stream(stream);
+    const int32_t* act = active ? active : inc_ptr;   // non-null: zero-fill pass on, n_active = 0 visits nothing
+    switch (ep) {
+        case 16: return head_scatter_t<16>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st, n_active, act);
+        case 32: return head_scatter_t<32>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st, n_active, act);
+        case 64: return head_scatter_t<64>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st, n_active, act);
+        case 128: return head_scatter_t<128>(n, inc_ptr, inc_slot, dlogits, hw, c, dz, st, n_active, act);
+    }
+    set_error("head_scatter: unsupported width %d", ep);
     return DGNN_EUNSUPPORTED;
 }
 

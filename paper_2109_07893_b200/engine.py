@@ -995,8 +995,8 @@ class Rank:
              ptr(eng.params.gw("head.w")), ptr(eng.params.gw("head.b")), ptr(self.ws_head),
              self.ws_head.numel(), st)
         call("dgnn_sum_f64", d["n"], ptr(self.loss_pp), self.loss_t.data_ptr() + 8 * t, 0, st)
-        call("dgnn_head_scatter", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), ptr(self.dlogits), ptr(hw), ep, C,
-             dz, st)
+        call("dgnn_head_scatter_active", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), d["nact"], ptr(d["act"]),
+             ptr(self.dlogits), ptr(hw), ep, C, dz, st)
 
     def _loss_grads(self, b, works):
         eng = self.eng
@@ -1028,8 +1028,8 @@ class Rank:
                 call("dgnn_head_grad", d["n"], ptr(d["u"]), ptr(d["v"]), z, ep, C, ptr(self.dlogits),
                      ptr(eng.params.gw("head.w")), ptr(eng.params.gw("head.b")), ptr(self.ws_head),
                      self.ws_head.numel(), st)
-            call("dgnn_head_scatter", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), ptr(self.dlogits), ptr(hw), ep, C,
-                 dz, st)
+            call("dgnn_head_scatter_active", eng.plan.N, ptr(d["ptr"]), ptr(d["slot"]), d["nact"], ptr(d["act"]),
+                 ptr(self.dlogits), ptr(hw), ep, C, dz, st)
             if works is not None:
                 works += self._scatter_owned_step(self.dZ_own, self.dY_vm, Ly.ho, c)
 

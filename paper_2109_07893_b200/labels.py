@@ -204,5 +204,8 @@ def frame_labels_device(pairs, labels, n: int, num_classes: int, device) -> dict
     order = torch.sort(verts, stable=True).indices
     ptr = torch.zeros(n + 1, dtype=torch.int64, device=p.device)
     ptr[1:] = torch.cumsum(torch.bincount(verts, minlength=n), 0)
+    # vertices with incident pairs (ascending): dgnn_head_scatter_active gathers only these
+    act = torch.nonzero(ptr[1:] != ptr[:-1]).reshape(-1).to(torch.int32)
     return dict(n=r, u=p[:, 0].to(torch.int32).contiguous(), v=p[:, 1].to(torch.int32).contiguous(),
-                y=y.to(torch.int32), ptr=ptr.to(torch.int32), slot=slots[order].to(torch.int32))
+                y=y.to(torch.int32), ptr=ptr.to(torch.int32), slot=slots[order].to(torch.int32), act=act,
+                nact=int(act.numel()))

@@ -660,3 +660,36 @@ def test_pair_lstm_forward_matches_single_cta_bitwise(hp, kx, rows):
         assert torch.equal(a[0], p[0]) and torch.equal(a[1], p[1])
         if keep:
             assert torch.equal(a[2], p[2])
+
+
+@pytest.mark.parametrize("ep,classes,slabs", [(64, 2, 1), (32, 2, 4), (16, 3, 1)])
+def test_head_scatter_active_matches_full_pass(ep, classes, slabs):
+    """dz seeds over the active-vertex list (zero-fill pass + gathers of the
+    vertices with incident pairs) equal the all-vertex pass bit for bit,
+    hub vertices and owner-layout (slabbed) frames included."""
+    from paper_2109_07893_b200 import _lib
+    from paper_2109_07893_b200._lib import call, ptr
+    from paper_2109_07893_b200.labels import frame_labels_device
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(ep + classes)
+    n, npairs = 50_000, 20_000
+    pairs = rng.integers(0, n, (npairs, 2))
+    pairs[:3000, 0] = 7                         # a hub
+    lab = rng.integers(0, classes, npairs)
+    d = frame_labels_device(pairs, lab, n, classes, dev)
+    assert d["nact"] == len(np.unique(pairs))
+    dl = torch.from_numpy(rng.standard_normal((npairs, classes))).to(dev)
+    hw = torch.from_numpy(rng.standard_normal((2 * ep, classes)).astype(np.float32)).to(dev)
+    rps = n // slabs
+    outs = []
+    for active in (False, True):
+        buf = torch.full((slabs * rps * ep + 4 * ep,), float("nan"), device=dev)
+        fr = _lib.Frame(buf.data_ptr(), ep, rps if slabs > 1 else 0, rps * ep if slabs > 1 else 0)
+        if active:
+            call("dgnn_head_scatter_active", n, ptr(d["ptr"]), ptr(d["slot"]), d["nact"], ptr(d["act"]), ptr(dl),
+                 ptr(hw), ep, classes, fr, _lib.stream_handle())
+        else:
+            call("dgnn_head_scatter", n, ptr(d["ptr"]), ptr(d["slot"]), ptr(dl), ptr(hw), ep, classes, fr,
+                 _lib.stream_handle())
+        outs.append(buf[:n * ep].cpu().numpy())
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
