@@ -460,32 +460,112 @@ __device__ __forceinline__ double lap_value(int64_t r, int c, double a, const do
     return transposed ? __dmul_rn(__dmul_rn(a, is[c]), is[r]) : __dmul_rn(__dmul_rn(a, is[r]), is[c]);
 }
 
+// Warp-cooperative count / write of one row of 17..kCtaRow entries (the
+// lanes of the owning warp).  Entries of a row are sorted by column; the
+// identity term of a row without a stored diagonal is inserted before its
+// first column > r.  Output order and values are the per-thread path's.
+__device__ __forceinline__ void lap_count_row_warp(int r, const int32_t* __restrict__ mrp,
+                                                   const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                                                   const double* __restrict__ is, int transposed,
+                                                   int32_t* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    int k = 0;
+    bool diag = false;
+    for (int e0 = mrp[r]; e0 < mrp[r + 1]; e0 += 32) {
+        const int e = e0 + lane;
+        bool nz = false, isd = false;
+        if (e < mrp[r + 1]) {
+            const int c = mcol[e];
+            isd = c == r;
+            nz = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
+        }
+        k += __popc(__ballot_sync(0xffffffffu, nz));
+        diag |= __any_sync(0xffffffffu, isd);
+    }
+    if (lane == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
+}
+
+__device__ __forceinline__ void lap_write_row_warp(int r, const int32_t* __restrict__ mrp,
+                                                   const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                                                   const double* __restrict__ is, int transposed,
+                                                   const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
+                                                   float* __restrict__ o32, double* __restrict__ o64, int64_t cap) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int rb = mrp[r], re = mrp[r + 1];
+    bool has_diag = false;
+    int before = 0, nzb = 0;   // stored entries with column < r, and how many of them are nonzero
+    for (int e0 = rb; e0 < re; e0 += 32) {
+        const int e = e0 + lane;
+        const int c = e < re ? mcol[e] : INT_MAX;
+        has_diag |= __any_sync(0xffffffffu, c == r);
+        before += __popc(__ballot_sync(0xffffffffu, c < r));
+        const bool nzl = c < r && lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
+        nzb += __popc(__ballot_sync(0xffffffffu, nzl));
+    }
+    const double dv = has_diag ? 0.0 : lap_value(r, r, 0.0, is, transposed);
+    const int dshift = (!has_diag && dv != 0.0) ? 1 : 0;
+    int64_t pos = orp[r];
+    for (int e0 = rb; e0 < re; e0 += 32) {
+        const int e = e0 + lane;
+        double v = 0.0;
+        int c = 0;
+        if (e < re) {
+            c = mcol[e];
+            v = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed);
+        }
+        const unsigned nzm = __ballot_sync(0xffffffffu, v != 0.0);
+        const int idx = e - rb;   // entry index within the row
+        const int64_t p = pos + __popc(nzm & lt) + (idx >= before ? dshift : 0);
+        if (v != 0.0 && p < cap) {
+            ocol[p] = c;
+            o32[p] = (float)v;
+            if (o64) o64[p] = v;
+        }
+        pos += __popc(nzm);
+    }
+    if (lane == 0 && dshift) {
+        // position: every nonzero stored entry with column < r precedes it
+        const int64_t p = orp[r] + nzb;
+        if (p < cap) {
+            ocol[p] = r;
+            o32[p] = (float)dv;
+            if (o64) o64[p] = dv;
+        }
+    }
+}
+
+// Thread per row; rows of 17..kCtaRow entries are then taken by their warp
+// together (ballot queue), rows past kCtaRow go to the CTA-per-row kernels.
+// The block size is a multiple of 32 and every lane stays to the end (the
+// warp-cooperative rows need whole warps).
 __global__ void lap_count_kernel(int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
                                  const double* __restrict__ mval, const double* __restrict__ is, int transposed,
                                  int32_t* __restrict__ cnt, int32_t* __restrict__ long_rows,
                                  int32_t* long_count) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r > n) return;
-    if (r == n) { cnt[n] = 0; return; }
-    const int deg = mrp[r + 1] - mrp[r];
-    if (deg > kCtaRow) {
-        long_rows[n - 1 - atomicAdd(long_count + 1, 1)] = (int32_t)r;
-        return;
+    if (r == n) cnt[n] = 0;
+    const bool in = r < n;
+    const int deg = in ? mrp[r + 1] - mrp[r] : 0;
+    if (in && deg > kCtaRow) long_rows[n - 1 - atomicAdd(long_count + 1, 1)] = (int32_t)r;
+    const bool mid = in && deg > kLongRow && deg <= kCtaRow;
+    if (in && deg <= kLongRow) {
+        int k = 0;
+        bool diag = false;
+        for (int e = mrp[r]; e < mrp[r + 1]; ++e) {
+            const int c = mcol[e];
+            const double a = mval ? mval[e] : 1.0;
+            if (c == r) diag = true;
+            k += lap_value(r, c, a, is, transposed) != 0.0;
+        }
+        if (!diag) k += lap_value(r, (int)r, 0.0, is, transposed) != 0.0;
+        cnt[r] = k;
     }
-    if (deg > kLongRow) {
-        long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
-        return;
+    for (unsigned m = __ballot_sync(0xffffffffu, mid); m; m &= m - 1) {
+        const int src = __ffs(m) - 1;
+        const int rr = __shfl_sync(0xffffffffu, (int)r, src);
+        lap_count_row_warp(rr, mrp, mcol, mval, is, transposed, cnt);
     }
-    int k = 0;
-    bool diag = false;
-    for (int e = mrp[r]; e < mrp[r + 1]; ++e) {
-        const int c = mcol[e];
-        const double a = mval ? mval[e] : 1.0;
-        if (c == r) diag = true;
-        k += lap_value(r, c, a, is, transposed) != 0.0;
-    }
-    if (!diag) k += lap_value(r, (int)r, 0.0, is, transposed) != 0.0;
-    cnt[r] = k;
 }
 
 __global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
@@ -493,116 +573,38 @@ __global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, con
                                  const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
                                  float* __restrict__ o32, double* __restrict__ o64, int64_t cap) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    if (mrp[r + 1] - mrp[r] > kLongRow) return;   // lap_write_long_kernel
-    int64_t pos = orp[r];
-    bool diag_done = false;
-    auto emit = [&](int c, double v) {
-        if (v != 0.0 && pos < cap) {
-            ocol[pos] = c;
-            o32[pos] = (float)v;
-            if (o64) o64[pos] = v;
-        }
-        pos += v != 0.0;
-    };
-    for (int e = mrp[r]; e < mrp[r + 1]; ++e) {
-        const int c = mcol[e];
-        const double a = mval ? mval[e] : 1.0;
-        if (!diag_done && c > r) {
-            emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
-            diag_done = true;
-        }
-        if (c == r) diag_done = true;
-        emit(c, lap_value(r, c, a, is, transposed));
-    }
-    if (!diag_done) emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
-}
-
-// Warp-per-row versions for the long rows up to kCtaRow entries.  Entries
-// of a row are sorted by column; the identity term of a row without a stored
-// diagonal is inserted before its first column > r.  Output order and values
-// are the thread kernels' exactly.
-__global__ void lap_count_warp_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
-                                      const double* __restrict__ mval, const double* __restrict__ is,
-                                      int transposed, int32_t* __restrict__ cnt,
-                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int lane = threadIdx.x & 31;
-    const int nl = *long_count;
-    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
-        const int r = long_rows[li];
-        int k = 0;
-        bool diag = false;
-        for (int e0 = mrp[r]; e0 < mrp[r + 1]; e0 += 32) {
-            const int e = e0 + lane;
-            bool nz = false, isd = false;
-            if (e < mrp[r + 1]) {
-                const int c = mcol[e];
-                isd = c == r;
-                nz = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
-            }
-            k += __popc(__ballot_sync(0xffffffffu, nz));
-            diag |= __any_sync(0xffffffffu, isd);
-        }
-        if (lane == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
-    }
-}
-
-__global__ void lap_write_warp_kernel(const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
-                                      const double* __restrict__ mval, const double* __restrict__ is,
-                                      int transposed, const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
-                                      float* __restrict__ o32, double* __restrict__ o64, int64_t cap,
-                                      const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    const int nl = *long_count;
-    for (int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += (gridDim.x * blockDim.x) >> 5) {
-        const int r = long_rows[li];
-        const int rb = mrp[r], re = mrp[r + 1];
-        // insertion of the identity term: before the first column > r when no
-        // column == r is stored (the thread kernel's diag_done logic)
-        bool has_diag = false;
-        int before = 0, nzb = 0;   // stored entries with column < r, and how many of them are nonzero
-        for (int e0 = rb; e0 < re; e0 += 32) {
-            const int e = e0 + lane;
-            const int c = e < re ? mcol[e] : INT_MAX;
-            has_diag |= __any_sync(0xffffffffu, c == r);
-            before += __popc(__ballot_sync(0xffffffffu, c < r));
-            const bool nzl = c < r && lap_value(r, c, mval ? mval[e] : 1.0, is, transposed) != 0.0;
-            nzb += __popc(__ballot_sync(0xffffffffu, nzl));
-        }
-        const double dv = has_diag ? 0.0 : lap_value(r, r, 0.0, is, transposed);
-        const int dshift = (!has_diag && dv != 0.0) ? 1 : 0;
+    const bool in = r < n;
+    const int deg = in ? mrp[r + 1] - mrp[r] : 0;
+    const bool mid = in && deg > kLongRow && deg <= kCtaRow;
+    if (in && deg <= kLongRow) {
         int64_t pos = orp[r];
-        for (int e0 = rb; e0 < re; e0 += 32) {
-            const int e = e0 + lane;
-            double v = 0.0;
-            int c = 0;
-            if (e < re) {
-                c = mcol[e];
-                v = lap_value(r, c, mval ? mval[e] : 1.0, is, transposed);
+        bool diag_done = false;
+        auto emit = [&](int c, double v) {
+            if (v != 0.0 && pos < cap) {
+                ocol[pos] = c;
+                o32[pos] = (float)v;
+                if (o64) o64[pos] = v;
             }
-            const unsigned nzm = __ballot_sync(0xffffffffu, v != 0.0);
-            const int idx = e - rb;   // entry index within the row
-            const int64_t p = pos + __popc(nzm & lt) + (idx >= before ? dshift : 0);
-            if (v != 0.0 && p < cap) {
-                ocol[p] = c;
-                o32[p] = (float)v;
-                if (o64) o64[p] = v;
+            pos += v != 0.0;
+        };
+        for (int e = mrp[r]; e < mrp[r + 1]; ++e) {
+            const int c = mcol[e];
+            const double a = mval ? mval[e] : 1.0;
+            if (!diag_done && c > r) {
+                emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
+                diag_done = true;
             }
-            pos += __popc(nzm);
+            if (c == r) diag_done = true;
+            emit(c, lap_value(r, c, a, is, transposed));
         }
-        if (lane == 0 && dshift) {
-            // position: every nonzero stored entry with column < r precedes it
-            const int64_t p = orp[r] + nzb;
-            if (p < cap) {
-                ocol[p] = r;
-                o32[p] = (float)dv;
-                if (o64) o64[p] = dv;
-            }
-        }
+        if (!diag_done) emit((int)r, lap_value(r, (int)r, 0.0, is, transposed));
+    }
+    for (unsigned m = __ballot_sync(0xffffffffu, mid); m; m &= m - 1) {
+        const int src = __ffs(m) - 1;
+        const int rr = __shfl_sync(0xffffffffu, (int)r, src);
+        lap_write_row_warp(rr, mrp, mcol, mval, is, transposed, orp, ocol, o32, o64, cap);
     }
 }
-
 
 // CTA-per-row versions for the rows past kCtaRow entries (the largest hubs
 // of heavy-tailed graphs; a warp per row made the largest hub a serial tail
@@ -946,9 +948,6 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
                                         long_count);
     ::dgnn::note_launch();
-    lap_count_warp_kernel<<<num_sms(), 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
-                                                long_count);
-    ::dgnn::note_launch();
     lap_count_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed,
                                                                      out_rowptr, long_rows, long_count);
     int rc = exclusive_scan_i32(out_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
@@ -956,9 +955,6 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     ::dgnn::note_launch();
     lap_write_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
                                         out_val32, out_val64, out_cap);
-    ::dgnn::note_launch();
-    lap_write_warp_kernel<<<num_sms(), 256, 0, st>>>(m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
-                                                out_val32, out_val64, out_cap, long_rows, long_count);
     ::dgnn::note_launch();
     lap_write_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(
         n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col, out_val32, out_val64, out_cap, long_rows,
