@@ -152,49 +152,6 @@ static int rowptr_launch(int32_t n, int64_t nnz, const int32_t* rows, int32_t* r
 // (rows longer than kMergeLong: a warp each, delta_merge_long_kernel)
 constexpr int kMergeLong = 16;
 
-__global__ void delta_count_kernel(int32_t n, const int32_t* __restrict__ orp,
-                                   const int32_t* __restrict__ drp, const int32_t* __restrict__ irp,
-                                   int32_t* __restrict__ nrp) {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r > n) return;
-    if (r == n) { nrp[n] = 0; return; }
-    nrp[r] = (orp[r + 1] - orp[r]) - (drp[r + 1] - drp[r]) + (irp[r + 1] - irp[r]);
-}
-
-__global__ void delta_merge_kernel(int32_t n, const int32_t* __restrict__ orp,
-                                   const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
-                                   const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
-                                   const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
-                                   int32_t* __restrict__ ncol, int64_t cap, int32_t* status,
-                                   int32_t* __restrict__ long_rows, int32_t* long_count) {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    if ((orp[r + 1] - orp[r]) + (irp[r + 1] - irp[r]) > kMergeLong) {   // delta_merge_long_kernel
-        long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
-        return;
-    }
-    int di = drp[r];
-    const int de = drp[r + 1];
-    int ii = irp[r];
-    const int ie = irp[r + 1];
-    int64_t pos = nrp[r];
-    const int64_t end = min((int64_t)nrp[r + 1], cap);
-    int bad = 0;
-    for (int o = orp[r], oe = orp[r + 1]; o < oe; ++o) {
-        const int c = ocol[o];
-        while (di < de && dcol[di] < c) { ++bad; ++di; }       // deletion of an absent entry
-        if (di < de && dcol[di] == c) { ++di; continue; }       // deleted
-        while (ii < ie && icol[ii] < c) { if (pos < end) ncol[pos] = icol[ii]; ++pos; ++ii; }
-        if (ii < ie && icol[ii] == c) { ++bad; ++ii; }         // insertion overlaps the common set
-        if (pos < end) ncol[pos] = c;
-        ++pos;
-    }
-    bad += de - di;
-    while (ii < ie) { if (pos < end) ncol[pos] = icol[ii]; ++pos; ++ii; }
-    if (pos != (int64_t)nrp[r + 1]) ++bad;
-    if (bad) atomicAdd(status, bad);
-}
-
 __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int key) {
     int lo = 0, hi = n;
     while (lo < hi) {
@@ -205,52 +162,121 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int key)
     return lo;
 }
 
-// Long rows (hubs): one CTA per row (a warp per row left a ~8000-entry hub
-// as a 250-step serial tail), every entry placed independently by
-// binary search -- an old entry c lands at (#old before it) - (#deletes < c)
-// + (#inserts < c), an insert at (#old < c) - (#deletes < c) + its index.
-// Same output as the two-pointer merge for a consistent delta; the same
-// inconsistencies (deleting an absent entry, inserting a present one) are
-// counted into `status`.
+__global__ void delta_count_kernel(int32_t n, const int32_t* __restrict__ orp,
+                                   const int32_t* __restrict__ drp, const int32_t* __restrict__ irp,
+                                   int32_t* __restrict__ nrp) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) { nrp[n] = 0; return; }
+    nrp[r] = (orp[r + 1] - orp[r]) - (drp[r + 1] - drp[r]) + (irp[r + 1] - irp[r]);
+}
+
+__device__ __forceinline__ int merge_row_split(int r, int tid, int nt, const int32_t* __restrict__ orp,
+                                               const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
+                                               const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
+                                               const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
+                                               int32_t* __restrict__ ncol, int64_t cap);
+constexpr int kMergeCtaRow = 512;   // = kMergeCta (defined with the hub kernel below)
+
+// Thread per row (two-pointer merge); rows of kMergeLong+1..512 entries are
+// then merged by their warp together (ballot queue), longer ones go to the
+// CTA-per-row kernel.  Every lane stays to the end (whole-warp ballots).
+__global__ void delta_merge_kernel(int32_t n, const int32_t* __restrict__ orp,
+                                   const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
+                                   const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
+                                   const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
+                                   int32_t* __restrict__ ncol, int64_t cap, int32_t* status,
+                                   int32_t* __restrict__ long_rows, int32_t* long_count) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool in = r < n;
+    const int len = in ? (orp[r + 1] - orp[r]) + (irp[r + 1] - irp[r]) : 0;
+    if (in && len > kMergeCtaRow) long_rows[atomicAdd(long_count, 1)] = (int32_t)r;   // delta_merge_long_kernel
+    const bool mid = in && len > kMergeLong && len <= kMergeCtaRow;
+    int bad = 0;
+    if (in && len <= kMergeLong) {
+        int di = drp[r];
+        const int de = drp[r + 1];
+        int ii = irp[r];
+        const int ie = irp[r + 1];
+        int64_t pos = nrp[r];
+        const int64_t end = min((int64_t)nrp[r + 1], cap);
+        for (int o = orp[r], oe = orp[r + 1]; o < oe; ++o) {
+            const int c = ocol[o];
+            while (di < de && dcol[di] < c) { ++bad; ++di; }       // deletion of an absent entry
+            if (di < de && dcol[di] == c) { ++di; continue; }       // deleted
+            while (ii < ie && icol[ii] < c) { if (pos < end) ncol[pos] = icol[ii]; ++pos; ++ii; }
+            if (ii < ie && icol[ii] == c) { ++bad; ++ii; }         // insertion overlaps the common set
+            if (pos < end) ncol[pos] = c;
+            ++pos;
+        }
+        bad += de - di;
+        while (ii < ie) { if (pos < end) ncol[pos] = icol[ii]; ++pos; ++ii; }
+        if (pos != (int64_t)nrp[r + 1]) ++bad;
+    }
+    const int lane = threadIdx.x & 31;
+    for (unsigned m = __ballot_sync(0xffffffffu, mid); m; m &= m - 1) {
+        const int rr = __shfl_sync(0xffffffffu, (int)r, __ffs(m) - 1);
+        bad += merge_row_split(rr, lane, 32, orp, ocol, drp, dcol, irp, icol, nrp, ncol, cap);
+    }
+    if (bad) atomicAdd(status, bad);
+}
+
+// Long rows: every entry placed independently by binary search -- an old
+// entry c lands at (#old before it) - (#deletes < c) + (#inserts < c), an
+// insert at (#old < c) - (#deletes < c) + its index.  Same output as the
+// two-pointer merge for a consistent delta; the same inconsistencies
+// (deleting an absent entry, inserting a present one) are counted into
+// `status`.  Rows of 17..kMergeCta entries: the owning warp of the
+// per-row kernel (tid = lane, nt = 32); hubs past kMergeCta: a CTA each (a
+// warp per row left a ~8000-entry hub as a 250-step serial tail).
 constexpr int kLongThreads = 256;   // CTA size of every hub-row kernel
 constexpr int kLongCTAs = 4;        // CTAs per SM of every hub-row kernel
+constexpr int kMergeCta = 512;
+
+__device__ __forceinline__ int merge_row_split(int r, int tid, int nt, const int32_t* __restrict__ orp,
+                                               const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
+                                               const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
+                                               const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
+                                               int32_t* __restrict__ ncol, int64_t cap) {
+    const int o0 = orp[r], no = orp[r + 1] - o0;
+    const int d0 = drp[r], nd = drp[r + 1] - d0;
+    const int i0 = irp[r], ni = irp[r + 1] - i0;
+    const int64_t base = nrp[r], end = min((int64_t)nrp[r + 1], cap);
+    int bad = 0;
+    for (int k = tid; k < no; k += nt) {
+        const int c = ocol[o0 + k];
+        const int kd = lower_bound_i32(dcol + d0, nd, c);
+        if (kd < nd && dcol[d0 + kd] == c) continue;            // deleted
+        const int ki = lower_bound_i32(icol + i0, ni, c);
+        if (ki < ni && icol[i0 + ki] == c) ++bad;               // insertion overlaps the common set
+        const int64_t p = base + k - kd + ki;
+        if (p < end) ncol[p] = c;
+    }
+    for (int k = tid; k < ni; k += nt) {
+        const int c = icol[i0 + k];
+        const int ko = lower_bound_i32(ocol + o0, no, c);
+        const int kd = lower_bound_i32(dcol + d0, nd, c);
+        const int64_t p = base + ko - kd + k;
+        if (p < end) ncol[p] = c;
+    }
+    for (int k = tid; k < nd; k += nt) {                        // deletions must exist
+        const int c = dcol[d0 + k];
+        const int ko = lower_bound_i32(ocol + o0, no, c);
+        if (!(ko < no && ocol[o0 + ko] == c)) ++bad;
+    }
+    if (tid == 0 && (int64_t)no - nd + ni != (int64_t)nrp[r + 1] - base) ++bad;
+    return bad;
+}
 
 __global__ void __launch_bounds__(kLongThreads) delta_merge_long_kernel(
         const int32_t* __restrict__ orp, const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
         const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
         const int32_t* __restrict__ nrp, int32_t* __restrict__ ncol, int64_t cap, int32_t* status,
         const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int tid = threadIdx.x, nt = blockDim.x;
     const int nl = *long_count;
     for (int li = blockIdx.x; li < nl; li += gridDim.x) {
-        const int r = long_rows[li];
-        const int o0 = orp[r], no = orp[r + 1] - o0;
-        const int d0 = drp[r], nd = drp[r + 1] - d0;
-        const int i0 = irp[r], ni = irp[r + 1] - i0;
-        const int64_t base = nrp[r], end = min((int64_t)nrp[r + 1], cap);
-        int bad = 0;
-        for (int k = tid; k < no; k += nt) {
-            const int c = ocol[o0 + k];
-            const int kd = lower_bound_i32(dcol + d0, nd, c);
-            if (kd < nd && dcol[d0 + kd] == c) continue;            // deleted
-            const int ki = lower_bound_i32(icol + i0, ni, c);
-            if (ki < ni && icol[i0 + ki] == c) ++bad;               // insertion overlaps the common set
-            const int64_t p = base + k - kd + ki;
-            if (p < end) ncol[p] = c;
-        }
-        for (int k = tid; k < ni; k += nt) {
-            const int c = icol[i0 + k];
-            const int ko = lower_bound_i32(ocol + o0, no, c);
-            const int kd = lower_bound_i32(dcol + d0, nd, c);
-            const int64_t p = base + ko - kd + k;
-            if (p < end) ncol[p] = c;
-        }
-        for (int k = tid; k < nd; k += nt) {                        // deletions must exist
-            const int c = dcol[d0 + k];
-            const int ko = lower_bound_i32(ocol + o0, no, c);
-            if (!(ko < no && ocol[o0 + ko] == c)) ++bad;
-        }
-        if (tid == 0 && (int64_t)no - nd + ni != (int64_t)nrp[r + 1] - base) ++bad;
+        const int bad = merge_row_split(long_rows[li], threadIdx.x, blockDim.x, orp, ocol, drp, dcol, irp, icol, nrp,
+                                        ncol, cap);
         if (bad) atomicAdd(status, bad);
     }
 }
@@ -278,16 +304,30 @@ __global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ 
                                          const int32_t* __restrict__ col, const double* __restrict__ val,
                                          int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval,
                                          int32_t* __restrict__ long_rows, int32_t* long_count) {
+    // thread per row; rows of kLongRow+1..kCtaRow entries are scattered by
+    // their warp together (ballot queue), longer ones by a CTA each
+    // (transpose_scatter_long_kernel).  The order inside a column is fixed
+    // by the segment sort that follows.
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    if (rp[r + 1] - rp[r] > kLongRow) {
-        long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
-        return;
+    const bool in = r < n;
+    const int len = in ? rp[r + 1] - rp[r] : 0;
+    if (in && len > kCtaRow) long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
+    const bool mid = in && len > kLongRow && len <= kCtaRow;
+    if (in && len <= kLongRow) {
+        for (int e = rp[r]; e < rp[r + 1]; ++e) {
+            const int pos = atomicAdd(&cursor[col[e]], 1);
+            tcol[pos] = (int32_t)r;
+            if (val) tval[pos] = val[e];
+        }
     }
-    for (int e = rp[r]; e < rp[r + 1]; ++e) {
-        const int pos = atomicAdd(&cursor[col[e]], 1);
-        tcol[pos] = (int32_t)r;
-        if (val) tval[pos] = val[e];
+    const int lane = threadIdx.x & 31;
+    for (unsigned m = __ballot_sync(0xffffffffu, mid); m; m &= m - 1) {
+        const int rr = __shfl_sync(0xffffffffu, (int)r, __ffs(m) - 1);
+        for (int e = rp[rr] + lane; e < rp[rr + 1]; e += 32) {
+            const int pos = atomicAdd(&cursor[col[e]], 1);
+            tcol[pos] = rr;
+            if (val) tval[pos] = val[e];
+        }
     }
 }
 
@@ -309,7 +349,7 @@ __global__ void __launch_bounds__(kLongThreads) transpose_scatter_long_kernel(
 constexpr int kSmallSeg = 32;
 constexpr int kRankMax = 1024;       // mid segments: rank sort of a shared-memory copy
 
-// Short segments: one thread sorts its column in registers/local memory.
+// Short segments: one thread sorts its column.
 __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp,
                                       const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
                                       int32_t* __restrict__ dst_col, double* __restrict__ dst_val,
@@ -323,17 +363,14 @@ __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp
         else long_list[atomicAdd(long_count, 1)] = (int32_t)c;
         return;
     }
-    int key[kSmallSeg];
-    int idx[kSmallSeg];
+    // each entry goes to its rank (keys are distinct rows: the sorted
+    // order); the re-reads hit L1 -- no local-memory arrays
     for (int i = 0; i < d; ++i) {
-        int k = src_col[b + i], j = i;
-        while (j > 0 && key[j - 1] > k) { key[j] = key[j - 1]; idx[j] = idx[j - 1]; --j; }
-        key[j] = k;
-        idx[j] = b + i;
-    }
-    for (int i = 0; i < d; ++i) {
-        dst_col[b + i] = key[i];
-        if (dst_val) dst_val[b + i] = src_val[idx[i]];
+        const int k = src_col[b + i];
+        int rank = 0;
+        for (int j = 0; j < d; ++j) rank += src_col[b + j] < k;
+        dst_col[b + rank] = k;
+        if (dst_val) dst_val[b + rank] = src_val[b + i];
     }
 }
 
