@@ -32,6 +32,7 @@ from . import _lib
 from ._lib import call, frame, ptr
 from .errors import ConfigError, ProtocolError
 from .labels import frame_labels_device
+from .materialize import GRAPH_PRIORITY
 from .materialize import Materializer, SnapshotEncoding
 from .params import DeviceParams, ParamLayout
 
@@ -1311,7 +1312,7 @@ class Engine:
         self.keep_graphs = KEEP_GRAPHS == "1"    # final decision after the rank buffers are placed
         # emulated ranks share one graph stream: a chunk head is rebuilt from
         # the previous rank's last raw snapshot in place, in stream order
-        self.shared_graph_stream = (torch.cuda.Stream(device=dev, priority=-1)
+        self.shared_graph_stream = (torch.cuda.Stream(device=dev, priority=GRAPH_PRIORITY)
                                     if (not self.fabric.distributed and workers > 1) else None)
         self.head_chain_on = HEAD_CHAIN != "0"
         self.head_chain = None

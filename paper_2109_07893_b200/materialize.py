@@ -27,12 +27,18 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
 from . import _lib
 from ._lib import call, ptr, query
 from .errors import CorruptDeltaError, InputError
+
+# priority of the graph-rebuild stream (-1: ahead of the compute stream's
+# kernels when both have work queued)
+GRAPH_PRIORITY = int(os.environ.get("DGNN_GRAPH_PRIORITY", "-1"))
 
 
 def _lap_keys(n: int, rows: np.ndarray, cols: np.ndarray, vals: np.ndarray | None) -> np.ndarray:
@@ -296,7 +302,7 @@ class Materializer:
         # a graph-bound pass (large value-carrying graphs) is not starved by
         # the compute stream's persistent kernels
         self.graph_stream = graph_stream if graph_stream is not None else \
-            torch.cuda.Stream(device=self.device, priority=-1)
+            torch.cuda.Stream(device=self.device, priority=GRAPH_PRIORITY)
         # encoded input on device: everything (resident) or a chunk-sized staging area
         if resident:
             self.full_dev = enc.full.to(self.device)
