@@ -77,6 +77,12 @@ SKIP_LAST_FORWARD = os.environ.get("DGNN_SKIP_LAST_FORWARD", "1") == "1"
 TM_HALO = os.environ.get("DGNN_TM_HALO", "1")
 # LSTM block weight gradient: dz staged in shared memory ("tc") or in TMEM ("ts")
 DW_KERNEL = "dgnn_lstm_weight_grad_" + os.environ.get("DGNN_DW_KERNEL", "tc")
+# keep_graphs mode: slot sets block 0 rotates through ("auto": 3 when they
+# fit, else 2)
+BLOCK0_SETS = os.environ.get("DGNN_BLOCK0_SETS", "auto")
+# diagnostic only (never in a measured line): keep the first epoch's graph
+# snapshots and skip every later rebuild, to measure the compute-only epoch
+DIAG_STATIC_GRAPH = os.environ.get("DGNN_DIAG_STATIC_GRAPH", "0") == "1"
 # the block weight gradient runs on a side stream, overlapping the rest of
 # the block's backward (it only feeds the gradient all-reduce); "0" in order
 DW_OVERLAP = os.environ.get("DGNN_DW_OVERLAP", "1") == "1"
@@ -135,7 +141,11 @@ class Rank:
                                 graph_stream=eng.shared_graph_stream)
         self.prefetched = {}     # block -> (slots, ready event) rebuilt ahead of its pass (two-set mode)
         self.set_turn = 0
-        self.built = {}          # block -> (slots, ready event, epoch tag) (keep_graphs mode)
+        self.built = {}          # block -> (slots, ready event, epoch tag, slot set) (keep_graphs mode)
+        self.block0_sets = 2     # slot sets block 0 rotates through across epochs (keep_graphs mode)
+        self.calls = 0           # begin_block calls so far
+        self.release_log = {}    # call -> event recorded at its start (all earlier work done)
+        self.set_last_use = {}   # slot set -> the begin_block call that last used it
         self.skip = eng.skip
         self.evolve = eng.evolve
         L = len(layers)
@@ -350,11 +360,15 @@ class Rank:
         released = torch.cuda.Event()
         released.record(torch.cuda.current_stream(self.dev))
         self.released = released
+        self.calls += 1
+        self.release_log[self.calls] = released
+        self.release_log.pop(self.calls - 64, None)
         if self.keep_graphs:
             ent = self.built.get(b)
-            if ent is None or (fresh and ent[2] != self.eng.epoch_id):
+            if ent is None or (fresh and ent[2] != self.eng.epoch_id and not DIAG_STATIC_GRAPH):
                 ent = self._build(b, self.eng.epoch_id, released, chained=not keep, count_bytes=count_bytes)
             self.slots, self.ready_ev = ent[0], ent[1]
+            self.set_last_use[ent[3]] = self.calls
             self.mat.account(self.ts, ledger, count_bytes)
         elif b in self.prefetched:
             self.slots, self.ready_ev = self.prefetched.pop(b)
@@ -395,8 +409,9 @@ class Rank:
             else:
                 self.w_in = self.wstate
 
-    def enable_keep_graphs(self):
-        self.mat.add_sets(self.eng.plan.nblk + 1 - len(self.mat.sets))
+    def enable_keep_graphs(self, block0_sets=2):
+        self.block0_sets = block0_sets
+        self.mat.add_sets(self.eng.plan.nblk + block0_sets - 1 - len(self.mat.sets))
         self.keep_graphs = True
 
     def prefetch(self, b, next_epoch=False, count_bytes=True):
@@ -407,6 +422,8 @@ class Rank:
         and each head can be rebuilt from its predecessor's last snapshot."""
         if not self.keep_graphs or b >= self.eng.plan.nblk:
             return
+        if DIAG_STATIC_GRAPH and b in self.built:
+            return
         tag = self.eng.epoch_id + (1 if next_epoch else 0)
         ent = self.built.get(b)
         if ent is not None and ent[2] == tag:
@@ -416,14 +433,20 @@ class Rank:
     def _build(self, b, tag, after, chained, count_bytes):
         plan = self.eng.plan
         ts = plan.steps_of(self.q, b)
-        # block 0 alternates between two sets across epochs: the next epoch's
-        # block 0 is rebuilt while this epoch's last rerun still reads it
-        set_idx = plan.nblk if (b == 0 and tag % 2) else b
+        # block 0 rotates through block0_sets sets across epochs: the next
+        # epoch's block 0 is rebuilt while this epoch's last rerun still reads
+        # it; with 3 sets the rebuild may start as soon as the epoch before
+        # last is done with its set (a whole epoch more to overlap with)
+        k = tag % self.block0_sets
+        set_idx = (0 if k == 0 else plan.nblk + k - 1) if b == 0 else b
+        u = self.set_last_use.get(set_idx)
+        if u is not None and u < self.calls and (u + 1) in self.release_log:
+            after = self.release_log[u + 1]      # the set's last user is done once the next block began
         handoff = self._handoff(ts) if chained else None
         slots = self.mat.materialize(ts, ledger=None, count_bytes=count_bytes, set_idx=set_idx, after=after,
                                      head_prev=self._neighbor_head(ts[0]) if chained else None, consume=False,
                                      handoff=handoff)
-        ent = (slots, self.mat.ready, tag)
+        ent = (slots, self.mat.ready, tag, set_idx)
         self.built[b] = ent
         return ent
 
@@ -1331,7 +1354,7 @@ class Engine:
         self.keep_graphs = self._plan_keep_graphs(dev)
         if self.keep_graphs:
             for r in self.ranks:
-                r.enable_keep_graphs()
+                r.enable_keep_graphs(self.block0_sets)
         # chunk heads across ranks: with keep_graphs every build runs in a
         # block-ascending chain (forward sweeps, next epoch's block 0), so a
         # chunk's last snapshot may also feed rank 0 of the next block; in
@@ -1356,11 +1379,16 @@ class Engine:
         part 3, fix 3) when the extra slot sets fit beside the rank buffers
         already placed, leaving 20% of HBM for labels, workspaces and the
         allocator."""
+        self.block0_sets = 2
         if KEEP_GRAPHS in ("0", "1"):
             return KEEP_GRAPHS == "1"
         plan = self.plan
-        need = len(self.ranks) * (plan.nblk + 1 - 2) * plan.chunk * Materializer.slot_bytes(self.enc)
         free, total = torch.cuda.mem_get_info(dev)
+        per_set = len(self.ranks) * plan.chunk * Materializer.slot_bytes(self.enc)
+        # a third set for block 0 when it fits too (the next epoch's rebuild
+        # then overlaps two epochs of compute)
+        self.block0_sets = 3 if (BLOCK0_SETS != "2" and (plan.nblk + 1) * per_set <= free - 0.2 * total) else 2
+        need = (plan.nblk + self.block0_sets - 1 - 2) * per_set
         return need <= free - 0.2 * total
 
     # ------------------------------------------------------------------ setup
