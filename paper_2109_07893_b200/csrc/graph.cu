@@ -52,16 +52,27 @@ int launch_status(const char* what) {
 const char* last_error() { return g_err; }
 
 // ---------------------------------------------------------------------------
-// device-wide exclusive scan of int32 (tile = 1024 threads x 4 items)
+// device-wide exclusive scan of int32 in one pass (tile = 1024 threads x 4
+// items): decoupled look-back -- each tile publishes its aggregate, then its
+// inclusive prefix once the predecessors' are known, in one 64-bit status
+// word per tile (flag << 32 | value); tiles take their index from a ticket
+// counter, so a tile only ever waits for tiles already running.  One memset
+// + one kernel instead of the tile / add kernels of a recursive scan.
 
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;
 constexpr int64_t kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kScanAgg = 1ull << 32, kScanIncl = 2ull << 32;
 
-__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(int32_t* d, int64_t n,
-                                                                  int32_t* sums) {
+__global__ void __launch_bounds__(kScanThreads) scan_lookback_kernel(int32_t* d, int64_t n,
+                                                                     unsigned long long* status,
+                                                                     unsigned int* ticket) {
     __shared__ int warp_tot[32];
-    const int64_t base = blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    __shared__ int s_tile, s_prefix;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
     int v[kScanItems];
     int s = 0;
 #pragma unroll
@@ -77,33 +88,52 @@ __global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(int32_t* d, in
         int x = warp_tot[lane];
         x = warp_inclusive_scan(x);
         warp_tot[lane] = x;
+        const int agg = __shfl_sync(0xffffffffu, x, 31);
+        // publish the aggregate, then look back (32 predecessors at a time)
+        if (lane == 0)
+            atomicExch(status + tile, (tile == 0 ? kScanIncl : kScanAgg) | (unsigned int)agg);
+        int prefix = 0;
+        if (tile > 0) {
+            int j = tile - 1;
+            for (;;) {
+                const int k = j - lane;
+                unsigned long long w = 0;
+                if (k >= 0) {
+                    do {
+                        w = atomicAdd(status + k, 0ull);
+                    } while ((w >> 32) == 0);
+                } else {
+                    w = kScanIncl;           // before tile 0: an inclusive zero
+                }
+                const unsigned done = __ballot_sync(0xffffffffu, (w >> 32) == 2);
+                // nearest predecessor with its inclusive prefix (none: all 32 aggregates count)
+                const int stop = done ? __ffs(done) - 1 : 31;
+                const int val = (lane <= stop) ? (int)(unsigned int)w : 0;
+                int sum = val;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                prefix += sum;
+                if (done) break;
+                j -= 32;
+            }
+            if (lane == 0) atomicExch(status + tile, kScanIncl | (unsigned int)(prefix + agg));
+        }
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
-    int run = incl - s + (wid > 0 ? warp_tot[wid - 1] : 0);
+    int run = incl - s + (wid > 0 ? warp_tot[wid - 1] : 0) + s_prefix;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         if (base + i < n) d[base + i] = run;
         run += v[i];
     }
-    if (threadIdx.x == kScanThreads - 1) sums[blockIdx.x] = run;
-}
-
-__global__ void scan_add_kernel(int32_t* d, int64_t n, const int32_t* sums) {
-    const int32_t add = sums[blockIdx.x];
-    const int64_t base = blockIdx.x * kScanTile;
-    for (int64_t i = base + threadIdx.x; i < base + kScanTile && i < n; i += blockDim.x) d[i] += add;
 }
 
 static int64_t round64(int64_t x) { return (x + 63) / 64 * 64; }
 
 size_t scan_workspace_bytes(int64_t n) {
-    int64_t total = 0;
-    do {
-        const int64_t nb = cdiv(n, kScanTile);
-        total += round64(nb);
-        n = nb;
-    } while (n > 1);
-    return (size_t)total * sizeof(int32_t) + 256;
+    const int64_t nb = cdiv(n, kScanTile);
+    return (size_t)round64(nb + 1) * sizeof(unsigned long long) + 256;
 }
 
 int exclusive_scan_i32(int32_t* d, int64_t n, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -113,16 +143,11 @@ int exclusive_scan_i32(int32_t* d, int64_t n, void* ws, size_t ws_bytes, cudaStr
         return DGNN_EWORKSPACE;
     }
     const int64_t nb = cdiv(n, kScanTile);
-    int32_t* sums = reinterpret_cast<int32_t*>(ws);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(ws);
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(status + nb);
+    cudaMemsetAsync(status, 0, (size_t)(nb + 1) * sizeof(unsigned long long), st);
     ::dgnn::note_launch();
-    scan_tiles_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(d, n, sums);
-    if (nb > 1) {
-        const int64_t used = round64(nb) * (int64_t)sizeof(int32_t);
-        int rc = exclusive_scan_i32(sums, nb, reinterpret_cast<char*>(ws) + used, ws_bytes - used, st);
-        if (rc) return rc;
-        ::dgnn::note_launch();
-        scan_add_kernel<<<(unsigned)nb, 256, 0, st>>>(d, n, sums);
-    }
+    scan_lookback_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(d, n, status, ticket);
     return launch_status("exclusive_scan_i32");
 }
 

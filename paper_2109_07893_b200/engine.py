@@ -1387,7 +1387,8 @@ class Engine:
         per_set = len(self.ranks) * plan.chunk * Materializer.slot_bytes(self.enc)
         # a third set for block 0 when it fits too (the next epoch's rebuild
         # then overlaps two epochs of compute)
-        self.block0_sets = 3 if (BLOCK0_SETS != "2" and (plan.nblk + 1) * per_set <= free - 0.2 * total) else 2
+        want = 3 if BLOCK0_SETS == "auto" else int(BLOCK0_SETS)
+        self.block0_sets = want if (plan.nblk + want - 2) * per_set <= free - 0.2 * total else 2
         need = (plan.nblk + self.block0_sets - 1 - 2) * per_set
         return need <= free - 0.2 * total
 
