@@ -166,9 +166,24 @@ __global__ void rowptr_kernel(int32_t n, int64_t nnz, const int32_t* __restrict_
     rowptr[r] = (int32_t)lo;
 }
 
+// entry-parallel form: entry e writes rowptr[r] = e for the rows r in
+// (rows[e-1], rows[e]] (e = nnz: up to n) -- one load per thread instead of
+// a binary search; for dense enough rows (average gap <= 32)
+__global__ void rowptr_scatter_kernel(int32_t n, int64_t nnz, const int32_t* __restrict__ rows,
+                                      int32_t* __restrict__ rowptr) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e > nnz) return;
+    const int lo = e == 0 ? 0 : rows[e - 1] + 1;
+    const int hi = e == nnz ? n : rows[e];
+    for (int r = lo; r <= hi; ++r) rowptr[r] = (int32_t)e;
+}
+
 static int rowptr_launch(int32_t n, int64_t nnz, const int32_t* rows, int32_t* rowptr, cudaStream_t st) {
     ::dgnn::note_launch();
-    rowptr_kernel<<<(unsigned)cdiv((int64_t)n + 1, 256), 256, 0, st>>>(n, nnz, rows, rowptr);
+    if (nnz > 0 && nnz * 32 >= (int64_t)n)
+        rowptr_scatter_kernel<<<(unsigned)cdiv(nnz + 1, 256), 256, 0, st>>>(n, nnz, rows, rowptr);
+    else
+        rowptr_kernel<<<(unsigned)cdiv((int64_t)n + 1, 256), 256, 0, st>>>(n, nnz, rows, rowptr);
     return launch_status("rowptr_from_sorted_rows");
 }
 
