@@ -616,15 +616,49 @@ __device__ __forceinline__ void lap_write_row_warp(int r, const int32_t* __restr
 // together (ballot queue), rows past kCtaRow go to the CTA-per-row kernels.
 // The block size is a multiple of 32 and every lane stays to the end (the
 // warp-cooperative rows need whole warps).
-__global__ void lap_count_kernel(int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
-                                 const double* __restrict__ mval, const double* __restrict__ is, int transposed,
-                                 int32_t* __restrict__ cnt, int32_t* __restrict__ long_rows,
-                                 int32_t* long_count) {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__device__ __forceinline__ void lap_count_row_cta(int r, const int32_t* __restrict__ mrp,
+                                                  const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                                                  const double* __restrict__ is, int transposed,
+                                                  int32_t* __restrict__ cnt);
+__device__ __forceinline__ void lap_write_row_cta(int r, const int32_t* __restrict__ mrp,
+                                                  const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                                                  const double* __restrict__ is, int transposed,
+                                                  const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
+                                                  float* __restrict__ o32, double* __restrict__ o64, int64_t cap);
+
+// The first `hubs` blocks take the rows past kCtaRow entries, a CTA per row:
+// block h scans its slice of rows for them (so the hub rows run alongside
+// the per-row blocks, in the same launch, with no device list).
+template <class F>
+__device__ __forceinline__ void for_hub_rows(int32_t n, const int32_t* __restrict__ mrp, int hubs, F f) {
+    __shared__ int s_list[kLongThreads];
+    __shared__ int s_n;
+    const int64_t per = cdiv((int64_t)n, (int64_t)hubs);
+    const int64_t r0 = blockIdx.x * per, r1 = min((int64_t)n, r0 + per);
+    for (int64_t w0 = r0; w0 < r1; w0 += blockDim.x) {
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const int64_t r = w0 + threadIdx.x;
+        if (r < r1 && mrp[r + 1] - mrp[r] > kCtaRow) s_list[atomicAdd(&s_n, 1)] = (int)r;
+        __syncthreads();
+        const int m = s_n;
+        for (int i = 0; i < m; ++i) f(s_list[i]);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kLongThreads) lap_count_kernel(
+        int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+        const double* __restrict__ mval, const double* __restrict__ is, int transposed,
+        int32_t* __restrict__ cnt, int hubs) {
+    if ((int)blockIdx.x < hubs) {
+        for_hub_rows(n, mrp, hubs, [&](int r) { lap_count_row_cta(r, mrp, mcol, mval, is, transposed, cnt); });
+        return;
+    }
+    const int64_t r = (blockIdx.x - hubs) * (int64_t)blockDim.x + threadIdx.x;
     if (r == n) cnt[n] = 0;
     const bool in = r < n;
     const int deg = in ? mrp[r + 1] - mrp[r] : 0;
-    if (in && deg > kCtaRow) long_rows[n - 1 - atomicAdd(long_count + 1, 1)] = (int32_t)r;
     const bool mid = in && deg > kLongRow && deg <= kCtaRow;
     if (in && deg <= kLongRow) {
         int k = 0;
@@ -645,11 +679,18 @@ __global__ void lap_count_kernel(int32_t n, const int32_t* __restrict__ mrp, con
     }
 }
 
-__global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
-                                 const double* __restrict__ mval, const double* __restrict__ is, int transposed,
-                                 const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
-                                 float* __restrict__ o32, double* __restrict__ o64, int64_t cap) {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kLongThreads) lap_write_kernel(
+        int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
+        const double* __restrict__ mval, const double* __restrict__ is, int transposed,
+        const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
+        float* __restrict__ o32, double* __restrict__ o64, int64_t cap, int hubs) {
+    if ((int)blockIdx.x < hubs) {
+        for_hub_rows(n, mrp, hubs, [&](int r) {
+            lap_write_row_cta(r, mrp, mcol, mval, is, transposed, orp, ocol, o32, o64, cap);
+        });
+        return;
+    }
+    const int64_t r = (blockIdx.x - hubs) * (int64_t)blockDim.x + threadIdx.x;
     const bool in = r < n;
     const int deg = in ? mrp[r + 1] - mrp[r] : 0;
     const bool mid = in && deg > kLongRow && deg <= kCtaRow;
@@ -692,130 +733,124 @@ __global__ void lap_write_kernel(int32_t n, const int32_t* __restrict__ mrp, con
 // and values are the thread kernels' exactly.
 constexpr int kLapIlp = 4;   // entries per thread per chunk of a hub row (loads in flight)
 
-__global__ void __launch_bounds__(kLongThreads) lap_count_long_kernel(
-        int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
-        const double* __restrict__ is, int transposed, int32_t* __restrict__ cnt,
-        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int nl = long_count[1];
+// CTA-cooperative count of one hub row (every thread of the CTA calls it)
+__device__ __forceinline__ void lap_count_row_cta(int r, const int32_t* __restrict__ mrp,
+                                                  const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                                                  const double* __restrict__ is, int transposed,
+                                                  int32_t* __restrict__ cnt) {
     const int nt = blockDim.x;
-    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
-        const int r = long_rows[n - 1 - li];
-        const int rb = mrp[r], re = mrp[r + 1];
-        int k = 0, diag = 0;
-        for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
-            int c[kLapIlp];
-            double a[kLapIlp];
+    const int rb = mrp[r], re = mrp[r + 1];
+    int k = 0, diag = 0;
+    for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
+        int c[kLapIlp];
+        double a[kLapIlp];
 #pragma unroll
-            for (int j = 0; j < kLapIlp; ++j) {
-                const int e = e0 + j * nt + threadIdx.x;
-                c[j] = e < re ? mcol[e] : -1;
-                a[j] = e < re && mval ? mval[e] : 1.0;
-            }
-            int nz = 0, isd = 0;
-#pragma unroll
-            for (int j = 0; j < kLapIlp; ++j) {
-                isd |= c[j] == r;
-                nz += c[j] >= 0 && lap_value(r, c[j], a[j], is, transposed) != 0.0;
-            }
-            k += __syncthreads_count(nz >= 1) + __syncthreads_count(nz >= 2) + __syncthreads_count(nz >= 3) +
-                 __syncthreads_count(nz >= 4);
-            diag |= __syncthreads_or(isd);
+        for (int j = 0; j < kLapIlp; ++j) {
+            const int e = e0 + j * nt + threadIdx.x;
+            c[j] = e < re ? mcol[e] : -1;
+            a[j] = e < re && mval ? mval[e] : 1.0;
         }
-        if (threadIdx.x == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
+        int nz = 0, isd = 0;
+#pragma unroll
+        for (int j = 0; j < kLapIlp; ++j) {
+            isd |= c[j] == r;
+            nz += c[j] >= 0 && lap_value(r, c[j], a[j], is, transposed) != 0.0;
+        }
+        k += __syncthreads_count(nz >= 1) + __syncthreads_count(nz >= 2) + __syncthreads_count(nz >= 3) +
+             __syncthreads_count(nz >= 4);
+        diag |= __syncthreads_or(isd);
     }
+    if (threadIdx.x == 0) cnt[r] = k + (!diag && lap_value(r, r, 0.0, is, transposed) != 0.0);
 }
 
-__global__ void __launch_bounds__(kLongThreads) lap_write_long_kernel(
-        int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol, const double* __restrict__ mval,
-        const double* __restrict__ is, int transposed, const int32_t* __restrict__ orp,
-        int32_t* __restrict__ ocol, float* __restrict__ o32, double* __restrict__ o64, int64_t cap,
-        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
+// CTA-cooperative write of one hub row (every thread of the CTA calls it)
+__device__ __forceinline__ void lap_write_row_cta(int r, const int32_t* __restrict__ mrp,
+                                                  const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                                                  const double* __restrict__ is, int transposed,
+                                                  const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
+                                                  float* __restrict__ o32, double* __restrict__ o64, int64_t cap) {
     __shared__ int s_warp[kLapIlp][kLongThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5, nt = blockDim.x;
     const unsigned lt = (1u << lane) - 1u;
-    const int nl = long_count[1];
-    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
-        const int r = long_rows[n - 1 - li];
-        const int rb = mrp[r], re = mrp[r + 1];
-        // insertion of the identity term: before the first column > r when no
-        // column == r is stored (the thread kernel's diag_done logic).  Columns
-        // are sorted, so the entries with column < r are a prefix of the row:
-        // before = its length, nzb = its nonzero entries.
-        int has_diag = 0, before = 0, nzb = 0;
-        for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
-            int c[kLapIlp];
-            double a[kLapIlp];
+    const int rb = mrp[r], re = mrp[r + 1];
+    // insertion of the identity term: before the first column > r when no
+    // column == r is stored (the thread kernel's diag_done logic).  Columns
+    // are sorted, so the entries with column < r are a prefix of the row:
+    // before = its length, nzb = its nonzero entries.
+    int has_diag = 0, before = 0, nzb = 0;
+    for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
+        int c[kLapIlp];
+        double a[kLapIlp];
 #pragma unroll
-            for (int j = 0; j < kLapIlp; ++j) {
-                const int e = e0 + j * nt + tid;
-                c[j] = e < re ? mcol[e] : INT_MAX;
-                a[j] = e < re && mval ? mval[e] : 1.0;
-            }
-            int lo = 0, nzl = 0, isd = 0;
-#pragma unroll
-            for (int j = 0; j < kLapIlp; ++j) {
-                isd |= c[j] == r;
-                lo += c[j] < r;
-                nzl += c[j] < r && lap_value(r, c[j], a[j], is, transposed) != 0.0;
-            }
-            has_diag |= __syncthreads_or(isd);
-#pragma unroll
-            for (int j = 1; j <= kLapIlp; ++j) {
-                before += __syncthreads_count(lo >= j);
-                nzb += __syncthreads_count(nzl >= j);
-            }
+        for (int j = 0; j < kLapIlp; ++j) {
+            const int e = e0 + j * nt + tid;
+            c[j] = e < re ? mcol[e] : INT_MAX;
+            a[j] = e < re && mval ? mval[e] : 1.0;
         }
-        const double dv = has_diag ? 0.0 : lap_value(r, r, 0.0, is, transposed);
-        const int dshift = (!has_diag && dv != 0.0) ? 1 : 0;
-        int64_t pos = orp[r];
-        for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
-            int c[kLapIlp];
-            double v[kLapIlp];
-            unsigned nzm[kLapIlp];
+        int lo = 0, nzl = 0, isd = 0;
 #pragma unroll
-            for (int j = 0; j < kLapIlp; ++j) {
-                const int e = e0 + j * nt + tid;
-                c[j] = e < re ? mcol[e] : 0;
-                v[j] = e < re && mval ? mval[e] : 1.0;
-            }
-#pragma unroll
-            for (int j = 0; j < kLapIlp; ++j) {
-                const int e = e0 + j * nt + tid;
-                v[j] = e < re ? lap_value(r, c[j], v[j], is, transposed) : 0.0;
-                nzm[j] = __ballot_sync(0xffffffffu, v[j] != 0.0);
-                if (lane == 0) s_warp[j][wid] = __popc(nzm[j]);
-            }
-            __syncthreads();
-            int run = 0;   // nonzeros of the earlier sub-chunks of this chunk
-#pragma unroll
-            for (int j = 0; j < kLapIlp; ++j) {
-                int off = 0, tot = 0;
-                for (int w = 0; w < nw; ++w) {
-                    const int x = s_warp[j][w];
-                    off += w < wid ? x : 0;
-                    tot += x;
-                }
-                const int e = e0 + j * nt + tid;
-                const int idx = e - rb;   // entry index within the row
-                const int64_t p = pos + run + off + __popc(nzm[j] & lt) + (idx >= before ? dshift : 0);
-                if (v[j] != 0.0 && p < cap) {
-                    ocol[p] = c[j];
-                    o32[p] = (float)v[j];
-                    if (o64) o64[p] = v[j];
-                }
-                run += tot;
-            }
-            pos += run;
-            __syncthreads();   // s_warp is rewritten by the next chunk
+        for (int j = 0; j < kLapIlp; ++j) {
+            isd |= c[j] == r;
+            lo += c[j] < r;
+            nzl += c[j] < r && lap_value(r, c[j], a[j], is, transposed) != 0.0;
         }
-        if (tid == 0 && dshift) {
-            // position: every nonzero stored entry with column < r precedes it
-            const int64_t p = orp[r] + nzb;
-            if (p < cap) {
-                ocol[p] = r;
-                o32[p] = (float)dv;
-                if (o64) o64[p] = dv;
+        has_diag |= __syncthreads_or(isd);
+#pragma unroll
+        for (int j = 1; j <= kLapIlp; ++j) {
+            before += __syncthreads_count(lo >= j);
+            nzb += __syncthreads_count(nzl >= j);
+        }
+    }
+    const double dv = has_diag ? 0.0 : lap_value(r, r, 0.0, is, transposed);
+    const int dshift = (!has_diag && dv != 0.0) ? 1 : 0;
+    int64_t pos = orp[r];
+    for (int e0 = rb; e0 < re; e0 += kLapIlp * nt) {
+        int c[kLapIlp];
+        double v[kLapIlp];
+        unsigned nzm[kLapIlp];
+#pragma unroll
+        for (int j = 0; j < kLapIlp; ++j) {
+            const int e = e0 + j * nt + tid;
+            c[j] = e < re ? mcol[e] : 0;
+            v[j] = e < re && mval ? mval[e] : 1.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kLapIlp; ++j) {
+            const int e = e0 + j * nt + tid;
+            v[j] = e < re ? lap_value(r, c[j], v[j], is, transposed) : 0.0;
+            nzm[j] = __ballot_sync(0xffffffffu, v[j] != 0.0);
+            if (lane == 0) s_warp[j][wid] = __popc(nzm[j]);
+        }
+        __syncthreads();
+        int run = 0;   // nonzeros of the earlier sub-chunks of this chunk
+#pragma unroll
+        for (int j = 0; j < kLapIlp; ++j) {
+            int off = 0, tot = 0;
+            for (int w = 0; w < nw; ++w) {
+                const int x = s_warp[j][w];
+                off += w < wid ? x : 0;
+                tot += x;
             }
+            const int e = e0 + j * nt + tid;
+            const int idx = e - rb;   // entry index within the row
+            const int64_t p = pos + run + off + __popc(nzm[j] & lt) + (idx >= before ? dshift : 0);
+            if (v[j] != 0.0 && p < cap) {
+                ocol[p] = c[j];
+                o32[p] = (float)v[j];
+                if (o64) o64[p] = v[j];
+            }
+            run += tot;
+        }
+        pos += run;
+        __syncthreads();   // s_warp is rewritten by the next chunk
+    }
+    if (tid == 0 && dshift) {
+        // position: every nonzero stored entry with column < r precedes it
+        const int64_t p = orp[r] + nzb;
+        if (p < cap) {
+            ocol[p] = r;
+            o32[p] = (float)dv;
+            if (o64) o64[p] = dv;
         }
     }
 }
@@ -1018,24 +1053,20 @@ int dgnn_laplacian(int32_t n, const int32_t* a_rowptr, const int32_t* m_rowptr, 
     size_t sws_bytes = ws_bytes - (size_t)round64(n) * sizeof(double) -
                        (size_t)round64((int64_t)n + 1) * sizeof(int32_t) - 64 * sizeof(int32_t);
     const unsigned g = (unsigned)cdiv((int64_t)n + 1, 128);
-    cudaMemsetAsync(long_count, 0, 2 * sizeof(int32_t), st);
+    (void)long_count;
     ::dgnn::note_launch();
     inv_sqrt_deg_kernel<<<g, 128, 0, st>>>(n, a_rowptr, is);
     ::dgnn::note_launch();
-    lap_count_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, long_rows,
-                                        long_count);
-    ::dgnn::note_launch();
-    lap_count_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed,
-                                                                     out_rowptr, long_rows, long_count);
+    // hub rows (> kCtaRow entries) in the same launches: the first `hubs`
+    // blocks, each scanning a slice of about 1700 rows at configs[2]
+    const int hubs = 4 * num_sms();
+    const unsigned gl = (unsigned)cdiv((int64_t)n + 1, kLongThreads) + hubs;
+    lap_count_kernel<<<gl, kLongThreads, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, hubs);
     int rc = exclusive_scan_i32(out_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
     if (rc) return rc;
     ::dgnn::note_launch();
-    lap_write_kernel<<<g, 128, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
-                                        out_val32, out_val64, out_cap);
-    ::dgnn::note_launch();
-    lap_write_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(
-        n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col, out_val32, out_val64, out_cap, long_rows,
-        long_count);
+    lap_write_kernel<<<gl, kLongThreads, 0, st>>>(n, m_rowptr, m_col, m_val, is, transposed, out_rowptr, out_col,
+                                                 out_val32, out_val64, out_cap, hubs);
     return launch_status("laplacian");
 }
 
