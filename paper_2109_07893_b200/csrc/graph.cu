@@ -202,6 +202,31 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int key)
     return lo;
 }
 
+constexpr int kLongThreads = 256;   // CTA size of every hub-row kernel
+constexpr int kLongCTAs = 4;        // hub-row CTAs per SM
+
+// The leading `hubs` blocks of a per-row launch take the hub rows, a CTA
+// per row: block h scans its slice of the rows for those `is_hub` picks and
+// runs `f(r)` on each with the whole CTA, alongside the per-row blocks of
+// the same launch (no device list, no second launch).
+template <class P, class F>
+__device__ __forceinline__ void for_hub_rows(int32_t n, int hubs, P is_hub, F f) {
+    __shared__ int s_list[kLongThreads];
+    __shared__ int s_n;
+    const int64_t per = cdiv((int64_t)n, (int64_t)hubs);
+    const int64_t r0 = blockIdx.x * per, r1 = min((int64_t)n, r0 + per);
+    for (int64_t w0 = r0; w0 < r1; w0 += blockDim.x) {
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const int64_t r = w0 + threadIdx.x;
+        if (r < r1 && is_hub((int)r)) s_list[atomicAdd(&s_n, 1)] = (int)r;
+        __syncthreads();
+        const int m = s_n;
+        for (int i = 0; i < m; ++i) f(s_list[i]);
+        __syncthreads();
+    }
+}
+
 __global__ void delta_count_kernel(int32_t n, const int32_t* __restrict__ orp,
                                    const int32_t* __restrict__ drp, const int32_t* __restrict__ irp,
                                    int32_t* __restrict__ nrp) {
@@ -216,21 +241,28 @@ __device__ __forceinline__ int merge_row_split(int r, int tid, int nt, const int
                                                const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
                                                const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
                                                int32_t* __restrict__ ncol, int64_t cap);
-constexpr int kMergeCtaRow = 512;   // = kMergeCta (defined with the hub kernel below)
+constexpr int kMergeCtaRow = 512;   // rows past this: a CTA each (the leading hub blocks)
 
 // Thread per row (two-pointer merge); rows of kMergeLong+1..512 entries are
 // then merged by their warp together (ballot queue), longer ones go to the
 // CTA-per-row kernel.  Every lane stays to the end (whole-warp ballots).
-__global__ void delta_merge_kernel(int32_t n, const int32_t* __restrict__ orp,
-                                   const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
-                                   const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp,
-                                   const int32_t* __restrict__ icol, const int32_t* __restrict__ nrp,
-                                   int32_t* __restrict__ ncol, int64_t cap, int32_t* status,
-                                   int32_t* __restrict__ long_rows, int32_t* long_count) {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kLongThreads) delta_merge_kernel(
+        int32_t n, const int32_t* __restrict__ orp, const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
+        const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+        const int32_t* __restrict__ nrp, int32_t* __restrict__ ncol, int64_t cap, int32_t* status, int hubs) {
+    if ((int)blockIdx.x < hubs) {
+        int bad = 0;
+        for_hub_rows(n, hubs, [&](int r) { return (orp[r + 1] - orp[r]) + (irp[r + 1] - irp[r]) > kMergeCtaRow; },
+                     [&](int r) {
+                         bad += merge_row_split(r, threadIdx.x, blockDim.x, orp, ocol, drp, dcol, irp, icol, nrp,
+                                                ncol, cap);
+                     });
+        if (bad) atomicAdd(status, bad);
+        return;
+    }
+    const int64_t r = (blockIdx.x - hubs) * (int64_t)blockDim.x + threadIdx.x;
     const bool in = r < n;
     const int len = in ? (orp[r + 1] - orp[r]) + (irp[r + 1] - irp[r]) : 0;
-    if (in && len > kMergeCtaRow) long_rows[atomicAdd(long_count, 1)] = (int32_t)r;   // delta_merge_long_kernel
     const bool mid = in && len > kMergeLong && len <= kMergeCtaRow;
     int bad = 0;
     if (in && len <= kMergeLong) {
@@ -266,12 +298,9 @@ __global__ void delta_merge_kernel(int32_t n, const int32_t* __restrict__ orp,
 // insert at (#old < c) - (#deletes < c) + its index.  Same output as the
 // two-pointer merge for a consistent delta; the same inconsistencies
 // (deleting an absent entry, inserting a present one) are counted into
-// `status`.  Rows of 17..kMergeCta entries: the owning warp of the
-// per-row kernel (tid = lane, nt = 32); hubs past kMergeCta: a CTA each (a
+// `status`.  Rows of 17..kMergeCtaRow entries: the owning warp of the
+// per-row kernel (tid = lane, nt = 32); hubs past it: a CTA each (a
 // warp per row left a ~8000-entry hub as a 250-step serial tail).
-constexpr int kLongThreads = 256;   // CTA size of every hub-row kernel
-constexpr int kLongCTAs = 4;        // CTAs per SM of every hub-row kernel
-constexpr int kMergeCta = 512;
 
 __device__ __forceinline__ int merge_row_split(int r, int tid, int nt, const int32_t* __restrict__ orp,
                                                const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
@@ -308,18 +337,6 @@ __device__ __forceinline__ int merge_row_split(int r, int tid, int nt, const int
     return bad;
 }
 
-__global__ void __launch_bounds__(kLongThreads) delta_merge_long_kernel(
-        const int32_t* __restrict__ orp, const int32_t* __restrict__ ocol, const int32_t* __restrict__ drp,
-        const int32_t* __restrict__ dcol, const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
-        const int32_t* __restrict__ nrp, int32_t* __restrict__ ncol, int64_t cap, int32_t* status,
-        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int nl = *long_count;
-    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
-        const int bad = merge_row_split(long_rows[li], threadIdx.x, blockDim.x, orp, ocol, drp, dcol, irp, icol, nrp,
-                                        ncol, cap);
-        if (bad) atomicAdd(status, bad);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // deterministic transpose
@@ -340,18 +357,26 @@ __global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ col, in
 constexpr int kLongRow = 16;
 constexpr int kCtaRow = 512;   // Laplacian rows past this: a CTA each (below: a warp each)
 
-__global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ rp,
-                                         const int32_t* __restrict__ col, const double* __restrict__ val,
-                                         int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval,
-                                         int32_t* __restrict__ long_rows, int32_t* long_count) {
+__global__ void __launch_bounds__(kLongThreads) transpose_scatter_kernel(
+        int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+        int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval, int hubs) {
     // thread per row; rows of kLongRow+1..kCtaRow entries are scattered by
     // their warp together (ballot queue), longer ones by a CTA each
     // (transpose_scatter_long_kernel).  The order inside a column is fixed
     // by the segment sort that follows.
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if ((int)blockIdx.x < hubs) {
+        for_hub_rows(n, hubs, [&](int r) { return rp[r + 1] - rp[r] > kCtaRow; }, [&](int r) {
+            for (int e = rp[r] + threadIdx.x; e < rp[r + 1]; e += blockDim.x) {
+                const int pos = atomicAdd(&cursor[col[e]], 1);
+                tcol[pos] = r;
+                if (val) tval[pos] = val[e];
+            }
+        });
+        return;
+    }
+    const int64_t r = (blockIdx.x - hubs) * (int64_t)blockDim.x + threadIdx.x;
     const bool in = r < n;
     const int len = in ? rp[r + 1] - rp[r] : 0;
-    if (in && len > kCtaRow) long_rows[atomicAdd(long_count, 1)] = (int32_t)r;
     const bool mid = in && len > kLongRow && len <= kCtaRow;
     if (in && len <= kLongRow) {
         for (int e = rp[r]; e < rp[r + 1]; ++e) {
@@ -371,20 +396,6 @@ __global__ void transpose_scatter_kernel(int32_t n, const int32_t* __restrict__ 
     }
 }
 
-__global__ void __launch_bounds__(kLongThreads) transpose_scatter_long_kernel(
-        const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-        int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval,
-        const int32_t* __restrict__ long_rows, const int32_t* __restrict__ long_count) {
-    const int cnt = *long_count;
-    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {   // a CTA per hub row
-        const int r = long_rows[li];
-        for (int e = rp[r] + threadIdx.x; e < rp[r + 1]; e += blockDim.x) {
-            const int pos = atomicAdd(&cursor[col[e]], 1);
-            tcol[pos] = r;
-            if (val) tval[pos] = val[e];
-        }
-    }
-}
 
 constexpr int kSmallSeg = 32;
 constexpr int kRankMax = 1024;       // mid segments: rank sort of a shared-memory copy
@@ -626,33 +637,13 @@ __device__ __forceinline__ void lap_write_row_cta(int r, const int32_t* __restri
                                                   const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
                                                   float* __restrict__ o32, double* __restrict__ o64, int64_t cap);
 
-// The first `hubs` blocks take the rows past kCtaRow entries, a CTA per row:
-// block h scans its slice of rows for them (so the hub rows run alongside
-// the per-row blocks, in the same launch, with no device list).
-template <class F>
-__device__ __forceinline__ void for_hub_rows(int32_t n, const int32_t* __restrict__ mrp, int hubs, F f) {
-    __shared__ int s_list[kLongThreads];
-    __shared__ int s_n;
-    const int64_t per = cdiv((int64_t)n, (int64_t)hubs);
-    const int64_t r0 = blockIdx.x * per, r1 = min((int64_t)n, r0 + per);
-    for (int64_t w0 = r0; w0 < r1; w0 += blockDim.x) {
-        if (threadIdx.x == 0) s_n = 0;
-        __syncthreads();
-        const int64_t r = w0 + threadIdx.x;
-        if (r < r1 && mrp[r + 1] - mrp[r] > kCtaRow) s_list[atomicAdd(&s_n, 1)] = (int)r;
-        __syncthreads();
-        const int m = s_n;
-        for (int i = 0; i < m; ++i) f(s_list[i]);
-        __syncthreads();
-    }
-}
-
 __global__ void __launch_bounds__(kLongThreads) lap_count_kernel(
         int32_t n, const int32_t* __restrict__ mrp, const int32_t* __restrict__ mcol,
         const double* __restrict__ mval, const double* __restrict__ is, int transposed,
         int32_t* __restrict__ cnt, int hubs) {
     if ((int)blockIdx.x < hubs) {
-        for_hub_rows(n, mrp, hubs, [&](int r) { lap_count_row_cta(r, mrp, mcol, mval, is, transposed, cnt); });
+        for_hub_rows(n, hubs, [&](int r) { return mrp[r + 1] - mrp[r] > kCtaRow; },
+                     [&](int r) { lap_count_row_cta(r, mrp, mcol, mval, is, transposed, cnt); });
         return;
     }
     const int64_t r = (blockIdx.x - hubs) * (int64_t)blockDim.x + threadIdx.x;
@@ -685,7 +676,7 @@ __global__ void __launch_bounds__(kLongThreads) lap_write_kernel(
         const int32_t* __restrict__ orp, int32_t* __restrict__ ocol,
         float* __restrict__ o32, double* __restrict__ o64, int64_t cap, int hubs) {
     if ((int)blockIdx.x < hubs) {
-        for_hub_rows(n, mrp, hubs, [&](int r) {
+        for_hub_rows(n, hubs, [&](int r) { return mrp[r + 1] - mrp[r] > kCtaRow; }, [&](int r) {
             lap_write_row_cta(r, mrp, mcol, mval, is, transposed, orp, ocol, o32, o64, cap);
         });
         return;
@@ -956,13 +947,9 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
     rc = exclusive_scan_i32(new_rowptr, (int64_t)n + 1, sws, sws_bytes, st);
     if (rc) return rc;
     ::dgnn::note_launch();
-    delta_merge_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, old_rowptr, old_col, drp, del_col, irp,
-                                                               ins_col, new_rowptr, new_col, new_cap, status,
-                                                               long_rows, long_count);
-    ::dgnn::note_launch();
-    delta_merge_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(
-        old_rowptr, old_col, drp, del_col, irp, ins_col, new_rowptr, new_col, new_cap, status, long_rows,
-        long_count);
+    const int hubs = kLongCTAs * num_sms();
+    delta_merge_kernel<<<(unsigned)cdiv(n, kLongThreads) + hubs, kLongThreads, 0, st>>>(
+        n, old_rowptr, old_col, drp, del_col, irp, ins_col, new_rowptr, new_col, new_cap, status, hubs);
     return launch_status("csr_apply_delta");
 }
 
@@ -1005,11 +992,11 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     if (rc) return rc;
     cudaMemcpyAsync(cursor, t_rowptr, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
     ::dgnn::note_launch();
-    transpose_scatter_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, rowptr, col, val, cursor, stage_col,
-                                                                      stage_val, long_rows, long_rows_count);
-    ::dgnn::note_launch();
-    transpose_scatter_long_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(
-        rowptr, col, val, cursor, stage_col, stage_val, long_rows, long_rows_count);
+    {
+        const int hubs = kLongCTAs * num_sms();
+        transpose_scatter_kernel<<<(unsigned)cdiv(n, kLongThreads) + hubs, kLongThreads, 0, st>>>(
+            n, rowptr, col, val, cursor, stage_col, stage_val, hubs);
+    }
     // the hub-row list is free once the scatter has run: it now takes the
     // columns past kRankMax, the cursor array the mid columns
     cudaMemsetAsync(long_rows_count, 0, sizeof(int32_t), st);
