@@ -554,7 +554,15 @@ def run_ours(args):
     # ---- e2e through the public drop-in API (host buffers, deltas streamed)
     e2e = None
     if not args.skip_e2e:
-        pcie_peak = pcie_h2d_peak()
+        # each rank alone on the bus (the uncontended pinned H2D rate is the roofline)
+        pcie_peak = None
+        for q in range(P):
+            if P > 1:
+                dist.barrier()
+            if q == rank:
+                pcie_peak = pcie_h2d_peak()
+        if P > 1:
+            dist.barrier()
         comm, transfer = pk.CommLedger(), pk.TransferLedger()
         hp = {k: v.copy() for k, v in params.items()}
         st = pk.init_adam(hp)
