@@ -285,15 +285,44 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
                 GtcIdx& ix = idx[si];
                 const int64_t r0 = (int64_t)tile * gtc::BM;
                 const int nr = (int)min((int64_t)gtc::BM, (int64_t)n - r0);
+                // all loads of a stage issued before any store (5 rowptr and up
+                // to 2 x 8 edge loads in flight per lane): one round trip to
+                // memory per 256 edges, so this warp keeps ahead of the gathers
                 const int eb = __ldg(rp + r0);
-                for (int i = lane; i <= gtc::BM; i += 32) ix.rp[i] = __ldg(rp + r0 + min(i, nr)) - eb;
+                {
+                    int q[5];
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) {
+                        const int i = lane + 32 * k;
+                        q[k] = i <= gtc::BM ? __ldg(rp + r0 + min(i, nr)) : 0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) {
+                        const int i = lane + 32 * k;
+                        if (i <= gtc::BM) ix.rp[i] = q[k] - eb;
+                    }
+                }
                 __syncwarp();
                 const int ne = ix.rp[nr];
                 const bool spill = ne > gtc::ECAP;
                 if (!spill) {
-                    for (int i = lane; i < ne; i += 32) {
-                        ix.col[i] = __ldg(col + eb + i);
-                        ix.val[i] = __ldg(val + eb + i);
+                    for (int i0 = 0; i0 < ne; i0 += 32 * 8) {
+                        int c8[8];
+                        float v8[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int i = i0 + 32 * k + lane;
+                            c8[k] = i < ne ? __ldg(col + eb + i) : 0;
+                            v8[k] = i < ne ? __ldg(val + eb + i) : 0.f;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int i = i0 + 32 * k + lane;
+                            if (i < ne) {
+                                ix.col[i] = c8[k];
+                                ix.val[i] = v8[k];
+                            }
+                        }
                     }
                 }
                 if (lane == 0) {
