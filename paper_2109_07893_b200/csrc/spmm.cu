@@ -79,25 +79,88 @@ __global__ void __launch_bounds__(256) hub_rows_kernel(int32_t n, const int32_t*
                                                        const float* __restrict__ val, dgnn_frame x,
                                                        const float* __restrict__ w, dgnn_frame s_out,
                                                        dgnn_frame r_out) {
-    constexpr int G = F / 4, EPS = 256 / G;
+    // Rows of kHubRow+1..kWarpHub entries: a warp each (SL slots of G lanes,
+    // slot sums combined by a fixed shuffle tree), several in flight per
+    // CTA; longer rows: the whole CTA (EPS slots, fixed smem tree).  q_j =
+    // sum_k s_k W[k][j] in k order.
+    constexpr int G = F / 4, EPS = 256 / G, SL = 32 / G;
+    constexpr int kWarpHub = 512;
     __shared__ int32_t list[256];
-    __shared__ int cnt;
+    __shared__ int cnt, nbig;
     __shared__ float4 part[EPS][G];
+    __shared__ float4 wrow[8][G];   // a warp's row aggregate (the W product reads it)
     const int slot = threadIdx.x / G, gl = threadIdx.x % G;
+    const int lane = threadIdx.x & 31, wslot = lane / G, wid = threadIdx.x >> 5;
+    auto emit = [&](int row, const float4& s4, bool lead, int jlane, int jstride, const float* sk) {
+        // s4: the row's aggregate (the G lead lanes hold F floats); sk: the same in shared memory
+        if constexpr (MODE == 0) {
+            if (lead) st4(frame_row<float>(r_out, row) + 4 * gl, s4);
+        } else {
+            float* rr = frame_row<float>(r_out, row);
+            if (lead) {
+                if (s_out.ptr) st4(frame_row<float>(s_out, row) + 4 * gl, s4);
+                if (MODE == 1) st4(rr + 4 * gl, relu4(s4));
+            }
+            for (int j = jlane; j < H; j += jstride) {
+                float q = 0.f;
+                for (int kk = 0; kk < F; ++kk) q = fmaf(sk[kk], __ldg(w + kk * H + j), q);
+                rr[(MODE == 1 ? F : 0) + j] = fmaxf(q, 0.f);
+            }
+        }
+    };
     for (int64_t base = (int64_t)blockIdx.x * 256; base < n; base += (int64_t)gridDim.x * 256) {
-        if (threadIdx.x == 0) cnt = 0;
+        if (threadIdx.x == 0) cnt = 0, nbig = 0;
         __syncthreads();
         const int64_t r = base + threadIdx.x;
-        if (r < n && rp[r + 1] - rp[r] > kHubRow) list[atomicAdd(&cnt, 1)] = (int32_t)r;
+        if (r < n) {
+            const int d = rp[r + 1] - rp[r];
+            if (d > kWarpHub) list[255 - atomicAdd(&nbig, 1)] = (int32_t)r;
+            else if (d > kHubRow) list[atomicAdd(&cnt, 1)] = (int32_t)r;
+        }
         __syncthreads();
-        const int nh = cnt;
-        for (int k = 0; k < nh; ++k) {
+        const int nh = cnt, nb = nbig;
+        // mid rows: warp wid takes rows wid, wid + 8, ...
+        for (int k = wid; k < nh; k += 8) {
             const int row = list[k];
+            const int eb = rp[row], ee = rp[row + 1];
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            int e = eb + wslot;
+            for (; e + 7 * SL < ee; e += 8 * SL) {
+                int c[8];
+                float v[8];
+                float4 xv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    c[j] = __ldg(col + e + j * SL);
+                    v[j] = __ldg(val + e + j * SL);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) xv[j] = ldg4(frame_row<const float>(x, c[j]) + 4 * gl);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) fma4(acc, v[j], xv[j]);
+            }
+            for (; e < ee; e += SL)
+                fma4(acc, __ldg(val + e), ldg4(frame_row<const float>(x, __ldg(col + e)) + 4 * gl));
+#pragma unroll
+            for (int o = 16; o >= G; o >>= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+                acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+            }
+            if (lane < G) wrow[wid][gl] = acc;
+            __syncwarp();
+            emit(row, acc, lane < G, lane, 32, reinterpret_cast<const float*>(&wrow[wid][0]));
+            __syncwarp();
+        }
+        // long rows: the whole CTA each
+        for (int k = 0; k < nb; ++k) {
+            const int row = list[255 - k];
             const int eb = rp[row], ee = rp[row + 1];
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             int e = eb + slot;
             // 8 of the slot's edges in flight at once (a hub of ~8000 edges was a
-            // 250-step chain of dependent col -> x loads); same summation order
+            // 250-step chain of dependent col -> x loads)
             for (; e + 7 * EPS < ee; e += 8 * EPS) {
                 int c[8];
                 float v[8];
@@ -125,21 +188,8 @@ __global__ void __launch_bounds__(256) hub_rows_kernel(int32_t n, const int32_t*
                 }
                 __syncthreads();
             }
-            if constexpr (MODE == 0) {
-                if (threadIdx.x < G) st4(frame_row<float>(r_out, row) + 4 * gl, part[0][gl]);
-            } else {
-                float* rr = frame_row<float>(r_out, row);
-                if (threadIdx.x < G) {
-                    if (s_out.ptr) st4(frame_row<float>(s_out, row) + 4 * gl, part[0][gl]);
-                    if (MODE == 1) st4(rr + 4 * gl, relu4(part[0][gl]));
-                }
-                const float* sv = reinterpret_cast<const float*>(&part[0][0]);
-                for (int j = threadIdx.x; j < H; j += blockDim.x) {
-                    float q = 0.f;
-                    for (int kk = 0; kk < F; ++kk) q = fmaf(sv[kk], __ldg(w + kk * H + j), q);
-                    rr[(MODE == 1 ? F : 0) + j] = fmaxf(q, 0.f);
-                }
-            }
+            const float* sv = reinterpret_cast<const float*>(&part[0][0]);
+            emit(row, part[0][gl], threadIdx.x < G, threadIdx.x, blockDim.x, sv);
             __syncthreads();
         }
         __syncthreads();
