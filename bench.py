@@ -54,7 +54,7 @@ CONFIGS = {
                         "AMLSim-style transaction graph: N=1M, T=64, 2M edges/snapshot (128M total), "
                         "heavy-tailed degrees, 2% churn"),
     "c4": dict(arch="cd-gcn", n=3_000_000, m=4_687_500, T=64, hidden=32, churn=0.10,
-               nblk={1: 8, 2: 2, 4: 1, 8: 1}, gen="device", scaling="strong", cpu_scale=256,
+               nblk={1: 4, 2: 2, 4: 1, 8: 1}, gen="device", scaling="strong", cpu_scale=256,
                workload="configs[3] Flickr/YouTube-scale: cd-gcn (skip-GCN+LSTM, 2 layers) hidden=32, "
                         "N=3M, T=64, 4,687,500 edges/snapshot (300M total), 10% churn, snapshot-partitioned"),
     "c5": dict(arch="cd-gcn", n=10_000_000, m=15_625_000, T=64, hidden=32, churn=0.01,
