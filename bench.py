@@ -290,6 +290,8 @@ def ncu_traffic(entry):
     pref = NCU_KERNEL.get(entry)
     if entry == "dgnn_gcn_forward":   # the aggregating instance at this config's width / cell
         pref = f"gcn_fwd_tc_kernel<{HIDDEN}, {HIDDEN}, {int(CFG['arch'] == 'cd-gcn')}, 1"
+    elif pref is not None and pref.startswith("lstm_"):   # the instance at this config's hidden width
+        pref = f"{pref}<{HIDDEN}>"
     if not files or pref is None:
         return None
     d = json.loads(files[-1].read_text())
