@@ -59,8 +59,11 @@ struct WsRoles {
 #ifndef DGNN_FWD_NEPI64
 #define DGNN_FWD_NEPI64 8
 #endif
+#ifndef DGNN_FWD_NEPI32
+#define DGNN_FWD_NEPI32 16
+#endif
 template <int HP>
-using FwdRoles = WsRoles<DGNN_FWD_NPROD, (HP >= 64 ? DGNN_FWD_NEPI64 : (HP >= 32 ? 16 : 8)), (HP >= 64 ? 3 : 4)>;
+using FwdRoles = WsRoles<DGNN_FWD_NPROD, (HP >= 64 ? DGNN_FWD_NEPI64 : (HP >= 32 ? DGNN_FWD_NEPI32 : 8)), (HP >= 64 ? 3 : 4)>;
 // forward activation landing ring (fp32 chunks, cp.async), decoupled from
 // the operand stages so loads run RAW_RING - 1 chunks ahead (6 at hidden 64:
 // the operand stages are 48 KB and the c_prev tile takes 32 KB)
