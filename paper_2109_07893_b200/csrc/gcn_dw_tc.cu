@@ -52,14 +52,14 @@ struct GdwShape {
     int MA, N, atoms_a, atoms_b, a_half, b_half, stage, stages, tmem_cols;
 };
 
-__host__ __device__ inline GdwShape gdw_shape(int ma, int fp) {
+__host__ __device__ inline GdwShape gdw_shape(int ma, int fp, int rows = gdw::ROWS) {
     GdwShape s;
     s.MA = ma;
     s.N = (fp + 31) / 32 * 32;
     s.atoms_a = s.MA / 32;
     s.atoms_b = s.N / 32;
-    s.a_half = (gdw::ROWS / 4) * s.atoms_a * 512;
-    s.b_half = (gdw::ROWS / 4) * s.atoms_b * 512;
+    s.a_half = (rows / 4) * s.atoms_a * 512;
+    s.b_half = (rows / 4) * s.atoms_b * 512;
     s.stage = 3 * s.a_half + 2 * s.b_half;   // A hi | A lo | mask | B hi | B lo
     s.stages = (gdw::SMEM_MAX - 1024 - 256) / s.stage;
     if (s.stages > gdw::MAX_STAGES) s.stages = gdw::MAX_STAGES;
@@ -87,11 +87,13 @@ __device__ __forceinline__ const float* gdw_row(const dgnn_frame& f, int32_t i) 
     return reinterpret_cast<const float*>(f.ptr) + (int64_t)s * f.slab_stride + (int64_t)r * f.ld;
 }
 
-template <int MA>
+// R: reduction rows per stage -- 64 for narrow operands (fp <= 32, M = 64),
+// so a stage still moves >= 12 KB per cp.async batch
+template <int MA, int R>
 __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows, int fp, int hp, int off,
                                                                     dgnn_frame s_in, dgnn_frame dr, dgnn_frame rk,
                                                                     float* __restrict__ slots) {
-    const GdwShape S = gdw_shape(MA, fp);
+    const GdwShape S = gdw_shape(MA, fp, R);
     extern __shared__ uint8_t gdw_smem_raw[];
     const uint32_t raw = smem_u32(gdw_smem_raw);
     uint8_t* base = gdw_smem_raw + ((1024 - (raw & 1023)) & 1023);
@@ -122,11 +124,11 @@ __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows
     fence_after();
 
     // contiguous row range of this CTA (multiple of the stage rows)
-    const int64_t per = cdiv(cdiv(rows, gridDim.x), gdw::ROWS) * gdw::ROWS;
+    const int64_t per = cdiv(cdiv(rows, gridDim.x), R) * R;
     const int64_t r_begin = blockIdx.x * per;
     const int64_t r_end = min((int64_t)rows, r_begin + per);
-    const int nst = r_end > r_begin ? (int)cdiv(r_end - r_begin, gdw::ROWS) : 0;
-    constexpr int PST = gdw::PERIOD / gdw::ROWS;
+    const int nst = r_end > r_begin ? (int)cdiv(r_end - r_begin, R) : 0;
+    constexpr int PST = gdw::PERIOD / R;
     const int nper = (nst + PST - 1) / PST;
     const int ga = hp / 4, gb = fp / 4;   // real 4-column groups of A (dq) and B (s)
 
@@ -137,16 +139,16 @@ __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows
         const int lt = threadIdx.x;
         const int ca = 4 * (lt % ga), ra = lt / ga, rsa = NLT / ga;
         const int cb = 4 * (lt % gb), rb = lt / gb, rsb = NLT / gb;
-        const uint32_t aoff0 = gdw_off(ra & 31, ca, S.atoms_a), astep = (uint32_t)(rsa / 4) * S.atoms_a * 512;
-        const uint32_t boff0 = gdw_off(rb & 31, cb, S.atoms_b), bstep = (uint32_t)(rsb / 4) * S.atoms_b * 512;
+        const uint32_t aoff0 = gdw_off(ra & (R - 1), ca, S.atoms_a), astep = (uint32_t)(rsa / 4) * S.atoms_a * 512;
+        const uint32_t boff0 = gdw_off(rb & (R - 1), cb, S.atoms_b), bstep = (uint32_t)(rsb / 4) * S.atoms_b * 512;
         for (int g = 0; g < nst; ++g) {
             const int s = g % S.stages;
             const int j = g / S.stages;
             if (j >= 1) mbar_wait(&bars->empty[s], (j - 1) & 1);
-            const int64_t r0 = r_begin + (int64_t)g * gdw::ROWS;
+            const int64_t r0 = r_begin + (int64_t)g * R;
             const uint32_t a_hi = sb + s * S.stage, mk = a_hi + 2 * S.a_half, b_hi = mk + S.a_half;
             uint32_t o = aoff0;
-            for (int r = ra; r < gdw::ROWS; r += rsa, o += astep) {
+            for (int r = ra; r < R; r += rsa, o += astep) {
                 const int64_t gr = r0 + r;
                 const bool ok = gr < r_end;
                 const float* pd = ok ? gdw_row(dr, (int32_t)gr) + off + ca : reinterpret_cast<const float*>(dr.ptr);
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows
                 cp_async16(mk + o, pm, ok ? 16u : 0u);
             }
             o = boff0;
-            for (int r = rb; r < gdw::ROWS; r += rsb, o += bstep) {
+            for (int r = rb; r < R; r += rsb, o += bstep) {
                 const int64_t gr = r0 + r;
                 const bool ok = gr < r_end;
                 const float* ps = ok ? gdw_row(s_in, (int32_t)gr) + cb : reinterpret_cast<const float*>(s_in.ptr);
@@ -169,15 +171,15 @@ __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows
         const int ct = threadIdx.x - 32 * gdw::NLOAD;
         const int ca = 4 * (ct % ga), ra = ct / ga, rsa = NCT / ga;
         const int cb = 4 * (ct % gb), rb = ct / gb, rsb = NCT / gb;
-        const uint32_t aoff0 = gdw_off(ra & 31, ca, S.atoms_a), astep = (uint32_t)(rsa / 4) * S.atoms_a * 512;
-        const uint32_t boff0 = gdw_off(rb & 31, cb, S.atoms_b), bstep = (uint32_t)(rsb / 4) * S.atoms_b * 512;
+        const uint32_t aoff0 = gdw_off(ra & (R - 1), ca, S.atoms_a), astep = (uint32_t)(rsa / 4) * S.atoms_a * 512;
+        const uint32_t boff0 = gdw_off(rb & (R - 1), cb, S.atoms_b), bstep = (uint32_t)(rsb / 4) * S.atoms_b * 512;
         for (int g = 0; g < nst; ++g) {
             const int s = g % S.stages;
             mbar_wait(&bars->landed[s], (g / S.stages) & 1);
             const uint32_t a_hi = sb + s * S.stage, a_lo = a_hi + S.a_half, mk = a_lo + S.a_half;
             const uint32_t b_hi = mk + S.a_half, b_lo = b_hi + S.b_half;
             uint32_t o = aoff0;
-            for (int r = ra; r < gdw::ROWS; r += rsa, o += astep) {
+            for (int r = ra; r < R; r += rsa, o += astep) {
                 const float4 d = lds128(a_hi + o), m = lds128(mk + o);
                 const float4 q = make_float4(m.x > 0.f ? d.x : 0.f, m.y > 0.f ? d.y : 0.f, m.z > 0.f ? d.z : 0.f,
                                              m.w > 0.f ? d.w : 0.f);
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows
                 sts128(a_lo + o, lo);
             }
             o = boff0;
-            for (int r = rb; r < gdw::ROWS; r += rsb, o += bstep) {
+            for (int r = rb; r < R; r += rsb, o += bstep) {
                 float4 hi, lo;
                 split4(lds128(b_hi + o), hi, lo);
                 sts128(b_hi + o, hi);
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(gdw::THREADS, 1) gcn_dw_tc_kernel(int32_t rows
                     const uint32_t a_hi = sb + s * S.stage, a_lo = a_hi + S.a_half;
                     const uint32_t b_hi = a_lo + 2 * S.a_half, b_lo = b_hi + S.b_half;
 #pragma unroll
-                    for (int kk = 0; kk < gdw::ROWS / 8; ++kk) {
+                    for (int kk = 0; kk < R / 8; ++kk) {
                         const uint32_t ao = 2 * kk * S.atoms_a * 512, bo = 2 * kk * S.atoms_b * 512;
                         const uint64_t ah = sdesc_mn(a_hi + ao, 512, S.atoms_a * 512, 1);
                         const uint64_t al = sdesc_mn(a_lo + ao, 512, S.atoms_a * 512, 1);
@@ -292,7 +294,8 @@ int gcn_dw_tc(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int fp, int 
     auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
     if (hp > 128 || fp > 128 || hp % 4 || fp % 4 || !pow2(hp / 4) || !pow2(fp / 4)) return -1;
     const int ma = hp <= 64 ? 64 : 128;
-    const GdwShape S = gdw_shape(ma, fp);
+    const int rows_st = (fp <= 32 && ma == 64) ? 64 : 32;
+    const GdwShape S = gdw_shape(ma, fp, rows_st);
     if (S.stages < 3) return -1;
     const size_t need = (size_t)num_sms() * S.N * S.MA * sizeof(float);
     if (ws_bytes < need) {
@@ -306,14 +309,18 @@ int gcn_dw_tc(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, int fp, int 
     // must not depend on dgnn_set_sm_reserve
     const int grid = num_sms();
     const int off = skip ? fp : 0;
-    if (ma == 64) {
-        cudaFuncSetAttribute(gcn_dw_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ma == 64 && rows_st == 64) {
+        cudaFuncSetAttribute(gcn_dw_tc_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_launch();
-        gcn_dw_tc_kernel<64><<<grid, gdw::THREADS, smem, st>>>(n, fp, hp, off, s, dr, r, slots);
+        gcn_dw_tc_kernel<64, 64><<<grid, gdw::THREADS, smem, st>>>(n, fp, hp, off, s, dr, r, slots);
+    } else if (ma == 64) {
+        cudaFuncSetAttribute(gcn_dw_tc_kernel<64, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        note_launch();
+        gcn_dw_tc_kernel<64, 32><<<grid, gdw::THREADS, smem, st>>>(n, fp, hp, off, s, dr, r, slots);
     } else {
-        cudaFuncSetAttribute(gcn_dw_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(gcn_dw_tc_kernel<128, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         note_launch();
-        gcn_dw_tc_kernel<128><<<grid, gdw::THREADS, smem, st>>>(n, fp, hp, off, s, dr, r, slots);
+        gcn_dw_tc_kernel<128, 32><<<grid, gdw::THREADS, smem, st>>>(n, fp, hp, off, s, dr, r, slots);
     }
     note_launch();
     gdw_reduce_kernel<<<(unsigned)cdiv((int64_t)fp * hp * 32, 256), 256, 0, st>>>(grid, ma, S.N, fp, hp, slots, gw);
