@@ -57,7 +57,7 @@ constexpr int BM = 128;
 #endif
 constexpr int NGATHER = DGNN_GTC_NGATHER, IDX_WARP = NGATHER, MMA_WARP = NGATHER + 1, EPI0 = NGATHER + 2, NEPI = 4;
 constexpr int THREADS = 32 * (EPI0 + NEPI);
-constexpr int ASTAGES = 2, ISTAGES = 3;
+constexpr int ASTAGES = 3, ISTAGES = 4;   // maxima (GtcLayout::AST / IST per width)
 constexpr int ECAP = 1024;   // edges per tile staged in shared memory (else read from global)
 }  // namespace gtc
 
@@ -82,10 +82,13 @@ struct GtcLayout {
     static constexpr int A_STAGE = 2 * A_HALF;
     static constexpr int B_HALF = KCH * HP * 64;
     static constexpr int EPI_BUF = 32 * HP * 4;            // per epilogue warp
-    static constexpr int OFF_B = gtc::ASTAGES * A_STAGE;
+    // A stages: 3 for narrow operands (more tiles' gathers in flight), 2 at FP = 64
+    static constexpr int AST = FP <= 32 ? 3 : 2;
+    static constexpr int IST = AST + 1;
+    static constexpr int OFF_B = AST * A_STAGE;
     static constexpr int OFF_EPI = OFF_B + 2 * B_HALF;
     static constexpr int OFF_IDX = OFF_EPI + gtc::NEPI * EPI_BUF;
-    static constexpr int OFF_BARS = OFF_IDX + gtc::ISTAGES * (int)sizeof(GtcIdx);
+    static constexpr int OFF_BARS = OFF_IDX + IST * (int)sizeof(GtcIdx);
     static constexpr int BYTES = OFF_BARS + (int)sizeof(GtcBars) + 1024;
     static constexpr int TMEM_COLS = 2 * HP <= 32 ? 32 : (2 * HP <= 64 ? 64 : 128);
 };
@@ -126,14 +129,14 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
     }
     if (warp == gtc::MMA_WARP) tmem_alloc(&bars->tmem, L::TMEM_COLS);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < gtc::ASTAGES; ++s) {
+        for (int s = 0; s < L::AST; ++s) {
             mbar_init(&bars->full[s], gtc::NGATHER);
             mbar_init(&bars->empty[s], 1);
             bars->claim[s] = 0;
             if (s == 0)
-                for (int k = gtc::ASTAGES; k < gtc::ISTAGES; ++k) bars->claim[k] = 0;
+                for (int k = L::AST; k < L::IST; ++k) bars->claim[k] = 0;
         }
-        for (int s = 0; s < gtc::ISTAGES; ++s) {
+        for (int s = 0; s < L::IST; ++s) {
             mbar_init(&bars->ifull[s], 1);
             mbar_init(&bars->iempty[s], gtc::NGATHER);
         }
@@ -154,10 +157,10 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
         const int sub = lane / G, gl = lane % G;
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-            const int s = it % gtc::ASTAGES, si = it % gtc::ISTAGES;
+            const int s = it % L::AST, si = it % L::IST;
             const GtcIdx& ix = idx[si];
-            if (AGG) mbar_wait_sleep(&bars->ifull[si], (it / gtc::ISTAGES) & 1);
-            if (it >= gtc::ASTAGES) mbar_wait_sleep(&bars->empty[s], ((it / gtc::ASTAGES) - 1) & 1);
+            if (AGG) mbar_wait_sleep(&bars->ifull[si], (it / L::IST) & 1);
+            if (it >= L::AST) mbar_wait_sleep(&bars->empty[s], ((it / L::AST) - 1) & 1);
             const uint32_t a_hi = sb + s * L::A_STAGE, a_lo = a_hi + L::A_HALF;
             const bool spill = AGG && ix.spill;
             // BWD skip: the skip term dpre[:, :F] of this tile's rows goes to ds
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             // A ring's empty[s] keeps every warp within one use of stage s).
             constexpr int CROWS = 2 * RW, NCHUNK = gtc::BM / CROWS;
             const int cslot = s;
-            const int cbase = (int)(it / gtc::ASTAGES) * (NCHUNK + gtc::NGATHER);
+            const int cbase = (int)(it / L::AST) * (NCHUNK + gtc::NGATHER);
             for (;;) {
                 int chunk = 0;
                 if (lane == 0) chunk = atomicAdd(&bars->claim[cslot], 1) - cbase;
@@ -280,8 +283,8 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
         if (AGG) {
             uint32_t it = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-                const int si = it % gtc::ISTAGES;
-                if (it >= gtc::ISTAGES) mbar_wait_sleep(&bars->iempty[si], ((it / gtc::ISTAGES) - 1) & 1);
+                const int si = it % L::IST;
+                if (it >= L::IST) mbar_wait_sleep(&bars->iempty[si], ((it / L::IST) - 1) & 1);
                 GtcIdx& ix = idx[si];
                 const int64_t r0 = (int64_t)tile * gtc::BM;
                 const int nr = (int)min((int64_t)gtc::BM, (int64_t)n - r0);
@@ -338,10 +341,10 @@ __global__ void __launch_bounds__(gtc::THREADS, 1) gcn_fwd_tc_kernel(
             const uint32_t idesc = idesc_tf32(gtc::BM, HP);
             uint32_t it = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-                const int s = it % gtc::ASTAGES;
+                const int s = it % L::AST;
                 const uint32_t a = it & 1, u = it >> 1;
                 if (u >= 1) mbar_wait_sleep(&bars->accempty[a], (u - 1) & 1);
-                mbar_wait_sleep(&bars->full[s], (it / gtc::ASTAGES) & 1);
+                mbar_wait_sleep(&bars->full[s], (it / L::AST) & 1);
                 fence_after();
                 const uint32_t d = bars->tmem + a * HP;
                 const uint32_t a_hi = sb + s * L::A_STAGE, a_lo = a_hi + L::A_HALF;
