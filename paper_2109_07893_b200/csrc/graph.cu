@@ -189,7 +189,8 @@ static int rowptr_launch(int32_t n, int64_t nnz, const int32_t* rows, int32_t* r
 
 // ---------------------------------------------------------------------------
 // K1: delta apply (delta.py:126-146), one thread per row, two-pointer merge
-// (rows longer than kMergeLong: a warp each, delta_merge_long_kernel)
+// (rows of kMergeLong+1..kMergeCtaRow entries: their warp; longer: a CTA each,
+// in the same launch)
 constexpr int kMergeLong = 16;
 
 __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int key) {
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(kLongThreads) transpose_scatter_kernel(
         int32_t* cursor, int32_t* __restrict__ tcol, double* __restrict__ tval, int hubs) {
     // thread per row; rows of kLongRow+1..kCtaRow entries are scattered by
     // their warp together (ballot queue), longer ones by a CTA each
-    // (transpose_scatter_long_kernel).  The order inside a column is fixed
+    // (the leading hub blocks of the same launch).  The order inside a column is fixed
     // by the segment sort that follows.
     if ((int)blockIdx.x < hubs) {
         for_hub_rows(n, hubs, [&](int r) { return rp[r + 1] - rp[r] > kCtaRow; }, [&](int r) {
@@ -715,10 +716,9 @@ __global__ void __launch_bounds__(kLongThreads) lap_write_kernel(
     }
 }
 
-// CTA-per-row versions for the rows past kCtaRow entries (the largest hubs
-// of heavy-tailed graphs; a warp per row made the largest hub a serial tail
-// of the whole call).  Their list is filled from the top of the long-row
-// array down (long_rows[n - 1 - i], counter long_count[1]).
+// CTA-per-row passes for the rows past kCtaRow entries (the largest hubs of
+// heavy-tailed graphs; a warp per row made the largest hub a serial tail of
+// the whole call), run by the leading blocks of the per-row launches.
 // Entries of a row are sorted by column; the identity term of a row without
 // a stored diagonal is inserted before its first column > r.  Output order
 // and values are the thread kernels' exactly.
@@ -937,7 +937,7 @@ int dgnn_csr_apply_delta(int32_t n, const int32_t* old_rowptr, const int32_t* ol
     int32_t* long_count = long_rows + round64((int64_t)n + 1);
     void* sws = long_count + 64;
     size_t sws_bytes = ws_bytes - 3 * (size_t)round64((int64_t)n + 1) * sizeof(int32_t) - 64 * sizeof(int32_t);
-    cudaMemsetAsync(long_count, 0, sizeof(int32_t), st);
+    (void)long_count;   // (workspace layout kept; hub rows need no list any more)
     int rc = rowptr_launch(n, n_del, del_row, drp, st);
     if (!rc) rc = rowptr_launch(n, n_ins, ins_row, irp, st);
     if (rc) return rc;
