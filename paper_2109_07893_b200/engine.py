@@ -1730,8 +1730,6 @@ class Engine:
         for b in range(plan.nblk):
             for r in self.ranks:
                 r.begin_block(b, keep=False, ledger=transfer, next_b=b + 1 if b + 1 < plan.nblk else b, fresh=True)
-            for r in self.ranks:
-                r.prefetch(b + 1)
             if b == plan.nblk - 1 and self.cfg.classes == 2 and SKIP_LAST_FORWARD:
                 # the last block's forward-sweep pass produces nothing that is
                 # read later: no checkpoint follows it and the loss comes from
@@ -1741,6 +1739,8 @@ class Engine:
                 self._record_forward_pass(b, "forward", comm)
             else:
                 self._layers_forward(b, "forward", comm)
+            for r in self.ranks:     # next block's rebuild: enqueued behind this block's forward (see below)
+                r.prefetch(b + 1)
             for r in self.ranks:
                 if self.cfg.classes != 2:
                     r.block_loss(b)
@@ -1754,10 +1754,14 @@ class Engine:
                 # the last rerun prefetches block 0 again: the next pass (the
                 # next epoch's forward sweep, or an evaluation) starts there
                 r.begin_block(b, keep=True, ledger=transfer, next_b=b - 1 if b > 0 else 0)
+            self._layers_forward(b, "rerun", comm)
             if b == 0:
+                # after the rerun's forward is enqueued: the rebuild's host-side
+                # launches (tens of ms at configs[2]) then run while the GPU
+                # computes instead of ahead of it (an epoch that starts from a
+                # synchronised host would otherwise wait for them)
                 for r in self.ranks:
                     r.prefetch(0, next_epoch=True)
-            self._layers_forward(b, "rerun", comm)
             if self.split_pipe or self.peer is not None:
                 if self.peer is not None:
                     self._peer_backward(b, comm)
