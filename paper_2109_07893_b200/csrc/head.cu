@@ -280,10 +280,15 @@ int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const dou
 // accumulators of its 8 dims (u and v side).  Pairs are assigned statically
 // (fixed grid), groups / warps / CTAs are combined in fixed order and the
 // per-CTA partials are reduced by head_lg_reduce_kernel: deterministic.
-static int head_ctas() { return num_sms(); }
+// two CTAs per SM (<= 128 registers): the pair loop is a chain of dependent
+// gathers, so resident warps are what hides it
+#ifndef DGNN_HEAD_CPS
+#define DGNN_HEAD_CPS 2
+#endif
+static int head_ctas() { return DGNN_HEAD_CPS * num_sms(); }
 
 template <int EP>
-__global__ void __launch_bounds__(256) head_loss_grad_kernel(int64_t npairs, const int32_t* __restrict__ u,
+__global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int64_t npairs, const int32_t* __restrict__ u,
                                                              const int32_t* __restrict__ v,
                                                              const int32_t* __restrict__ y, dgnn_frame z, int C,
                                                              const float* __restrict__ hw,
