@@ -169,12 +169,26 @@ int tn_run(int64_t rows, int M, int N, LA la, LB lb, double* out, int64_t ldo, d
     return launch_status(what);
 }
 
-// deterministic fp64 sum (single CTA, fixed order)
+// deterministic fp64 sum (single CTA, fixed order): each thread keeps 8
+// partial sums (8 loads in flight instead of one dependent chain), combined
+// by a fixed tree, then the CTA tree
 __global__ void __launch_bounds__(1024) sum_f64_kernel(int64_t n, const double* __restrict__ x,
                                                         double* __restrict__ out, int accumulate) {
     __shared__ double sh[1024];
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    double p[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const int64_t step = 8 * (int64_t)blockDim.x;
+    int64_t i = threadIdx.x;
+    for (; i + 7 * (int64_t)blockDim.x < n; i += step) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = x[i + k * (int64_t)blockDim.x];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) p[k] += v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (i + k * (int64_t)blockDim.x < n) p[k] += x[i + k * (int64_t)blockDim.x];
+    const double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
     sh[threadIdx.x] = s;
     __syncthreads();
     for (int o = 512; o > 0; o >>= 1) {
