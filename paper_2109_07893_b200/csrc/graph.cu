@@ -401,18 +401,45 @@ __global__ void __launch_bounds__(kLongThreads) transpose_scatter_kernel(
 constexpr int kSmallSeg = 32;
 constexpr int kRankMax = 1024;       // mid segments: rank sort of a shared-memory copy
 
-// Short segments: one thread sorts its column.
-__global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp,
-                                      const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
-                                      int32_t* __restrict__ dst_col, double* __restrict__ dst_val,
-                                      int32_t* __restrict__ mid_list, int32_t* mid_count,
-                                      int32_t* __restrict__ long_list, int32_t* long_count) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// Short segments: one thread sorts its column.  Mid segments (kSmallSeg < d
+// <= kRankMax; most hub columns of a heavy-tailed graph): a CTA each, keys
+// staged in shared memory, each entry placed at its rank = #smaller keys
+// (keys are distinct rows, so the order is the sort's) -- run by the leading
+// `hubs` blocks of the same launch (column-slice scan), alongside the
+// per-column blocks.  Long segments (> kRankMax) go to the chunk kernels
+// through a device list.
+__device__ __forceinline__ void seg_sort_mid_cta(int c, const int32_t* __restrict__ trp,
+                                                 const int32_t* __restrict__ src_col,
+                                                 const double* __restrict__ src_val, int32_t* __restrict__ dst_col,
+                                                 double* __restrict__ dst_val) {
+    __shared__ int32_t skey[kRankMax];
+    const int b = trp[c], d = trp[c + 1] - b;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) skey[i] = src_col[b + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const int k = skey[i];
+        int rank = 0;
+        for (int j = 0; j < d; ++j) rank += skey[j] < k;
+        dst_col[b + rank] = k;
+        if (dst_val) dst_val[b + rank] = src_val[b + i];
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kLongThreads) seg_sort_small_kernel(
+        int32_t n, const int32_t* __restrict__ trp, const int32_t* __restrict__ src_col,
+        const double* __restrict__ src_val, int32_t* __restrict__ dst_col, double* __restrict__ dst_val,
+        int32_t* __restrict__ long_list, int32_t* long_count, int hubs) {
+    if ((int)blockIdx.x < hubs) {
+        for_hub_rows(n, hubs, [&](int c) { const int d = trp[c + 1] - trp[c]; return d > kSmallSeg && d <= kRankMax; },
+                     [&](int c) { seg_sort_mid_cta(c, trp, src_col, src_val, dst_col, dst_val); });
+        return;
+    }
+    const int64_t c = (blockIdx.x - hubs) * (int64_t)blockDim.x + threadIdx.x;
     if (c >= n) return;
     const int b = trp[c], e = trp[c + 1], d = e - b;
-    if (d > kSmallSeg) {                       // hub column: handed to a block-per-segment kernel
-        if (d <= kRankMax) mid_list[atomicAdd(mid_count, 1)] = (int32_t)c;
-        else long_list[atomicAdd(long_count, 1)] = (int32_t)c;
+    if (d > kSmallSeg) {                       // hub column: the leading blocks or the chunk kernels
+        if (d > kRankMax) long_list[atomicAdd(long_count, 1)] = (int32_t)c;
         return;
     }
     // each entry goes to its rank (keys are distinct rows: the sorted
@@ -423,33 +450,6 @@ __global__ void seg_sort_small_kernel(int32_t n, const int32_t* __restrict__ trp
         for (int j = 0; j < d; ++j) rank += src_col[b + j] < k;
         dst_col[b + rank] = k;
         if (dst_val) dst_val[b + rank] = src_val[b + i];
-    }
-}
-
-// Mid segments (kSmallSeg < d <= kRankMax; most hub columns of a heavy-tailed
-// graph): one CTA per segment, keys staged in shared memory, each entry placed
-// at its rank = #smaller keys (keys are distinct rows, so the order is the
-// sort's).  A 1024-thread bitonic network per 40-entry column left most of
-// its threads idle behind ~20 barriers.
-__global__ void __launch_bounds__(kLongThreads) seg_sort_mid_kernel(
-        const int32_t* __restrict__ trp, const int32_t* __restrict__ src_col, const double* __restrict__ src_val,
-        int32_t* __restrict__ dst_col, double* __restrict__ dst_val, const int32_t* __restrict__ mid_list,
-        const int32_t* __restrict__ mid_count) {
-    __shared__ int32_t skey[kRankMax];
-    const int cnt = *mid_count;
-    for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
-        const int c = mid_list[li];
-        const int b = trp[c], d = trp[c + 1] - b;
-        for (int i = threadIdx.x; i < d; i += blockDim.x) skey[i] = src_col[b + i];
-        __syncthreads();
-        for (int i = threadIdx.x; i < d; i += blockDim.x) {
-            const int k = skey[i];
-            int rank = 0;
-            for (int j = 0; j < d; ++j) rank += skey[j] < k;
-            dst_col[b + rank] = k;
-            if (dst_val) dst_val[b + rank] = src_val[b + i];
-        }
-        __syncthreads();
     }
 }
 
@@ -1001,12 +1001,11 @@ int dgnn_csr_transpose_staged(int32_t n, int64_t nnz, const int32_t* rowptr, con
     // columns past kRankMax, the cursor array the mid columns
     cudaMemsetAsync(long_rows_count, 0, sizeof(int32_t), st);
     ::dgnn::note_launch();
-    seg_sort_small_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, t_rowptr, stage_col, stage_val, t_col,
-                                                                   val ? t_val : nullptr, cursor, long_count,
-                                                                   long_rows, long_rows_count);
-    ::dgnn::note_launch();
-    seg_sort_mid_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col, stage_val, t_col,
-                                                                   val ? t_val : nullptr, cursor, long_count);
+    {
+        const int hubs = kLongCTAs * num_sms();
+        seg_sort_small_kernel<<<(unsigned)cdiv(n, kLongThreads) + hubs, kLongThreads, 0, st>>>(
+            n, t_rowptr, stage_col, stage_val, t_col, val ? t_val : nullptr, long_rows, long_rows_count, hubs);
+    }
     ::dgnn::note_launch();
     seg_chunk_sort_kernel<<<num_sms() * kLongCTAs, kLongThreads, 0, st>>>(t_rowptr, stage_col,
                                                                      val ? stage_val : nullptr, long_rows,
