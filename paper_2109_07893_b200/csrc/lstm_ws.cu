@@ -62,13 +62,19 @@ struct WsRoles {
 #ifndef DGNN_FWD_NEPI32
 #define DGNN_FWD_NEPI32 16
 #endif
+#ifndef DGNN_FWD_ST64
+#define DGNN_FWD_ST64 3
+#endif
+#ifndef DGNN_FWD_RAW64
+#define DGNN_FWD_RAW64 6
+#endif
 template <int HP>
-using FwdRoles = WsRoles<DGNN_FWD_NPROD, (HP >= 64 ? DGNN_FWD_NEPI64 : (HP >= 32 ? DGNN_FWD_NEPI32 : 8)), (HP >= 64 ? 3 : 4)>;
+using FwdRoles = WsRoles<DGNN_FWD_NPROD, (HP >= 64 ? DGNN_FWD_NEPI64 : (HP >= 32 ? DGNN_FWD_NEPI32 : 8)), (HP >= 64 ? DGNN_FWD_ST64 : 4)>;
 // forward activation landing ring (fp32 chunks, cp.async), decoupled from
 // the operand stages so loads run RAW_RING - 1 chunks ahead (6 at hidden 64:
 // the operand stages are 48 KB and the c_prev tile takes 32 KB)
 template <int HP>
-constexpr int raw_ring() { return HP >= 64 ? 6 : 8; }
+constexpr int raw_ring() { return HP >= 64 ? DGNN_FWD_RAW64 : 8; }
 // backward: 8 dz-producer warps fed from shared memory by one loader warp
 // (the extra warp), 3-stage A/B ring to leave room for the raw input ring
 #ifndef DGNN_BWD_NPROD
