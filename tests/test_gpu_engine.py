@@ -307,3 +307,22 @@ def test_tm_halo_matches_redistribution_bitwise(workers, nblk, window, monkeypat
         assert np.array_equal(ga[k], gb[k]), k
     assert ca.as_dict() == cb.as_dict() and ca.events == cb.events
     assert ta.as_dict() == tb.as_dict()
+
+
+@pytest.mark.parametrize("name", ["cdgcn_small", "tmgcn_small"])
+def test_block0_slot_sets_do_not_change_results(name, monkeypatch):
+    """keep_graphs with two or three block-0 slot sets (the next epochs'
+    rebuilds overlap one or two epochs of compute): identical trajectories
+    over three epochs (every epoch rebuilds its graphs into a rotated set)."""
+    import paper_2109_07893_b200.engine as engine_mod
+    fx, cfg, data, train, test, _ = product_case(name)
+    out = {}
+    for sets in ("2", "3"):
+        monkeypatch.setattr(engine_mod, "BLOCK0_SETS", sets)
+        monkeypatch.setattr(engine_mod, "KEEP_GRAPHS", "auto")
+        pk.api.clear_engines()
+        out[sets] = pk.train_distributed(cfg, data, train, test, epochs=3, seed=3, workers=2, nblk=1)
+    (ta, pa, *_), (tb, pb, *_) = out["2"], out["3"]
+    assert [a["loss"] for a in ta] == [b["loss"] for b in tb]
+    for k in pa:
+        assert np.array_equal(pa[k], pb[k]), k
