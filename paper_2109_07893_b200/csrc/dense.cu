@@ -7,6 +7,8 @@
 // in fp64 and added to an fp64 gradient accumulator -- bit-reproducible from
 // run to run, no floating-point atomics anywhere.
 #include "common.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace dgnn {
 
@@ -169,33 +171,52 @@ int tn_run(int64_t rows, int M, int N, LA la, LB lb, double* out, int64_t ldo, d
     return launch_status(what);
 }
 
-// deterministic fp64 sum (single CTA, fixed order): each thread keeps 8
-// partial sums (8 loads in flight instead of one dependent chain), combined
-// by a fixed tree, then the CTA tree
-__global__ void __launch_bounds__(1024) sum_f64_kernel(int64_t n, const double* __restrict__ x,
-                                                        double* __restrict__ out, int accumulate) {
-    __shared__ double sh[1024];
+// deterministic fp64 sum, one 8-CTA cluster (8 SMs of load bandwidth; a
+// single CTA was latency-bound at ~50 GB/s): thread g of the cluster keeps 8
+// partial sums over x[g + k * 8192 + j * 65536] (8 loads in flight), combined
+// by a fixed tree, then a fixed shuffle tree per warp, the 32 warp sums in
+// order, and the 8 CTA sums read by CTA 0 over distributed shared memory in
+// rank order.  The order depends only on n, never on the schedule.
+constexpr int kSumCtas = 8;
+__global__ void __cluster_dims__(kSumCtas, 1, 1) __launch_bounds__(1024)
+    sum_f64_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ out, int accumulate) {
+    __shared__ double wsum[32];
+    __shared__ double csum;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    constexpr int64_t T = (int64_t)kSumCtas * 1024;
     double p[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    const int64_t step = 8 * (int64_t)blockDim.x;
-    int64_t i = threadIdx.x;
-    for (; i + 7 * (int64_t)blockDim.x < n; i += step) {
+    int64_t i = (int64_t)rank * 1024 + threadIdx.x;
+    for (; i + 7 * T < n; i += 8 * T) {
         double v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = x[i + k * (int64_t)blockDim.x];
+        for (int k = 0; k < 8; ++k) v[k] = x[i + k * T];
 #pragma unroll
         for (int k = 0; k < 8; ++k) p[k] += v[k];
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-        if (i + k * (int64_t)blockDim.x < n) p[k] += x[i + k * (int64_t)blockDim.x];
-    const double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-    sh[threadIdx.x] = s;
+        if (i + k * T < n) p[k] += x[i + k * T];
+    double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
     __syncthreads();
-    for (int o = 512; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
+    if (threadIdx.x < 32) {
+        double w = wsum[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xffffffffu, w, o);
+        if (threadIdx.x == 0) csum = w;
     }
-    if (threadIdx.x == 0) *out = accumulate ? (*out + sh[0]) : sh[0];
+    cl.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+        double c[kSumCtas];
+#pragma unroll
+        for (int q = 0; q < kSumCtas; ++q) c[q] = *cl.map_shared_rank(&csum, q);
+        const double t = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
+        *out = accumulate ? (*out + t) : t;
+    }
+    cl.sync();   // keep every CTA's csum alive until CTA 0 has read it
 }
 
 __global__ void axpy_kernel(int64_t n, float coef, const float* __restrict__ y, float* __restrict__ z,
@@ -301,7 +322,7 @@ int dgnn_gcn_weight_grad(int32_t n, dgnn_frame s, dgnn_frame dr, dgnn_frame r, i
 
 int dgnn_sum_f64(int64_t n, const double* x, double* out, int accumulate, void* stream) {
     ::dgnn::note_launch();
-    sum_f64_kernel<<<1, 1024, 0, as_stream(stream)>>>(n, x, out, accumulate);
+    sum_f64_kernel<<<kSumCtas, 1024, 0, as_stream(stream)>>>(n, x, out, accumulate);
     return launch_status("sum_f64");
 }
 

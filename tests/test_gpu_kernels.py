@@ -693,3 +693,28 @@ def test_head_scatter_active_matches_full_pass(ep, classes, slabs):
                  _lib.stream_handle())
         outs.append(buf[:n * ep].cpu().numpy())
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 8191, 8192 * 8 + 3, 1_000_003])
+def test_sum_f64_deterministic(n):
+    """dgnn_sum_f64 (one 8-CTA cluster, fixed order): within fp64 rounding of
+    an exact (math.fsum) sum, accumulate adds onto *out, and repeated calls
+    agree bit for bit."""
+    import math
+    from paper_2109_07893_b200 import _lib
+    from paper_2109_07893_b200._lib import call, ptr
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n) * np.exp(rng.uniform(-5, 5, n))
+    xd = torch.from_numpy(x).to(dev)
+    out = torch.zeros(3, dtype=torch.float64, device=dev)
+    out[2] = 0.25
+    st = _lib.stream_handle()
+    call("dgnn_sum_f64", n, ptr(xd), out.data_ptr(), 0, st)
+    call("dgnn_sum_f64", n, ptr(xd), out.data_ptr() + 8, 0, st)
+    call("dgnn_sum_f64", n, ptr(xd), out.data_ptr() + 16, 1, st)
+    got = out.cpu().numpy()
+    exact = math.fsum(x)
+    assert got[0] == got[1]
+    assert abs(got[0] - exact) <= 1e-15 * max(1.0, float(np.abs(x).sum()))
+    assert got[2] == 0.25 + got[0]
