@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int3
     // without any are zero-filled by a flat float4 pass and the lane
     // groups visit only the active vertices (same arithmetic per row).
     constexpr int CM = CC ? CC : kMaxClasses;
+    constexpr int HS_U = CC ? 4 : 1;                // slots per lane in flight (compile-time classes)
     constexpr int PER = (EP + GL - 1) / GL;         // outputs per lane
     const int C = CC ? CC : C_rt;
     extern __shared__ float hws[];                  // [2*EP][C]
@@ -180,13 +181,42 @@ __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int3
 #pragma unroll
         for (int i = 0; i < 2 * CM; ++i) sacc[i] = 0.0;
         if (ok) {
+            // HS_U incidence slots per lane in flight (slot -> dlogit loads
+            // issued together), folded in slot order: the same per-lane
+            // summation order as one slot at a time
             const int e1 = ptr[x + 1];
-            for (int e = ptr[x] + gl; e < e1; e += GL) {
+            int e = ptr[x] + gl;
+            for (; e + (HS_U - 1) * GL < e1; e += HS_U * GL) {
+                int sl[HS_U];
+#pragma unroll
+                for (int q = 0; q < HS_U; ++q) sl[q] = slot[e + q * GL];
+                double d[HS_U][CM];
+#pragma unroll
+                for (int q = 0; q < HS_U; ++q)
+#pragma unroll
+                    for (int c = 0; c < CM; ++c) d[q][c] = c < C ? dl[(int64_t)(sl[q] >> 1) * C + c] : 0.0;
+#pragma unroll
+                for (int q = 0; q < HS_U; ++q) {
+                    const bool side = sl[q] & 1;   // predicated adds: sacc stays in registers
+#pragma unroll
+                    for (int c = 0; c < CM; ++c)
+                        if (c < C) {
+                            if (side) sacc[CM + c] += d[q][c];
+                            else sacc[c] += d[q][c];
+                        }
+                }
+            }
+            for (; e < e1; e += GL) {
                 const int sl = slot[e];
-                const int p = sl >> 1, side = sl & 1;
+                const int p = sl >> 1;
+                const bool side = sl & 1;
 #pragma unroll
                 for (int c = 0; c < CM; ++c)
-                    if (c < C) sacc[side * CM + c] += dl[(int64_t)p * C + c];
+                    if (c < C) {
+                        const double d = dl[(int64_t)p * C + c];
+                        if (side) sacc[CM + c] += d;
+                        else sacc[c] += d;
+                    }
             }
         }
 #pragma unroll
@@ -312,9 +342,23 @@ __global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int6
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc_u[j][0] = acc_u[j][1] = acc_v[j][0] = acc_v[j][1] = 0.0;
     acc_b[0] = acc_b[1] = 0.0;
+    // the next pair's endpoints and label are loaded one iteration ahead, so
+    // an iteration waits on one gather latency (z rows), not two
+    int32_t un = 0, vn = 0, yn = 0;
+    if (gid < npairs) {
+        un = u[gid];
+        vn = v[gid];
+        yn = y[gid];
+    }
     for (int64_t p = gid; p < npairs; p += ngroups) {
-        const float4* zu = reinterpret_cast<const float4*>(frame_row<const float>(z, u[p]) + k0);
-        const float4* zv = reinterpret_cast<const float4*>(frame_row<const float>(z, v[p]) + k0);
+        const int32_t uc = un, vc = vn, lab = yn;
+        if (p + ngroups < npairs) {
+            un = u[p + ngroups];
+            vn = v[p + ngroups];
+            yn = y[p + ngroups];
+        }
+        const float4* zu = reinterpret_cast<const float4*>(frame_row<const float>(z, uc) + k0);
+        const float4* zv = reinterpret_cast<const float4*>(frame_row<const float>(z, vc) + k0);
         const float4 a0 = zu[0], a1 = zu[1], b0 = zv[0], b1 = zv[1];
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
@@ -335,7 +379,6 @@ __global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int6
             const double l0 = (double)(lg[0] + hb[0]), l1 = (double)(lg[1] + hb[1]);
             const double mx = l0 > l1 ? l0 : l1;
             const double lz = log(exp(l0 - mx) + exp(l1 - mx));
-            const int lab = y[p];
             loss_pp[p] = -(((lab ? l1 : l0) - mx) - lz);
             dl[0] = (exp((l0 - mx) - lz) - (lab == 0 ? 1.0 : 0.0)) * scale;
             dl[1] = (exp((l1 - mx) - lz) - (lab == 1 ? 1.0 : 0.0)) * scale;
