@@ -136,6 +136,51 @@ __global__ void head_grad_reduce_kernel(int nchunks, int ep, int C, const double
 #ifndef DGNN_HS_GLA
 #define DGNN_HS_GLA 4
 #endif
+// threshold (incident slots) above which a vertex is summed by its whole warp
+#ifndef DGNN_HS_HUB
+#define DGNN_HS_HUB 64
+#endif
+constexpr int HS_HUB = DGNN_HS_HUB;
+
+// sacc[side][c] += dl[p][c] over the incidence slots e = e, e + stride, ...
+// below e1, in slot order; U slots in flight (slot -> dlogit loads issued
+// together); predicated adds keep sacc in registers
+template <int CM, int U>
+__device__ __forceinline__ void hs_fold(int e, int e1, int stride, const int32_t* __restrict__ slot,
+                                        const double* __restrict__ dl, int C, double* sacc) {
+    for (; e + (U - 1) * stride < e1; e += U * stride) {
+        int sl[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) sl[q] = slot[e + q * stride];
+        double d[U][CM];
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+#pragma unroll
+            for (int c = 0; c < CM; ++c) d[q][c] = c < C ? dl[(int64_t)(sl[q] >> 1) * C + c] : 0.0;
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const bool side = sl[q] & 1;
+#pragma unroll
+            for (int c = 0; c < CM; ++c)
+                if (c < C) {
+                    if (side) sacc[CM + c] += d[q][c];
+                    else sacc[c] += d[q][c];
+                }
+        }
+    }
+    for (; e < e1; e += stride) {
+        const int sl = slot[e];
+        const bool side = sl & 1;
+#pragma unroll
+        for (int c = 0; c < CM; ++c)
+            if (c < C) {
+                const double d = dl[(int64_t)(sl >> 1) * C + c];
+                if (side) sacc[CM + c] += d;
+                else sacc[c] += d;
+            }
+    }
+}
+
 template <int EP, int CC, int GL>   // CC: classes (compile time), 0: runtime C <= kMaxClasses
 __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int32_t* __restrict__ ptr,
                                                            const int32_t* __restrict__ slot,
@@ -146,9 +191,9 @@ __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int3
     //       = S_0[x] . W_u^T + S_1[x] . W_v^T,  S_side[x][c] = sum dl[p][c]:
     // 8 lanes per vertex (4 vertices per warp in flight) sum the 2C fp64
     // dlogits over the incidence list, 8 slots at a time, in a fixed
-    // butterfly, then form the E outputs -- a hub vertex (heavy-tailed
-    // graphs: tens of thousands of incident pairs) costs 1/GL of a serial
-    // walk and no vector work per pair.
+    // butterfly, then form the E outputs -- no vector work per pair; a
+    // vertex with more than HS_HUB incident slots (heavy-tailed graphs) is
+    // summed by its whole warp.
     // With `act` (the vertices that have incident pairs, ascending), rows
     // without any are zero-filled by a flat float4 pass and the lane
     // groups visit only the active vertices (same arithmetic per row).
@@ -180,49 +225,33 @@ __global__ void __launch_bounds__(256) head_scatter_kernel(int32_t n, const int3
         double sacc[2 * CM];
 #pragma unroll
         for (int i = 0; i < 2 * CM; ++i) sacc[i] = 0.0;
-        if (ok) {
-            // HS_U incidence slots per lane in flight (slot -> dlogit loads
-            // issued together), folded in slot order: the same per-lane
-            // summation order as one slot at a time
-            const int e1 = ptr[x + 1];
-            int e = ptr[x] + gl;
-            for (; e + (HS_U - 1) * GL < e1; e += HS_U * GL) {
-                int sl[HS_U];
-#pragma unroll
-                for (int q = 0; q < HS_U; ++q) sl[q] = slot[e + q * GL];
-                double d[HS_U][CM];
-#pragma unroll
-                for (int q = 0; q < HS_U; ++q)
-#pragma unroll
-                    for (int c = 0; c < CM; ++c) d[q][c] = c < C ? dl[(int64_t)(sl[q] >> 1) * C + c] : 0.0;
-#pragma unroll
-                for (int q = 0; q < HS_U; ++q) {
-                    const bool side = sl[q] & 1;   // predicated adds: sacc stays in registers
-#pragma unroll
-                    for (int c = 0; c < CM; ++c)
-                        if (c < C) {
-                            if (side) sacc[CM + c] += d[q][c];
-                            else sacc[c] += d[q][c];
-                        }
-                }
-            }
-            for (; e < e1; e += GL) {
-                const int sl = slot[e];
-                const int p = sl >> 1;
-                const bool side = sl & 1;
-#pragma unroll
-                for (int c = 0; c < CM; ++c)
-                    if (c < C) {
-                        const double d = dl[(int64_t)p * C + c];
-                        if (side) sacc[CM + c] += d;
-                        else sacc[c] += d;
-                    }
-            }
-        }
+        const int e0 = ok ? ptr[x] : 0, e1 = ok ? ptr[x + 1] : 0;
+        const bool hub = e1 - e0 > HS_HUB;
+        if (ok && !hub) hs_fold<CM, HS_U>(e0 + gl, e1, GL, slot, dl, C, sacc);
 #pragma unroll
         for (int i = 0; i < 2 * CM; ++i)
 #pragma unroll
             for (int o = GL / 2; o > 0; o >>= 1) sacc[i] += __shfl_xor_sync(0xffffffffu, sacc[i], o);
+        // vertices with more than HS_HUB incident slots are summed by the
+        // whole warp (32 lanes, fixed butterfly), one at a time, and the
+        // owning group takes the sums: a hub costs 1/32 of a serial walk
+        // instead of 1/GL, and the same in the all-vertex and active passes
+        unsigned hubs = __ballot_sync(0xffffffffu, ok && hub && gl == 0);
+        while (hubs) {
+            const int src = __ffs(hubs) - 1;
+            hubs &= hubs - 1;
+            const int h0 = __shfl_sync(0xffffffffu, e0, src), h1 = __shfl_sync(0xffffffffu, e1, src);
+            double hs[2 * CM];
+#pragma unroll
+            for (int i = 0; i < 2 * CM; ++i) hs[i] = 0.0;
+            hs_fold<CM, HS_U>(h0 + lane, h1, 32, slot, dl, C, hs);
+#pragma unroll
+            for (int i = 0; i < 2 * CM; ++i) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) hs[i] += __shfl_xor_sync(0xffffffffu, hs[i], o);
+                if (lane / GL == src / GL) sacc[i] = hs[i];
+            }
+        }
         if (!ok) continue;
         float* out = frame_row<float>(dz, x);
         float v[PER];

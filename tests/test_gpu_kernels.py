@@ -666,7 +666,8 @@ def test_pair_lstm_forward_matches_single_cta_bitwise(hp, kx, rows):
 def test_head_scatter_active_matches_full_pass(ep, classes, slabs):
     """dz seeds over the active-vertex list (zero-fill pass + gathers of the
     vertices with incident pairs) equal the all-vertex pass bit for bit,
-    hub vertices and owner-layout (slabbed) frames included."""
+    hub vertices and owner-layout (slabbed) frames included, and both match
+    the per-vertex sums computed in numpy."""
     from paper_2109_07893_b200 import _lib
     from paper_2109_07893_b200._lib import call, ptr
     from paper_2109_07893_b200.labels import frame_labels_device
@@ -674,7 +675,9 @@ def test_head_scatter_active_matches_full_pass(ep, classes, slabs):
     rng = np.random.default_rng(ep + classes)
     n, npairs = 50_000, 20_000
     pairs = rng.integers(0, n, (npairs, 2))
-    pairs[:3000, 0] = 7                         # a hub
+    pairs[:3000, 0] = 7                         # hubs (summed by a whole warp)
+    pairs[3000:3200, 1] = 11
+    pairs[3200:3265, 0] = 13                    # just above the warp threshold
     lab = rng.integers(0, classes, npairs)
     d = frame_labels_device(pairs, lab, n, classes, dev)
     assert d["nact"] == len(np.unique(pairs))
@@ -693,6 +696,14 @@ def test_head_scatter_active_matches_full_pass(ep, classes, slabs):
                  _lib.stream_handle())
         outs.append(buf[:n * ep].cpu().numpy())
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    # against the per-vertex sums in numpy (fp64): dz[x] = S_u[x] W_u^T + S_v[x] W_v^T
+    dln, hwn = dl.cpu().numpy(), hw.cpu().numpy().astype(np.float64)
+    su, sv = np.zeros((n, classes)), np.zeros((n, classes))
+    np.add.at(su, pairs[:, 0], dln)
+    np.add.at(sv, pairs[:, 1], dln)
+    ref = su @ hwn[:ep].T + sv @ hwn[ep:].T
+    got = outs[1].reshape(n, ep).astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref) + 1e-9 * np.abs(ref).max())
 
 
 @pytest.mark.parametrize("n", [0, 1, 7, 8191, 8192 * 8 + 3, 1_000_003])
