@@ -331,18 +331,23 @@ int head_scatter_t(int32_t n, const int32_t* ptr, const int32_t* slot, const dou
 
 
 // Fused head loss + head-parameter gradient (one pass over the labelled
-// pairs, training.py:698-735).  LP = EP / 8 lanes per pair (8 embedding
+// pairs, training.py:698-735).  LP = EP / D lanes per pair (D embedding
 // dims each), 32 / LP pairs per warp in flight.  Logits are reduced over the
 // group in a fixed butterfly and taken from the group leader, which does
 // the fp64 softmax CE, writes loss_pp and dlogits (the scatter kernel reads
 // them) and broadcasts dl to its group; every lane folds a * dl into fp64
-// accumulators of its 8 dims (u and v side).  Pairs are assigned statically
+// accumulators of its D dims (u and v side).  Pairs are assigned statically
 // (fixed grid), groups / warps / CTAs are combined in fixed order and the
 // per-CTA partials are reduced by head_lg_reduce_kernel: deterministic.
 // two CTAs per SM (<= 128 registers): the pair loop is a chain of dependent
 // gathers, so resident warps are what hides it
 #ifndef DGNN_HEAD_CPS
 #define DGNN_HEAD_CPS 2
+#endif
+// embedding dims per lane: 8 (4 removes the register spills at two CTAs per
+// SM but measured slower: 63 -> 80 us at configs[2], scripts/head_lg_time.py)
+#ifndef DGNN_HEAD_DIMS
+#define DGNN_HEAD_DIMS 8
 #endif
 static int head_ctas() { return DGNN_HEAD_CPS * num_sms(); }
 
@@ -355,7 +360,8 @@ __global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int6
                                                              double* __restrict__ loss_pp,
                                                              double* __restrict__ dlogits,
                                                              double* __restrict__ part) {
-    constexpr int LP = EP / 8;                 // lanes per pair
+    constexpr int D = DGNN_HEAD_DIMS;          // embedding dims per lane
+    constexpr int LP = EP / D;                 // lanes per pair
     constexpr int ROWS = 2 * EP + 1;           // head.w rows (u side, v side) + bias
     __shared__ float hws[2 * EP * kMaxClasses];
     __shared__ double red[8][ROWS * 2];        // per-warp partials (C <= 2 staged here; see below)
@@ -366,38 +372,41 @@ __global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int6
     const unsigned gmask = (LP == 32 ? 0xffffffffu : (((1u << LP) - 1u) << (grp * LP)));
     const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LP;
     const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / LP;
-    const int k0 = 8 * gl;
-    double acc_u[8][2], acc_v[8][2], acc_b[2];
+    const int k0 = D * gl;
+    double acc_u[D][2], acc_v[D][2], acc_b[2];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc_u[j][0] = acc_u[j][1] = acc_v[j][0] = acc_v[j][1] = 0.0;
+    for (int j = 0; j < D; ++j) acc_u[j][0] = acc_u[j][1] = acc_v[j][0] = acc_v[j][1] = 0.0;
     acc_b[0] = acc_b[1] = 0.0;
-    // the next pair's endpoints and label are loaded one iteration ahead, so
+    // the next pair's endpoints are loaded one iteration ahead, so
     // an iteration waits on one gather latency (z rows), not two
-    int32_t un = 0, vn = 0, yn = 0;
+    int32_t un = 0, vn = 0;
     if (gid < npairs) {
         un = u[gid];
         vn = v[gid];
-        yn = y[gid];
     }
     for (int64_t p = gid; p < npairs; p += ngroups) {
-        const int32_t uc = un, vc = vn, lab = yn;
+        const int32_t uc = un, vc = vn;
+        const int lab = gl == 0 ? y[p] : 0;   // issued here, used after the logits
         if (p + ngroups < npairs) {
             un = u[p + ngroups];
             vn = v[p + ngroups];
-            yn = y[p + ngroups];
         }
         const float4* zu = reinterpret_cast<const float4*>(frame_row<const float>(z, uc) + k0);
         const float4* zv = reinterpret_cast<const float4*>(frame_row<const float>(z, vc) + k0);
-        const float4 a0 = zu[0], a1 = zu[1], b0 = zv[0], b1 = zv[1];
-        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        float a[D], b[D];
+#pragma unroll
+        for (int q = 0; q < D / 4; ++q) {
+            const float4 aq = zu[q], bq = zv[q];
+            a[4 * q] = aq.x, a[4 * q + 1] = aq.y, a[4 * q + 2] = aq.z, a[4 * q + 3] = aq.w;
+            b[4 * q] = bq.x, b[4 * q + 1] = bq.y, b[4 * q + 2] = bq.z, b[4 * q + 3] = bq.w;
+        }
         float lg[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             float t = 0.f;
             if (c < C) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) t += a[j] * hws[(k0 + j) * C + c] + b[j] * hws[(EP + k0 + j) * C + c];
+                for (int j = 0; j < D; ++j) t += a[j] * hws[(k0 + j) * C + c] + b[j] * hws[(EP + k0 + j) * C + c];
             }
 #pragma unroll
             for (int o = LP / 2; o > 0; o >>= 1) t += __shfl_xor_sync(gmask, t, o);
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int6
         dl[0] = __shfl_sync(gmask, dl[0], grp * LP);
         dl[1] = __shfl_sync(gmask, dl[1], grp * LP);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < D; ++j)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 acc_u[j][c] += (double)a[j] * dl[c];
@@ -430,7 +439,7 @@ __global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int6
 #pragma unroll
     for (int span = 16; span >= LP; span >>= 1) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < D; ++j)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 acc_u[j][c] += __shfl_down_sync(0xffffffffu, acc_u[j][c], span);
@@ -441,7 +450,7 @@ __global__ void __launch_bounds__(256, DGNN_HEAD_CPS) head_loss_grad_kernel(int6
     }
     if (lane < LP) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < D; ++j)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 red[warp][(k0 + j) * 2 + c] = acc_u[j][c];
@@ -485,7 +494,7 @@ template <int EP>
 int head_loss_grad_t(int64_t npairs, const int32_t* u, const int32_t* v, const int32_t* y, dgnn_frame z,
                      const float* hw, const float* hb, double scale, double* loss_pp, double* dlogits, double* ghw,
                      double* ghb, double* part, cudaStream_t st) {
-    int64_t blocks = cdiv(npairs, 256 / (EP / 8));
+    int64_t blocks = cdiv(npairs, 256 / (EP / DGNN_HEAD_DIMS));
     blocks = blocks > head_ctas() ? head_ctas() : (blocks < 1 ? 1 : blocks);
     note_launch();
     head_loss_grad_kernel<EP><<<(unsigned)blocks, 256, 0, st>>>(npairs, u, v, y, z, 2, hw, hb, scale, loss_pp,
