@@ -10,10 +10,12 @@
 #include <vector>
 #include <algorithm>
 #include <random>
+#include <cmath>
 
 int main() {
     // HP_C3: the configs[2] shape (1M vertices, E = 32, 400k pairs per step,
-    // heavy-tailed endpoints: x = n u^3)
+    // heavy-tailed endpoints: x = n u^2.2, ~1.5k slots on the top vertex as
+    // in the configs[2] label sets)
     const int n = HP_C3 ? 1000000 : 750000, C = 2;
     constexpr int ep = HP_C3 ? 32 : 64;
     const int64_t npairs = HP_C3 ? 400000 : 190000;
@@ -23,7 +25,7 @@ int main() {
     for (int64_t p = 0; p < npairs; ++p)
         for (int side = 0; side < 2; ++side) {
             const double u = U(g);
-            const int x = HP_C3 ? std::min(n - 1, (int)(n * u * u * u)) : (int)(g() % n);
+            const int x = HP_C3 ? std::min(n - 1, (int)(n * std::pow(u, 2.2))) : (int)(g() % n);
             inc.push_back({x, (int)(2 * p + side)});
         }
     std::sort(inc.begin(), inc.end());
