@@ -73,6 +73,10 @@ __global__ void __launch_bounds__(256) spmm_f32_kernel(int32_t n, const int32_t*
 // at a time and computes each hub among them: G = F/4 lanes per edge slot,
 // 256/G slots each summing a strided share of the edges in order, slots
 // combined by a fixed tree; q_j = sum_k s_k W[k][j] in k order.
+// edges of a CTA slot in flight per step on rows of more than kWarpHub entries
+#ifndef DGNN_HUB_UB
+#define DGNN_HUB_UB 8
+#endif
 template <int F, int H, int MODE>
 __global__ void __launch_bounds__(256) hub_rows_kernel(int32_t n, const int32_t* __restrict__ rp,
                                                        const int32_t* __restrict__ col,
@@ -159,21 +163,22 @@ __global__ void __launch_bounds__(256) hub_rows_kernel(int32_t n, const int32_t*
             const int eb = rp[row], ee = rp[row + 1];
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             int e = eb + slot;
-            // 8 of the slot's edges in flight at once (a hub of ~8000 edges was a
+            // UB of the slot's edges in flight at once (a hub of ~8000 edges was a
             // 250-step chain of dependent col -> x loads)
-            for (; e + 7 * EPS < ee; e += 8 * EPS) {
-                int c[8];
-                float v[8];
-                float4 xv[8];
+            constexpr int UB = DGNN_HUB_UB;
+            for (; e + (UB - 1) * EPS < ee; e += UB * EPS) {
+                int c[UB];
+                float v[UB];
+                float4 xv[UB];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < UB; ++j) {
                     c[j] = __ldg(col + e + j * EPS);
                     v[j] = __ldg(val + e + j * EPS);
                 }
 #pragma unroll
-                for (int j = 0; j < 8; ++j) xv[j] = ldg4(frame_row<const float>(x, c[j]) + 4 * gl);
+                for (int j = 0; j < UB; ++j) xv[j] = ldg4(frame_row<const float>(x, c[j]) + 4 * gl);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) fma4(acc, v[j], xv[j]);
+                for (int j = 0; j < UB; ++j) fma4(acc, v[j], xv[j]);
             }
             for (; e < ee; e += EPS)
                 fma4(acc, __ldg(val + e), ldg4(frame_row<const float>(x, __ldg(col + e)) + 4 * gl));
