@@ -356,7 +356,8 @@ int dgnn_head_predict(int64_t npairs, const int32_t* u, const int32_t* v, const 
                       dgnn_frame z, int32_t ep, int32_t c, const float* hw, const float* hb,
                       int64_t* correct, void* stream);
 
-/* Deterministic sum of fp64 values into *out (out = sum, or += if accumulate). */
+/* Deterministic sum of fp64 values into *out (out = sum, or += if
+ * accumulate): one 8-CTA cluster, summation order fixed by n alone. */
 int dgnn_sum_f64(int64_t n, const double* x, double* out, int accumulate, void* stream);
 
 /* ---------------- parameters / optimiser (K9) --------------------------- */
